@@ -1,0 +1,295 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 HOT implicit-MPM step (BASELINE.json metric: implicit MPM
+particle-steps/s, fp64, fixed tolerance; plus the dominant kernel's HBM roofline).
+
+Workload: BASELINE config 2, stiffness-contrast twisting bars (scenes/cfg2_twisting_bars.json:
+four 0.6 x 0.08 x 0.08 bars, dx = 0.6/128, 8 ppc jittered, 1,193,126 particles, soft/stiff
+segments E = 1e5 / 1e9, ends driven by rotating kinematic colliders at +-1 rad/s, fixed-
+corotated (the reference's only model), eps = 1e-5).  One step = one advance_step
+(simulation.hpp:286-323): activation + binning + P2G, the HOT solve, G2P + strain + advect.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference CPU path (the oracle port, all host threads) on a
+bounded slab of the same workload.  Under torchrun (N > 1) each rank runs an independent
+replica of the workload (the slab-sharded path is not built yet), scaling "weak".
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
+METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
+UNIT = "particle-steps/s"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k] and "Not" not in r[3 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_slab(particles, frac_x=0.05):
+    """Bounded CPU sample: the particles of the first `frac_x` metres of every bar (both driven
+    ends' physics is represented by the left end collider)."""
+    keep = particles["x"][:, 0] < frac_x
+    return {k: v[keep] for k, v in particles.items()}
+
+
+def run_cpu_reference(sc, particles, steps, warmup, threads, frac_x=0.05):
+    """The reference CPU path (oracle port of hotmpm::advance_step) on the bounded slab."""
+    from oracle import oracle as O
+
+    O.set_threads(threads)
+    slab = cpu_slab(particles, frac_x)
+    orc = O.Oracle(3)
+    orc.set_scene(sc.source)
+    orc.set_particles(slab["x"], slab["v"], slab["mass"], slab["volume"], slab["F"].reshape(-1),
+                      slab["C"].reshape(-1), slab["material"])
+    t_all, n_steps = 0.0, 0
+    outer = []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        st = orc.advance_step((k + 1) / sc.fps)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            t_all += dt
+            n_steps += 1
+            outer.append(st["outer_iterations"])
+    n = slab["x"].shape[0]
+    return dict(value=n * n_steps / t_all, particles=n, steps=n_steps, seconds=t_all, outer=outer,
+                ms_per_step=1000 * t_all / max(n_steps, 1))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scene", default=SCENE)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank, world, local_rank = dist_env()
+    from paper_1911_07913_b200 import load_scene_file, sample_scene_particles
+
+    sc = load_scene_file(args.scene)
+    particles = sample_scene_particles(sc)
+    n_particles = particles["x"].shape[0]
+    config = {"workload": "cfg2 twisting bars (BASELINE configs[1]), FCR, eps=1e-5", "scene": os.path.basename(args.scene),
+              "particles": n_particles, "dx": sc.dx, "ppc": 8, "levels": sc.levels, "window": sc.window,
+              "epsilon": sc.epsilon, "l2": "inputs larger than L2 (level-0 matrix > 126 MB)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        r = run_cpu_reference(sc, particles, max(args.steps, 1), args.warmup, threads, frac_x=0.03)
+        sample = (f"{r['particles']} particles (x < 0.03 m slab of all four bars), {args.warmup} warm-up + "
+                  f"{r['steps']} timed steps from t=0, {threads} threads; outer iterations {r['outer']}")
+        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling)",
+                "config": config,
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                                 "sample": sample},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    device = local_rank
+    torch.cuda.set_device(device)
+    from paper_1911_07913_b200 import Simulation
+
+    sim = Simulation(sc, device=device)
+    sim.set_particles(**particles)
+    stream = torch.cuda.ExternalStream(sim.stream(), device=device)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(device)
+
+    step_no = 0
+
+    def frame_end():
+        return (step_no + 1) / sc.fps
+
+    for _ in range(args.warmup):
+        sim.advance_step(frame_end())
+        step_no += 1
+    sim.clear_diagnostics()
+
+    # ---- device-resident timed region
+    barrier()
+    sim.profile(True)
+    launches0 = sim.kernel_launches()
+    outer = []
+    with ClockSampler(device) as clocks:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = sim.advance_step(frame_end())
+            step_no += 1
+            outer.append(st["outer_iterations"])
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = sim.kernel_launches() - launches0
+    prof = sim.profile_read()
+    sim.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{device}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n_particles * world * args.steps / (ms / 1000.0)
+
+    # ---- end-to-end through the public API with host buffers (pinned)
+    host = sim.particles()
+    pinned = {}
+    for k, v in list(host.items()):
+        t = torch.empty(v.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = v
+        pinned[k] = t.numpy()
+    static = {}
+    for k in ("mass", "volume", "material"):
+        a = particles[k]
+        t = torch.empty(a.shape, dtype=torch.int32 if k == "material" else torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        static[k] = t.numpy()
+    h2d = sum(pinned[k].nbytes for k in ("x", "v", "F", "C")) + sum(a.nbytes for a in static.values())
+    d2h = sum(pinned[k].nbytes for k in ("x", "v", "F", "C"))
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        sim.set_particles(pinned["x"], pinned["v"], static["mass"], static["volume"], pinned["F"], pinned["C"],
+                          static["material"])
+        sim.advance_step(frame_end())
+        step_no += 1
+        out = sim.particles()
+        for k in ("x", "v", "F", "C"):
+            pinned[k][...] = out[k]
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=f"cuda:{device}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = n_particles * world * e2e_steps / (e2e_ms / 1000.0)
+
+    # ---- roofline of the dominant HBM-bound phase (algorithmic bytes / event-timed duration)
+    peaks, peak_kind = measured_peaks()
+    hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
+                  k in ("sgs_level0", "sgs_coarse", "residual_restrict", "p2g_bc", "node_gradient", "lbfgs_vectors",
+                        "g2p_strain_advect", "assemble_rows", "prolong")}
+    top = max(hbm_phases, key=lambda k: hbm_phases[k]["ms"]) if hbm_phases else None
+    roofline = None
+    if top:
+        ph = hbm_phases[top]
+        achieved = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
+        roofline = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
+                    "share_of_step": ph["ms"] / ms, "launches": ph["launches"]}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = run_cpu_reference(sc, particles, 1, 0, 1)
+        cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
+                        "sample": f"{r['particles']} particles (x < 0.05 m slab of all four bars), 1 step from t=0, "
+                                  f"oracle port of hotmpm::advance_step, 1 thread (reference default), "
+                                  f"{r['seconds']:.1f} s, outer iterations {r['outer']}"}
+
+    if rank == 0:
+        phases = {k: round(v["ms"] / args.steps, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
+                  if v["ms"] > 0}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling, reference schema)",
+                "config": dict(config, parallelism=f"replicas x{world}" if world > 1 else "single GPU",
+                               outer_iterations=outer, phase_ms_per_step=phases),
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                        "steps": e2e_steps},
+                "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu_baseline,
+                "clocks": clocks.summary()}
+        print(json.dumps(line))
+    sim.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1364 @@
+// Host orchestration of the B200 HOT step and the C-ABI (include/hot_c_api.h).
+//
+// hot_advance_step restates advance_step (simulation.hpp:286-323); the solve restates
+// solve_quasi_newton (solvers.hpp:191-231) with every vector and matrix resident in HBM.
+// The host only sees the scalars the reference's control flow branches on (line-search
+// energies, g.p, the CN residual, y.s / |y| / |s| and the coarse PCG status), read back
+// once per line-search trial / accepted iterate.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hot_c_api.h"
+#include "hot_internal.h"
+
+namespace hotb200 {
+
+long long sample_scene(const hot_scene& sc, std::vector<double>& x, std::vector<double>& v, std::vector<double>& mass,
+                       std::vector<double>& vol, std::vector<double>& F, std::vector<double>& C,
+                       std::vector<int>& mat);
+
+static std::atomic<long long> g_launches{0};
+long long kernel_launch_count() { return g_launches.load(); }
+void count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+namespace {
+
+struct SolverFailure : std::runtime_error {
+  explicit SolverFailure(const std::string& m) : std::runtime_error(m) {}
+};
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct Unsupported : std::runtime_error {
+  explicit Unsupported(const std::string& m) : std::runtime_error(m) {}
+};
+
+#define HOT_CUDA(x)                                                                                      \
+  do {                                                                                                   \
+    cudaError_t e_ = (x);                                                                                \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+/// Grow-only device buffer (non-copyable; swap exchanges ownership).
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) HOT_CUDA(cudaFree(p));
+    p = nullptr;
+    size_t nb = std::max<size_t>(bytes, 256);
+    HOT_CUDA(cudaMalloc(&p, nb));
+    cap = nb;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+constexpr int kMaxLevels = 8;
+constexpr int kMaxWindow = 64;
+
+struct Level {
+  int n = 0;
+  int lo[3] = {0, 0, 0}, ext[3] = {0, 0, 0};
+  DBuf map, coords, cols, H, dinv, dir, flags;
+  DBuf wave_of, wave_counts, wave_start, wave_cursor, wave_rows, wave_start_c;
+  int nwaves = 0;
+  long long active_slots = 0;
+  DBuf b, u, r;  // V-cycle vectors
+  DenseMap dmap() const {
+    DenseMap m;
+    for (int a = 0; a < 3; ++a) {
+      m.lo[a] = lo[a];
+      m.ext[a] = ext[a];
+    }
+    m.idx = map.as<int>();
+    return m;
+  }
+  LevelView view() const {
+    LevelView v;
+    v.n = n;
+    v.coords = coords.as<int>();
+    v.map = dmap();
+    v.cols = cols.as<int>();
+    v.H = H.as<double>();
+    v.dinv = dinv.as<double>();
+    v.dir = dir.as<uint8_t>();
+    return v;
+  }
+};
+
+struct ProfEvent {
+  int phase;
+  cudaEvent_t a, b;
+};
+
+const char* kPhaseNames[] = {"activate_bin", "p2g_bc", "particle_energy", "node_gradient", "particle_tensors",
+                             "assemble_rows", "hierarchy", "sgs_level0", "sgs_coarse", "residual_restrict",
+                             "coarse_pcg", "prolong", "lbfgs_vectors", "g2p_strain_advect", "upload_download"};
+constexpr int kPhases = sizeof(kPhaseNames) / sizeof(kPhaseNames[0]);
+enum Phase {
+  P_ACTIVATE,
+  P_P2G,
+  P_ENERGY,
+  P_GRADIENT,
+  P_TENSORS,
+  P_ASSEMBLE,
+  P_HIER,
+  P_SGS0,
+  P_SGSC,
+  P_RESID,
+  P_PCG,
+  P_PROLONG,
+  P_VEC,
+  P_G2P,
+  P_IO
+};
+
+}  // namespace
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // scene / config (copied)
+  double dx = 0.01, fps = 24, cn_factor = 24;
+  double grav[3] = {0, 0, 0};
+  std::vector<DevMaterial> mats_h;
+  std::vector<DevCollider> cols_h;
+  hot_solver_config cfg{};
+
+  // particles (SoA on device)
+  long long np = 0;
+  DBuf px, pv, pF, pC, pmass, pvol, pmat, stage;
+  double time = 0;
+  int frame = 0;
+  long long step_index = 0, inversions = 0;
+  std::vector<hot_diag_row> diag;
+
+  // grid (level 0 storage lives in L[0])
+  Level L[kMaxLevels];
+  int nlevels = 0;
+  bool have_state = false, have_H = false;
+  double dt = 0;
+  DBuf gmass, gvel, gmom, gbc, gcn;
+  DBuf bin_of, bin_counts, bin_start, bin_cursor, bin_pid, scan_tmp;
+  DBuf mats_d, cols_d;
+
+  // solver vectors
+  DBuf dv, g, gnew, pdir, q, stress, Tu, vout, hist_s[kMaxWindow + 1], hist_y[kMaxWindow + 1];
+  DBuf pcg_r, pcg_z, pcg_p, pcg_Ap;
+  DBuf partials, scal, coef_a, coef_b, iflags, bounds;
+  double* host_scal = nullptr;  // pinned
+  int* host_int = nullptr;      // pinned
+  int nred = 0;
+
+  // profiling
+  bool prof = false;
+  std::vector<ProfEvent> events;
+  std::vector<cudaEvent_t> event_pool;
+  double phase_bytes[kPhases] = {0};
+
+  Context() = default;
+  ~Context() {
+    for (auto& e : events) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (host_scal) cudaFreeHost(host_scal);
+    if (host_int) cudaFreeHost(host_int);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ------------------------------------------------------------------ helpers
+  ParticlesView pview() const {
+    ParticlesView P;
+    P.x = px.as<double>();
+    P.v = pv.as<double>();
+    P.F = pF.as<double>();
+    P.C = pC.as<double>();
+    P.mass = pmass.as<double>();
+    P.vol = pvol.as<double>();
+    P.mat = pmat.as<int>();
+    P.n = np;
+    return P;
+  }
+  GridView gview() const {
+    GridView G;
+    G.n = L[0].n;
+    G.coords = L[0].coords.as<int>();
+    G.map = L[0].dmap();
+    G.mass = gmass.as<double>();
+    G.vel = gvel.as<double>();
+    G.mom = gmom.as<double>();
+    G.dir = L[0].dir.as<uint8_t>();
+    G.bc_vel = gbc.as<double>();
+    G.cn_scale = gcn.as<double>();
+    return G;
+  }
+  BinsView bview() const {
+    BinsView b;
+    b.start = bin_start.as<int>();
+    b.pid = bin_pid.as<int>();
+    return b;
+  }
+  cudaEvent_t take_event() {
+    if (event_pool.empty()) {
+      cudaEvent_t e;
+      HOT_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  int prof_begin(int phase) {
+    if (!prof) return -1;
+    ProfEvent pe{phase, take_event(), take_event()};
+    cudaEventRecord(pe.a, stream);
+    events.push_back(pe);
+    return (int)events.size() - 1;
+  }
+  void prof_end(int h, double bytes = 0) {
+    if (h < 0) return;
+    cudaEventRecord(events[h].b, stream);
+    phase_bytes[events[h].phase] += bytes;
+  }
+  void sync() { HOT_CUDA(cudaStreamSynchronize(stream)); }
+  void check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+  void read_scalars(int nd, int ni) {
+    if (nd) HOT_CUDA(cudaMemcpyAsync(host_scal, scal.p, sizeof(double) * nd, cudaMemcpyDeviceToHost, stream));
+    if (ni) HOT_CUDA(cudaMemcpyAsync(host_int, iflags.p, sizeof(int) * ni, cudaMemcpyDeviceToHost, stream));
+    sync();
+    check_launch();
+  }
+
+  void init(int dev) {
+    device = dev;
+    HOT_CUDA(cudaSetDevice(dev));
+    HOT_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
+    HOT_CUDA(cudaMallocHost(&host_int, sizeof(int) * 64));
+    nred = 2 * num_sms();
+    partials.ensure(sizeof(double) * 4 * (nred + 64));
+    scal.ensure(sizeof(double) * 64);
+    iflags.ensure(sizeof(int) * 64);
+    bounds.ensure(sizeof(int) * 8);
+    coef_a.ensure(sizeof(double) * kMaxWindow);
+    coef_b.ensure(sizeof(double) * kMaxWindow);
+  }
+
+  void set_scene(const hot_scene& s) {
+    if (s.dim != 3) throw Unsupported("the B200 path is built for dim = 3 (2D: see DESIGN.md, next)");
+    if (!(s.dx > 0)) throw std::invalid_argument("activate_grid: dx must be positive");
+    dx = s.dx;
+    fps = s.fps;
+    cn_factor = s.cn_length_factor;
+    for (int a = 0; a < 3; ++a) grav[a] = s.gravity[a];
+    mats_h.clear();
+    for (int i = 0; i < s.n_materials; ++i) mats_h.push_back(make_material(s.materials[i]));
+    if ((int)mats_h.size() > kMaxMaterials) throw std::invalid_argument("too many materials");
+    cols_h.clear();
+    for (int i = 0; i < s.n_colliders; ++i) cols_h.push_back(make_collider(s.colliders[i]));
+    mats_d.ensure(sizeof(DevMaterial) * std::max<size_t>(1, mats_h.size()));
+    if (!mats_h.empty())
+      HOT_CUDA(cudaMemcpy(mats_d.p, mats_h.data(), sizeof(DevMaterial) * mats_h.size(), cudaMemcpyHostToDevice));
+    cols_d.ensure(sizeof(DevCollider) * std::max<size_t>(1, cols_h.size()));
+    if (!cols_h.empty())
+      HOT_CUDA(cudaMemcpy(cols_d.p, cols_h.data(), sizeof(DevCollider) * cols_h.size(), cudaMemcpyHostToDevice));
+    cfg.epsilon = s.epsilon;
+    cfg.tau = s.tau;
+    cfg.levels = s.levels;
+    cfg.window = s.window;
+    cfg.ls_shrink = 0.5;
+    cfg.ls_armijo = 1e-4;
+    cfg.ls_max_steps = 30;
+    cfg.cg_cap = 10000;
+    cfg.outer_cap = 1000;
+    cfg.kind = s.solver;
+    cfg.embedding = s.embedding;
+    cfg.pinned_coarse_iterations = 256;
+    cfg.cn_length_factor = s.cn_length_factor;
+  }
+
+  /// Material::elastic / von_mises / snow (constitutive.hpp:12-52) + stiffness_scale
+  /// (constitutive.hpp:255-258): ||dP/dF(I)||_F = sqrt(3 (2mu+la)^2 + 6 la^2 + 6 ((2mu+0)/... )).
+  static DevMaterial make_material(const hot_material& m) {
+    if (!(m.youngs > 0.0)) throw std::invalid_argument("material: Young's modulus must be positive");
+    if (!(m.poisson >= 0.0 && m.poisson < 0.5)) throw std::invalid_argument("material: Poisson ratio must lie in [0, 0.5)");
+    DevMaterial d{};
+    d.mu = m.youngs / (2.0 * (1.0 + m.poisson));
+    d.lambda = m.youngs * m.poisson / ((1.0 + m.poisson) * (1.0 - 2.0 * m.poisson));
+    d.plasticity = m.plasticity;
+    if (m.plasticity == 1) {
+      if (!(m.yield_stress > 0.0)) throw std::invalid_argument("material: yield stress must be positive");
+      d.yield_stress = m.yield_stress;
+    } else if (m.plasticity == 2) {
+      if (!(m.clamp_lo <= 1.0 && 1.0 <= m.clamp_hi)) throw std::invalid_argument("material: snow clamp must bracket 1");
+      d.clamp_lo = m.clamp_lo;
+      d.clamp_hi = m.clamp_hi;
+    }
+    // dP/dF at F = I in diagonal space: (mm) block 2mu I + la 11^T; 2x2 blocks with
+    // bd = 2mu - la*0, bs = (psi_i+psi_j)/2 = 0 -> entries (mu, mu).  Frobenius norm is basis
+    // invariant (Q orthogonal): sum of squares of Mhat.
+    const double a = 2.0 * d.mu + d.lambda, b = d.lambda;
+    const double mh = 0.5 * (2.0 * d.mu);
+    const double fro2 = 3.0 * a * a + 6.0 * b * b + 3.0 * 4.0 * mh * mh;
+    d.xi = std::sqrt(fro2);
+    return d;
+  }
+
+  static DevCollider make_collider(const hot_collider& c) {
+    DevCollider d{};
+    d.shape = c.shape.kind;
+    d.motion = c.motion.kind;
+    d.radius = c.shape.radius;
+    for (int a = 0; a < 3; ++a) {
+      switch (c.shape.kind) {
+        case 0:
+          d.a[a] = c.shape.min[a];
+          d.b[a] = c.shape.max[a];
+          break;
+        case 1:
+          d.a[a] = c.shape.center[a];
+          break;
+        case 2:
+          d.a[a] = c.shape.point[a];
+          d.b[a] = c.shape.normal[a];
+          break;
+        case 3:
+          d.a[a] = c.shape.center[a];
+          break;
+      }
+      d.vel[a] = c.motion.velocity[a];
+      d.rot_center[a] = c.motion.center[a];
+    }
+    if (c.shape.kind == 3) {
+      const double n = std::sqrt(c.shape.axis[0] * c.shape.axis[0] + c.shape.axis[1] * c.shape.axis[1] +
+                                 c.shape.axis[2] * c.shape.axis[2]);
+      for (int a = 0; a < 3; ++a) d.b[a] = c.shape.axis[a] / n;
+    }
+    if (c.motion.kind == 2) {
+      const double n = std::sqrt(c.motion.axis[0] * c.motion.axis[0] + c.motion.axis[1] * c.motion.axis[1] +
+                                 c.motion.axis[2] * c.motion.axis[2]);
+      for (int a = 0; a < 3; ++a) d.rot_w[a] = c.motion.omega * (c.motion.axis[a] / n);
+    }
+    return d;
+  }
+
+  // ------------------------------------------------------------------ particles
+  void upload(long long n, const double* x, const double* v, const double* mass, const double* vol, const double* F,
+              const double* C, const int* mat) {
+    const int h = prof_begin(P_IO);
+    np = n;
+    const size_t n3 = sizeof(double) * 3 * std::max<long long>(n, 1), n9 = sizeof(double) * 9 * std::max<long long>(n, 1);
+    px.ensure(n3);
+    pv.ensure(n3);
+    pF.ensure(n9);
+    pC.ensure(n9);
+    pmass.ensure(sizeof(double) * std::max<long long>(n, 1));
+    pvol.ensure(sizeof(double) * std::max<long long>(n, 1));
+    pmat.ensure(sizeof(int) * std::max<long long>(n, 1));
+    stage.ensure(n9);
+    auto soa = [&](const double* src, DBuf& dst, int comps, double fill_diag) {
+      if (src) {
+        HOT_CUDA(cudaMemcpyAsync(stage.p, src, sizeof(double) * comps * n, cudaMemcpyHostToDevice, stream));
+        launch_aos_to_soa(stage.as<double>(), dst.as<double>(), n, comps, stream);
+        // the staging buffer is reused by the next component: order on the stream suffices
+      } else {
+        HOT_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(double) * comps * n, stream));
+        if (fill_diag != 0.0) {
+          std::vector<double> eye(9 * n, 0.0);
+          for (long long p = 0; p < n; ++p) eye[0 * n + p] = eye[4 * n + p] = eye[8 * n + p] = 1.0;
+          HOT_CUDA(cudaMemcpyAsync(dst.p, eye.data(), sizeof(double) * 9 * n, cudaMemcpyHostToDevice, stream));
+          sync();
+        }
+      }
+    };
+    if (n > 0) {
+      if (!x) throw std::invalid_argument("positions are required");
+      soa(x, px, 3, 0.0);
+      soa(v, pv, 3, 0.0);
+      soa(F, pF, 9, 1.0);
+      soa(C, pC, 9, 0.0);
+      if (mass)
+        HOT_CUDA(cudaMemcpyAsync(pmass.p, mass, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+      else
+        HOT_CUDA(cudaMemsetAsync(pmass.p, 0, sizeof(double) * n, stream));
+      if (vol)
+        HOT_CUDA(cudaMemcpyAsync(pvol.p, vol, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+      else
+        HOT_CUDA(cudaMemsetAsync(pvol.p, 0, sizeof(double) * n, stream));
+      if (mat)
+        HOT_CUDA(cudaMemcpyAsync(pmat.p, mat, sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+      else
+        HOT_CUDA(cudaMemsetAsync(pmat.p, 0, sizeof(int) * n, stream));
+    }
+    prof_end(h, (double)n * (3 + 3 + 9 + 9 + 2) * 8 + 4.0 * n);
+    have_state = false;
+    sync();
+    if (mat && n) {
+      for (long long p = 0; p < n; ++p)
+        if (mat[p] < 0 || mat[p] >= (int)mats_h.size()) throw std::invalid_argument("particle material id out of range");
+    }
+  }
+
+  void download(double* x, double* v, double* F, double* C) {
+    const int h = prof_begin(P_IO);
+    stage.ensure(sizeof(double) * 9 * std::max<long long>(np, 1));
+    auto aos = [&](const DBuf& src, double* dst, int comps) {
+      if (!dst || np == 0) return;
+      launch_soa_to_aos(src.as<double>(), stage.as<double>(), np, comps, stream);
+      HOT_CUDA(cudaMemcpyAsync(dst, stage.p, sizeof(double) * comps * np, cudaMemcpyDeviceToHost, stream));
+    };
+    aos(px, x, 3);
+    aos(pv, v, 3);
+    aos(pF, F, 9);
+    aos(pC, C, 9);
+    prof_end(h, (double)np * 24 * 8);
+    sync();
+  }
+
+  // ------------------------------------------------------------------ step stages
+  /// activate_grid (grid.hpp:137-165) + particle binning by stencil centre.
+  void activate() {
+    const int h = prof_begin(P_ACTIVATE);
+    const ParticlesView P = pview();
+    int init[8] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN, 0, 0};
+    HOT_CUDA(cudaMemcpyAsync(bounds.p, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    launch_particle_bounds(P, dx, bounds.as<int>(), bounds.as<int>() + 6, stream);
+    int hb[8];
+    HOT_CUDA(cudaMemcpyAsync(hb, bounds.p, sizeof(hb), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (hb[6]) throw std::invalid_argument("activate_grid: non-finite particle position");
+    Level& l0 = L[0];
+    if (np == 0) {
+      l0.n = 0;
+      for (int a = 0; a < 3; ++a) l0.lo[a] = 0, l0.ext[a] = 1;
+    } else {
+      for (int a = 0; a < 3; ++a) {
+        l0.lo[a] = hb[a];
+        l0.ext[a] = hb[3 + a] + 2 - hb[a] + 1;
+      }
+    }
+    const long long len = (long long)l0.ext[0] * l0.ext[1] * l0.ext[2];
+    if (len > (1LL << 31)) throw std::invalid_argument("activate_grid: particle bounding box exceeds 2^31 nodes");
+    l0.flags.ensure(len + 16);
+    l0.map.ensure(sizeof(int) * len);
+    scan_tmp.ensure(sizeof(int) * (len / 4096 + 64));
+    HOT_CUDA(cudaMemsetAsync(l0.flags.p, 0, len + 16, stream));
+    DenseMap dm = l0.dmap();
+    launch_mark_active(P, dx, dm, l0.flags.as<uint8_t>(), stream);
+    // coords sized for the worst case (every box node active) only when needed
+    l0.coords.ensure(sizeof(int) * 3 * std::min<long long>(len, 27LL * std::max<long long>(np, 1)));
+    launch_flags_to_index(l0.flags.as<uint8_t>(), len, l0.ext, l0.lo, l0.map.as<int>(), l0.coords.as<int>(),
+                          scan_tmp.as<int>(), iflags.as<int>() + 8, stream);
+    int n_nodes = 0;
+    HOT_CUDA(cudaMemcpyAsync(&n_nodes, iflags.as<int>() + 8, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    l0.n = n_nodes;
+    const int n = n_nodes;
+    gmass.ensure(sizeof(double) * std::max(n, 1));
+    gvel.ensure(sizeof(double) * 3 * std::max(n, 1));
+    gmom.ensure(sizeof(double) * 3 * std::max(n, 1));
+    gbc.ensure(sizeof(double) * 3 * std::max(n, 1));
+    gcn.ensure(sizeof(double) * std::max(n, 1));
+    l0.dir.ensure(std::max(n, 1));
+    bin_of.ensure(sizeof(int) * std::max<long long>(np, 1));
+    bin_counts.ensure(sizeof(int) * (n + 2));
+    bin_start.ensure(sizeof(int) * (n + 2));
+    bin_cursor.ensure(sizeof(int) * (n + 2));
+    bin_pid.ensure(sizeof(int) * std::max<long long>(np, 1));
+    scan_tmp.ensure(sizeof(int) * ((long long)n / 4096 + 64 + len / 4096));
+    launch_bin_particles(P, dx, l0.dmap(), n, bin_of.as<int>(), bin_counts.as<int>(), bin_start.as<int>(),
+                         bin_cursor.as<int>(), bin_pid.as<int>(), scan_tmp.as<int>(), stream);
+    prof_end(h, (double)np * 24 * 3 + 5.0 * len);
+    nlevels = 0;
+    have_H = false;
+  }
+
+  void p2g_bc(double time_now) {
+    const int h = prof_begin(P_P2G);
+    launch_p2g(pview(), bview(), gview(), dx, mats_d.as<DevMaterial>(), cn_factor * dx * dx, dt, stream);
+    launch_apply_bc(gview(), dx, cols_d.as<DevCollider>(), (int)cols_h.size(), stream);
+    (void)time_now;
+    prof_end(h, (double)np * 128 + (double)L[0].n * 64);
+  }
+
+  void ensure_solver_buffers() {
+    const int n = std::max(L[0].n, 1);
+    const size_t v = sizeof(double) * 3 * n;
+    dv.ensure(v);
+    g.ensure(v);
+    gnew.ensure(v);
+    pdir.ensure(v);
+    q.ensure(v);
+    vout.ensure(v);
+    stress.ensure(sizeof(double) * 9 * std::max<long long>(np, 1));
+  }
+
+  /// hot_stage_prepare / advance_step :297-305 at a given dt.
+  void prepare(double dt_in, double time_now) {
+    dt = dt_in;
+    activate();
+    p2g_bc(time_now);
+    ensure_solver_buffers();
+    have_state = true;
+    check_launch();
+  }
+
+  // ------------------------------------------------------------------ objective
+  int* flag_bad() { return iflags.as<int>() + 0; }
+
+  /// E(dv + alpha p) with stress stored for the gradient; returns through scal[0].
+  void energy_async(const double* dvp, const double* p, double alpha, bool want_stress) {
+    int h = prof_begin(P_ENERGY);
+    double* part = partials.as<double>();
+    launch_particle_energy(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, p, alpha,
+                           want_stress ? stress.as<double>() : nullptr, part, nred, flag_bad(), stream);
+    launch_node_energy(gview(), dt, grav, dvp, p, alpha, part + nred, nred, stream);
+    launch_sum_partials(part, 2 * nred, scal.as<double>() + 0, stream);
+    prof_end(h, (double)np * (24 + 72 + 8 + 4 + 27 * 28) + (want_stress ? 72.0 * np : 0.0));
+  }
+
+  /// g(dv) from the stored stress; scaled-norm^2 into scal[2].
+  void gradient_async(const double* dvp, double* gout) {
+    const int h = prof_begin(P_GRADIENT);
+    double* part = partials.as<double>() + 2 * nred;
+    launch_node_gradient(pview(), bview(), gview(), dx, dt, grav, stress.as<double>(), dvp, gout, part, nred,
+                         flag_bad(), stream);
+    launch_sum_partials(part, nred, scal.as<double>() + 2, stream);
+    prof_end(h, (double)L[0].n * (27 * 8 * 96.0 / 8) + 72.0 * np);
+  }
+
+  void check_flags() {
+    if (host_int[0] == 1) throw std::invalid_argument("energy: non-finite dv");
+    if (host_int[0] == 2) throw std::logic_error("scaled_norm: zero characteristic scale (material misconfiguration)");
+    if (host_int[1] == 1) throw SolverFailure("pcg: preconditioner is not positive definite");
+    if (host_int[1] == 2) throw SolverFailure("pcg: system matrix is not positive definite");
+  }
+
+  // ------------------------------------------------------------------ matrix + hierarchy
+  void alloc_level(Level& l) {
+    const long long n = std::max(l.n, 1);
+    l.cols.ensure(sizeof(int) * n * kSlotPitch);
+    l.H.ensure(sizeof(double) * n * 9 * kSlotPitch);
+    l.dinv.ensure(sizeof(double) * 9 * n);
+    l.b.ensure(sizeof(double) * 3 * n);
+    l.u.ensure(sizeof(double) * 3 * n);
+    l.r.ensure(sizeof(double) * 3 * n);
+    l.wave_of.ensure(sizeof(int) * n);
+    l.wave_rows.ensure(sizeof(int) * n);
+  }
+
+  void assemble(const double* dvp, bool project) {
+    Level& l0 = L[0];
+    alloc_level(l0);
+    int h = prof_begin(P_TENSORS);
+    Tu.ensure(sizeof(double) * 45 * std::max<long long>(np, 1));
+    launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, project ? 1 : 0, Tu.as<double>(),
+                            flag_bad(), stream);
+    prof_end(h, (double)np * (24 + 72 + 8 + 4 + 45 * 8));
+    h = prof_begin(P_ASSEMBLE);
+    launch_fill_cols(l0.view(), stream);
+    launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), stream);
+    prof_end(h, (double)l0.n * 9 * kSlots * 8);
+    have_H = true;
+    nlevels = 1;
+  }
+
+  /// Diag inverse + wave schedule for level m (multigrid.hpp:227-251).
+  void finalize(int m) {
+    Level& l = L[m];
+    int mm[2] = {INT_MAX, INT_MIN};
+    HOT_CUDA(cudaMemcpyAsync(iflags.as<int>() + 10, mm, sizeof(mm), cudaMemcpyHostToDevice, stream));
+    HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 12, 0, sizeof(int), stream));
+    launch_finalize_level(l.view(), m > 0 ? 1 : 0, l.wave_of.as<int>(), iflags.as<int>() + 10, iflags.as<int>() + 12,
+                          stream);
+    int hb[3];
+    HOT_CUDA(cudaMemcpyAsync(hb, iflags.as<int>() + 10, sizeof(hb), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (hb[2]) throw std::logic_error("multigrid: singular diagonal block");
+    if (l.n == 0) {
+      l.nwaves = 0;
+      return;
+    }
+    const int wmin = hb[0], nw = hb[1] - hb[0] + 1;
+    l.wave_counts.ensure(sizeof(int) * (nw + 2));
+    l.wave_start.ensure(sizeof(int) * (nw + 2));
+    l.wave_cursor.ensure(sizeof(int) * (nw + 2));
+    scan_tmp.ensure(sizeof(int) * (nw / 4096 + 64));
+    launch_bucket_rows(l.wave_of.as<int>(), l.n, wmin, l.wave_counts.as<int>(), l.wave_start.as<int>(),
+                       l.wave_cursor.as<int>(), l.wave_rows.as<int>(), nw, scan_tmp.as<int>(), stream);
+    std::vector<int> counts(nw);
+    HOT_CUDA(cudaMemcpyAsync(counts.data(), l.wave_counts.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::vector<int> starts;
+    int acc = 0;
+    for (int w = 0; w < nw; ++w)
+      if (counts[w] > 0) {
+        starts.push_back(acc);
+        acc += counts[w];
+      }
+    starts.push_back(acc);
+    l.nwaves = (int)starts.size() - 1;
+    l.wave_start_c.ensure(sizeof(int) * starts.size());
+    HOT_CUDA(cudaMemcpyAsync(l.wave_start_c.p, starts.data(), sizeof(int) * starts.size(), cudaMemcpyHostToDevice,
+                             stream));
+    sync();
+  }
+
+  /// build_hierarchy (multigrid.hpp:258-294), linear node embedding.
+  void build_hierarchy(int levels, int embedding) {
+    if (levels < 1) throw std::invalid_argument("build_hierarchy: need at least one level");
+    if (levels > kMaxLevels) throw std::invalid_argument("build_hierarchy: too many levels");
+    if (embedding != 1 && levels > 1) throw Unsupported("quadratic embedding is not built for the device path");
+    const int h = prof_begin(P_HIER);
+    finalize(0);
+    nlevels = 1;
+    for (int m = 1; m < levels; ++m) {
+      Level& f = L[m - 1];
+      Level& c = L[m];
+      if (f.n == 0) break;
+      for (int a = 0; a < 3; ++a) {
+        c.lo[a] = f.lo[a] >> 1;
+        c.ext[a] = ((f.lo[a] + f.ext[a] - 1) >> 1) + 1 - c.lo[a] + 1;
+      }
+      const long long len = (long long)c.ext[0] * c.ext[1] * c.ext[2];
+      c.flags.ensure(len + 16);
+      c.map.ensure(sizeof(int) * len);
+      c.coords.ensure(sizeof(int) * 3 * std::min<long long>(len, 8LL * f.n));
+      scan_tmp.ensure(sizeof(int) * (len / 4096 + 64));
+      HOT_CUDA(cudaMemsetAsync(c.flags.p, 0, len + 16, stream));
+      launch_mark_parents(f.view(), c.dmap(), c.flags.as<uint8_t>(), stream);
+      launch_flags_to_index(c.flags.as<uint8_t>(), len, c.ext, c.lo, c.map.as<int>(), c.coords.as<int>(),
+                            scan_tmp.as<int>(), iflags.as<int>() + 8, stream);
+      int nc = 0;
+      HOT_CUDA(cudaMemcpyAsync(&nc, iflags.as<int>() + 8, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      sync();
+      if (nc == 0) break;  // truncated hierarchy (multigrid.hpp:281-284)
+      c.n = nc;
+      alloc_level(c);
+      c.dir.ensure(std::max(nc, 1));
+      HOT_CUDA(cudaMemsetAsync(c.dir.p, 0, nc, stream));
+      launch_coarse_dirichlet(f.view(), c.dmap(), c.dir.as<uint8_t>(), stream);
+      launch_fill_cols(c.view(), stream);
+      launch_galerkin(f.view(), c.view(), stream);
+      check_launch();
+      nlevels = m + 1;
+      finalize(m);
+    }
+    // PCG scratch on the coarsest level
+    const Level& bot = L[nlevels - 1];
+    const size_t v = sizeof(double) * 3 * std::max(bot.n, 1);
+    pcg_r.ensure(v);
+    pcg_z.ensure(v);
+    pcg_p.ensure(v);
+    pcg_Ap.ensure(v);
+    prof_end(h);
+    check_launch();
+  }
+
+  static int coop_grid(int max_blocks, int rows) {
+    const int want = (rows + 7) / 8;  // 8 warps per block, one row per warp
+    return std::max(1, std::min(max_blocks, want));
+  }
+
+  void sgs(int m, double* u, const double* b) {
+    Level& l = L[m];
+    const int h = prof_begin(m == 0 ? P_SGS0 : P_SGSC);
+    launch_sgs(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
+               coop_grid(sgs_max_blocks(), l.n), stream);
+    prof_end(h, 2.0 * (72.0 * l.active_slots + 72.0 * l.n + 24.0 * l.n + 48.0 * l.n));
+  }
+
+  /// vcycle (multigrid.hpp:363-392), adaptive coarse mode; coarse iterations accumulate into
+  /// iflags[2].
+  void vcycle(const double* b0, double* out, bool pinned, int pinned_cap) {
+    const int M = nlevels;
+    launch_zero_dirichlet_copy(b0, L[0].b.as<double>(), L[0].dir.as<uint8_t>(), L[0].n, stream);
+    for (int m = 0; m < M - 1; ++m) {
+      Level& l = L[m];
+      HOT_CUDA(cudaMemsetAsync(l.u.p, 0, sizeof(double) * 3 * l.n, stream));
+      sgs(m, l.u.as<double>(), l.b.as<double>());
+      const int h = prof_begin(P_RESID);
+      launch_residual(l.view(), l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
+      launch_restrict(l.view(), L[m + 1].view(), l.r.as<double>(), L[m + 1].b.as<double>(), stream);
+      prof_end(h, 72.0 * l.active_slots + 72.0 * l.n + 24.0 * L[m + 1].n);
+    }
+    Level& bot = L[M - 1];
+    {
+      const int h = prof_begin(P_PCG);
+      const double rel = pinned ? 1e-14 : 0.5;
+      const int cap = pinned ? pinned_cap : 10000;
+      launch_pcg(bot.view(), bot.b.as<double>(), bot.u.as<double>(), pcg_r.as<double>(), pcg_z.as<double>(),
+                 pcg_p.as<double>(), pcg_Ap.as<double>(), rel, cap, partials.as<double>() + 3 * nred,
+                 iflags.as<int>() + 4, iflags.as<int>() + 2, coop_grid(pcg_max_blocks(), bot.n), stream);
+      prof_end(h);
+      // status word -> iflags[1] (max over the solve)
+      copy_status();
+    }
+    for (int m = M - 2; m >= 0; --m) {
+      Level& l = L[m];
+      const int h = prof_begin(P_PROLONG);
+      launch_prolong_add(l.view(), L[m + 1].view(), L[m + 1].u.as<double>(), l.u.as<double>(), stream);
+      prof_end(h, 24.0 * L[m + 1].n + 48.0 * l.n);
+      sgs(m, l.u.as<double>(), l.b.as<double>());
+    }
+    HOT_CUDA(cudaMemcpyAsync(out, L[0].u.p, sizeof(double) * 3 * L[0].n, cudaMemcpyDeviceToDevice, stream));
+    check_launch();
+  }
+
+  void copy_status();
+
+  long long count_active_slots(int m);
+
+  // ------------------------------------------------------------------ L-BFGS (solvers.hpp:82-231)
+  struct HistEntry {
+    int slot;
+    double rho;
+  };
+
+  void lbfgs_direction(const std::deque<HistEntry>& hist, double* out) {
+    const int hvec = prof_begin(P_VEC);
+    const long long n3 = 3LL * L[0].n;
+    double* qv = q.as<double>();
+    double* part = partials.as<double>();
+    launch_neg_copy(g.as<double>(), qv, n3, stream);
+    const int m = (int)hist.size();
+    // newest -> oldest: alpha_k = rho_k s_k.q ; q -= alpha_k y_k
+    for (int k = 0; k < m; ++k) {
+      const HistEntry& e = hist[hist.size() - 1 - k];
+      const double* yprev = k > 0 ? hist_y[hist[hist.size() - k].slot].as<double>() : nullptr;
+      launch_axpy_dot(qv, yprev, coef_a.as<double>(), k - 1, -1.0, hist_s[e.slot].as<double>(), n3, part, nred,
+                      stream);
+      launch_finalize_coef(part, nred, e.rho, nullptr, k, coef_a.as<double>(), stream);
+    }
+    if (m > 0)
+      launch_axpy_dot(qv, hist_y[hist[0].slot].as<double>(), coef_a.as<double>(), m - 1, -1.0, nullptr, n3, nullptr,
+                      nred, stream);
+    prof_end(hvec, (4.0 * m + 2) * 8.0 * n3);
+    vcycle(qv, out, false, 0);
+    const int hv2 = prof_begin(P_VEC);
+    // oldest -> newest: beta = rho_k y_k.r ; r += (alpha_k - beta) s_k
+    for (int k = m - 1; k >= 0; --k) {
+      const HistEntry& e = hist[hist.size() - 1 - k];
+      const double* sprev = k < m - 1 ? hist_s[hist[hist.size() - 2 - k].slot].as<double>() : nullptr;
+      launch_axpy_dot(out, sprev, coef_b.as<double>(), k + 1, +1.0, hist_y[e.slot].as<double>(), n3, part, nred,
+                      stream);
+      launch_finalize_coef(part, nred, e.rho, coef_a.as<double>(), k, coef_b.as<double>(), stream);
+    }
+    if (m > 0)
+      launch_axpy_dot(out, hist_s[hist[hist.size() - 1].slot].as<double>(), coef_b.as<double>(), 0, +1.0, nullptr,
+                      n3, nullptr, nred, stream);
+    prof_end(hv2, (4.0 * m) * 8.0 * n3);
+  }
+
+  struct SolveOut {
+    int outer = 0;
+    long long inner = 0;
+    bool converged = false;
+  };
+
+  /// solve_quasi_newton (solvers.hpp:191-231); dv result in this->dv.
+  SolveOut solve_qn(int levels, int frame_no, long long step_no) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = L[0].n;
+    const long long n3 = 3LL * n;
+    SolveOut out;
+    if (cfg.window > kMaxWindow) throw std::invalid_argument("L-BFGS window too large");
+    const double target = cfg.epsilon * std::sqrt((double)n);
+    HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
+    HOT_CUDA(cudaMemsetAsync(iflags.p, 0, sizeof(int) * 8, stream));
+    energy_async(dv.as<double>(), nullptr, 0.0, true);
+    gradient_async(dv.as<double>(), g.as<double>());
+    read_scalars(3, 2);
+    check_flags();
+    double e_curr = host_scal[0];
+    double residual = std::sqrt(host_scal[2]);
+    if (residual <= target) {
+      out.converged = true;
+      return out;
+    }
+    assemble(dv.as<double>(), true);
+    build_hierarchy(levels, cfg.embedding);
+    for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
+    for (int k = 0; k <= cfg.window; ++k) {
+      hist_s[k].ensure(sizeof(double) * std::max<long long>(n3, 1));
+      hist_y[k].ensure(sizeof(double) * std::max<long long>(n3, 1));
+    }
+    std::deque<HistEntry> hist;
+    long long work = 0;
+    for (int outer = 1; outer <= cfg.outer_cap; ++outer) {
+      HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 2, 0, sizeof(int), stream));
+      lbfgs_direction(hist, pdir.as<double>());
+      // accept(): g.p then the Armijo backtracking (solvers.hpp:66-78, 169-186)
+      const int hv = prof_begin(P_VEC);
+      launch_dot_partials(g.as<double>(), pdir.as<double>(), n3, partials.as<double>() + 3 * nred, nred, stream);
+      launch_sum_partials(partials.as<double>() + 3 * nred, nred, scal.as<double>() + 1, stream);
+      prof_end(hv, 16.0 * n3);
+      double alpha = 1.0;
+      energy_async(dv.as<double>(), pdir.as<double>(), alpha, true);
+      read_scalars(2, 3);
+      check_flags();
+      const double gdotp = host_scal[1];
+      if (!(gdotp < 0.0)) throw SolverFailure("line_search: not a descent direction");
+      double e_trial = host_scal[0];
+      int k = 0;
+      while (!(e_trial <= e_curr + cfg.ls_armijo * alpha * gdotp)) {
+        if (++k >= cfg.ls_max_steps) throw SolverFailure("line_search: no acceptable step (gradient/Hessian inconsistency)");
+        alpha *= cfg.ls_shrink;
+        energy_async(dv.as<double>(), pdir.as<double>(), alpha, true);
+        read_scalars(1, 1);
+        check_flags();
+        e_trial = host_scal[0];
+      }
+      // s = alpha p ; dv += s ; g_new ; y = g_new - g
+      const int slot = next_slot(hist);
+      const int hv3 = prof_begin(P_VEC);
+      launch_scale(pdir.as<double>(), alpha, hist_s[slot].as<double>(), n3, stream);
+      launch_add_scaled(dv.as<double>(), pdir.as<double>(), alpha, dv.as<double>(), n3, stream);
+      prof_end(hv3, 40.0 * n3);
+      gradient_async(dv.as<double>(), gnew.as<double>());
+      const int hv4 = prof_begin(P_VEC);
+      launch_ys_dots(gnew.as<double>(), g.as<double>(), hist_y[slot].as<double>(), hist_s[slot].as<double>(), n3,
+                     partials.as<double>() + 3 * nred, nred, stream);
+      launch_sum_partials(partials.as<double>() + 3 * nred, nred, scal.as<double>() + 3, stream);
+      launch_sum_partials(partials.as<double>() + 4 * nred, nred, scal.as<double>() + 4, stream);
+      launch_sum_partials(partials.as<double>() + 5 * nred, nred, scal.as<double>() + 5, stream);
+      prof_end(hv4, 32.0 * n3);
+      g.swap(gnew);
+      read_scalars(6, 3);
+      check_flags();
+      residual = std::sqrt(host_scal[2]);
+      e_curr = e_trial;
+      const long long inner_this = host_int[2];
+      work += inner_this;
+      hot_diag_row row;
+      row.frame = frame_no;
+      row.step = step_no;
+      row.outer_iteration = outer;
+      row.scaled_residual = residual;
+      row.energy = e_curr;
+      row.step_length = alpha;
+      row.inner_iterations = inner_this;
+      row.work_units = work;
+      row.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      diag.push_back(row);
+      // history.push (solvers.hpp:87-93)
+      const double ys = host_scal[3], yn = std::sqrt(host_scal[4]), sn = std::sqrt(host_scal[5]);
+      if (ys > 1e-12 * yn * sn) {
+        if ((int)hist.size() == std::max(1, cfg.window)) hist.pop_front();
+        hist.push_back({slot, 1.0 / ys});
+      }
+      out.outer = outer;
+      out.inner += inner_this;
+      if (residual <= target) {
+        out.converged = true;
+        break;
+      }
+    }
+    if (!out.converged) {
+      char buf[128];
+      std::snprintf(buf, sizeof(buf), "quasi-newton solve: outer iteration cap reached (residual %f)", residual);
+      throw SolverFailure(buf);
+    }
+    return out;
+  }
+
+  /// window+1 buffers: the new pair never overwrites a pair still in the history (a
+  /// curvature-rejected push keeps the oldest pair alive).
+  int next_slot(const std::deque<HistEntry>& hist) const {
+    const int W = std::max(1, cfg.window);
+    std::vector<char> used(W + 1, 0);
+    for (const auto& e : hist) used[e.slot] = 1;
+    for (int s = 0; s <= W; ++s)
+      if (!used[s]) return s;
+    return 0;
+  }
+
+  SolveOut step_grid(int frame_no, long long step_no) {
+    if (cfg.kind == 4) return solve_qn(1, frame_no, step_no);
+    if (cfg.kind != 0) throw Unsupported("projected-Newton solvers are not built for the device path (SURVEY 8f)");
+    return solve_qn(cfg.levels, frame_no, step_no);
+  }
+
+  // ------------------------------------------------------------------ advance_step
+  void advance(double frame_end, hot_step_stats* st) {
+    double v_max = 0.0;
+    if (np > 0) {
+      HOT_CUDA(cudaMemsetAsync(scal.as<double>() + 8, 0, sizeof(double), stream));
+      launch_vmax(pview(), reinterpret_cast<unsigned long long*>(scal.as<double>() + 8), stream);
+      HOT_CUDA(cudaMemcpyAsync(host_scal + 8, scal.as<double>() + 8, sizeof(double), cudaMemcpyDeviceToHost, stream));
+      sync();
+      v_max = host_scal[8];
+    }
+    const double frame = 1.0 / fps;
+    double dtn = v_max <= 0.0 ? frame : std::min(frame, 0.6 * dx / v_max);  // cfl_dt (grid.hpp:168-173)
+    if (frame_end > 0.0) dtn = std::min(dtn, frame_end - time);
+    if (!(dtn > 0.0)) throw SolverFailure("advance_step: non-positive time step");
+    prepare(dtn, time);
+    SolveOut so;
+    try {
+      so = step_grid(frame, step_index);
+    } catch (const SolverFailure& e) {
+      throw SolverFailure("step " + std::to_string(step_index) + ": " + e.what());
+    }
+    // grid.velocity = v^{n+1}; g2p; update_strain; advect
+    launch_final_velocity(gview(), dv.as<double>(), vout.as<double>(), stream);
+    gvel.swap(vout);
+    const int h = prof_begin(P_G2P);
+    HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 6, 0, sizeof(int), stream));
+    launch_g2p_strain_advect(pview(), gview(), dx, dtn, mats_d.as<DevMaterial>(), iflags.as<int>() + 6, stream);
+    prof_end(h, (double)np * (24 + 24 + 72 + 72 + 4 + 24 + 96));
+    int inv = 0;
+    HOT_CUDA(cudaMemcpyAsync(&inv, iflags.as<int>() + 6, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    check_launch();
+    inversions += inv;
+    time += dtn;
+    ++step_index;
+    have_state = false;
+    if (st) {
+      st->dt = dtn;
+      st->outer_iterations = so.outer;
+      st->inner_total = so.inner;
+      st->node_count = L[0].n;
+      st->converged = so.converged ? 1 : 0;
+    }
+  }
+};
+
+namespace {
+__global__ void k_status_max(int* iflags) {
+  // pcg writes its status into iflags[4]; keep the first failure in iflags[1]
+  if (iflags[4] != 0 && iflags[1] == 0) iflags[1] = iflags[4];
+}
+__global__ void k_count_active(const int* __restrict__ cols, long long n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    c += (cols[t] >= 0) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+}  // namespace
+
+void Context::copy_status() {
+  { k_status_max<<<1, 1, 0, stream>>>(iflags.as<int>()); count_launches(1); }
+}
+
+long long Context::count_active_slots(int m) {
+  Level& l = L[m];
+  if (l.n == 0) return 0;
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(scal.as<double>() + 12);
+  HOT_CUDA(cudaMemsetAsync(d, 0, 8, stream));
+  { k_count_active<<<num_sms() * 4, 256, 0, stream>>>(l.cols.as<int>(), (long long)l.n * kSlotPitch, d); count_launches(1); }
+  unsigned long long h = 0;
+  HOT_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, stream));
+  sync();
+  return (long long)h;
+}
+
+}  // namespace hotb200
+
+// ==========================================================================================
+// C-ABI
+// ==========================================================================================
+using hotb200::Context;
+using hotb200::CudaError;
+
+struct hot_ctx {
+  Context c;
+};
+
+namespace {
+
+template <typename F>
+int guard(hot_ctx* ctx, F&& f) {
+  try {
+    f();
+    return HOT_OK;
+  } catch (const hotb200::SolverFailure& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_SOLVER_FAILURE;
+  } catch (const hotb200::CudaError& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_CUDA;
+  } catch (const hotb200::Unsupported& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_UNSUPPORTED;
+  } catch (const std::invalid_argument& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_DOMAIN;
+  } catch (const std::logic_error& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_LOGIC;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->c.err = e.what();
+    return HOT_E_CUDA;
+  }
+}
+
+thread_local std::string g_create_error;
+
+void need_state(Context& c) {
+  if (!c.have_state) throw std::logic_error("no prepared grid state (call hot_stage_prepare)");
+}
+
+}  // namespace
+
+extern "C" {
+
+int hot_version(void) { return HOT_API_VERSION; }
+
+int hot_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int hot_create(hot_ctx** out, const hot_scene* scene, int device) {
+  if (!out || !scene) return HOT_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* h = new hot_ctx;
+  const int rc = guard(h, [&] {
+    h->c.init(device);
+    h->c.set_scene(*scene);
+  });
+  if (rc != HOT_OK) {
+    g_create_error = h->c.err;
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return HOT_OK;
+}
+
+void hot_destroy(hot_ctx* ctx) { delete ctx; }
+
+const char* hot_last_error(const hot_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_create_error.c_str(); }
+
+int hot_set_solver(hot_ctx* ctx, const hot_solver_config* cfg) {
+  return guard(ctx, [&] {
+    if (cfg->levels < 1) throw std::invalid_argument("levels must be at least 1");
+    if (cfg->window < 1) throw std::invalid_argument("window must be at least 1");
+    ctx->c.cfg = *cfg;
+  });
+}
+
+int hot_sample_scene_particles(const hot_scene* scene, long long* n, double* x, double* v, double* mass, double* volume,
+                               double* F, double* C, int* material) {
+  return guard(nullptr, [&] {
+    std::vector<double> X, Vv, M, Vol, Fm, Cm;
+    std::vector<int> mat;
+    const long long cnt = hotb200::sample_scene(*scene, X, Vv, M, Vol, Fm, Cm, mat);
+    *n = cnt;
+    if (!x) return;
+    std::memcpy(x, X.data(), X.size() * 8);
+    if (v) std::memcpy(v, Vv.data(), Vv.size() * 8);
+    if (mass) std::memcpy(mass, M.data(), M.size() * 8);
+    if (volume) std::memcpy(volume, Vol.data(), Vol.size() * 8);
+    if (F) std::memcpy(F, Fm.data(), Fm.size() * 8);
+    if (C) std::memcpy(C, Cm.data(), Cm.size() * 8);
+    if (material) std::memcpy(material, mat.data(), mat.size() * 4);
+  });
+}
+
+int hot_upload_particles(hot_ctx* ctx, long long n, const double* x, const double* v, const double* mass,
+                         const double* volume, const double* F, const double* C, const int* material) {
+  return guard(ctx, [&] { ctx->c.upload(n, x, v, mass, volume, F, C, material); });
+}
+
+int hot_download_particles(hot_ctx* ctx, double* x, double* v, double* F, double* C) {
+  return guard(ctx, [&] { ctx->c.download(x, v, F, C); });
+}
+
+int hot_particle_count(hot_ctx* ctx, long long* n) {
+  *n = ctx->c.np;
+  return HOT_OK;
+}
+
+int hot_set_time(hot_ctx* ctx, double time, int frame, long long step_index) {
+  ctx->c.time = time;
+  ctx->c.frame = frame;
+  ctx->c.step_index = step_index;
+  return HOT_OK;
+}
+
+int hot_get_time(hot_ctx* ctx, double* time, int* frame, long long* step_index, long long* inversion_warnings) {
+  if (time) *time = ctx->c.time;
+  if (frame) *frame = ctx->c.frame;
+  if (step_index) *step_index = ctx->c.step_index;
+  if (inversion_warnings) *inversion_warnings = ctx->c.inversions;
+  return HOT_OK;
+}
+
+int hot_advance_step(hot_ctx* ctx, double frame_end, hot_step_stats* out) {
+  return guard(ctx, [&] { ctx->c.advance(frame_end, out); });
+}
+
+int hot_diagnostics(hot_ctx* ctx, hot_diag_row* rows, int cap, int* n) {
+  const int cnt = (int)ctx->c.diag.size();
+  *n = cnt;
+  if (rows)
+    for (int i = 0; i < std::min(cap, cnt); ++i) rows[i] = ctx->c.diag[i];
+  return HOT_OK;
+}
+
+int hot_clear_diagnostics(hot_ctx* ctx) {
+  ctx->c.diag.clear();
+  return HOT_OK;
+}
+
+int hot_stage_prepare(hot_ctx* ctx, double dt, double time) {
+  return guard(ctx, [&] { ctx->c.prepare(dt, time); ctx->c.sync(); });
+}
+
+int hot_stage_node_count(hot_ctx* ctx, int* n) {
+  *n = ctx->c.L[0].n;
+  return HOT_OK;
+}
+
+int hot_stage_grid(hot_ctx* ctx, int* coords, double* mass, double* velocity, double* momentum, unsigned char* dirichlet,
+                   double* bc_velocity, double* cn_scale) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    need_state(c);
+    const int n = c.L[0].n;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) HOT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    };
+    cp(coords, c.L[0].coords.p, sizeof(int) * 3 * n);
+    cp(mass, c.gmass.p, sizeof(double) * n);
+    cp(velocity, c.gvel.p, sizeof(double) * 3 * n);
+    cp(momentum, c.gmom.p, sizeof(double) * 3 * n);
+    cp(dirichlet, c.L[0].dir.p, n);
+    cp(bc_velocity, c.gbc.p, sizeof(double) * 3 * n);
+    cp(cn_scale, c.gcn.p, sizeof(double) * n);
+    c.sync();
+  });
+}
+
+int hot_stage_set_grid(hot_ctx* ctx, const double* velocity, const unsigned char* dirichlet, const double* bc_velocity) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    need_state(c);
+    const int n = c.L[0].n;
+    if (velocity) HOT_CUDA(cudaMemcpyAsync(c.gvel.p, velocity, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    if (dirichlet) HOT_CUDA(cudaMemcpyAsync(c.L[0].dir.p, dirichlet, n, cudaMemcpyHostToDevice, c.stream));
+    if (bc_velocity)
+      HOT_CUDA(cudaMemcpyAsync(c.gbc.p, bc_velocity, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+  });
+}
+
+int hot_stage_energy(hot_ctx* ctx, const double* dv, double* energy) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    need_state(c);
+    const int n = c.L[0].n;
+    HOT_CUDA(cudaMemcpyAsync(c.q.p, dv, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    HOT_CUDA(cudaMemsetAsync(c.iflags.p, 0, sizeof(int) * 8, c.stream));
+    c.energy_async(c.q.as<double>(), nullptr, 0.0, true);
+    c.read_scalars(1, 2);
+    c.check_flags();
+    *energy = c.host_scal[0];
+  });
+}
+
+int hot_stage_gradient(hot_ctx* ctx, const double* dv, double* gout, double* scaled_norm) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    need_state(c);
+    const int n = c.L[0].n;
+    HOT_CUDA(cudaMemcpyAsync(c.q.p, dv, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    HOT_CUDA(cudaMemsetAsync(c.iflags.p, 0, sizeof(int) * 8, c.stream));
+    c.energy_async(c.q.as<double>(), nullptr, 0.0, true);
+    c.gradient_async(c.q.as<double>(), c.gnew.as<double>());
+    if (gout) HOT_CUDA(cudaMemcpyAsync(gout, c.gnew.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    c.read_scalars(3, 2);
+    c.check_flags();
+    if (scaled_norm) *scaled_norm = std::sqrt(c.host_scal[2]);
+  });
+}
+
+int hot_stage_assemble(hot_ctx* ctx, const double* dv, int project) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    need_state(c);
+    const int n = c.L[0].n;
+    HOT_CUDA(cudaMemcpyAsync(c.q.p, dv, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    HOT_CUDA(cudaMemsetAsync(c.iflags.p, 0, sizeof(int) * 8, c.stream));
+    c.assemble(c.q.as<double>(), project != 0);
+    c.read_scalars(0, 1);
+    c.check_flags();
+    c.L[0].active_slots = c.count_active_slots(0);
+  });
+}
+
+int hot_stage_build_hierarchy(hot_ctx* ctx, int levels, int embedding) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    if (!c.have_H) throw std::logic_error("no matrix assembled");
+    c.build_hierarchy(levels, embedding);
+    for (int m = 0; m < c.nlevels; ++m) c.L[m].active_slots = c.count_active_slots(m);
+  });
+}
+
+int hot_stage_level_count(hot_ctx* ctx, int* levels) {
+  *levels = ctx->c.nlevels;
+  return HOT_OK;
+}
+
+int hot_stage_level_shape(hot_ctx* ctx, int level, int* rows, int* slots) {
+  return guard(ctx, [&] {
+    if (level < 0 || level >= ctx->c.nlevels) throw std::logic_error("no such level");
+    *rows = ctx->c.L[level].n;
+    *slots = hotb200::kSlots;
+  });
+}
+
+int hot_stage_level_matrix(hot_ctx* ctx, int level, double* blocks, int* cols, int* coords, unsigned char* dirichlet) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    if (level < 0 || level >= c.nlevels) throw std::logic_error("no such level");
+    const hotb200::Level& l = c.L[level];
+    const long long n = l.n;
+    std::vector<int> cl(n * hotb200::kSlotPitch);
+    std::vector<double> H(n * 9 * hotb200::kSlotPitch);
+    HOT_CUDA(cudaMemcpyAsync(cl.data(), l.cols.p, sizeof(int) * cl.size(), cudaMemcpyDeviceToHost, c.stream));
+    HOT_CUDA(cudaMemcpyAsync(H.data(), l.H.p, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, c.stream));
+    if (coords) HOT_CUDA(cudaMemcpyAsync(coords, l.coords.p, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    if (dirichlet) HOT_CUDA(cudaMemcpyAsync(dirichlet, l.dir.p, n, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    for (long long i = 0; i < n; ++i)
+      for (int s = 0; s < hotb200::kSlots; ++s) {
+        const int col = cl[i * hotb200::kSlotPitch + s];
+        if (cols) cols[i * hotb200::kSlots + s] = col;
+        if (blocks)
+          for (int e = 0; e < 9; ++e)
+            blocks[(i * hotb200::kSlots + s) * 9 + e] = col < 0 ? 0.0 : H[(i * 9 + e) * hotb200::kSlotPitch + s];
+      }
+  });
+}
+
+int hot_stage_matvec(hot_ctx* ctx, int level, const double* x, double* y) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    if (level < 0 || level >= c.nlevels) throw std::logic_error("no such level");
+    hotb200::Level& l = c.L[level];
+    HOT_CUDA(cudaMemcpyAsync(l.b.p, x, sizeof(double) * 3 * l.n, cudaMemcpyHostToDevice, c.stream));
+    hotb200::launch_spmv(l.view(), l.b.as<double>(), l.r.as<double>(), c.stream);
+    HOT_CUDA(cudaMemcpyAsync(y, l.r.p, sizeof(double) * 3 * l.n, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.check_launch();
+  });
+}
+
+int hot_stage_vcycle(hot_ctx* ctx, const double* b, double* u, int* coarse_iterations) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    if (c.nlevels < 1) throw std::logic_error("no hierarchy");
+    const int n = c.L[0].n;
+    HOT_CUDA(cudaMemcpyAsync(c.q.p, b, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    HOT_CUDA(cudaMemsetAsync(c.iflags.p, 0, sizeof(int) * 8, c.stream));
+    c.vcycle(c.q.as<double>(), c.pdir.as<double>(), false, 0);
+    HOT_CUDA(cudaMemcpyAsync(u, c.pdir.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    c.read_scalars(0, 3);
+    c.check_flags();
+    if (coarse_iterations) *coarse_iterations = c.host_int[2];
+  });
+}
+
+int hot_stage_step_grid(hot_ctx* ctx, double* velocity, double* dv, int* outer, long long* inner, int* converged,
+                        int frame, long long step) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    need_state(c);
+    auto so = c.step_grid(frame, step);
+    const int n = c.L[0].n;
+    hotb200::launch_final_velocity(c.gview(), c.dv.as<double>(), c.vout.as<double>(), c.stream);
+    if (velocity) HOT_CUDA(cudaMemcpyAsync(velocity, c.vout.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    if (dv) HOT_CUDA(cudaMemcpyAsync(dv, c.dv.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (outer) *outer = so.outer;
+    if (inner) *inner = so.inner;
+    if (converged) *converged = so.converged;
+  });
+}
+
+void* hot_stream(hot_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+int hot_profile_enable(hot_ctx* ctx, int enable) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    c.sync();
+    for (auto& e : c.events) {
+      c.event_pool.push_back(e.a);
+      c.event_pool.push_back(e.b);
+    }
+    c.events.clear();
+    for (double& b : c.phase_bytes) b = 0;
+    c.prof = enable != 0;
+  });
+}
+
+int hot_profile_read(hot_ctx* ctx, char* names, double* total_ms, long long* launches, double* bytes, int cap, int* n) {
+  return guard(ctx, [&] {
+    Context& c = ctx->c;
+    c.sync();
+    std::vector<double> ms(hotb200::kPhases, 0.0);
+    std::vector<long long> cnt(hotb200::kPhases, 0);
+    for (auto& e : c.events) {
+      float t = 0.f;
+      HOT_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
+      ms[e.phase] += t;
+      cnt[e.phase] += 1;
+    }
+    const int k = std::min(cap, hotb200::kPhases);
+    for (int i = 0; i < k; ++i) {
+      std::snprintf(names + 32 * i, 32, "%s", hotb200::kPhaseNames[i]);
+      total_ms[i] = ms[i];
+      launches[i] = cnt[i];
+      bytes[i] = c.phase_bytes[i];
+    }
+    *n = k;
+  });
+}
+
+long long hot_kernel_launches(hot_ctx* ctx) {
+  (void)ctx;
+  return hotb200::kernel_launch_count();
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// Internal (host <-> kernel) declarations of the B200 HOT step.  Not part of the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hot_device.cuh"
+
+namespace hotb200 {
+
+/// Particle state, structure-of-arrays in the caller's (reference) particle order:
+/// x[a*n+p], v[a*n+p], F[k*n+p] / C[k*n+p] with k = 3*row+col.
+struct ParticlesView {
+  double* x;
+  double* v;
+  double* F;
+  double* C;
+  double* mass;
+  double* vol;
+  int* mat;
+  long long n;
+};
+
+/// Particles binned by their stencil-centre node (round(x/dx)); ids ascending in a bin.
+struct BinsView {
+  const int* start;  // n_nodes + 1
+  const int* pid;    // n_particles
+};
+
+/// One multigrid level in diagonal storage, component-major per row:
+/// H[(row*9 + e)*kSlotPitch + slot], e = 3*r + c of the 3x3 block, slot lexicographic in
+/// {-2..2}^3 (objective.hpp:24-32).  cols[row*kSlotPitch + slot] = -1 when inactive.
+struct LevelView {
+  int n;
+  const int* coords;  // 3*n, lexicographic
+  DenseMap map;
+  const int* cols;
+  double* H;
+  double* dinv;       // 9*n row-major
+  const uint8_t* dir;
+};
+
+struct GridView {
+  int n;
+  const int* coords;
+  DenseMap map;
+  double* mass;
+  double* vel;     // 3n
+  double* mom;     // 3n
+  uint8_t* dir;
+  double* bc_vel;  // 3n
+  double* cn_scale;
+};
+
+struct DevCollider {
+  int shape;   // 0 box, 1 sphere, 2 half-space, 3 cylinder
+  int motion;  // 0 static, 1 linear, 2 rotation
+  double a[3], b[3];  // box min/max | sphere centre | half-space point/normal | cylinder centre/axis(unit)
+  double radius;
+  double vel[3];
+  double rot_center[3], rot_w[3];  // omega * unit axis
+};
+
+// ---------------------------------------------------------------- grid (k_grid.cu)
+void launch_particle_bounds(const ParticlesView& P, double dx, int* bounds6, int* bad_flag, cudaStream_t s);
+void launch_mark_active(const ParticlesView& P, double dx, DenseMap map, uint8_t* flags, cudaStream_t s);
+/// Exclusive scan of dense flags into idx (-1 for inactive) + compaction of coords.  Returns
+/// the active count through *count_dev.  tile_sums must hold ceil(len/4096)+1 ints.
+void launch_flags_to_index(const uint8_t* flags, long long len, const int* ext, const int* lo, int* idx, int* coords,
+                           int* tile_sums, int* count_dev, cudaStream_t s);
+void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n_nodes, int* bin_of, int* counts,
+                          int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s);
+void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
+                double dt, cudaStream_t s);
+void launch_apply_bc(GridView g, double dx, const DevCollider* cols, int n_cols, cudaStream_t s);
+/// Generic exclusive scan over n ints (out may alias nothing); tmp >= ceil(n/4096)+1 ints.
+void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, int* total_dev, cudaStream_t s);
+
+// ---------------------------------------------------------------- objective (k_objective.cu)
+/// Per-particle pass at nodal increment dv + alpha*p (p may be null): V_p psi partial sums
+/// into partials[blockIdx] and, when stress != null, stores V_p * P F^T (9 per particle).
+void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
+                            const double* dv, const double* p, double alpha, double* stress, double* partials,
+                            int nblocks, int* bad_flag, cudaStream_t s);
+void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
+                        double* partials, int nblocks, cudaStream_t s);
+/// g_i = dt * sum_p (V P F^T) grad w + m_i (dv_i - dt*grav); 0 on Dirichlet; partial sums of
+/// |g_i|^2 / scale_i^2 into partials.
+void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
+                          const double* stress, const double* dv, double* gout, double* partials, int nblocks,
+                          int* bad_flag, cudaStream_t s);
+void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s);
+
+// vector helpers (deterministic block partials + fixed-order final sums)
+void launch_dot_partials(const double* a, const double* b, long long n, double* partials, int nblocks, cudaStream_t s);
+/// q <- q - coef_dev[k]*y (if y) then partial dot(s, q)
+void launch_axpy_dot(double* q, const double* y, const double* coef_dev, int coef_idx, double coef_scale,
+                     const double* s_vec, long long n, double* partials, int nblocks, cudaStream_t s);
+/// coef_dev[k] = rho * sum(partials)  (alpha_k),  or coef_dev[k] = alpha_dev[k] - rho*sum (second loop)
+void launch_finalize_coef(const double* partials, int n, double rho, const double* alpha_dev, int idx, double* coef_dev,
+                          cudaStream_t s);
+void launch_neg_copy(const double* a, double* out, long long n, cudaStream_t s);
+/// out = a + alpha * b (two roundings, no contraction)
+void launch_add_scaled(const double* a, const double* b, double alpha, double* out, long long n, cudaStream_t s);
+void launch_scale(const double* a, double alpha, double* out, long long n, cudaStream_t s);
+void launch_sub(const double* a, const double* b, double* out, long long n, cudaStream_t s);
+/// y = g_new - g; partials for y.s, y.y, s.s (3 x nblocks)
+void launch_ys_dots(const double* g_new, const double* g_old, double* y, const double* s, long long n,
+                    double* partials, int nblocks, cudaStream_t s_);
+void launch_zero_dirichlet_copy(const double* in, double* out, const uint8_t* dir, int n, cudaStream_t s);
+void launch_final_velocity(GridView g, const double* dv, double* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- assembly (k_assembly.cu)
+void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
+                             const double* dv, int project, double* Tu, int* bad_flag, cudaStream_t s);
+void launch_fill_cols(LevelView L, cudaStream_t s);
+void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
+                          const double* Tu, cudaStream_t s);
+
+// ---------------------------------------------------------------- multigrid (k_multigrid.cu)
+void launch_mark_parents(LevelView fine, DenseMap cmap, uint8_t* flags, cudaStream_t s);
+void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaStream_t s);
+void launch_galerkin(LevelView fine, LevelView coarse, cudaStream_t s);
+/// diag inverse, singular check, wave id per row (level 0: colour mod 3; coarse: wavefront).
+void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
+                           cudaStream_t s);
+void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
+                        int nwaves, int* scan_tmp, cudaStream_t s);
+void launch_spmv(LevelView L, const double* x, double* y, cudaStream_t s);
+void launch_residual(LevelView L, const double* b, const double* u, double* r, cudaStream_t s);
+void launch_restrict(LevelView fine, LevelView coarse, const double* rf, double* bc, cudaStream_t s);
+void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, double* uf, cudaStream_t s);
+/// One symmetric Gauss-Seidel sweep (forward + backward over the wave schedule), as a
+/// cooperative persistent kernel with a grid barrier between waves.
+void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
+                int grid_blocks, cudaStream_t s);
+/// Jacobi-PCG from zero (pcg.hpp:17-46) as one cooperative kernel; writes x, iterations,
+/// status (0 ok, 1 rho<0, 2 pAp<=0) into stat[0..1] and accumulates iterations into *iter_acc.
+void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
+                int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s);
+int sgs_max_blocks();
+int pcg_max_blocks();
+
+// ---------------------------------------------------------------- transfer (k_transfer.cu)
+void launch_g2p_strain_advect(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
+                              int* inverted, cudaStream_t s);
+void launch_vmax(const ParticlesView& P, unsigned long long* vmax_bits, cudaStream_t s);
+
+void launch_aos_to_soa(const double* in, double* out, long long n, int comps, cudaStream_t s);
+void launch_soa_to_aos(const double* in, double* out, long long n, int comps, cudaStream_t s);
+
+int num_sms();
+
+/// Kernel launches issued by this process (all contexts); every launch_* wrapper counts.
+long long kernel_launch_count();
+void count_launches(int k);
+
+}  // namespace hotb200

@@ -1,0 +1,429 @@
+// Grid activation, particle binning, APIC P2G (+ node characteristic norm) and collider
+// boundary scripts on B200.
+//
+//   activate_grid   grid.hpp:137-165   dense bounding-box flags + scan: the scan over the
+//                                       row-major box IS the lexicographic order, so node
+//                                       indices equal the reference's sort+unique indices
+//                                       bit for bit, with no sort.
+//   p2g             transfer.hpp:46-64 node-centric gather over particles binned by their
+//                                       stencil-centre node: deterministic, no float atomics.
+//   compute_node_cn objective.hpp:450-473  fused into the P2G gather.
+//   apply_boundary_scripts simulation.hpp:259-272
+#include <cuda_runtime.h>
+
+#include "hot_internal.h"
+
+namespace hotb200 {
+
+namespace {
+
+constexpr int kTile = 4096;      // scan tile (256 threads x 16 items)
+constexpr int kScanThreads = 256;
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) >= o) v += t;
+  }
+  return v;
+}
+
+/// Block-wide exclusive scan of one int per thread (blockDim = 256); returns the block total.
+__device__ __forceinline__ int block_excl_scan(int v, int* total) {
+  __shared__ int warp_sums[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int inc = warp_incl_scan(v);
+  if (lane == 31) warp_sums[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int ws = lane < kScanThreads / 32 ? warp_sums[lane] : 0;
+    const int wi = warp_incl_scan(ws);
+    if (lane < kScanThreads / 32) warp_sums[lane] = wi - ws;
+    if (lane == kScanThreads / 32 - 1) *total = wi;
+  }
+  __syncthreads();
+  const int r = inc - v + warp_sums[wid];
+  __syncthreads();
+  return r;
+}
+
+__global__ void k_particle_bounds(const double* __restrict__ x, long long n, double dx, int* bounds6, int* bad) {
+  int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double xa = x[a * n + p];
+      if (!isfinite(xa)) {
+        atomicExch(bad, 1);
+        continue;
+      }
+      const int b = stencil_base_1d(xa / dx);
+      mn[a] = min(mn[a], b);
+      mx[a] = max(mx[a], b);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(bounds6 + a, mn[a]);
+      atomicMax(bounds6 + 3 + a, mx[a]);
+    }
+  }
+}
+
+/// Marks every node with nonzero quadratic weight (grid.hpp:147-152).  weight > 0 iff every
+/// 1D factor > 0 (the factors are bounded below by ~1e-32, so the product never underflows).
+__global__ void k_mark_active(const double* __restrict__ x, long long n, double dx, DenseMap map,
+                              uint8_t* __restrict__ flags) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    double c[3];
+    int base[3];
+    bool ok[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      c[a] = x[a * n + p] / dx;
+      base[a] = stencil_base_1d(c[a]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ok[a][k] = bspline_w(c[a] - (double)(base[a] + k)) > 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (!ok[0][i]) continue;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (!ok[1][j]) continue;
+        const long long row = ((long long)(base[0] + i - map.lo[0]) * map.ext[1] + (base[1] + j - map.lo[1])) * map.ext[2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (ok[2][k]) flags[row + (base[2] + k - map.lo[2])] = 1;
+      }
+    }
+  }
+}
+
+__global__ void k_tile_counts(const uint8_t* __restrict__ flags, long long len, int* tile_sums) {
+  const long long t0 = (long long)blockIdx.x * kTile + threadIdx.x * 16;
+  int cnt = 0;
+  if (t0 + 16 <= len) {
+    const uint4 v = *reinterpret_cast<const uint4*>(flags + t0);
+    cnt = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);  // flags are 0/1 bytes
+  } else {
+    for (long long i = t0; i < len; ++i) cnt += flags[i];
+  }
+  __shared__ int tot;
+  block_excl_scan(cnt, &tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+/// Single-block exclusive scan of n ints in place; writes the grand total.
+__global__ void k_scan_small(int* data, int n, int* total) {
+  __shared__ int carry_s, tot;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += kScanThreads) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? data[i] : 0;
+    const int ex = block_excl_scan(v, &tot);
+    const int carry = carry_s;
+    if (i < n) data[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry_s;
+}
+
+__global__ void k_tile_index(const uint8_t* __restrict__ flags, long long len, int e1, int e2, int lo0, int lo1,
+                             int lo2, const int* __restrict__ tile_sums, int* __restrict__ idx,
+                             int* __restrict__ coords) {
+  const long long t0 = (long long)blockIdx.x * kTile + threadIdx.x * 16;
+  uint8_t f[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = (t0 + i < len) ? flags[t0 + i] : 0;
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) cnt += f[i];
+  __shared__ int tot;
+  int r = block_excl_scan(cnt, &tot) + tile_sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const long long l = t0 + i;
+    if (l >= len) break;
+    if (f[i]) {
+      idx[l] = r;
+      const int z = (int)(l % e2);
+      const long long q = l / e2;
+      const int y = (int)(q % e1);
+      const int xx = (int)(q / e1);
+      coords[3 * r] = xx + lo0;
+      coords[3 * r + 1] = y + lo1;
+      coords[3 * r + 2] = z + lo2;
+      ++r;
+    } else {
+      idx[l] = -1;
+    }
+  }
+}
+
+__global__ void k_int_tile_sums(const int* __restrict__ in, int n, int* tile_sums) {
+  int s = 0;
+  const long long t0 = (long long)blockIdx.x * kTile + threadIdx.x * 16;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (t0 + i < n) s += in[t0 + i];
+  __shared__ int tot;
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void k_int_tile_scan(const int* __restrict__ in, int n, const int* __restrict__ tile_sums, int* out) {
+  const long long t0 = (long long)blockIdx.x * kTile + threadIdx.x * 16;
+  int v[16];
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = (t0 + i < n) ? in[t0 + i] : 0;
+    s += v[i];
+  }
+  __shared__ int tot;
+  int r = block_excl_scan(s, &tot) + tile_sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (t0 + i < n) out[t0 + i] = r;
+    r += v[i];
+  }
+}
+
+__global__ void k_bin_count(const double* __restrict__ x, long long n, double dx, DenseMap map, int* bin_of,
+                            int* counts) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = stencil_base_1d(x[a * n + p] / dx) + 1;
+    const int j = dense_lookup(map, c[0], c[1], c[2]);  // the centre node always has weight > 0
+    bin_of[p] = j;
+    atomicAdd(counts + j, 1);
+  }
+}
+
+__global__ void k_bin_scatter(const int* __restrict__ bin_of, long long n, int* cursor, int* pid) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const int pos = atomicAdd(cursor + bin_of[p], 1);
+    pid[pos] = (int)p;
+  }
+}
+
+/// Canonical (ascending particle id) order inside each bin, so every gather below is
+/// run-to-run deterministic.
+__global__ void k_bin_sort(const int* __restrict__ start, int n_nodes, int* pid) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_nodes; j += gridDim.x * blockDim.x) {
+    const int b = start[j], e = start[j + 1];
+    for (int i = b + 1; i < e; ++i) {
+      const int v = pid[i];
+      int k = i - 1;
+      while (k >= b && pid[k] > v) {
+        pid[k + 1] = pid[k];
+        --k;
+      }
+      pid[k + 1] = v;
+    }
+  }
+}
+
+/// APIC P2G gather (transfer.hpp:46-64) fused with the node characteristic norm
+/// (objective.hpp:450-473).  One thread per node; neighbour bins visited lexicographically.
+__global__ void k_p2g(ParticlesView P, BinsView bins, GridView g, double dx, const DevMaterial* __restrict__ mats,
+                      double ell, double dt) {
+  const long long n = P.n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const int ci0 = g.coords[3 * i], ci1 = g.coords[3 * i + 1], ci2 = g.coords[3 * i + 2];
+    const double xi0 = (double)ci0 * dx, xi1 = (double)ci1 * dx, xi2 = (double)ci2 * dx;
+    double m = 0.0, mom0 = 0.0, mom1 = 0.0, mom2 = 0.0, num = 0.0;
+    for (int o = 0; o < 27; ++o) {
+      const int j = dense_lookup(g.map, ci0 + o / 9 - 1, ci1 + (o / 3) % 3 - 1, ci2 + o % 3 - 1);
+      if (j < 0) continue;
+      const int e = bins.start[j + 1];
+      for (int t = bins.start[j]; t < e; ++t) {
+        const int p = bins.pid[t];
+        const double px0 = P.x[p], px1 = P.x[n + p], px2 = P.x[2 * n + p];
+        const double w = bspline_w(px0 / dx - (double)ci0) * bspline_w(px1 / dx - (double)ci1) *
+                         bspline_w(px2 / dx - (double)ci2);
+        if (w <= 0.0) continue;
+        const double mp = P.mass[p];
+        const double wm = w * mp;
+        const double d0 = xi0 - px0, d1 = xi1 - px1, d2 = xi2 - px2;
+        const double* C = P.C;
+        const double a0 = P.v[p] + (C[p] * d0 + C[n + p] * d1 + C[2 * n + p] * d2);
+        const double a1 = P.v[n + p] + (C[3 * n + p] * d0 + C[4 * n + p] * d1 + C[5 * n + p] * d2);
+        const double a2 = P.v[2 * n + p] + (C[6 * n + p] * d0 + C[7 * n + p] * d1 + C[8 * n + p] * d2);
+        m += wm;
+        mom0 += wm * a0;
+        mom1 += wm * a1;
+        mom2 += wm * a2;
+        num += w * (mp * mats[P.mat[p]].xi);
+      }
+    }
+    g.mass[i] = m;
+    g.mom[3 * i] = mom0;
+    g.mom[3 * i + 1] = mom1;
+    g.mom[3 * i + 2] = mom2;
+    if (m > 0.0) {
+      g.vel[3 * i] = mom0 / m;
+      g.vel[3 * i + 1] = mom1 / m;
+      g.vel[3 * i + 2] = mom2 / m;
+    } else {
+      g.vel[3 * i] = g.vel[3 * i + 1] = g.vel[3 * i + 2] = 0.0;
+    }
+    const double xi = m > 0.0 ? num / m : 0.0;
+    g.cn_scale[i] = ell * xi * dt;
+    g.dir[i] = 0;
+    g.bc_vel[3 * i] = g.bc_vel[3 * i + 1] = g.bc_vel[3 * i + 2] = 0.0;
+  }
+}
+
+// Collider tests mirror simulation.hpp:20-65 with explicit round-to-nearest arithmetic so the
+// Dirichlet set matches the CPU's uncontracted evaluation bit for bit.
+__device__ __forceinline__ double dot3_rn(const double a[3], const double b[3]) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
+}
+
+__device__ bool inside_collider(const DevCollider& c, const double x[3]) {
+  switch (c.shape) {
+    case 0:
+      for (int a = 0; a < 3; ++a)
+        if (x[a] < c.a[a] || x[a] > c.b[a]) return false;
+      return true;
+    case 1: {
+      double r[3];
+      for (int a = 0; a < 3; ++a) r[a] = __dsub_rn(x[a], c.a[a]);
+      return __dsqrt_rn(dot3_rn(r, r)) <= c.radius;
+    }
+    case 2: {
+      double r[3];
+      for (int a = 0; a < 3; ++a) r[a] = __dsub_rn(x[a], c.a[a]);
+      return dot3_rn(r, c.b) <= 0.0;
+    }
+    case 3: {
+      double r[3];
+      for (int a = 0; a < 3; ++a) r[a] = __dsub_rn(x[a], c.a[a]);
+      const double t = dot3_rn(r, c.b);
+      double q[3];
+      for (int a = 0; a < 3; ++a) q[a] = __dsub_rn(r[a], __dmul_rn(t, c.b[a]));
+      return __dsqrt_rn(dot3_rn(q, q)) <= c.radius;
+    }
+  }
+  return false;
+}
+
+__global__ void k_apply_bc(GridView g, double dx, const DevCollider* __restrict__ cols, int n_cols) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const double x[3] = {__dmul_rn((double)g.coords[3 * i], dx), __dmul_rn((double)g.coords[3 * i + 1], dx),
+                         __dmul_rn((double)g.coords[3 * i + 2], dx)};
+    for (int k = 0; k < n_cols; ++k) {
+      const DevCollider c = cols[k];
+      if (!inside_collider(c, x)) continue;
+      double v[3] = {0.0, 0.0, 0.0};
+      if (c.motion == 1) {
+        v[0] = c.vel[0];
+        v[1] = c.vel[1];
+        v[2] = c.vel[2];
+      } else if (c.motion == 2) {
+        const double r0 = x[0] - c.rot_center[0], r1 = x[1] - c.rot_center[1], r2 = x[2] - c.rot_center[2];
+        v[0] = c.rot_w[1] * r2 - c.rot_w[2] * r1;
+        v[1] = c.rot_w[2] * r0 - c.rot_w[0] * r2;
+        v[2] = c.rot_w[0] * r1 - c.rot_w[1] * r0;
+      }
+      g.dir[i] = 1;
+      for (int a = 0; a < 3; ++a) {
+        g.vel[3 * i + a] = v[a];
+        g.bc_vel[3 * i + a] = v[a];
+      }
+      break;
+    }
+  }
+}
+
+int grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  const long long cap = (long long)num_sms() * 32;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+void launch_particle_bounds(const ParticlesView& P, double dx, int* bounds6, int* bad_flag, cudaStream_t s) {
+  if (P.n == 0) return;
+  { k_particle_bounds<<<grid_for(P.n, 256), 256, 0, s>>>(P.x, P.n, dx, bounds6, bad_flag); count_launches(1); }
+}
+
+void launch_mark_active(const ParticlesView& P, double dx, DenseMap map, uint8_t* flags, cudaStream_t s) {
+  if (P.n == 0) return;
+  { k_mark_active<<<grid_for(P.n, 256), 256, 0, s>>>(P.x, P.n, dx, map, flags); count_launches(1); }
+}
+
+void launch_flags_to_index(const uint8_t* flags, long long len, const int* ext, const int* lo, int* idx, int* coords,
+                           int* tile_sums, int* count_dev, cudaStream_t s) {
+  const int tiles = (int)((len + kTile - 1) / kTile);
+  if (tiles == 0) {
+    cudaMemsetAsync(count_dev, 0, sizeof(int), s);
+    return;
+  }
+  { k_tile_counts<<<tiles, kScanThreads, 0, s>>>(flags, len, tile_sums); count_launches(1); }
+  { k_scan_small<<<1, kScanThreads, 0, s>>>(tile_sums, tiles, count_dev); count_launches(1); }
+  { k_tile_index<<<tiles, kScanThreads, 0, s>>>(flags, len, ext[1], ext[2], lo[0], lo[1], lo[2], tile_sums, idx, coords); count_launches(1); }
+}
+
+void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, int* total_dev, cudaStream_t s) {
+  const int tiles = (n + kTile - 1) / kTile;
+  if (tiles == 0) {
+    if (total_dev) cudaMemsetAsync(total_dev, 0, sizeof(int), s);
+    return;
+  }
+  { k_int_tile_sums<<<tiles, kScanThreads, 0, s>>>(in, n, tmp); count_launches(1); }
+  { k_scan_small<<<1, kScanThreads, 0, s>>>(tmp, tiles, total_dev); count_launches(1); }
+  { k_int_tile_scan<<<tiles, kScanThreads, 0, s>>>(in, n, tmp, out); count_launches(1); }
+}
+
+void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n_nodes, int* bin_of, int* counts,
+                          int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s) {
+  cudaMemsetAsync(counts, 0, sizeof(int) * (n_nodes + 1), s);
+  if (P.n > 0) { k_bin_count<<<grid_for(P.n, 256), 256, 0, s>>>(P.x, P.n, dx, map, bin_of, counts); count_launches(1); }
+  launch_exclusive_scan(counts, start, n_nodes + 1, scan_tmp, nullptr, s);
+  cudaMemcpyAsync(cursor, start, sizeof(int) * n_nodes, cudaMemcpyDeviceToDevice, s);
+  if (P.n > 0) { k_bin_scatter<<<grid_for(P.n, 256), 256, 0, s>>>(bin_of, P.n, cursor, pid); count_launches(1); }
+  if (n_nodes > 0) { k_bin_sort<<<grid_for(n_nodes, 128), 128, 0, s>>>(start, n_nodes, pid); count_launches(1); }
+}
+
+void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
+                double dt, cudaStream_t s) {
+  if (g.n == 0) return;
+  { k_p2g<<<grid_for(g.n, 128), 128, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
+}
+
+void launch_apply_bc(GridView g, double dx, const DevCollider* cols, int n_cols, cudaStream_t s) {
+  if (g.n == 0 || n_cols == 0) return;
+  { k_apply_bc<<<grid_for(g.n, 128), 128, 0, s>>>(g, dx, cols, n_cols); count_launches(1); }
+}
+
+}  // namespace hotb200

@@ -1,0 +1,311 @@
+// Incremental potential on B200: per-particle energy/stress at a nodal velocity increment
+// (objective.hpp:236-257), node-centric gradient gather (objective.hpp:260-287) fused with
+// the characteristic-norm residual (objective.hpp:476-486), and the L-BFGS vector algebra
+// (solvers.hpp:82-129) as fused, deterministic reductions (fixed block partials summed in
+// fixed order; no float atomics).
+#include <cuda_runtime.h>
+
+#include "hot_internal.h"
+#include "hot_particle.cuh"
+
+namespace hotb200 {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+/// Deterministic block sum (fixed tree); result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[NT / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) ws[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) r += ws[w];
+  }
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
+                                                                 const DevMaterial* __restrict__ mats,
+                                                                 const double* __restrict__ dv,
+                                                                 const double* __restrict__ pd, double alpha,
+                                                                 double* __restrict__ stress,
+                                                                 double* __restrict__ partials, int* bad) {
+  double acc = 0.0;
+  const long long n = P.n;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    M3 F, Fn;
+    if (!virtual_F(P, p, g, dx, dt, dv, pd, alpha, F, Fn)) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    const DevMaterial mt = mats[P.mat[p]];
+    M3 U, V;
+    double s[3];
+    svd3(F, U, s, V);
+    const double vol = P.vol[p];
+    acc += vol * fcr_psi(s, mt.mu, mt.lambda);
+    if (stress) {
+      const M3 Pk = fcr_P(F, U, V, mt.mu, mt.lambda);
+      const M3 PFt = m3_mul_bt(Pk, Fn);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) stress[k * n + p] = vol * PFt.m[k];
+    }
+  }
+  const double b = block_sum<kRedThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, double dt, double g0, double g1, double g2,
+                                                             const double* __restrict__ dv,
+                                                             const double* __restrict__ pd, double alpha,
+                                                             double* __restrict__ partials) {
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      d[a] = dv[3 * i + a];
+      if (pd) d[a] = __dadd_rn(d[a], __dmul_rn(alpha, pd[3 * i + a]));
+    }
+    const double m = g.mass[i];
+    const double sq = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+    const double gu = g0 * (g.vel[3 * i] + d[0]) + g1 * (g.vel[3 * i + 1] + d[1]) + g2 * (g.vel[3 * i + 2] + d[2]);
+    acc += 0.5 * m * sq - dt * m * gu;
+  }
+  const double b = block_sum<kRedThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_node_gradient(ParticlesView P, BinsView bins, GridView g, double dx,
+                                                               double dt, double g0, double g1, double g2,
+                                                               const double* __restrict__ stress,
+                                                               const double* __restrict__ dv, double* __restrict__ gout,
+                                                               double* __restrict__ partials, int* bad) {
+  const long long n = P.n;
+  double acc_norm = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    const int ci0 = g.coords[3 * i], ci1 = g.coords[3 * i + 1], ci2 = g.coords[3 * i + 2];
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    for (int o = 0; o < 27; ++o) {
+      const int j = dense_lookup(g.map, ci0 + o / 9 - 1, ci1 + (o / 3) % 3 - 1, ci2 + o % 3 - 1);
+      if (j < 0) continue;
+      const int e = bins.start[j + 1];
+      for (int t = bins.start[j]; t < e; ++t) {
+        const int p = bins.pid[t];
+        const double o0 = P.x[p] / dx - (double)ci0;
+        const double o1 = P.x[n + p] / dx - (double)ci1;
+        const double o2 = P.x[2 * n + p] / dx - (double)ci2;
+        const double w0 = bspline_w(o0), w1 = bspline_w(o1), w2 = bspline_w(o2);
+        if (w0 * w1 * w2 <= 0.0) continue;
+        const double gr0 = bspline_dw(o0) / dx * w1 * w2;
+        const double gr1 = bspline_dw(o1) / dx * w0 * w2;
+        const double gr2 = bspline_dw(o2) / dx * w0 * w1;
+        const double* Q = stress;
+        f0 += Q[p] * gr0 + Q[n + p] * gr1 + Q[2 * n + p] * gr2;
+        f1 += Q[3 * n + p] * gr0 + Q[4 * n + p] * gr1 + Q[5 * n + p] * gr2;
+        f2 += Q[6 * n + p] * gr0 + Q[7 * n + p] * gr1 + Q[8 * n + p] * gr2;
+      }
+    }
+    const double m = g.mass[i];
+    double gi[3] = {dt * f0 + m * (dv[3 * i] - dt * g0), dt * f1 + m * (dv[3 * i + 1] - dt * g1),
+                    dt * f2 + m * (dv[3 * i + 2] - dt * g2)};
+    if (g.dir[i]) gi[0] = gi[1] = gi[2] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gout[3 * i + a] = gi[a];
+    const double sc = g.cn_scale[i];
+    if (!(sc > 0.0)) atomicExch(bad, 2);
+    acc_norm += (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
+  }
+  const double b = block_sum<kRedThreads>(acc_norm);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sum_partials(const double* __restrict__ partials, int n,
+                                                              double* out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  const double b = block_sum<kRedThreads>(acc);
+  if (threadIdx.x == 0) *out = b;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_dot_partials(const double* __restrict__ a,
+                                                              const double* __restrict__ b, long long n,
+                                                              double* __restrict__ partials) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc += a[i] * b[i];
+  const double r = block_sum<kRedThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_axpy_dot(double* __restrict__ q, const double* __restrict__ y,
+                                                          const double* __restrict__ coef_dev, int idx, int add,
+                                                          const double* __restrict__ s, long long n,
+                                                          double* __restrict__ partials) {
+  const double c = y ? coef_dev[idx] : 0.0;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double v = q[i];
+    if (y) {
+      const double cy = __dmul_rn(c, y[i]);
+      v = add ? __dadd_rn(v, cy) : __dsub_rn(v, cy);
+      q[i] = v;
+    }
+    if (s) acc += s[i] * v;
+  }
+  if (partials) {
+    const double r = block_sum<kRedThreads>(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = r;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_finalize_coef(const double* __restrict__ partials, int n, double rho,
+                                                               const double* __restrict__ alpha_dev, int idx,
+                                                               double* coef_dev) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  const double b = block_sum<kRedThreads>(acc);
+  if (threadIdx.x == 0) coef_dev[idx] = alpha_dev ? alpha_dev[idx] - rho * b : rho * b;
+}
+
+__global__ void k_neg_copy(const double* __restrict__ a, double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = -a[i];
+}
+__global__ void k_add_scaled(const double* __restrict__ a, const double* __restrict__ b, double alpha,
+                             double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(a[i], __dmul_rn(alpha, b[i]));
+}
+__global__ void k_scale(const double* __restrict__ a, double alpha, double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = alpha * a[i];
+}
+__global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                      long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_ys_dots(const double* __restrict__ gn, const double* __restrict__ go,
+                                                         double* __restrict__ y, const double* __restrict__ s,
+                                                         long long n, double* __restrict__ partials) {
+  double ys = 0.0, yy = 0.0, ss = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double yi = gn[i] - go[i];
+    y[i] = yi;
+    const double si = s[i];
+    ys += yi * si;
+    yy += yi * yi;
+    ss += si * si;
+  }
+  const double a = block_sum<kRedThreads>(ys);
+  const double b = block_sum<kRedThreads>(yy);
+  const double c = block_sum<kRedThreads>(ss);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = a;
+    partials[gridDim.x + blockIdx.x] = b;
+    partials[2 * gridDim.x + blockIdx.x] = c;
+  }
+}
+
+__global__ void k_zero_dir_copy(const double* __restrict__ in, double* __restrict__ out, const uint8_t* __restrict__ dir,
+                                int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const bool z = dir[i] != 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[3 * i + a] = z ? 0.0 : in[3 * i + a];
+  }
+}
+
+/// v^{n+1} = v^n + dv, Dirichlet nodes carry bc_velocity exactly (solvers.hpp:376-379).
+__global__ void k_final_velocity(GridView g, const double* __restrict__ dv, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      out[3 * i + a] = g.dir[i] ? g.bc_vel[3 * i + a] : g.vel[3 * i + a] + dv[3 * i + a];
+  }
+}
+
+int vgrid(long long n) {
+  long long b = (n + 255) / 256;
+  const long long cap = (long long)num_sms() * 8;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
+                            const double* dv, const double* p, double alpha, double* stress, double* partials,
+                            int nblocks, int* bad_flag, cudaStream_t s) {
+  { k_particle_energy<<<nblocks, kRedThreads, 0, s>>>(P, g, dx, dt, mats, dv, p, alpha, stress, partials, bad_flag); count_launches(1); }
+}
+
+void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
+                        double* partials, int nblocks, cudaStream_t s) {
+  { k_node_energy<<<nblocks, kRedThreads, 0, s>>>(g, dt, grav[0], grav[1], grav[2], dv, p, alpha, partials); count_launches(1); }
+}
+
+void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
+                          const double* stress, const double* dv, double* gout, double* partials, int nblocks,
+                          int* bad_flag, cudaStream_t s) {
+  { k_node_gradient<<<nblocks, kRedThreads, 0, s>>>(P, bins, g, dx, dt, grav[0], grav[1], grav[2], stress, dv, gout,
+                                                  partials, bad_flag); count_launches(1); }
+}
+
+void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s) {
+  { k_sum_partials<<<1, kRedThreads, 0, s>>>(partials, n, out); count_launches(1); }
+}
+
+void launch_dot_partials(const double* a, const double* b, long long n, double* partials, int nblocks, cudaStream_t s) {
+  { k_dot_partials<<<nblocks, kRedThreads, 0, s>>>(a, b, n, partials); count_launches(1); }
+}
+
+void launch_axpy_dot(double* q, const double* y, const double* coef_dev, int coef_idx, double coef_scale,
+                     const double* s_vec, long long n, double* partials, int nblocks, cudaStream_t s) {
+  { k_axpy_dot<<<nblocks, kRedThreads, 0, s>>>(q, y, coef_dev, coef_idx, coef_scale > 0 ? 1 : 0, s_vec, n, partials); count_launches(1); }
+}
+
+void launch_finalize_coef(const double* partials, int n, double rho, const double* alpha_dev, int idx, double* coef_dev,
+                          cudaStream_t s) {
+  { k_finalize_coef<<<1, kRedThreads, 0, s>>>(partials, n, rho, alpha_dev, idx, coef_dev); count_launches(1); }
+}
+
+void launch_neg_copy(const double* a, double* out, long long n, cudaStream_t s) {
+  if (n) { k_neg_copy<<<vgrid(n), 256, 0, s>>>(a, out, n); count_launches(1); }
+}
+void launch_add_scaled(const double* a, const double* b, double alpha, double* out, long long n, cudaStream_t s) {
+  if (n) { k_add_scaled<<<vgrid(n), 256, 0, s>>>(a, b, alpha, out, n); count_launches(1); }
+}
+void launch_scale(const double* a, double alpha, double* out, long long n, cudaStream_t s) {
+  if (n) { k_scale<<<vgrid(n), 256, 0, s>>>(a, alpha, out, n); count_launches(1); }
+}
+void launch_sub(const double* a, const double* b, double* out, long long n, cudaStream_t s) {
+  if (n) { k_sub<<<vgrid(n), 256, 0, s>>>(a, b, out, n); count_launches(1); }
+}
+void launch_ys_dots(const double* g_new, const double* g_old, double* y, const double* s, long long n,
+                    double* partials, int nblocks, cudaStream_t st) {
+  { k_ys_dots<<<nblocks, kRedThreads, 0, st>>>(g_new, g_old, y, s, n, partials); count_launches(1); }
+}
+void launch_zero_dirichlet_copy(const double* in, double* out, const uint8_t* dir, int n, cudaStream_t s) {
+  if (n) { k_zero_dir_copy<<<vgrid(n), 256, 0, s>>>(in, out, dir, n); count_launches(1); }
+}
+void launch_final_velocity(GridView g, const double* dv, double* out, cudaStream_t s) {
+  if (g.n) { k_final_velocity<<<vgrid(g.n), 256, 0, s>>>(g, dv, out); count_launches(1); }
+}
+
+}  // namespace hotb200
