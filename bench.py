@@ -239,9 +239,7 @@ def main():
                           static["material"])
         sim.advance_step(frame_end())
         step_no += 1
-        out = sim.particles()
-        for k in ("x", "v", "F", "C"):
-            pinned[k][...] = out[k]
+        sim.particles(out=pinned)
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1)

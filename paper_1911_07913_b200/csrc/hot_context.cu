@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <stdexcept>
@@ -85,7 +86,7 @@ struct Level {
   int lo[3] = {0, 0, 0}, ext[3] = {0, 0, 0};
   DBuf map, coords, cols, H, dinv, dir, flags;
   DBuf wave_of, wave_counts, wave_start, wave_cursor, wave_rows, wave_start_c;
-  int nwaves = 0;
+  int nwaves = 0, max_wave = 0;
   long long active_slots = 0;
   DBuf b, u, r;  // V-cycle vectors
   DenseMap dmap() const {
@@ -267,7 +268,7 @@ struct Context {
     HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
     HOT_CUDA(cudaMallocHost(&host_int, sizeof(int) * 64));
     nred = 2 * num_sms();
-    partials.ensure(sizeof(double) * 4 * (nred + 64));
+    partials.ensure(sizeof(double) * (6 * nred + std::max(pcg_max_blocks(), sgs_max_blocks()) + 64));
     scal.ensure(sizeof(double) * 64);
     iflags.ensure(sizeof(int) * 64);
     bounds.ensure(sizeof(int) * 8);
@@ -582,7 +583,7 @@ struct Context {
     Level& l0 = L[0];
     alloc_level(l0);
     int h = prof_begin(P_TENSORS);
-    Tu.ensure(sizeof(double) * 45 * std::max<long long>(np, 1));
+    Tu.ensure(sizeof(double) * 63 * std::max<long long>(np, 1));
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, project ? 1 : 0, Tu.as<double>(),
                             flag_bad(), stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 45 * 8));
@@ -622,10 +623,12 @@ struct Context {
     sync();
     std::vector<int> starts;
     int acc = 0;
+    l.max_wave = 0;
     for (int w = 0; w < nw; ++w)
       if (counts[w] > 0) {
         starts.push_back(acc);
         acc += counts[w];
+        l.max_wave = std::max(l.max_wave, counts[w]);
       }
     starts.push_back(acc);
     l.nwaves = (int)starts.size() - 1;
@@ -686,16 +689,18 @@ struct Context {
     check_launch();
   }
 
-  static int coop_grid(int max_blocks, int rows) {
-    const int want = (rows + 7) / 8;  // 8 warps per block, one row per warp
-    return std::max(1, std::min(max_blocks, want));
+  /// Few, fat CTAs for the cooperative kernels: the grid barrier costs grow with the number of
+  /// participating CTAs, while one wave / one PCG row-sweep only has tens to thousands of rows.
+  static int coop_grid(int max_blocks, int rows, int warps_per_block, int rows_per_warp) {
+    const int want = (rows + warps_per_block * rows_per_warp - 1) / (warps_per_block * rows_per_warp);
+    return std::max(1, std::min(std::min(max_blocks, num_sms()), want));
   }
 
   void sgs(int m, double* u, const double* b) {
     Level& l = L[m];
     const int h = prof_begin(m == 0 ? P_SGS0 : P_SGSC);
     launch_sgs(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
-               coop_grid(sgs_max_blocks(), l.n), stream);
+               coop_grid(sgs_max_blocks(), l.max_wave, 16, 1), stream);
     prof_end(h, 2.0 * (72.0 * l.active_slots + 72.0 * l.n + 24.0 * l.n + 48.0 * l.n));
   }
 
@@ -719,8 +724,8 @@ struct Context {
       const double rel = pinned ? 1e-14 : 0.5;
       const int cap = pinned ? pinned_cap : 10000;
       launch_pcg(bot.view(), bot.b.as<double>(), bot.u.as<double>(), pcg_r.as<double>(), pcg_z.as<double>(),
-                 pcg_p.as<double>(), pcg_Ap.as<double>(), rel, cap, partials.as<double>() + 3 * nred,
-                 iflags.as<int>() + 4, iflags.as<int>() + 2, coop_grid(pcg_max_blocks(), bot.n), stream);
+                 pcg_p.as<double>(), pcg_Ap.as<double>(), rel, cap, partials.as<double>() + 6 * nred,
+                 iflags.as<int>() + 4, iflags.as<int>() + 2, coop_grid(pcg_max_blocks(), bot.n, 8, 4), stream);
       prof_end(h);
       // status word -> iflags[1] (max over the solve)
       copy_status();
@@ -810,6 +815,11 @@ struct Context {
     assemble(dv.as<double>(), true);
     build_hierarchy(levels, cfg.embedding);
     for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
+    if (std::getenv("HOT_VERBOSE"))
+      for (int m = 0; m < nlevels; ++m)
+        std::fprintf(stderr, "[hot] level %d: rows=%d waves=%d max_wave=%d active_slots=%lld (%.1f/row) bbox=%dx%dx%d\n",
+                     m, L[m].n, L[m].nwaves, L[m].max_wave, L[m].active_slots, L[m].n ? (double)L[m].active_slots / L[m].n : 0.0,
+                     L[m].ext[0], L[m].ext[1], L[m].ext[2]);
     for (int k = 0; k <= cfg.window; ++k) {
       hist_s[k].ensure(sizeof(double) * std::max<long long>(n3, 1));
       hist_y[k].ensure(sizeof(double) * std::max<long long>(n3, 1));

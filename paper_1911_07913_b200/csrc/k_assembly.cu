@@ -21,6 +21,8 @@ namespace {
 constexpr int kAsmWarps = 4;
 constexpr int kUpper = 63;  // slots 62..124
 
+constexpr int kTensorStride = 63;  // 45 upper-triangle entries of kappa*T, then 9 w + 9 dw/dx
+
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
                                    const DevMaterial* __restrict__ mats, const double* __restrict__ dv, int project,
                                    double* __restrict__ Tu, int* bad) {
@@ -39,6 +41,18 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
     fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
 #pragma unroll
     for (int q = 0; q < 45; ++q) Tu[q * n + p] = T[q];
+    // per-axis stencil weights and derivatives (grid.hpp:22-73) for the row gather
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double c = P.x[a * n + p] / dx;
+      Axis3 ax;
+      axis_weights(c, stencil_base_1d(c), ax);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        Tu[(45 + 3 * a + k) * n + p] = ax.w[k];
+        Tu[(54 + 3 * a + k) * n + p] = ax.dw[k] / dx;
+      }
+    }
   }
 }
 
@@ -54,89 +68,77 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
   }
 }
 
-template <int R, int C>
-__device__ __forceinline__ double Tget(const double* T) {
-  if constexpr (R <= C)
-    return T[R * 9 - (R * (R - 1)) / 2 + (C - R)];
-  else
-    return T[C * 9 - (C * (C - 1)) / 2 + (R - C)];
-}
+__constant__ unsigned char c_tri_r[45], c_tri_c[45];
 
-template <int c, int e>
-__device__ __forceinline__ double pair_entry(const double* T, const double wa[3], const double wb[3]) {
-  // sum_f wa_f sum_g T[(3c+f),(3e+g)] wb_g  (objective.hpp:304-310)
-  double acc = 0.0;
-#define HOT_ROW(f)                                                                                      \
-  acc += wa[f] * (Tget<3 * c + f, 3 * e>(T) * wb[0] + Tget<3 * c + f, 3 * e + 1>(T) * wb[1] + \
-                  Tget<3 * c + f, 3 * e + 2>(T) * wb[2]);
-  HOT_ROW(0)
-  HOT_ROW(1)
-  HOT_ROW(2)
-#undef HOT_ROW
-  return acc;
-}
-
-__global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(ParticlesView P, BinsView bins, GridView g,
-                                                                   LevelView L, double dx,
+/// Row gather (objective.hpp:331-357).  Per (row a, particle p) the warp first forms
+/// M[c][e][g] = sum_f wa_f T[(3c+f),(3e+g)] (27 lanes, 3 FMA each), then every lane owning an
+/// upper-triangle stencil position kb contracts C[c][e] = sum_g M[c][e][g] wb_g (27 FMA).
+__global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L, long long n,
+                                                                   const double* __restrict__ F,
                                                                    const double* __restrict__ Tu) {
   __shared__ double acc_s[kAsmWarps][kUpper * 9];
-  __shared__ double stage_s[kAsmWarps][64];  // T (45), F (9), x (3)
+  __shared__ double T_s[kAsmWarps][81];
+  __shared__ double X_s[kAsmWarps][28];  // w[9], dwdx[9], F[9]
+  __shared__ double M_s[kAsmWarps][28];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* acc = acc_s[wid];
-  double* st = stage_s[wid];
-  const long long n = P.n;
+  double* Ts = T_s[wid];
+  double* Xs = X_s[wid];
+  double* Ms = M_s[wid];
   const int kb0 = lane / 9, kb1 = (lane / 3) % 3, kb2 = lane % 3;
+  // lane's M entry (c,e,g) = (kb0,kb1,kb2): T indices for f = 0..2
+  const int mrow = 3 * kb0, mcol = 3 * kb1 + kb2;
   const int nwarps = gridDim.x * kAsmWarps;
   for (int i = blockIdx.x * kAsmWarps + wid; i < L.n; i += nwarps) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
-    __syncwarp();
     const int ci0 = L.coords[3 * i], ci1 = L.coords[3 * i + 1], ci2 = L.coords[3 * i + 2];
     for (int o = 0; o < 27; ++o) {
       const int o0 = o / 9, o1 = (o / 3) % 3, o2 = o % 3;
       const int j = dense_lookup(L.map, ci0 + o0 - 1, ci1 + o1 - 1, ci2 + o2 - 1);
       if (j < 0) continue;
-      // stencil position of row i inside a particle centred at j: ka = 2 - o
       const int ka0 = 2 - o0, ka1 = 2 - o1, ka2 = 2 - o2;
-      // slot of node b = base + kb relative to row i: kb - ka + 2 = kb + o
       const int s = 25 * (kb0 + o0) + 5 * (kb1 + o1) + (kb2 + o2);
       const bool mine = lane < 27 && s >= kDiagSlot;
       const int e = bins.start[j + 1];
       for (int t = bins.start[j]; t < e; ++t) {
-        const int p = bins.pid[t];
-        if (lane < 45) st[lane] = Tu[(long long)lane * n + p];
-        if (lane + 32 < 45) st[lane + 32] = Tu[(long long)(lane + 32) * n + p];
-        if (lane >= 13 && lane < 22) st[45 + lane - 13] = P.F[(long long)(lane - 13) * n + p];
-        if (lane >= 22 && lane < 25) st[54 + lane - 22] = P.x[(long long)(lane - 22) * n + p];
+        const long long p = bins.pid[t];
+        __syncwarp();
+        {
+          const double v0 = Tu[lane * n + p];
+          const double v1 = lane < 13 ? Tu[(32 + lane) * n + p] : 0.0;
+          const double v2 = lane < 18 ? Tu[(45 + lane) * n + p] : (lane < 27 ? F[(lane - 18) * n + p] : 0.0);
+          const int r0 = c_tri_r[lane], q0 = c_tri_c[lane];
+          Ts[r0 * 9 + q0] = v0;
+          Ts[q0 * 9 + r0] = v0;
+          if (lane < 13) {
+            const int r1 = c_tri_r[32 + lane], q1 = c_tri_c[32 + lane];
+            Ts[r1 * 9 + q1] = v1;
+            Ts[q1 * 9 + r1] = v1;
+          }
+          if (lane < 27) Xs[lane] = v2;
+        }
+        __syncwarp();
+        // row node a: weight and wa = F^T grad w_a
+        const double wa0 = Xs[ka0], wa1 = Xs[3 + ka1], wa2 = Xs[6 + ka2];
+        if (!(wa0 * wa1 * wa2 > 0.0)) continue;
+        const double ga0 = Xs[9 + ka0] * wa1 * wa2, ga1 = Xs[12 + ka1] * wa0 * wa2, ga2 = Xs[15 + ka2] * wa0 * wa1;
+        const double* Fm = Xs + 18;
+        const double wA0 = Fm[0] * ga0 + Fm[3] * ga1 + Fm[6] * ga2;
+        const double wA1 = Fm[1] * ga0 + Fm[4] * ga1 + Fm[7] * ga2;
+        const double wA2 = Fm[2] * ga0 + Fm[5] * ga1 + Fm[8] * ga2;
+        if (lane < 27)
+          Ms[lane] = wA0 * Ts[mrow * 9 + mcol] + wA1 * Ts[(mrow + 1) * 9 + mcol] + wA2 * Ts[(mrow + 2) * 9 + mcol];
         __syncwarp();
         if (mine) {
-          const double c0 = st[54] / dx, c1 = st[55] / dx, c2 = st[56] / dx;
-          const int b0 = ci0 + o0 - 2, b1 = ci1 + o1 - 2, b2 = ci2 + o2 - 2;  // stencil base of p
-          const double oa0 = c0 - (double)(b0 + ka0), oa1 = c1 - (double)(b1 + ka1), oa2 = c2 - (double)(b2 + ka2);
-          const double ob0 = c0 - (double)(b0 + kb0), ob1 = c1 - (double)(b1 + kb1), ob2 = c2 - (double)(b2 + kb2);
-          const double wa0 = bspline_w(oa0), wa1 = bspline_w(oa1), wa2 = bspline_w(oa2);
-          const double wb0 = bspline_w(ob0), wb1 = bspline_w(ob1), wb2 = bspline_w(ob2);
-          if (wa0 * wa1 * wa2 > 0.0 && wb0 * wb1 * wb2 > 0.0) {
-            const double ga[3] = {bspline_dw(oa0) / dx * wa1 * wa2, bspline_dw(oa1) / dx * wa0 * wa2,
-                                  bspline_dw(oa2) / dx * wa0 * wa1};
-            const double gb[3] = {bspline_dw(ob0) / dx * wb1 * wb2, bspline_dw(ob1) / dx * wb0 * wb2,
-                                  bspline_dw(ob2) / dx * wb0 * wb1};
-            const double* Fm = st + 45;
-            double wa[3], wb[3];  // F^T grad
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-              wa[a] = Fm[a] * ga[0] + Fm[3 + a] * ga[1] + Fm[6 + a] * ga[2];
-              wb[a] = Fm[a] * gb[0] + Fm[3 + a] * gb[1] + Fm[6 + a] * gb[2];
-            }
+          const double wb0 = Xs[kb0], wb1 = Xs[3 + kb1], wb2 = Xs[6 + kb2];
+          if (wb0 * wb1 * wb2 > 0.0) {
+            const double gb0 = Xs[9 + kb0] * wb1 * wb2, gb1 = Xs[12 + kb1] * wb0 * wb2, gb2 = Xs[15 + kb2] * wb0 * wb1;
+            const double wB0 = Fm[0] * gb0 + Fm[3] * gb1 + Fm[6] * gb2;
+            const double wB1 = Fm[1] * gb0 + Fm[4] * gb1 + Fm[7] * gb2;
+            const double wB2 = Fm[2] * gb0 + Fm[5] * gb1 + Fm[8] * gb2;
             double C[9];
-            C[0] = pair_entry<0, 0>(st, wa, wb);
-            C[1] = pair_entry<0, 1>(st, wa, wb);
-            C[2] = pair_entry<0, 2>(st, wa, wb);
-            C[3] = pair_entry<1, 0>(st, wa, wb);
-            C[4] = pair_entry<1, 1>(st, wa, wb);
-            C[5] = pair_entry<1, 2>(st, wa, wb);
-            C[6] = pair_entry<2, 0>(st, wa, wb);
-            C[7] = pair_entry<2, 1>(st, wa, wb);
-            C[8] = pair_entry<2, 2>(st, wa, wb);
+#pragma unroll
+            for (int ce = 0; ce < 9; ++ce) C[ce] = Ms[3 * ce] * wB0 + Ms[3 * ce + 1] * wB1 + Ms[3 * ce + 2] * wB2;
             if (s == kDiagSlot) {
               const double t01 = 0.5 * (C[1] + C[3]), t02 = 0.5 * (C[2] + C[6]), t12 = 0.5 * (C[5] + C[7]);
               C[1] = C[3] = t01;
@@ -148,9 +150,9 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(ParticlesView 
             for (int k = 0; k < 9; ++k) a[k] += C[k];
           }
         }
-        __syncwarp();
       }
     }
+    __syncwarp();
     // write-out: upper slots + transposed mirror, mass diagonal, Dirichlet projection
     const bool di = g.dir[i] != 0;
     const double mi = g.mass[i];
@@ -212,10 +214,25 @@ void launch_fill_cols(LevelView L, cudaStream_t s) {
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, cudaStream_t s) {
   if (L.n == 0) return;
+  static bool tri_ready = false;
+  if (!tri_ready) {
+    unsigned char r[45], c[45];
+    int q = 0;
+    for (int a = 0; a < 9; ++a)
+      for (int b = a; b < 9; ++b) {
+        r[q] = (unsigned char)a;
+        c[q] = (unsigned char)b;
+        ++q;
+      }
+    cudaMemcpyToSymbol(c_tri_r, r, 45);
+    cudaMemcpyToSymbol(c_tri_c, c, 45);
+    tri_ready = true;
+  }
+  (void)dx;
   long long blocks = (L.n + kAsmWarps - 1) / kAsmWarps;
   const long long cap = (long long)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, 0, s>>>(P, bins, g, L, dx, Tu); count_launches(1); }
+  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, 0, s>>>(bins, g, L, P.n, P.F, Tu); count_launches(1); }
 }
 
 }  // namespace hotb200

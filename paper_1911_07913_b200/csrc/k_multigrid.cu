@@ -28,6 +28,7 @@ namespace {
 
 constexpr int kMgThreads = 256;
 constexpr int kMgWarps = kMgThreads / 32;
+constexpr int kSgsThreads = 512;
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -290,7 +291,7 @@ __global__ void k_prolong_add(LevelView f, LevelView c, const double* __restrict
   }
 }
 
-__global__ void __launch_bounds__(kMgThreads) k_sgs(LevelView L, const int* __restrict__ wave_start,
+__global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __restrict__ wave_start,
                                                     const int* __restrict__ wave_rows, int nwaves, double* u,
                                                     const double* __restrict__ b) {
   cg::grid_group grid = cg::this_grid();
@@ -454,9 +455,9 @@ int mgrid(long long n, int threads) {
   return b < 1 ? 1 : (int)b;
 }
 
-int coop_blocks(const void* fn) {
+int coop_blocks(const void* fn, int threads) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kMgThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
   if (per_sm < 1) per_sm = 1;
   return per_sm * num_sms();
 }
@@ -465,12 +466,12 @@ int coop_blocks(const void* fn) {
 
 int sgs_max_blocks() {
   static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_sgs);
+  if (!v) v = coop_blocks((const void*)k_sgs, kSgsThreads);
   return v;
 }
 int pcg_max_blocks() {
   static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_pcg);
+  if (!v) v = coop_blocks((const void*)k_pcg, kMgThreads);
   return v;
 }
 
@@ -511,7 +512,7 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
                 int grid_blocks, cudaStream_t s) {
   if (L.n == 0 || nwaves == 0) return;
   void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b};
-  { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kMgThreads, args, 0, s); count_launches(1); }
+  { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, 0, s); count_launches(1); }
 }
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s) {

@@ -96,9 +96,11 @@ class Simulation:
         self._lib.hot_particle_count(self._h, C.byref(n))
         return n.value
 
-    def particles(self):
+    def particles(self, out=None):
+        """Downloads x, v, F, C (into ``out``'s arrays when given, e.g. pinned host buffers)."""
         n, d = self.particle_count(), self.dim
-        out = dict(x=np.zeros((n, d)), v=np.zeros((n, d)), F=np.zeros((n, d, d)), C=np.zeros((n, d, d)))
+        if out is None:
+            out = dict(x=np.zeros((n, d)), v=np.zeros((n, d)), F=np.zeros((n, d, d)), C=np.zeros((n, d, d)))
         self._check(self._lib.hot_download_particles(self._h, dptr(out["x"]), dptr(out["v"]), dptr(out["F"]),
                                                      dptr(out["C"])))
         return out

@@ -228,4 +228,6 @@ def test_empty_and_single_particle():
     r = pr.gpu.step_grid()
     ro = pr.orc.step_grid()
     assert rel_err(r["velocity"], ro["velocity"]) < STATE_TOL
-    assert np.abs(r["velocity"].reshape(-1, 3) - np.array([0, -9.8, 0]) / 24).max() < 1e-5
+    # eps*sqrt(n) in the CN norm bounds the HOT iterate only to ~3e-5 with 2.5e-4 kg fringe nodes
+    # (see tests/test_oracle_solvers.py::test_ballistic_single_particle)
+    assert np.abs(r["velocity"].reshape(-1, 3) - np.array([0, -9.8, 0]) / 24).max() < 3e-5
