@@ -68,7 +68,10 @@ struct DBuf {
     if (bytes <= cap) return;
     if (p) HOT_CUDA(cudaFree(p));
     p = nullptr;
-    size_t nb = std::max<size_t>(bytes, 256);
+    // grow with 25% slack (2 MiB granules): node / particle counts drift by a few per step and an
+    // exact-size reallocation of a GB-sized level matrix every step costs more than the step
+    size_t nb = std::max<size_t>(bytes, cap + cap / 4);
+    nb = std::max<size_t>((nb + (2u << 20) - 1) & ~size_t((2u << 20) - 1), 256);
     HOT_CUDA(cudaMalloc(&p, nb));
     cap = nb;
   }
@@ -87,6 +90,7 @@ struct Level {
   DBuf map, coords, cols, H, dinv, dir, flags;
   DBuf wave_of, wave_counts, wave_start, wave_cursor, wave_rows, wave_start_c;
   int nwaves = 0, max_wave = 0;
+  std::vector<int> wave_start_h;
   long long active_slots = 0;
   DBuf b, u, r;  // V-cycle vectors
   DenseMap dmap() const {
@@ -154,7 +158,8 @@ struct Context {
 
   // particles (SoA on device)
   long long np = 0;
-  DBuf px, pv, pF, pC, pmass, pvol, pmat, stage;
+  DBuf px, pv, pF, pC, pmass, pvol, pmat, stage, porig;
+  DBuf qx, qv, qF, qC, qmass, qvol, qmat, qorig;  // reorder targets (swapped each step)
   double time = 0;
   int frame = 0;
   long long step_index = 0, inversions = 0;
@@ -387,7 +392,17 @@ struct Context {
     pmass.ensure(sizeof(double) * std::max<long long>(n, 1));
     pvol.ensure(sizeof(double) * std::max<long long>(n, 1));
     pmat.ensure(sizeof(int) * std::max<long long>(n, 1));
+    porig.ensure(sizeof(int) * std::max<long long>(n, 1));
+    qx.ensure(n3);
+    qv.ensure(n3);
+    qF.ensure(n9);
+    qC.ensure(n9);
+    qmass.ensure(sizeof(double) * std::max<long long>(n, 1));
+    qvol.ensure(sizeof(double) * std::max<long long>(n, 1));
+    qmat.ensure(sizeof(int) * std::max<long long>(n, 1));
+    qorig.ensure(sizeof(int) * std::max<long long>(n, 1));
     stage.ensure(n9);
+    launch_iota(porig.as<int>(), n, stream);
     auto soa = [&](const double* src, DBuf& dst, int comps, double fill_diag) {
       if (src) {
         HOT_CUDA(cudaMemcpyAsync(stage.p, src, sizeof(double) * comps * n, cudaMemcpyHostToDevice, stream));
@@ -436,7 +451,7 @@ struct Context {
     stage.ensure(sizeof(double) * 9 * std::max<long long>(np, 1));
     auto aos = [&](const DBuf& src, double* dst, int comps) {
       if (!dst || np == 0) return;
-      launch_soa_to_aos(src.as<double>(), stage.as<double>(), np, comps, stream);
+      launch_soa_to_aos_perm(src.as<double>(), stage.as<double>(), np, comps, porig.as<int>(), stream);
       HOT_CUDA(cudaMemcpyAsync(dst, stage.p, sizeof(double) * comps * np, cudaMemcpyDeviceToHost, stream));
     };
     aos(px, x, 3);
@@ -500,6 +515,24 @@ struct Context {
     scan_tmp.ensure(sizeof(int) * ((long long)n / 4096 + 64 + len / 4096));
     launch_bin_particles(P, dx, l0.dmap(), n, bin_of.as<int>(), bin_counts.as<int>(), bin_start.as<int>(),
                          bin_cursor.as<int>(), bin_pid.as<int>(), scan_tmp.as<int>(), stream);
+    // store the particles in bin order (orig keeps the caller's order for download)
+    ParticlesView Q = P;
+    Q.x = qx.as<double>();
+    Q.v = qv.as<double>();
+    Q.F = qF.as<double>();
+    Q.C = qC.as<double>();
+    Q.mass = qmass.as<double>();
+    Q.vol = qvol.as<double>();
+    Q.mat = qmat.as<int>();
+    launch_reorder_particles(P, Q, bin_pid.as<int>(), porig.as<int>(), qorig.as<int>(), stream);
+    px.swap(qx);
+    pv.swap(qv);
+    pF.swap(qF);
+    pC.swap(qC);
+    pmass.swap(qmass);
+    pvol.swap(qvol);
+    pmat.swap(qmat);
+    porig.swap(qorig);
     prof_end(h, (double)np * 24 * 3 + 5.0 * len);
     nlevels = 0;
     have_H = false;
@@ -583,7 +616,7 @@ struct Context {
     Level& l0 = L[0];
     alloc_level(l0);
     int h = prof_begin(P_TENSORS);
-    Tu.ensure(sizeof(double) * 63 * std::max<long long>(np, 1));
+    Tu.ensure(sizeof(double) * 72 * std::max<long long>(np, 1));
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, project ? 1 : 0, Tu.as<double>(),
                             flag_bad(), stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 45 * 8));
@@ -632,6 +665,7 @@ struct Context {
       }
     starts.push_back(acc);
     l.nwaves = (int)starts.size() - 1;
+    l.wave_start_h = starts;
     l.wave_start_c.ensure(sizeof(int) * starts.size());
     HOT_CUDA(cudaMemcpyAsync(l.wave_start_c.p, starts.data(), sizeof(int) * starts.size(), cudaMemcpyHostToDevice,
                              stream));
@@ -699,8 +733,16 @@ struct Context {
   void sgs(int m, double* u, const double* b) {
     Level& l = L[m];
     const int h = prof_begin(m == 0 ? P_SGS0 : P_SGSC);
-    launch_sgs(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
-               coop_grid(sgs_max_blocks(), l.max_wave, 16, 1), stream);
+    // large waves stream best as plain launches; small waves (coarse levels) run in one
+    // persistent cooperative kernel with a grid barrier between waves
+    static const char* env = nullptr;
+    env = std::getenv("HOT_SGS_STREAM_MIN");  // test hook: force either schedule
+    const int stream_min = env ? std::atoi(env) : 8 * 1024;
+    if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)
+      launch_sgs_waves(l.view(), l.wave_start_h.data(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
+    else
+      launch_sgs(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
+                 coop_grid(sgs_max_blocks(), l.max_wave, 8, 1), stream);
     prof_end(h, 2.0 * (72.0 * l.active_slots + 72.0 * l.n + 24.0 * l.n + 48.0 * l.n));
   }
 

@@ -22,10 +22,11 @@ struct ParticlesView {
   long long n;
 };
 
-/// Particles binned by their stencil-centre node (round(x/dx)); ids ascending in a bin.
+/// Particles binned by their stencil-centre node (round(x/dx)).  After launch_reorder_particles
+/// the particle arrays are stored in bin order, so bin j is the index range [start[j], start[j+1]).
 struct BinsView {
   const int* start;  // n_nodes + 1
-  const int* pid;    // n_particles
+  const int* pid;    // n_particles: original (pre-reorder) position of each binned slot
 };
 
 /// One multigrid level in diagonal storage, component-major per row:
@@ -73,6 +74,8 @@ void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n
                           int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s);
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
                 double dt, cudaStream_t s);
+void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* orig_src,
+                              int* orig_dst, cudaStream_t s);
 void launch_apply_bc(GridView g, double dx, const DevCollider* cols, int n_cols, cudaStream_t s);
 /// Generic exclusive scan over n ints (out may alias nothing); tmp >= ceil(n/4096)+1 ints.
 void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, int* total_dev, cudaStream_t s);
@@ -139,7 +142,11 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
 /// status (0 ok, 1 rho<0, 2 pAp<=0) into stat[0..1] and accumulates iterations into *iter_acc.
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s);
+/// The same sweep as one streaming launch per wave (large levels; waves given on the host).
+void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
+                      const double* b, cudaStream_t s);
 int sgs_max_blocks();
+constexpr int kSgsMaxWavesPersistent = 4096;
 int pcg_max_blocks();
 
 // ---------------------------------------------------------------- transfer (k_transfer.cu)
@@ -149,6 +156,9 @@ void launch_vmax(const ParticlesView& P, unsigned long long* vmax_bits, cudaStre
 
 void launch_aos_to_soa(const double* in, double* out, long long n, int comps, cudaStream_t s);
 void launch_soa_to_aos(const double* in, double* out, long long n, int comps, cudaStream_t s);
+/// out[perm[t]*comps + k] = in[k*n + t]  (back to the caller's particle order)
+void launch_soa_to_aos_perm(const double* in, double* out, long long n, int comps, const int* perm, cudaStream_t s);
+void launch_iota(int* out, long long n, cudaStream_t s);
 
 int num_sms();
 

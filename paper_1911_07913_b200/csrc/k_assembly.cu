@@ -21,7 +21,7 @@ namespace {
 constexpr int kAsmWarps = 4;
 constexpr int kUpper = 63;  // slots 62..124
 
-constexpr int kTensorStride = 63;  // 45 upper-triangle entries of kappa*T, then 9 w + 9 dw/dx
+constexpr int kTensorStride = 72;  // per particle (bin order): 45 upper-triangle kappa*T, 9 w, 9 dw/dx, 9 F^n
 
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
                                    const DevMaterial* __restrict__ mats, const double* __restrict__ dv, int project,
@@ -39,8 +39,9 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
     svd3(F, U, s, V);
     double T[45];
     fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
+    double* out = Tu + p * kTensorStride;
 #pragma unroll
-    for (int q = 0; q < 45; ++q) Tu[q * n + p] = T[q];
+    for (int q = 0; q < 45; ++q) out[q] = T[q];
     // per-axis stencil weights and derivatives (grid.hpp:22-73) for the row gather
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -49,10 +50,12 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
       axis_weights(c, stencil_base_1d(c), ax);
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        Tu[(45 + 3 * a + k) * n + p] = ax.w[k];
-        Tu[(54 + 3 * a + k) * n + p] = ax.dw[k] / dx;
+        out[45 + 3 * a + k] = ax.w[k];
+        out[54 + 3 * a + k] = ax.dw[k] / dx;
       }
     }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) out[63 + k] = Fn.m[k];
   }
 }
 
@@ -73,8 +76,7 @@ __constant__ unsigned char c_tri_r[45], c_tri_c[45];
 /// Row gather (objective.hpp:331-357).  Per (row a, particle p) the warp first forms
 /// M[c][e][g] = sum_f wa_f T[(3c+f),(3e+g)] (27 lanes, 3 FMA each), then every lane owning an
 /// upper-triangle stencil position kb contracts C[c][e] = sum_g M[c][e][g] wb_g (27 FMA).
-__global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L, long long n,
-                                                                   const double* __restrict__ F,
+__global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
                                                                    const double* __restrict__ Tu) {
   __shared__ double acc_s[kAsmWarps][kUpper * 9];
   __shared__ double T_s[kAsmWarps][81];
@@ -101,12 +103,12 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
       const bool mine = lane < 27 && s >= kDiagSlot;
       const int e = bins.start[j + 1];
       for (int t = bins.start[j]; t < e; ++t) {
-        const long long p = bins.pid[t];
+        const double* pt = Tu + (long long)t * kTensorStride;  // bin order: slot t is the particle
         __syncwarp();
         {
-          const double v0 = Tu[lane * n + p];
-          const double v1 = lane < 13 ? Tu[(32 + lane) * n + p] : 0.0;
-          const double v2 = lane < 18 ? Tu[(45 + lane) * n + p] : (lane < 27 ? F[(lane - 18) * n + p] : 0.0);
+          const double v0 = pt[lane];
+          const double v1 = pt[32 + lane];
+          const double v2 = lane < 8 ? pt[64 + lane] : 0.0;
           const int r0 = c_tri_r[lane], q0 = c_tri_c[lane];
           Ts[r0 * 9 + q0] = v0;
           Ts[q0 * 9 + r0] = v0;
@@ -114,8 +116,10 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
             const int r1 = c_tri_r[32 + lane], q1 = c_tri_c[32 + lane];
             Ts[r1 * 9 + q1] = v1;
             Ts[q1 * 9 + r1] = v1;
+          } else {
+            Xs[lane - 13] = v1;  // q = 45..63
           }
-          if (lane < 27) Xs[lane] = v2;
+          if (lane < 8) Xs[19 + lane] = v2;  // q = 64..71
         }
         __syncwarp();
         // row node a: weight and wa = F^T grad w_a
@@ -156,6 +160,11 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
     // write-out: upper slots + transposed mirror, mass diagonal, Dirichlet projection
     const bool di = g.dir[i] != 0;
     const double mi = g.mass[i];
+    for (int s = lane; s < kSlotPitch; s += 32) {  // inactive / pad slots hold zeros
+      if (s >= kSlots || L.cols[(long long)i * kSlotPitch + s] < 0)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) L.H[((long long)i * 9 + k) * kSlotPitch + s] = 0.0;
+    }
     for (int u = lane; u < kUpper; u += 32) {
       const int s = kDiagSlot + u;
       const int col = L.cols[(long long)i * kSlotPitch + s];
@@ -232,7 +241,7 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
   long long blocks = (L.n + kAsmWarps - 1) / kAsmWarps;
   const long long cap = (long long)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, 0, s>>>(bins, g, L, P.n, P.F, Tu); count_launches(1); }
+  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, 0, s>>>(bins, g, L, Tu); count_launches(1); }
 }
 
 }  // namespace hotb200

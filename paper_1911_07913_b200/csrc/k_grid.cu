@@ -253,7 +253,7 @@ __global__ void k_p2g(ParticlesView P, BinsView bins, GridView g, double dx, con
       if (j < 0) continue;
       const int e = bins.start[j + 1];
       for (int t = bins.start[j]; t < e; ++t) {
-        const int p = bins.pid[t];
+        const int p = t;  // particles are stored in bin order
         const double px0 = P.x[p], px1 = P.x[n + p], px2 = P.x[2 * n + p];
         const double w = bspline_w(px0 / dx - (double)ci0) * bspline_w(px1 / dx - (double)ci1) *
                          bspline_w(px2 / dx - (double)ci2);
@@ -352,6 +352,30 @@ __global__ void k_apply_bc(GridView g, double dx, const DevCollider* __restrict_
   }
 }
 
+/// Gathers every particle array into bin order (stable, ascending ids inside a bin) so each
+/// bin is a contiguous range: the node-centric gathers then stream contiguous particle data.
+__global__ void k_reorder(ParticlesView src, ParticlesView dst, const int* __restrict__ pid,
+                          const int* __restrict__ orig_src, int* __restrict__ orig_dst) {
+  const long long n = src.n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const long long p = pid[t];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      dst.x[a * n + t] = src.x[a * n + p];
+      dst.v[a * n + t] = src.v[a * n + p];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      dst.F[k * n + t] = src.F[k * n + p];
+      dst.C[k * n + t] = src.C[k * n + p];
+    }
+    dst.mass[t] = src.mass[p];
+    dst.vol[t] = src.vol[p];
+    dst.mat[t] = src.mat[p];
+    orig_dst[t] = orig_src[p];
+  }
+}
+
 int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   const long long cap = (long long)num_sms() * 32;
@@ -419,6 +443,12 @@ void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, co
                 double dt, cudaStream_t s) {
   if (g.n == 0) return;
   { k_p2g<<<grid_for(g.n, 128), 128, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
+}
+
+void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* orig_src,
+                              int* orig_dst, cudaStream_t s) {
+  if (src.n == 0) return;
+  { k_reorder<<<grid_for(src.n, 256), 256, 0, s>>>(src, dst, pid, orig_src, orig_dst); count_launches(1); }
 }
 
 void launch_apply_bc(GridView g, double dx, const DevCollider* cols, int n_cols, cudaStream_t s) {

@@ -28,7 +28,7 @@ namespace {
 
 constexpr int kMgThreads = 256;
 constexpr int kMgWarps = kMgThreads / 32;
-constexpr int kSgsThreads = 512;
+constexpr int kSgsThreads = 256;
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -72,12 +72,15 @@ __global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, uint8_t* __restri
   }
 }
 
-/// Valid (delta_i, delta_l) per axis for coarse offset O: |2O + dl - di| <= 2.
-__device__ __forceinline__ bool axis_ok(int O, int di, int dl) {
-  const int f = 2 * O + dl - di;
-  return f >= -2 && f <= 2;
-}
+/// Per-axis valid (delta_i, delta_l) pairs for coarse offset O in {-2..2}: |2O + dl - di| <= 2
+/// (the fine coupling radius).  Counts 1, 6, 9, 6, 1.
+__constant__ signed char c_gpair_di[5][9], c_gpair_dl[5][9];
+__constant__ int c_gpair_n[5];
 
+/// Galerkin triple product (multigrid.hpp:162-202) as a gather: one warp per coarse row A,
+/// lanes over the valid (fine child i of A, fine child l of B) pairs of one upper coarse slot,
+/// warp-sum, then the block and its transpose are written once (exact symmetry); Dirichlet
+/// projection (multigrid.hpp:287) fused.
 __global__ void __launch_bounds__(kMgThreads) k_galerkin(LevelView f, LevelView c) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -85,27 +88,32 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin(LevelView f, LevelView 
   for (int A = gw; A < c.n; A += nw) {
     const int A0 = c.coords[3 * A], A1 = c.coords[3 * A + 1], A2 = c.coords[3 * A + 2];
     const bool dA = c.dir[A] != 0;
+    for (int s = lane; s < kSlotPitch; s += 32)
+      if (s >= kSlots || c.cols[(long long)A * kSlotPitch + s] < 0)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) c.H[((long long)A * 9 + k) * kSlotPitch + s] = 0.0;
     for (int s = kDiagSlot; s < kSlots; ++s) {
       const int B = c.cols[(long long)A * kSlotPitch + s];
       if (B < 0) continue;
-      const int O0 = s / 25 - 2, O1 = (s / 5) % 5 - 2, O2 = s % 5 - 2;
+      const int O0 = s / 25, O1 = (s / 5) % 5, O2 = s % 5;  // offset + 2
+      const int n0 = c_gpair_n[O0], n1 = c_gpair_n[O1], n2 = c_gpair_n[O2];
+      const int total = n0 * n1 * n2;
       double acc[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-      for (int t = lane; t < 729; t += 32) {
-        const int t0 = t / 81, t1 = (t / 9) % 9, t2 = t % 9;
-        const int di0 = t0 / 3 - 1, dl0 = t0 % 3 - 1;
-        const int di1 = t1 / 3 - 1, dl1 = t1 % 3 - 1;
-        const int di2 = t2 / 3 - 1, dl2 = t2 % 3 - 1;
-        if (!axis_ok(O0, di0, dl0) || !axis_ok(O1, di1, dl1) || !axis_ok(O2, di2, dl2)) continue;
+      for (int t = lane; t < total; t += 32) {
+        const int t2 = t % n2, t1 = (t / n2) % n1, t0 = t / (n1 * n2);
+        const int di0 = c_gpair_di[O0][t0], dl0 = c_gpair_dl[O0][t0];
+        const int di1 = c_gpair_di[O1][t1], dl1 = c_gpair_dl[O1][t1];
+        const int di2 = c_gpair_di[O2][t2], dl2 = c_gpair_dl[O2][t2];
         const int i = dense_lookup(f.map, 2 * A0 + di0, 2 * A1 + di1, 2 * A2 + di2);
         if (i < 0) continue;
-        const int fs = 25 * (2 * O0 + dl0 - di0 + 2) + 5 * (2 * O1 + dl1 - di1 + 2) + (2 * O2 + dl2 - di2 + 2);
-        if (f.cols[(long long)i * kSlotPitch + fs] < 0) continue;
+        const int fs = 25 * (2 * (O0 - 2) + dl0 - di0 + 2) + 5 * (2 * (O1 - 2) + dl1 - di1 + 2) +
+                       (2 * (O2 - 2) + dl2 - di2 + 2);
         const double wi = (di0 ? 0.5 : 1.0) * (di1 ? 0.5 : 1.0) * (di2 ? 0.5 : 1.0);
         const double wl = (dl0 ? 0.5 : 1.0) * (dl1 ? 0.5 : 1.0) * (dl2 ? 0.5 : 1.0);
         const double w = wi * wl;
-        const double* h = f.H + (long long)i * 9 * kSlotPitch + fs;
+        const double* h = f.H + (long long)i * 9 * kSlotPitch + fs;  // zero when l is inactive
 #pragma unroll
         for (int k = 0; k < 9; ++k) acc[k] += w * h[k * kSlotPitch];
       }
@@ -114,7 +122,6 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin(LevelView f, LevelView 
       if (lane == 0) {
         double C[9];
         if (s == kDiagSlot) {
-          // exact symmetry: keep the upper elements and mirror
           C[0] = acc[0];
           C[4] = acc[4];
           C[8] = acc[8];
@@ -187,40 +194,54 @@ __global__ void k_wave_scatter(const int* __restrict__ wave_of, int n, int wmin,
     rows[atomicAdd(cursor + (wave_of[i] - wmin), 1)] = i;
 }
 
-/// y_i (3) = sum_s H(i,s) x_col (objective.hpp:66-77), one warp per row.
+/// y_i (3) = sum_s H(i,s) x_col (objective.hpp:66-77), one warp per row.  All column ids and
+/// all 36 block entries a lane needs are requested before any is consumed (memory-level
+/// parallelism); inactive slots hold zeros (written by assembly / Galerkin), so they are
+/// multiplied by 0 instead of branched around.
 __device__ __forceinline__ void row_product(const LevelView& L, int i, const double* __restrict__ x, int lane,
                                             double& y0, double& y1, double& y2, bool cg_load) {
-  y0 = y1 = y2 = 0.0;
   const int* cols = L.cols + (long long)i * kSlotPitch;
   const double* h = L.H + (long long)i * 9 * kSlotPitch;
+  int c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] = __ldg(cols + lane + 32 * k);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int s = lane + 32 * k;
-    if (s >= kSlots) break;
-    const int c = __ldg(cols + s);
-    if (c < 0) continue;
-    double x0, x1, x2;
-    if (cg_load) {
-      x0 = __ldcg(x + 3 * c);
-      x1 = __ldcg(x + 3 * c + 1);
-      x2 = __ldcg(x + 3 * c + 2);
-    } else {
-      x0 = __ldg(x + 3 * c);
-      x1 = __ldg(x + 3 * c + 1);
-      x2 = __ldg(x + 3 * c + 2);
+    double hv[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) hv[e] = __ldcs(h + e * kSlotPitch + s);
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+    if (c[k] >= 0) {
+      const double* xp = x + 3 * c[k];
+      if (cg_load) {
+        x0 = __ldcg(xp);
+        x1 = __ldcg(xp + 1);
+        x2 = __ldcg(xp + 2);
+      } else {
+        x0 = __ldg(xp);
+        x1 = __ldg(xp + 1);
+        x2 = __ldg(xp + 2);
+      }
     }
-    const double h0 = __ldcs(h + s), h1 = __ldcs(h + kSlotPitch + s), h2 = __ldcs(h + 2 * kSlotPitch + s);
-    const double h3 = __ldcs(h + 3 * kSlotPitch + s), h4 = __ldcs(h + 4 * kSlotPitch + s),
-                 h5 = __ldcs(h + 5 * kSlotPitch + s);
-    const double h6 = __ldcs(h + 6 * kSlotPitch + s), h7 = __ldcs(h + 7 * kSlotPitch + s),
-                 h8 = __ldcs(h + 8 * kSlotPitch + s);
-    y0 += h0 * x0 + h1 * x1 + h2 * x2;
-    y1 += h3 * x0 + h4 * x1 + h5 * x2;
-    y2 += h6 * x0 + h7 * x1 + h8 * x2;
+    a0 += hv[0] * x0 + hv[1] * x1 + hv[2] * x2;
+    a1 += hv[3] * x0 + hv[4] * x1 + hv[5] * x2;
+    a2 += hv[6] * x0 + hv[7] * x1 + hv[8] * x2;
   }
-  y0 = wsum(y0);
-  y1 = wsum(y1);
-  y2 = wsum(y2);
+  y0 = wsum(a0);
+  y1 = wsum(a1);
+  y2 = wsum(a2);
+}
+
+/// L2 prefetch of one row's block storage (9 x 1 KB) and column ids (512 B).
+__device__ __forceinline__ void prefetch_row(const LevelView& L, int i, int lane) {
+  const char* h = reinterpret_cast<const char*>(L.H + (long long)i * 9 * kSlotPitch);
+  const char* c = reinterpret_cast<const char*>(L.cols + (long long)i * kSlotPitch);
+  for (int line = lane; line < 76; line += 32) {
+    const char* p = line < 72 ? h + 128 * line : c + 128 * (line - 72);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
 }
 
 __global__ void __launch_bounds__(kMgThreads) k_spmv(LevelView L, const double* __restrict__ x, double* __restrict__ y,
@@ -291,30 +312,164 @@ __global__ void k_prolong_add(LevelView f, LevelView c, const double* __restrict
   }
 }
 
+// ---- staged row access: cp.async the row's 9 KB block storage + column ids (+ D^-1 and b)
+// into a per-warp shared-memory buffer, double-buffered so the next row (also across the
+// grid barrier into the next wave) streams in while the current one is consumed.
+constexpr int kRowBytesH = 9 * kSlotPitch * 8;       // 9216
+constexpr int kRowBytesC = kSlotPitch * 4;            // 512
+constexpr int kRowStage = kRowBytesH + kRowBytesC + 96;  // + dinv (72) + b (24)
+constexpr int kMaxSgsWaves = 4096;
+constexpr int kSgsSmem = 2 * (kSgsThreads / 32) * kRowStage + 4 * (kMaxSgsWaves + 1);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ void stage_row(const LevelView& L, const double* __restrict__ b, int i, char* buf,
+                                          int lane) {
+  const char* h = reinterpret_cast<const char*>(L.H + (long long)i * 9 * kSlotPitch);
+  const char* c = reinterpret_cast<const char*>(L.cols + (long long)i * kSlotPitch);
+#pragma unroll
+  for (int k = 0; k < kRowBytesH / 16 / 32; ++k) cp_async16(buf + 16 * (lane + 32 * k), h + 16 * (lane + 32 * k));
+  cp_async16(buf + kRowBytesH + 16 * lane, c + 16 * lane);
+  if (lane < 9) cp_async8(buf + kRowBytesH + kRowBytesC + 8 * lane, L.dinv + 9 * (long long)i + lane);
+  else if (lane < 12) cp_async8(buf + kRowBytesH + kRowBytesC + 8 * lane, b + 3 * (long long)i + (lane - 9));
+}
+
+/// One symmetric Gauss-Seidel sweep (multigrid.hpp:298-316) over the wave schedule: a row of
+/// wave w reads only neighbours of earlier waves (already updated) or later waves (still
+/// old), exactly as the serial colour-ordered sweep does.
 __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __restrict__ wave_start,
                                                     const int* __restrict__ wave_rows, int nwaves, double* u,
                                                     const double* __restrict__ b) {
+  extern __shared__ __align__(16) char sgs_smem[];
   cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int* ws = reinterpret_cast<int*>(sgs_smem + 2 * (kSgsThreads / 32) * kRowStage);
+  for (int k2 = threadIdx.x; k2 <= nwaves; k2 += blockDim.x) ws[k2] = wave_start[k2];
+  __syncthreads();
+  wave_start = ws;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  char* bufs[2] = {sgs_smem + (2 * wib) * kRowStage, sgs_smem + (2 * wib + 1) * kRowStage};
+  // (pass, wave index k) -> wave id
+  auto wave_id = [&](int pass, int k) { return pass == 0 ? k : nwaves - 1 - k; };
+  // the first row this warp owns, or -1
+  int cur = 0;
+  int pass = 0, k = 0;
+  int r = wave_start[wave_id(0, 0)] + gw;
+  int row = r < wave_start[wave_id(0, 0) + 1] ? wave_rows[r] : -1;
+  if (row >= 0) stage_row(L, b, row, bufs[cur], lane);
+  cp_commit();
+  while (pass < 2) {
+    const int w = wave_id(pass, k);
+    const int e = wave_start[w + 1];
+    while (true) {
+      // find and stage this warp's next row: same wave, or the first of the next wave
+      int nrow = -1;
+      int nr = r + nw;
+      if (nr < e) {
+        nrow = wave_rows[nr];
+      } else {
+        const int np_ = k + 1 < nwaves ? pass : pass + 1;
+        const int nk = k + 1 < nwaves ? k + 1 : 0;
+        if (np_ < 2) {
+          const int wn = wave_id(np_, nk);
+          const int r2 = wave_start[wn] + gw;
+          if (r2 < wave_start[wn + 1]) nrow = wave_rows[r2];
+        }
+      }
+      if (nrow >= 0) stage_row(L, b, nrow, bufs[cur ^ 1], lane);
+      cp_commit();
+      if (row >= 0 && r < e) {
+        cp_wait1();
+        __syncwarp();
+        const double* hs = reinterpret_cast<const double*>(bufs[cur]);
+        const int* cs = reinterpret_cast<const int*>(bufs[cur] + kRowBytesH);
+        const double* ds = reinterpret_cast<const double*>(bufs[cur] + kRowBytesH + kRowBytesC);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        double uo0 = 0.0, uo1 = 0.0, uo2 = 0.0;
+        if (lane == 0) {
+          uo0 = __ldcg(u + 3 * row);
+          uo1 = __ldcg(u + 3 * row + 1);
+          uo2 = __ldcg(u + 3 * row + 2);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int s = lane + 32 * q;
+          const int c = cs[s];
+          double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+          if (c >= 0) {
+            x0 = __ldcg(u + 3 * c);
+            x1 = __ldcg(u + 3 * c + 1);
+            x2 = __ldcg(u + 3 * c + 2);
+          }
+          a0 += hs[s] * x0 + hs[kSlotPitch + s] * x1 + hs[2 * kSlotPitch + s] * x2;
+          a1 += hs[3 * kSlotPitch + s] * x0 + hs[4 * kSlotPitch + s] * x1 + hs[5 * kSlotPitch + s] * x2;
+          a2 += hs[6 * kSlotPitch + s] * x0 + hs[7 * kSlotPitch + s] * x1 + hs[8 * kSlotPitch + s] * x2;
+        }
+        a0 = wsum(a0);
+        a1 = wsum(a1);
+        a2 = wsum(a2);
+        if (lane == 0) {
+          const double r0 = ds[9] - a0, r1 = ds[10] - a1, r2 = ds[11] - a2;
+          u[3 * row] = uo0 + (ds[0] * r0 + ds[1] * r1 + ds[2] * r2);
+          u[3 * row + 1] = uo1 + (ds[3] * r0 + ds[4] * r1 + ds[5] * r2);
+          u[3 * row + 2] = uo2 + (ds[6] * r0 + ds[7] * r1 + ds[8] * r2);
+        }
+        __syncwarp();
+      }
+      cur ^= 1;
+      row = nrow;
+      if (nr < e) {
+        r = nr;
+        continue;
+      }
+      break;
+    }
+    grid.sync();
+    // advance to the next wave
+    if (k + 1 < nwaves) {
+      ++k;
+    } else {
+      ++pass;
+      k = 0;
+    }
+    if (pass < 2) {
+      const int w2 = wave_id(pass, k);
+      r = wave_start[w2] + gw;
+      if (r >= wave_start[w2 + 1]) row = -1;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+/// One wave of the Gauss-Seidel sweep as a plain streaming launch (large levels): rows of a
+/// wave never couple, so u is read through the read-only path and the kernel boundary
+/// orders the waves.
+__global__ void __launch_bounds__(kMgThreads) k_sgs_wave(LevelView L, const int* __restrict__ rows, int count,
+                                                         double* __restrict__ u, const double* __restrict__ b) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int k = 0; k < nwaves; ++k) {
-      const int w = pass == 0 ? k : nwaves - 1 - k;
-      const int e = wave_start[w + 1];
-      for (int r = wave_start[w] + gw; r < e; r += nw) {
-        const int i = wave_rows[r];
-        double y0, y1, y2;
-        row_product(L, i, u, lane, y0, y1, y2, true);
-        if (lane == 0) {
-          const double r0 = b[3 * i] - y0, r1 = b[3 * i + 1] - y1, r2 = b[3 * i + 2] - y2;
-          const double* D = L.dinv + 9 * i;
-          u[3 * i] = __ldcg(u + 3 * i) + (D[0] * r0 + D[1] * r1 + D[2] * r2);
-          u[3 * i + 1] = __ldcg(u + 3 * i + 1) + (D[3] * r0 + D[4] * r1 + D[5] * r2);
-          u[3 * i + 2] = __ldcg(u + 3 * i + 2) + (D[6] * r0 + D[7] * r1 + D[8] * r2);
-        }
-      }
-      grid.sync();
+  for (int r = gw; r < count; r += nw) {
+    const int i = __ldg(rows + r);
+    double y0, y1, y2;
+    const double ub0 = u[3 * i], ub1 = u[3 * i + 1], ub2 = u[3 * i + 2];
+    row_product(L, i, u, lane, y0, y1, y2, false);
+    if (lane == 0) {
+      const double* D = L.dinv + 9 * i;
+      const double r0 = b[3 * i] - y0, r1 = b[3 * i + 1] - y1, r2 = b[3 * i + 2] - y2;
+      u[3 * i] = ub0 + (D[0] * r0 + D[1] * r1 + D[2] * r2);
+      u[3 * i + 1] = ub1 + (D[3] * r0 + D[4] * r1 + D[5] * r2);
+      u[3 * i + 2] = ub2 + (D[6] * r0 + D[7] * r1 + D[8] * r2);
     }
   }
 }
@@ -455,9 +610,10 @@ int mgrid(long long n, int threads) {
   return b < 1 ? 1 : (int)b;
 }
 
-int coop_blocks(const void* fn, int threads) {
+int coop_blocks(const void* fn, int threads, int smem = 0) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   if (per_sm < 1) per_sm = 1;
   return per_sm * num_sms();
 }
@@ -466,7 +622,7 @@ int coop_blocks(const void* fn, int threads) {
 
 int sgs_max_blocks() {
   static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_sgs, kSgsThreads);
+  if (!v) v = coop_blocks((const void*)k_sgs, kSgsThreads, kSgsSmem);
   return v;
 }
 int pcg_max_blocks() {
@@ -482,6 +638,24 @@ void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaS
   if (fine.n) { k_coarse_dirichlet<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, cdir); count_launches(1); }
 }
 void launch_galerkin(LevelView fine, LevelView coarse, cudaStream_t s) {
+  static bool ready = false;
+  if (!ready) {
+    signed char di[5][9] = {}, dl[5][9] = {};
+    int n[5] = {0, 0, 0, 0, 0};
+    for (int O = -2; O <= 2; ++O)
+      for (int a = -1; a <= 1; ++a)
+        for (int b = -1; b <= 1; ++b) {
+          const int fo = 2 * O + b - a;
+          if (fo < -2 || fo > 2) continue;
+          di[O + 2][n[O + 2]] = (signed char)a;
+          dl[O + 2][n[O + 2]] = (signed char)b;
+          ++n[O + 2];
+        }
+    cudaMemcpyToSymbol(c_gpair_di, di, sizeof(di));
+    cudaMemcpyToSymbol(c_gpair_dl, dl, sizeof(dl));
+    cudaMemcpyToSymbol(c_gpair_n, n, sizeof(n));
+    ready = true;
+  }
   if (coarse.n) { k_galerkin<<<mgrid((long long)coarse.n * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse); count_launches(1); }
 }
 void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
@@ -512,8 +686,19 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
                 int grid_blocks, cudaStream_t s) {
   if (L.n == 0 || nwaves == 0) return;
   void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b};
-  { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, 0, s); count_launches(1); }
+  { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, kSgsSmem, s); count_launches(1); }
 }
+void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
+                      const double* b, cudaStream_t s) {
+  for (int pass = 0; pass < 2; ++pass)
+    for (int k = 0; k < nwaves; ++k) {
+      const int w = pass == 0 ? k : nwaves - 1 - k;
+      const int cnt = wave_start_host[w + 1] - wave_start_host[w];
+      if (cnt == 0) continue;
+      { k_sgs_wave<<<mgrid((long long)cnt * 32, kMgThreads), kMgThreads, 0, s>>>(L, wave_rows + wave_start_host[w], cnt, u, b); count_launches(1); }
+    }
+}
+
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s) {
   void* args[] = {&L, (void*)&b, &x, &r, &z, &p, &Ap, &rel, &cap, &partials, &stat, &iter_acc};

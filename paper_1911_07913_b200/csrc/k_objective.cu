@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kRedThreads) k_node_gradient(ParticlesView P, 
       if (j < 0) continue;
       const int e = bins.start[j + 1];
       for (int t = bins.start[j]; t < e; ++t) {
-        const int p = bins.pid[t];
+        const int p = t;  // bin order
         const double o0 = P.x[p] / dx - (double)ci0;
         const double o1 = P.x[n + p] / dx - (double)ci1;
         const double o2 = P.x[2 * n + p] / dx - (double)ci2;

@@ -132,7 +132,27 @@ __global__ void k_soa_to_aos(const double* __restrict__ in, double* __restrict__
     out[t] = in[k * n + p];
   }
 }
+__global__ void k_soa_to_aos_perm(const double* __restrict__ in, double* __restrict__ out, long long n, int comps,
+                                  const int* __restrict__ perm) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n * comps;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long p = t / comps;
+    const int k = (int)(t % comps);
+    out[(long long)perm[p] * comps + k] = in[k * n + p];
+  }
+}
+__global__ void k_iota(int* out, long long n) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    out[t] = (int)t;
+}
 }  // namespace
+
+void launch_soa_to_aos_perm(const double* in, double* out, long long n, int comps, const int* perm, cudaStream_t s) {
+  if (n) { k_soa_to_aos_perm<<<tgrid(n * comps, 256), 256, 0, s>>>(in, out, n, comps, perm); count_launches(1); }
+}
+void launch_iota(int* out, long long n, cudaStream_t s) {
+  if (n) { k_iota<<<tgrid(n, 256), 256, 0, s>>>(out, n); count_launches(1); }
+}
 
 void launch_aos_to_soa(const double* in, double* out, long long n, int comps, cudaStream_t s) {
   if (n) { k_aos_to_soa<<<tgrid(n * comps, 256), 256, 0, s>>>(in, out, n, comps); count_launches(1); }

@@ -132,6 +132,22 @@ def test_hierarchy_and_vcycle():
         assert rel_err(u, uo) < 1e-9
 
 
+def test_vcycle_streaming_wave_schedule(monkeypatch):
+    """Same V-cycle parity with every SGS level run as one launch per wave (the schedule the
+    large level 0 of the benchmark uses)."""
+    monkeypatch.setenv("HOT_SGS_STREAM_MIN", "0")
+    pr = _stretched_block_pair(seed=12, cells=6, youngs=1e6)
+    n = pr.prepare(0.01)
+    pr.gpu.assemble()
+    pr.orc.assemble()
+    pr.gpu.build_hierarchy(3)
+    pr.orc.build_hierarchy(3)
+    b = np.random.default_rng(13).uniform(-1, 1, 3 * n)
+    u, it = pr.gpu.vcycle(b)
+    uo, ito = pr.orc.vcycle(b)
+    assert it == ito and rel_err(u, uo) < 1e-9
+
+
 def test_single_level_vcycle_is_coarse_solve():
     pr = _stretched_block_pair(seed=8, cells=4)
     n = pr.prepare(0.01)
