@@ -70,7 +70,7 @@ struct DBuf {
     p = nullptr;
     // grow with 25% slack (2 MiB granules): node / particle counts drift by a few per step and an
     // exact-size reallocation of a GB-sized level matrix every step costs more than the step
-    size_t nb = std::max<size_t>(bytes, cap + cap / 4);
+    size_t nb = std::max<size_t>(bytes + bytes / 4, cap + cap / 4);
     nb = std::max<size_t>((nb + (2u << 20) - 1) & ~size_t((2u << 20) - 1), 256);
     HOT_CUDA(cudaMalloc(&p, nb));
     cap = nb;
@@ -176,7 +176,7 @@ struct Context {
 
   // solver vectors
   DBuf dv, g, gnew, pdir, q, stress, Tu, vout, hist_s[kMaxWindow + 1], hist_y[kMaxWindow + 1];
-  DBuf pcg_r, pcg_z, pcg_p, pcg_Ap;
+  DBuf pcg_r, pcg_z, pcg_p, pcg_Ap, sgs_trace;
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
   int* host_int = nullptr;      // pinned
@@ -727,7 +727,7 @@ struct Context {
   /// participating CTAs, while one wave / one PCG row-sweep only has tens to thousands of rows.
   static int coop_grid(int max_blocks, int rows, int warps_per_block, int rows_per_warp) {
     const int want = (rows + warps_per_block * rows_per_warp - 1) / (warps_per_block * rows_per_warp);
-    return std::max(1, std::min(std::min(max_blocks, num_sms()), want));
+    return std::max(1, std::min(std::min(max_blocks, 2 * num_sms()), want));
   }
 
   void sgs(int m, double* u, const double* b) {
@@ -741,8 +741,32 @@ struct Context {
     if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)
       launch_sgs_waves(l.view(), l.wave_start_h.data(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
     else
+    {
+      long long* trace = nullptr;
+      if (std::getenv("HOT_SGS_TRACE")) {
+        sgs_trace.ensure(sizeof(long long) * 4 * 1025);
+        HOT_CUDA(cudaMemsetAsync(sgs_trace.p, 0, sizeof(long long) * 4 * 1025, stream));
+        trace = sgs_trace.as<long long>();
+      }
       launch_sgs(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
-                 coop_grid(sgs_max_blocks(), l.max_wave, 8, 1), stream);
+                 std::max(1, std::min(sgs_max_blocks(), l.max_wave)), stream, trace);
+      if (trace) {
+        std::vector<long long> t(4 * 1025);
+        HOT_CUDA(cudaMemcpy(t.data(), trace, sizeof(long long) * t.size(), cudaMemcpyDeviceToHost));
+        double stage = 0, comp = 0, tail = 0, bar = 0;
+        int nw = std::min(l.nwaves * 2, 1023);
+        for (int w = 1; w < nw; ++w) {
+          if (!t[4 * w] || !t[4 * w + 1] || !t[4 * w + 3] || !t[4 * (w + 1)]) continue;
+          stage += t[4 * w + 1] - t[4 * w];
+          tail += t[4 * w + 3] - t[4 * w + 1];
+          bar += t[4 * (w + 1)] - t[4 * w + 3];
+        }
+        const double mhz = (double)(t[4 * (nw - 1) + 2] - t[4 * 1 + 2]) / (double)(t[4 * (nw - 1) + 1] - t[4 * 1 + 1]) * 1e3;
+        std::fprintf(stderr, "[hot] sgs level %d trace over %d waves (ns/wave): post-barrier bookkeeping %.0f, "
+                     "staging wait %.0f, compute %.0f, barrier %.0f; SM clock %.0f MHz\n", m, nw, stage / nw, comp / nw,
+                     tail / nw, bar / nw, mhz);
+      }
+    }
     prof_end(h, 2.0 * (72.0 * l.active_slots + 72.0 * l.n + 24.0 * l.n + 48.0 * l.n));
   }
 

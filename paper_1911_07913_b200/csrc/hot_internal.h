@@ -137,7 +137,7 @@ void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, doub
 /// One symmetric Gauss-Seidel sweep (forward + backward over the wave schedule), as a
 /// cooperative persistent kernel with a grid barrier between waves.
 void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
-                int grid_blocks, cudaStream_t s);
+                int grid_blocks, cudaStream_t s, long long* trace = nullptr);
 /// Jacobi-PCG from zero (pcg.hpp:17-46) as one cooperative kernel; writes x, iterations,
 /// status (0 ok, 1 rho<0, 2 pAp<=0) into stat[0..1] and accumulates iterations into *iter_acc.
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,

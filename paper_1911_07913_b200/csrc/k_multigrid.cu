@@ -16,6 +16,7 @@
 //   coarse_solve/pcg   Jacobi-PCG from zero as one cooperative kernel (3 grid barriers per
 //                      iteration, deterministic block reductions).
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "hot_internal.h"
@@ -28,7 +29,7 @@ namespace {
 
 constexpr int kMgThreads = 256;
 constexpr int kMgWarps = kMgThreads / 32;
-constexpr int kSgsThreads = 256;
+constexpr int kSgsThreads = 128;  // one thread per diagonal-storage slot
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -205,6 +206,13 @@ __device__ __forceinline__ void row_product(const LevelView& L, int i, const dou
   int c[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) c[k] = __ldg(cols + lane + 32 * k);
+  double xv[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double* xp = x + 3 * (c[k] >= 0 ? c[k] : 0);  // inactive slots: zero block, any finite x
+#pragma unroll
+    for (int a = 0; a < 3; ++a) xv[k][a] = cg_load ? __ldcg(xp + a) : __ldg(xp + a);
+  }
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -212,22 +220,9 @@ __device__ __forceinline__ void row_product(const LevelView& L, int i, const dou
     double hv[9];
 #pragma unroll
     for (int e = 0; e < 9; ++e) hv[e] = __ldcs(h + e * kSlotPitch + s);
-    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-    if (c[k] >= 0) {
-      const double* xp = x + 3 * c[k];
-      if (cg_load) {
-        x0 = __ldcg(xp);
-        x1 = __ldcg(xp + 1);
-        x2 = __ldcg(xp + 2);
-      } else {
-        x0 = __ldg(xp);
-        x1 = __ldg(xp + 1);
-        x2 = __ldg(xp + 2);
-      }
-    }
-    a0 += hv[0] * x0 + hv[1] * x1 + hv[2] * x2;
-    a1 += hv[3] * x0 + hv[4] * x1 + hv[5] * x2;
-    a2 += hv[6] * x0 + hv[7] * x1 + hv[8] * x2;
+    a0 += hv[0] * xv[k][0] + hv[1] * xv[k][1] + hv[2] * xv[k][2];
+    a1 += hv[3] * xv[k][0] + hv[4] * xv[k][1] + hv[5] * xv[k][2];
+    a2 += hv[6] * xv[k][0] + hv[7] * xv[k][1] + hv[8] * xv[k][2];
   }
   y0 = wsum(a0);
   y1 = wsum(a1);
@@ -319,7 +314,7 @@ constexpr int kRowBytesH = 9 * kSlotPitch * 8;       // 9216
 constexpr int kRowBytesC = kSlotPitch * 4;            // 512
 constexpr int kRowStage = kRowBytesH + kRowBytesC + 96;  // + dinv (72) + b (24)
 constexpr int kMaxSgsWaves = 4096;
-constexpr int kSgsSmem = 2 * (kSgsThreads / 32) * kRowStage + 4 * (kMaxSgsWaves + 1);
+constexpr int kSgsSmem = 4 * (kMaxSgsWaves + 1);
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -345,110 +340,156 @@ __device__ __forceinline__ void stage_row(const LevelView& L, const double* __re
 
 /// One symmetric Gauss-Seidel sweep (multigrid.hpp:298-316) over the wave schedule: a row of
 /// wave w reads only neighbours of earlier waves (already updated) or later waves (still
-/// old), exactly as the serial colour-ordered sweep does.
+/// old), exactly as the serial colour-ordered sweep does.  Persistent cooperative kernel for
+/// the small coarse-level waves: after the wave's rows are updated each warp issues L2
+/// prefetches (fire-and-forget, so they do not queue ahead of the next gathers in the SM's
+/// load FIFO) for its row of the next wave, then the grid barrier.
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+/// Everything a row update needs except the neighbour values of u: it does not depend on the
+/// wave, so it is loaded before the grid barrier that precedes the row's wave.
+struct SgsRow {
+  int i, c;
+  double h[9];
+  double D[9], b[3], uo[3];  // thread 0 only
+};
+
+__device__ __forceinline__ void sgs_load_row(const LevelView& L, const double* __restrict__ b, const double* u,
+                                             int i, int s, SgsRow& R) {
+  R.i = i;
+  R.c = -1;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) R.h[q] = 0.0;
+  if (s >= kSlots) return;  // pad threads issue no loads (the barrier thread is one of them)
+  R.c = __ldg(L.cols + (long long)i * kSlotPitch + s);
+  const double* h = L.H + (long long)i * 9 * kSlotPitch + s;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) R.h[q] = __ldcs(h + q * kSlotPitch);  // inactive slots hold zeros
+  if (s == 0) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) R.D[q] = __ldg(L.dinv + 9 * (long long)i + q);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      R.b[a] = __ldg(b + 3 * (long long)i + a);
+      R.uo[a] = __ldcg(u + 3 * (long long)i + a);  // only row i itself ever writes u_i
+    }
+  }
+}
+
+/// Grid barrier for the cooperative SGS kernel.  The arriving thread is the CTA's last (a pad
+/// slot that never issues loads), so the release fence does not wait on the row prefetches of
+/// the other threads.  Arrival counts grow monotonically: round t completes at t * gridDim.x.
+__device__ __forceinline__ void sgs_grid_barrier(unsigned int* bar, unsigned int round) {
+  __syncthreads();
+  if (threadIdx.x == blockDim.x - 1) {
+    const unsigned int target = round * gridDim.x;
+    unsigned int prev;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(bar) : "memory");
+    if (prev == target - 1) {
+      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(bar + 1), "r"(round) : "memory");
+    } else {
+      unsigned int g;
+      do {
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      } while (g < round);
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __restrict__ wave_start,
                                                     const int* __restrict__ wave_rows, int nwaves, double* u,
-                                                    const double* __restrict__ b) {
+                                                    const double* __restrict__ b, long long* trace, int prefetch,
+                                                    unsigned int* bar) {
+  // One CTA (128 threads = one per diagonal-storage slot) per row; after the barrier only the
+  // gather of the neighbours' u (one L2 round trip), the FMA and the CTA reduction remain.
   extern __shared__ __align__(16) char sgs_smem[];
+  __shared__ double red[kSgsThreads / 32][3];
   cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  int* ws = reinterpret_cast<int*>(sgs_smem + 2 * (kSgsThreads / 32) * kRowStage);
+  const bool tr = trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
+  int* ws = reinterpret_cast<int*>(sgs_smem);
   for (int k2 = threadIdx.x; k2 <= nwaves; k2 += blockDim.x) ws[k2] = wave_start[k2];
   __syncthreads();
-  wave_start = ws;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  char* bufs[2] = {sgs_smem + (2 * wib) * kRowStage, sgs_smem + (2 * wib + 1) * kRowStage};
-  // (pass, wave index k) -> wave id
-  auto wave_id = [&](int pass, int k) { return pass == 0 ? k : nwaves - 1 - k; };
-  // the first row this warp owns, or -1
-  int cur = 0;
-  int pass = 0, k = 0;
-  int r = wave_start[wave_id(0, 0)] + gw;
-  int row = r < wave_start[wave_id(0, 0) + 1] ? wave_rows[r] : -1;
-  if (row >= 0) stage_row(L, b, row, bufs[cur], lane);
-  cp_commit();
-  while (pass < 2) {
-    const int w = wave_id(pass, k);
-    const int e = wave_start[w + 1];
-    while (true) {
-      // find and stage this warp's next row: same wave, or the first of the next wave
-      int nrow = -1;
-      int nr = r + nw;
-      if (nr < e) {
-        nrow = wave_rows[nr];
-      } else {
-        const int np_ = k + 1 < nwaves ? pass : pass + 1;
-        const int nk = k + 1 < nwaves ? k + 1 : 0;
-        if (np_ < 2) {
-          const int wn = wave_id(np_, nk);
-          const int r2 = wave_start[wn] + gw;
-          if (r2 < wave_start[wn + 1]) nrow = wave_rows[r2];
-        }
+  (void)prefetch;
+  SgsRow R;
+  bool have = false;
+  {
+    const int r0 = ws[0] + blockIdx.x;
+    if (r0 < ws[1]) {
+      sgs_load_row(L, b, u, __ldg(wave_rows + r0), s, R);
+      have = true;
+    }
+  }
+  int wave_counter = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int k = 0; k < nwaves; ++k) {
+      const int w = pass == 0 ? k : nwaves - 1 - k;
+      const int e = ws[w + 1];
+      if (tr && wave_counter < 1024) {
+        trace[4 * wave_counter + 1] = gtimer();
+        trace[4 * wave_counter + 2] = clock64();
       }
-      if (nrow >= 0) stage_row(L, b, nrow, bufs[cur ^ 1], lane);
-      cp_commit();
-      if (row >= 0 && r < e) {
-        cp_wait1();
-        __syncwarp();
-        const double* hs = reinterpret_cast<const double*>(bufs[cur]);
-        const int* cs = reinterpret_cast<const int*>(bufs[cur] + kRowBytesH);
-        const double* ds = reinterpret_cast<const double*>(bufs[cur] + kRowBytesH + kRowBytesC);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        double uo0 = 0.0, uo1 = 0.0, uo2 = 0.0;
-        if (lane == 0) {
-          uo0 = __ldcg(u + 3 * row);
-          uo1 = __ldcg(u + 3 * row + 1);
-          uo2 = __ldcg(u + 3 * row + 2);
+      for (int r = ws[w] + blockIdx.x; r < e; r += gridDim.x) {
+        if (!have) sgs_load_row(L, b, u, __ldg(wave_rows + r), s, R);
+        have = false;
+        double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+        if (s < kSlots) {
+          const double* xp = u + 3 * (R.c >= 0 ? R.c : 0);
+          x0 = __ldcg(xp);
+          x1 = __ldcg(xp + 1);
+          x2 = __ldcg(xp + 2);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int s = lane + 32 * q;
-          const int c = cs[s];
-          double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-          if (c >= 0) {
-            x0 = __ldcg(u + 3 * c);
-            x1 = __ldcg(u + 3 * c + 1);
-            x2 = __ldcg(u + 3 * c + 2);
-          }
-          a0 += hs[s] * x0 + hs[kSlotPitch + s] * x1 + hs[2 * kSlotPitch + s] * x2;
-          a1 += hs[3 * kSlotPitch + s] * x0 + hs[4 * kSlotPitch + s] * x1 + hs[5 * kSlotPitch + s] * x2;
-          a2 += hs[6 * kSlotPitch + s] * x0 + hs[7 * kSlotPitch + s] * x1 + hs[8 * kSlotPitch + s] * x2;
-        }
+        double a0 = R.h[0] * x0 + R.h[1] * x1 + R.h[2] * x2;
+        double a1 = R.h[3] * x0 + R.h[4] * x1 + R.h[5] * x2;
+        double a2 = R.h[6] * x0 + R.h[7] * x1 + R.h[8] * x2;
         a0 = wsum(a0);
         a1 = wsum(a1);
         a2 = wsum(a2);
         if (lane == 0) {
-          const double r0 = ds[9] - a0, r1 = ds[10] - a1, r2 = ds[11] - a2;
-          u[3 * row] = uo0 + (ds[0] * r0 + ds[1] * r1 + ds[2] * r2);
-          u[3 * row + 1] = uo1 + (ds[3] * r0 + ds[4] * r1 + ds[5] * r2);
-          u[3 * row + 2] = uo2 + (ds[6] * r0 + ds[7] * r1 + ds[8] * r2);
+          red[wid][0] = a0;
+          red[wid][1] = a1;
+          red[wid][2] = a2;
         }
-        __syncwarp();
+        __syncthreads();
+        if (s == 0) {
+          double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int q = 0; q < kSgsThreads / 32; ++q) {
+            y0 += red[q][0];
+            y1 += red[q][1];
+            y2 += red[q][2];
+          }
+          const double r0 = R.b[0] - y0, r1 = R.b[1] - y1, r2 = R.b[2] - y2;
+          const int i = R.i;
+          u[3 * i] = R.uo[0] + (R.D[0] * r0 + R.D[1] * r1 + R.D[2] * r2);
+          u[3 * i + 1] = R.uo[1] + (R.D[3] * r0 + R.D[4] * r1 + R.D[5] * r2);
+          u[3 * i + 2] = R.uo[2] + (R.D[6] * r0 + R.D[7] * r1 + R.D[8] * r2);
+        }
+        __syncthreads();
       }
-      cur ^= 1;
-      row = nrow;
-      if (nr < e) {
-        r = nr;
-        continue;
+      if (tr && wave_counter < 1024) trace[4 * wave_counter + 3] = gtimer();
+      {  // prepare this CTA's first row of the next wave
+        const int np_ = k + 1 < nwaves ? pass : pass + 1;
+        const int nk = k + 1 < nwaves ? k + 1 : 0;
+        if (np_ < 2) {
+          const int wn = np_ == 0 ? nk : nwaves - 1 - nk;
+          const int rn = ws[wn] + blockIdx.x;
+          if (rn < ws[wn + 1]) {
+            sgs_load_row(L, b, u, __ldg(wave_rows + rn), s, R);
+            have = true;
+          }
+        }
       }
-      break;
-    }
-    grid.sync();
-    // advance to the next wave
-    if (k + 1 < nwaves) {
-      ++k;
-    } else {
-      ++pass;
-      k = 0;
-    }
-    if (pass < 2) {
-      const int w2 = wave_id(pass, k);
-      r = wave_start[w2] + gw;
-      if (r >= wave_start[w2 + 1]) row = -1;
+      sgs_grid_barrier(bar, (unsigned int)(wave_counter + 1));
+      if (tr && wave_counter < 1024) trace[4 * (wave_counter + 1)] = gtimer();
+      ++wave_counter;
     }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 /// One wave of the Gauss-Seidel sweep as a plain streaming launch (large levels): rows of a
@@ -683,9 +724,14 @@ void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, doub
   if (fine.n) { k_prolong_add<<<mgrid(fine.n, 128), 128, 0, s>>>(fine, coarse, uc, uf); count_launches(1); }
 }
 void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
-                int grid_blocks, cudaStream_t s) {
+                int grid_blocks, cudaStream_t s, long long* trace) {
   if (L.n == 0 || nwaves == 0) return;
-  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b};
+  static const int prefetch = std::getenv("HOT_SGS_NOPREFETCH") ? 0 : 1;
+  int pf = prefetch;
+  static unsigned int* bar = nullptr;
+  if (!bar) cudaMalloc(&bar, 2 * sizeof(unsigned int));
+  cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
+  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &trace, &pf, &bar};
   { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, kSgsSmem, s); count_launches(1); }
 }
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
