@@ -21,7 +21,7 @@ namespace {
 constexpr int kAsmWarps = 4;
 constexpr int kUpper = 63;  // slots 62..124
 
-constexpr int kTensorStride = 72;  // per particle (bin order): 45 upper-triangle kappa*T, 9 w, 9 dw/dx, 9 F^n
+constexpr int kTensorStride = 162;  // per particle (bin order): kappa*T (81, full symmetric), W (27 x 3): W_k = F^nT grad w_k (0 where w_k = 0)
 
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
                                    const DevMaterial* __restrict__ mats, const double* __restrict__ dv, int project,
@@ -40,22 +40,38 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
     double T[45];
     fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
     double* out = Tu + p * kTensorStride;
+    {
+      int q = 0;
 #pragma unroll
-    for (int q = 0; q < 45; ++q) out[q] = T[q];
-    // per-axis stencil weights and derivatives (grid.hpp:22-73) for the row gather
+      for (int r = 0; r < 9; ++r)
+#pragma unroll
+        for (int c = r; c < 9; ++c) {
+          out[r * 9 + c] = T[q];
+          out[c * 9 + r] = T[q];
+          ++q;
+        }
+    }
+    // W_k = F^nT grad w_k for the 27 stencil nodes (grid.hpp:58-73, objective.hpp:337-339); nodes
+    // with zero weight get W = 0, which is how the reference skips them (transfer.hpp:36-37)
+    Axis3 ax[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double c = P.x[a * n + p] / dx;
-      Axis3 ax;
-      axis_weights(c, stencil_base_1d(c), ax);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        out[45 + 3 * a + k] = ax.w[k];
-        out[54 + 3 * a + k] = ax.dw[k] / dx;
-      }
+      axis_weights(c, stencil_base_1d(c), ax[a]);
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) out[63 + k] = Fn.m[k];
+    for (int k = 0; k < 27; ++k) {
+      const int k0 = k / 9, k1 = (k / 3) % 3, k2 = k % 3;
+      const double w0 = ax[0].w[k0], w1 = ax[1].w[k1], w2 = ax[2].w[k2];
+      double W[3] = {0.0, 0.0, 0.0};
+      if (w0 * w1 * w2 > 0.0) {
+        const double g0 = ax[0].dw[k0] / dx * w1 * w2, g1 = ax[1].dw[k1] / dx * w0 * w2, g2 = ax[2].dw[k2] / dx * w0 * w1;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) W[q] = Fn.m[q] * g0 + Fn.m[3 + q] * g1 + Fn.m[6 + q] * g2;
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) out[81 + 3 * k + q] = W[q];
+    }
   }
 }
 
@@ -71,25 +87,30 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
   }
 }
 
-__constant__ unsigned char c_tri_r[45], c_tri_c[45];
-
 /// Row gather (objective.hpp:331-357).  Per (row a, particle p) the warp first forms
 /// M[c][e][g] = sum_f wa_f T[(3c+f),(3e+g)] (27 lanes, 3 FMA each), then every lane owning an
 /// upper-triangle stencil position kb contracts C[c][e] = sum_g M[c][e][g] wb_g (27 FMA).
+/// A bin's particles are contiguous (bin order), so they are staged in chunks with cp.async,
+/// and within a bin a lane's target slot is fixed: its block accumulates in registers and is
+/// folded into the row's shared-memory accumulator once per bin.
+constexpr int kAsmChunk = 4;
+
+__device__ __forceinline__ void asm_cp16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+
 __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
                                                                    const double* __restrict__ Tu) {
   __shared__ double acc_s[kAsmWarps][kUpper * 9];
-  __shared__ double T_s[kAsmWarps][81];
-  __shared__ double X_s[kAsmWarps][28];  // w[9], dwdx[9], F[9]
-  __shared__ double M_s[kAsmWarps][28];
+  __shared__ __align__(16) double S_s[kAsmWarps][kAsmChunk * kTensorStride];  // T | w | dw/dx | F per particle
+  __shared__ __align__(16) double M_s[kAsmWarps][36];                          // M[ce][g], g padded to 4
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* acc = acc_s[wid];
-  double* Ts = T_s[wid];
-  double* Xs = X_s[wid];
   double* Ms = M_s[wid];
   const int kb0 = lane / 9, kb1 = (lane / 3) % 3, kb2 = lane % 3;
-  // lane's M entry (c,e,g) = (kb0,kb1,kb2): T indices for f = 0..2
-  const int mrow = 3 * kb0, mcol = 3 * kb1 + kb2;
+  const int tb = 27 * kb0 + 3 * kb1 + kb2;  // lane's M entry (c,e,g) reads T[(3c+f)*9 + 3e+g]
+  const int mslot = 4 * (3 * kb0 + kb1) + kb2;
   const int nwarps = gridDim.x * kAsmWarps;
   for (int i = blockIdx.x * kAsmWarps + wid; i < L.n; i += nwarps) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
@@ -98,62 +119,52 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
       const int o0 = o / 9, o1 = (o / 3) % 3, o2 = o % 3;
       const int j = dense_lookup(L.map, ci0 + o0 - 1, ci1 + o1 - 1, ci2 + o2 - 1);
       if (j < 0) continue;
-      const int ka0 = 2 - o0, ka1 = 2 - o1, ka2 = 2 - o2;
+      const int ka3 = 3 * (9 * (2 - o0) + 3 * (2 - o1) + (2 - o2));
       const int s = 25 * (kb0 + o0) + 5 * (kb1 + o1) + (kb2 + o2);
       const bool mine = lane < 27 && s >= kDiagSlot;
-      const int e = bins.start[j + 1];
-      for (int t = bins.start[j]; t < e; ++t) {
-        const double* pt = Tu + (long long)t * kTensorStride;  // bin order: slot t is the particle
+      double Cr[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Cr[k] = 0.0;
+      const int pb = bins.start[j], pe = bins.start[j + 1];
+      for (int c0 = pb; c0 < pe; c0 += kAsmChunk) {
+        const int cnt = min(kAsmChunk, pe - c0);
         __syncwarp();
         {
-          const double v0 = pt[lane];
-          const double v1 = pt[32 + lane];
-          const double v2 = lane < 8 ? pt[64 + lane] : 0.0;
-          const int r0 = c_tri_r[lane], q0 = c_tri_c[lane];
-          Ts[r0 * 9 + q0] = v0;
-          Ts[q0 * 9 + r0] = v0;
-          if (lane < 13) {
-            const int r1 = c_tri_r[32 + lane], q1 = c_tri_c[32 + lane];
-            Ts[r1 * 9 + q1] = v1;
-            Ts[q1 * 9 + r1] = v1;
-          } else {
-            Xs[lane - 13] = v1;  // q = 45..63
-          }
-          if (lane < 8) Xs[19 + lane] = v2;  // q = 64..71
+          const char* src = reinterpret_cast<const char*>(Tu + (long long)c0 * kTensorStride);
+          char* dst = reinterpret_cast<char*>(S_s[wid]);
+          const int chunks = cnt * kTensorStride * 8 / 16;
+          for (int q = lane; q < chunks; q += 32) asm_cp16(dst + 16 * q, src + 16 * q);
+          asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
         }
         __syncwarp();
-        // row node a: weight and wa = F^T grad w_a
-        const double wa0 = Xs[ka0], wa1 = Xs[3 + ka1], wa2 = Xs[6 + ka2];
-        if (!(wa0 * wa1 * wa2 > 0.0)) continue;
-        const double ga0 = Xs[9 + ka0] * wa1 * wa2, ga1 = Xs[12 + ka1] * wa0 * wa2, ga2 = Xs[15 + ka2] * wa0 * wa1;
-        const double* Fm = Xs + 18;
-        const double wA0 = Fm[0] * ga0 + Fm[3] * ga1 + Fm[6] * ga2;
-        const double wA1 = Fm[1] * ga0 + Fm[4] * ga1 + Fm[7] * ga2;
-        const double wA2 = Fm[2] * ga0 + Fm[5] * ga1 + Fm[8] * ga2;
-        if (lane < 27)
-          Ms[lane] = wA0 * Ts[mrow * 9 + mcol] + wA1 * Ts[(mrow + 1) * 9 + mcol] + wA2 * Ts[(mrow + 2) * 9 + mcol];
-        __syncwarp();
-        if (mine) {
-          const double wb0 = Xs[kb0], wb1 = Xs[3 + kb1], wb2 = Xs[6 + kb2];
-          if (wb0 * wb1 * wb2 > 0.0) {
-            const double gb0 = Xs[9 + kb0] * wb1 * wb2, gb1 = Xs[12 + kb1] * wb0 * wb2, gb2 = Xs[15 + kb2] * wb0 * wb1;
-            const double wB0 = Fm[0] * gb0 + Fm[3] * gb1 + Fm[6] * gb2;
-            const double wB1 = Fm[1] * gb0 + Fm[4] * gb1 + Fm[7] * gb2;
-            const double wB2 = Fm[2] * gb0 + Fm[5] * gb1 + Fm[8] * gb2;
-            double C[9];
+        for (int t = 0; t < cnt; ++t) {
+          const double* Ts = S_s[wid] + t * kTensorStride;
+          const double* Ws = Ts + 81;
+          const double wA0 = Ws[ka3], wA1 = Ws[ka3 + 1], wA2 = Ws[ka3 + 2];  // zero when w_a = 0
+          __syncwarp();
+          if (lane < 27) Ms[mslot] = wA0 * Ts[tb] + wA1 * Ts[tb + 9] + wA2 * Ts[tb + 18];
+          __syncwarp();
+          if (mine) {
+            const double wB0 = Ws[3 * lane], wB1 = Ws[3 * lane + 1], wB2 = Ws[3 * lane + 2];
 #pragma unroll
-            for (int ce = 0; ce < 9; ++ce) C[ce] = Ms[3 * ce] * wB0 + Ms[3 * ce + 1] * wB1 + Ms[3 * ce + 2] * wB2;
-            if (s == kDiagSlot) {
-              const double t01 = 0.5 * (C[1] + C[3]), t02 = 0.5 * (C[2] + C[6]), t12 = 0.5 * (C[5] + C[7]);
-              C[1] = C[3] = t01;
-              C[2] = C[6] = t02;
-              C[5] = C[7] = t12;
+            for (int ce = 0; ce < 9; ++ce) {
+              const double2 m01 = *reinterpret_cast<const double2*>(Ms + 4 * ce);
+              const double m2 = Ms[4 * ce + 2];
+              Cr[ce] += m01.x * wB0 + m01.y * wB1 + m2 * wB2;
             }
-            double* a = acc + (s - kDiagSlot) * 9;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) a[k] += C[k];
           }
         }
+      }
+      if (mine) {
+        if (s == kDiagSlot) {  // symmetrise the diagonal contribution (objective.hpp:349-351)
+          const double t01 = 0.5 * (Cr[1] + Cr[3]), t02 = 0.5 * (Cr[2] + Cr[6]), t12 = 0.5 * (Cr[5] + Cr[7]);
+          Cr[1] = Cr[3] = t01;
+          Cr[2] = Cr[6] = t02;
+          Cr[5] = Cr[7] = t12;
+        }
+        double* ap = acc + (s - kDiagSlot) * 9;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) ap[k] += Cr[k];
       }
     }
     __syncwarp();
@@ -223,20 +234,6 @@ void launch_fill_cols(LevelView L, cudaStream_t s) {
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, cudaStream_t s) {
   if (L.n == 0) return;
-  static bool tri_ready = false;
-  if (!tri_ready) {
-    unsigned char r[45], c[45];
-    int q = 0;
-    for (int a = 0; a < 9; ++a)
-      for (int b = a; b < 9; ++b) {
-        r[q] = (unsigned char)a;
-        c[q] = (unsigned char)b;
-        ++q;
-      }
-    cudaMemcpyToSymbol(c_tri_r, r, 45);
-    cudaMemcpyToSymbol(c_tri_c, c, 45);
-    tri_ready = true;
-  }
   (void)dx;
   long long blocks = (L.n + kAsmWarps - 1) / kAsmWarps;
   const long long cap = (long long)num_sms() * 16;
