@@ -30,6 +30,9 @@ import numpy as np  # noqa: E402
 
 SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
+FP64_PEAK_TFLOPS = 34.79  # DFMA throughput measured on this pool's B200 (profiles/r01_fp64_peak.json)
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
+TRAFFIC = {}
 UNIT = "particle-steps/s"
 
 
@@ -55,7 +58,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -127,7 +130,7 @@ def run_cpu_reference(sc, particles, steps, warmup, threads, frac_x=0.05):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scene", default=SCENE)
@@ -249,19 +252,28 @@ def main():
         e2e_ms = float(t.item())
     e2e_value = n_particles * world * e2e_steps / (e2e_ms / 1000.0)
 
-    # ---- roofline of the dominant HBM-bound phase (algorithmic bytes / event-timed duration)
+    # ---- rooflines (algorithmic bytes or flops / CUDA-event duration on the context stream)
     peaks, peak_kind = measured_peaks()
     hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
-                  k in ("sgs_level0", "sgs_coarse", "residual_restrict", "p2g_bc", "node_gradient", "lbfgs_vectors",
-                        "g2p_strain_advect", "assemble_rows", "prolong")}
+                  k in ("sgs_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
+                        "lbfgs_vectors")}
+    # the north star's HBM-bound smoother / SpMV / P2G class: report the largest by time
     top = max(hbm_phases, key=lambda k: hbm_phases[k]["ms"]) if hbm_phases else None
     roofline = None
     if top:
         ph = hbm_phases[top]
         achieved = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
         roofline = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
-                    "share_of_step": ph["ms"] / ms, "launches": ph["launches"]}
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": TRAFFIC.get(top), "peak_kind": peak_kind,
+                    "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                    "bytes_per_launch": ph["bytes"] / max(ph["launches"], 1)}
+    roofline_fp64 = None
+    if "assemble_rows" in prof and prof["assemble_rows"]["ms"] > 0:
+        ph = prof["assemble_rows"]
+        ach = ph["flops"] / (ph["ms"] / 1000.0) / 1e12
+        roofline_fp64 = {"bound": "fp64", "kernel": "assemble_rows", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "share_of_step": ph["ms"] / ms,
+                         "peak_kind": "measured (profiles/r01_fp64_peak.json, tools/microbench/fp64peak.cu)"}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -281,7 +293,8 @@ def main():
                                outer_iterations=outer, phase_ms_per_step=phases),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps},
-                "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu_baseline,
+                "gpu_launches": int(launches), "roofline": roofline, "roofline_fp64": roofline_fp64,
+                "cpu_baseline": cpu_baseline,
                 "clocks": clocks.summary()}
         print(json.dumps(line))
     sim.close()

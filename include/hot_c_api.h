@@ -182,7 +182,9 @@ int hot_stage_step_grid(hot_ctx* ctx, double* velocity, double* dv, int* outer, 
 void* hot_stream(hot_ctx* ctx);
 /* Per-phase device timing (CUDA events on the context stream). enable=1 starts/resets. */
 int hot_profile_enable(hot_ctx* ctx, int enable);
-/* Fills up to cap (name, total_ms, launches, bytes) records; returns count in *n. */
+/* Fills up to cap (name, total_ms, launches, bytes) records; returns count in *n.  bytes are
+ * algorithmic HBM bytes; a negative value is minus the algorithmic fp64 flop count of an
+ * ALU-bound phase (the level-0 assembly). */
 int hot_profile_read(hot_ctx* ctx, char* names /* cap*32 */, double* total_ms, long long* launches,
                      double* bytes, int cap, int* n);
 /* Kernel launches issued by this context since creation (all phases). */

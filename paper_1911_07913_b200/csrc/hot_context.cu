@@ -187,6 +187,7 @@ struct Context {
   std::vector<ProfEvent> events;
   std::vector<cudaEvent_t> event_pool;
   double phase_bytes[kPhases] = {0};
+  double phase_flops[kPhases] = {0};
 
   Context() = default;
   ~Context() {
@@ -249,10 +250,11 @@ struct Context {
     events.push_back(pe);
     return (int)events.size() - 1;
   }
-  void prof_end(int h, double bytes = 0) {
+  void prof_end(int h, double bytes = 0, double flops = 0) {
     if (h < 0) return;
     cudaEventRecord(events[h].b, stream);
     phase_bytes[events[h].phase] += bytes;
+    phase_flops[events[h].phase] += flops;
   }
   void sync() { HOT_CUDA(cudaStreamSynchronize(stream)); }
   void check_launch() {
@@ -543,7 +545,7 @@ struct Context {
     launch_p2g(pview(), bview(), gview(), dx, mats_d.as<DevMaterial>(), cn_factor * dx * dx, dt, stream);
     launch_apply_bc(gview(), dx, cols_d.as<DevCollider>(), (int)cols_h.size(), stream);
     (void)time_now;
-    prof_end(h, (double)np * 128 + (double)L[0].n * 64);
+    prof_end(h, (double)np * 136 + (double)L[0].n * 88);  // x v C m mat | mass mom vel cn dir bc
   }
 
   void ensure_solver_buffers() {
@@ -623,7 +625,8 @@ struct Context {
     h = prof_begin(P_ASSEMBLE);
     launch_fill_cols(l0.view(), stream);
     launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), stream);
-    prof_end(h, (double)l0.n * 9 * kSlots * 8);
+    // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
+    prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
     have_H = true;
     nlevels = 1;
   }
@@ -782,7 +785,7 @@ struct Context {
       const int h = prof_begin(P_RESID);
       launch_residual(l.view(), l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
       launch_restrict(l.view(), L[m + 1].view(), l.r.as<double>(), L[m + 1].b.as<double>(), stream);
-      prof_end(h, 72.0 * l.active_slots + 72.0 * l.n + 24.0 * L[m + 1].n);
+      prof_end(h, 72.0 * l.active_slots + 72.0 * l.n + 48.0 * L[m + 1].n);  // H, u b r (3 x 24 R), restrict
     }
     Level& bot = L[M - 1];
     {
@@ -1013,7 +1016,7 @@ struct Context {
     const int h = prof_begin(P_G2P);
     HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 6, 0, sizeof(int), stream));
     launch_g2p_strain_advect(pview(), gview(), dx, dtn, mats_d.as<DevMaterial>(), iflags.as<int>() + 6, stream);
-    prof_end(h, (double)np * (24 + 24 + 72 + 72 + 4 + 24 + 96));
+    prof_end(h, (double)np * (24 + 24 + 72 + 72 + 4 + 24 + 96) + 24.0 * L[0].n);
     int inv = 0;
     HOT_CUDA(cudaMemcpyAsync(&inv, iflags.as<int>() + 6, sizeof(int), cudaMemcpyDeviceToHost, stream));
     sync();
@@ -1426,7 +1429,7 @@ int hot_profile_read(hot_ctx* ctx, char* names, double* total_ms, long long* lau
       std::snprintf(names + 32 * i, 32, "%s", hotb200::kPhaseNames[i]);
       total_ms[i] = ms[i];
       launches[i] = cnt[i];
-      bytes[i] = c.phase_bytes[i];
+      bytes[i] = c.phase_bytes[i] > 0 ? c.phase_bytes[i] : -c.phase_flops[i];  // < 0: fp64 flops
     }
     *n = k;
   });

@@ -240,7 +240,8 @@ class Simulation:
         out = {}
         for i in range(n.value):
             name = names.raw[32 * i:32 * (i + 1)].split(b"\0", 1)[0].decode()
-            out[name] = dict(ms=ms[i], launches=launches[i], bytes=bytes_[i])
+            b = bytes_[i]
+            out[name] = dict(ms=ms[i], launches=launches[i], bytes=max(b, 0.0), flops=max(-b, 0.0))
         return out
 
     def kernel_launches(self):
