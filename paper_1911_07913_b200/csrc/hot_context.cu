@@ -176,7 +176,7 @@ struct Context {
 
   // solver vectors
   DBuf dv, g, gnew, pdir, q, stress, Tu, vout, hist_s[kMaxWindow + 1], hist_y[kMaxWindow + 1];
-  DBuf pcg_r, pcg_z, pcg_p, pcg_Ap, sgs_trace;
+  DBuf pcg_r, pcg_z, pcg_p, pcg_Ap, sgs_trace, gal_x;
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
   int* host_int = nullptr;      // pinned
@@ -710,7 +710,8 @@ struct Context {
       HOT_CUDA(cudaMemsetAsync(c.dir.p, 0, nc, stream));
       launch_coarse_dirichlet(f.view(), c.dmap(), c.dir.as<uint8_t>(), stream);
       launch_fill_cols(c.view(), stream);
-      launch_galerkin(f.view(), c.view(), stream);
+      gal_x.ensure(sizeof(double) * 64 * 9 * std::max(f.n, 1));
+      launch_galerkin(f.view(), c.view(), gal_x.as<double>(), stream);
       check_launch();
       nlevels = m + 1;
       finalize(m);
@@ -741,7 +742,11 @@ struct Context {
     static const char* env = nullptr;
     env = std::getenv("HOT_SGS_STREAM_MIN");  // test hook: force either schedule
     const int stream_min = env ? std::atoi(env) : 8 * 1024;
-    if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)
+    const char* sched = std::getenv("HOT_SGS_LEVEL0");  // "waves" | "stream" (default)
+    const bool per_wave = sched && std::strcmp(sched, "waves") == 0;
+    if (l.max_wave >= stream_min && !per_wave)
+      launch_sgs_stream(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
+    else if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)
       launch_sgs_waves(l.view(), l.wave_start_h.data(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
     else
     {

@@ -124,7 +124,8 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
 // ---------------------------------------------------------------- multigrid (k_multigrid.cu)
 void launch_mark_parents(LevelView fine, DenseMap cmap, uint8_t* flags, cudaStream_t s);
 void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaStream_t s);
-void launch_galerkin(LevelView fine, LevelView coarse, cudaStream_t s);
+/// X: scratch of 64*9 doubles per fine row.
+void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s);
 /// diag inverse, singular check, wave id per row (level 0: colour mod 3; coarse: wavefront).
 void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
                            cudaStream_t s);
@@ -143,6 +144,9 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s);
 /// The same sweep as one streaming launch per wave (large levels; waves given on the host).
+/// Level-0 smoother: both passes, all waves, one persistent kernel with bulk-copy row streaming.
+void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
+                       const double* b, cudaStream_t s);
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s);
 int sgs_max_blocks();

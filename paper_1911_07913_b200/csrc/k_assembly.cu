@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
     for (int s = lane; s < kSlotPitch; s += 32) {  // inactive / pad slots hold zeros
       if (s >= kSlots || L.cols[(long long)i * kSlotPitch + s] < 0)
 #pragma unroll
-        for (int k = 0; k < 9; ++k) L.H[((long long)i * 9 + k) * kSlotPitch + s] = 0.0;
+        for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + s, 0.0);
     }
     for (int u = lane; u < kUpper; u += 32) {
       const int s = kDiagSlot + u;
@@ -198,13 +198,13 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
         for (int k = 0; k < 9; ++k) C[k] = 0.0;
       }
 #pragma unroll
-      for (int k = 0; k < 9; ++k) L.H[((long long)i * 9 + k) * kSlotPitch + s] = C[k];
+      for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + s, C[k]);
       if (s != kDiagSlot) {
         const int sm = kSlots - 1 - s;
 #pragma unroll
         for (int r = 0; r < 3; ++r)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) L.H[((long long)col * 9 + 3 * r + c) * kSlotPitch + sm] = C[3 * c + r];
+          for (int c = 0; c < 3; ++c) __stcs(L.H + ((long long)col * 9 + 3 * r + c) * kSlotPitch + sm, C[3 * c + r]);
       }
     }
     __syncwarp();

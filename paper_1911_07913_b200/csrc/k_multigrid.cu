@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kMgThreads = 256;
 constexpr int kMgWarps = kMgThreads / 32;
+constexpr int kUpper = 63;
 constexpr int kSgsThreads = 128;  // one thread per diagonal-storage slot
 
 __device__ __forceinline__ double wsum(double v) {
@@ -73,80 +74,127 @@ __global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, uint8_t* __restri
   }
 }
 
-/// Per-axis valid (delta_i, delta_l) pairs for coarse offset O in {-2..2}: |2O + dl - di| <= 2
-/// (the fine coupling radius).  Counts 1, 6, 9, 6, 1.
-__constant__ signed char c_gpair_di[5][9], c_gpair_dl[5][9];
-__constant__ int c_gpair_n[5];
+/// Galerkin triple product H_c = R H_f R^T (multigrid.hpp:162-202) in two gathers, each
+/// fine block read once:
+///   X[i][B] = sum_{l in ch(B)} w_lB H_f(i,l)        one warp per fine row, its 9 KB row staged
+///                                                  in shared memory; 64 coarse targets
+///                                                  B = floor(i/2) - 1 + [0,4)^3 per row
+///   H_c(A,B) = sum_{i in ch(A)} w_iA X[i][B]        one thread per upper coarse block, then the
+///                                                  block and its transpose are written once
+/// (exact symmetry); Dirichlet projection (multigrid.hpp:287) fused.  Linear embedding: child
+/// 2B+d of B has weight prod_a (d_a ? 1/2 : 1).
+constexpr int kGalX = 64 * 9;  // doubles of X per fine row
+constexpr int kGalXWarps = 4;
 
-/// Galerkin triple product (multigrid.hpp:162-202) as a gather: one warp per coarse row A,
-/// lanes over the valid (fine child i of A, fine child l of B) pairs of one upper coarse slot,
-/// warp-sum, then the block and its transpose are written once (exact symmetry); Dirichlet
-/// projection (multigrid.hpp:287) fused.
-__global__ void __launch_bounds__(kMgThreads) k_galerkin(LevelView f, LevelView c) {
+__global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, double* __restrict__ X) {
+  __shared__ double hs[kGalXWarps][9 * kSlotPitch];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  double* H = hs[wib];
+  for (int i = gw; i < f.n; i += nw) {
+    const double* src = f.H + (long long)i * 9 * kSlotPitch;
+    __syncwarp();
+    for (int q = lane; q < 9 * kSlotPitch; q += 32) H[q] = __ldcs(src + q);
+    __syncwarp();
+    int base[3];  // 2*(floor(c/2)-1) - c: -2 (even) or -3 (odd)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int c = f.coords[3 * i + a];
+      base[a] = 2 * ((c >> 1) - 1) - c;
+    }
+    for (int tq = lane; tq < 64; tq += 32) {
+      const int t0 = tq >> 4, t1 = (tq >> 2) & 3, t2 = tq & 3;
+      double acc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+#pragma unroll
+      for (int d0 = -1; d0 <= 1; ++d0) {
+        const int f0 = 2 * t0 + d0 + base[0];
+        if (f0 < -2 || f0 > 2) continue;
+#pragma unroll
+        for (int d1 = -1; d1 <= 1; ++d1) {
+          const int f1 = 2 * t1 + d1 + base[1];
+          if (f1 < -2 || f1 > 2) continue;
+#pragma unroll
+          for (int d2 = -1; d2 <= 1; ++d2) {
+            const int f2 = 2 * t2 + d2 + base[2];
+            if (f2 < -2 || f2 > 2) continue;
+            const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
+            const int s = 25 * (f0 + 2) + 5 * (f1 + 2) + (f2 + 2);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[k] += w * H[k * kSlotPitch + s];  // zero when l is inactive
+          }
+        }
+      }
+      double* dst = X + (long long)i * kGalX + 9 * tq;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dst[k] = acc[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kMgThreads) k_galerkin_c(LevelView f, LevelView c, const double* __restrict__ X) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int A = gw; A < c.n; A += nw) {
     const int A0 = c.coords[3 * A], A1 = c.coords[3 * A + 1], A2 = c.coords[3 * A + 2];
     const bool dA = c.dir[A] != 0;
+    // children of A (fine nodes 2A + d) and their X base offsets
+    int ch[27];
+#pragma unroll
+    for (int t = 0; t < 27; ++t) ch[t] = dense_lookup(f.map, 2 * A0 + t / 9 - 1, 2 * A1 + (t / 3) % 3 - 1, 2 * A2 + t % 3 - 1);
     for (int s = lane; s < kSlotPitch; s += 32)
       if (s >= kSlots || c.cols[(long long)A * kSlotPitch + s] < 0)
 #pragma unroll
-        for (int k = 0; k < 9; ++k) c.H[((long long)A * 9 + k) * kSlotPitch + s] = 0.0;
-    for (int s = kDiagSlot; s < kSlots; ++s) {
+        for (int k = 0; k < 9; ++k) __stcs(c.H + ((long long)A * 9 + k) * kSlotPitch + s, 0.0);
+    for (int u = lane; u < kUpper; u += 32) {
+      const int s = kDiagSlot + u;
       const int B = c.cols[(long long)A * kSlotPitch + s];
       if (B < 0) continue;
-      const int O0 = s / 25, O1 = (s / 5) % 5, O2 = s % 5;  // offset + 2
-      const int n0 = c_gpair_n[O0], n1 = c_gpair_n[O1], n2 = c_gpair_n[O2];
-      const int total = n0 * n1 * n2;
+      const int O0 = s / 25 - 2, O1 = (s / 5) % 5 - 2, O2 = s % 5 - 2;
       double acc[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-      for (int t = lane; t < total; t += 32) {
-        const int t2 = t % n2, t1 = (t / n2) % n1, t0 = t / (n1 * n2);
-        const int di0 = c_gpair_di[O0][t0], dl0 = c_gpair_dl[O0][t0];
-        const int di1 = c_gpair_di[O1][t1], dl1 = c_gpair_dl[O1][t1];
-        const int di2 = c_gpair_di[O2][t2], dl2 = c_gpair_dl[O2][t2];
-        const int i = dense_lookup(f.map, 2 * A0 + di0, 2 * A1 + di1, 2 * A2 + di2);
-        if (i < 0) continue;
-        const int fs = 25 * (2 * (O0 - 2) + dl0 - di0 + 2) + 5 * (2 * (O1 - 2) + dl1 - di1 + 2) +
-                       (2 * (O2 - 2) + dl2 - di2 + 2);
-        const double wi = (di0 ? 0.5 : 1.0) * (di1 ? 0.5 : 1.0) * (di2 ? 0.5 : 1.0);
-        const double wl = (dl0 ? 0.5 : 1.0) * (dl1 ? 0.5 : 1.0) * (dl2 ? 0.5 : 1.0);
-        const double w = wi * wl;
-        const double* h = f.H + (long long)i * 9 * kSlotPitch + fs;  // zero when l is inactive
 #pragma unroll
-        for (int k = 0; k < 9; ++k) acc[k] += w * h[k * kSlotPitch];
+      for (int t = 0; t < 27; ++t) {
+        const int i = ch[t];
+        if (i < 0) continue;
+        const int d0 = t / 9 - 1, d1 = (t / 3) % 3 - 1, d2 = t % 3 - 1;
+        // B - (floor(i/2) - 1) per axis; floor((2A+d)/2) = A + (d < 0 ? -1 : 0)
+        const int q0 = O0 + 1 - (d0 < 0 ? -1 : 0), q1 = O1 + 1 - (d1 < 0 ? -1 : 0), q2 = O2 + 1 - (d2 < 0 ? -1 : 0);
+        if ((unsigned)q0 > 3u || (unsigned)q1 > 3u || (unsigned)q2 > 3u) continue;
+        const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
+        const double* x = X + (long long)i * kGalX + 9 * (16 * q0 + 4 * q1 + q2);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] += w * __ldg(x + k);
+      }
+      double C[9];
+      if (s == kDiagSlot) {
+        C[0] = acc[0];
+        C[4] = acc[4];
+        C[8] = acc[8];
+        C[1] = C[3] = acc[1];
+        C[2] = C[6] = acc[2];
+        C[5] = C[7] = acc[5];
+        if (dA) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) C[k] = (k % 4 == 0) ? 1.0 : 0.0;
+        }
+      } else {
+        const bool zero = dA || c.dir[B] != 0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) C[k] = zero ? 0.0 : acc[k];
       }
 #pragma unroll
-      for (int k = 0; k < 9; ++k) acc[k] = wsum(acc[k]);
-      if (lane == 0) {
-        double C[9];
-        if (s == kDiagSlot) {
-          C[0] = acc[0];
-          C[4] = acc[4];
-          C[8] = acc[8];
-          C[1] = C[3] = acc[1];
-          C[2] = C[6] = acc[2];
-          C[5] = C[7] = acc[5];
-          if (dA) {
+      for (int k = 0; k < 9; ++k) __stcs(c.H + ((long long)A * 9 + k) * kSlotPitch + s, C[k]);
+      if (s != kDiagSlot) {
+        const int sm = kSlots - 1 - s;
 #pragma unroll
-            for (int k = 0; k < 9; ++k) C[k] = (k % 4 == 0) ? 1.0 : 0.0;
-          }
-        } else {
-          const bool zero = dA || c.dir[B] != 0;
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-          for (int k = 0; k < 9; ++k) C[k] = zero ? 0.0 : acc[k];
-        }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) c.H[((long long)A * 9 + k) * kSlotPitch + s] = C[k];
-        if (s != kDiagSlot) {
-          const int sm = kSlots - 1 - s;
-#pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) c.H[((long long)B * 9 + 3 * r + q) * kSlotPitch + sm] = C[3 * q + r];
-        }
+          for (int q = 0; q < 3; ++q) __stcs(c.H + ((long long)B * 9 + 3 * r + q) * kSlotPitch + sm, C[3 * q + r]);
       }
     }
   }
@@ -495,22 +543,211 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __r
 /// One wave of the Gauss-Seidel sweep as a plain streaming launch (large levels): rows of a
 /// wave never couple, so u is read through the read-only path and the kernel boundary
 /// orders the waves.
-__global__ void __launch_bounds__(kMgThreads) k_sgs_wave(LevelView L, const int* __restrict__ rows, int count,
-                                                         double* __restrict__ u, const double* __restrict__ b) {
+/// One Gauss-Seidel wave (rows of one colour class; no two couple), one warp per row.
+/// Launched with programmatic dependent launch: the row's 9 KB of blocks and its column ids do
+/// not depend on the previous wave, so they are loaded into registers BEFORE
+/// griddepcontrol.wait and stream in while the previous wave drains; only the u gathers (L2,
+/// ld.cg: written by the previous wave) and b, dinv wait.
+constexpr int kWaveThreads = 128;
+__global__ void __launch_bounds__(kWaveThreads) k_sgs_wave(LevelView L, const int* __restrict__ rows, int count,
+                                                           double* __restrict__ u, const double* __restrict__ b,
+                                                           int pdl) {
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = gw; r < count; r += nw) {
-    const int i = __ldg(rows + r);
-    double y0, y1, y2;
-    const double ub0 = u[3 * i], ub1 = u[3 * i + 1], ub2 = u[3 * i + 2];
-    row_product(L, i, u, lane, y0, y1, y2, false);
-    if (lane == 0) {
-      const double* D = L.dinv + 9 * i;
-      const double r0 = b[3 * i] - y0, r1 = b[3 * i + 1] - y1, r2 = b[3 * i + 2] - y2;
-      u[3 * i] = ub0 + (D[0] * r0 + D[1] * r1 + D[2] * r2);
-      u[3 * i + 1] = ub1 + (D[3] * r0 + D[4] * r1 + D[5] * r2);
-      u[3 * i + 2] = ub2 + (D[6] * r0 + D[7] * r1 + D[8] * r2);
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool live = r < count;
+  const int i = live ? __ldg(rows + r) : 0;
+  int c[4];
+  double hv[4][9];
+  if (live) {
+    const int* cols = L.cols + (long long)i * kSlotPitch;
+    const double* h = L.H + (long long)i * 9 * kSlotPitch;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = __ldg(cols + lane + 32 * k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int e = 0; e < 9; ++e) hv[k][e] = __ldcs(h + e * kSlotPitch + lane + 32 * k);
+  }
+  if (pdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  if (!live) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double* xp = u + 3 * (c[k] >= 0 ? c[k] : 0);  // inactive slots: zero block
+    const double x0 = __ldcg(xp), x1 = __ldcg(xp + 1), x2 = __ldcg(xp + 2);
+    a0 += hv[k][0] * x0 + hv[k][1] * x1 + hv[k][2] * x2;
+    a1 += hv[k][3] * x0 + hv[k][4] * x1 + hv[k][5] * x2;
+    a2 += hv[k][6] * x0 + hv[k][7] * x1 + hv[k][8] * x2;
+  }
+  const double y0 = wsum(a0), y1 = wsum(a1), y2 = wsum(a2);
+  if (lane == 0) {
+    const double* D = L.dinv + 9 * i;
+    const double ub0 = __ldcg(u + 3 * i), ub1 = __ldcg(u + 3 * i + 1), ub2 = __ldcg(u + 3 * i + 2);
+    const double r0 = __ldcg(b + 3 * i) - y0, r1 = __ldcg(b + 3 * i + 1) - y1, r2 = __ldcg(b + 3 * i + 2) - y2;
+    u[3 * i] = ub0 + (D[0] * r0 + D[1] * r1 + D[2] * r2);
+    u[3 * i + 1] = ub1 + (D[3] * r0 + D[4] * r1 + D[5] * r2);
+    u[3 * i + 2] = ub2 + (D[6] * r0 + D[7] * r1 + D[8] * r2);
+  }
+}
+
+/// Level-0 symmetric Gauss-Seidel, all waves of both passes in ONE persistent cooperative
+/// kernel (one CTA per SM).  Each warp owns a ring of kStreamStages row buffers in shared memory
+/// filled by the bulk-copy engine (cp.async.bulk, completion on an mbarrier): a row's blocks
+/// (9 KB) and column ids (512 B) are contiguous in the diagonal storage, so one row = two bulk
+/// copies, issued by lane 0 and bypassing the L1 miss path.  The producer walks the warp's
+/// flat (wave, row) sequence kStreamStages rows ahead of the consumer, ACROSS wave boundaries:
+/// blocks and columns do not depend on u, so HBM streaming never drains at the grid barrier
+/// between waves; only the u gathers (ld.cg, L2) wait for it.  Row arithmetic is identical to
+/// k_sgs_wave (same summation order).
+constexpr int kStreamWarps = 8;
+constexpr int kStreamStages = 2;
+constexpr int kStreamRowBytes = 9 * kSlotPitch * 8 + kSlotPitch * 4;  // 9728
+constexpr int kStreamSmem = kStreamWarps * kStreamStages * kStreamRowBytes + kStreamWarps * kStreamStages * 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+struct StreamCursor {  // position in a warp's flat (wave, row) sequence
+  int q, m;           // q: 0..2*nwaves-1 (forward then backward), m: this warp's m-th row of wave w(q)
+};
+
+__global__ void __launch_bounds__(kStreamWarps * 32, 1)
+    k_sgs_stream(LevelView L, const int* __restrict__ wave_start, const int* __restrict__ wave_rows, int nwaves,
+                 double* u, const double* __restrict__ b, unsigned int* bar) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kStreamWarps + wib, nw = gridDim.x * kStreamWarps;
+  unsigned char* ring = sm_raw + (size_t)wib * kStreamStages * kStreamRowBytes;
+  unsigned long long* mb =
+      reinterpret_cast<unsigned long long*>(sm_raw + (size_t)kStreamWarps * kStreamStages * kStreamRowBytes) +
+      wib * kStreamStages;
+  const int nq = 2 * nwaves;
+  auto wave_of = [&](int q) { return q < nwaves ? q : nq - 1 - q; };
+  auto count_of = [&](int q) {
+    const int w = wave_of(q);
+    return __ldg(wave_start + w + 1) - __ldg(wave_start + w);
+  };
+  // advance a cursor to the next existing row of this warp (or q == nq)
+  auto settle = [&](StreamCursor& c) {
+    while (c.q < nq && gw + c.m * nw >= count_of(c.q)) {
+      ++c.q;
+      c.m = 0;
+    }
+  };
+  unsigned long long policy = 0;
+  if (lane == 0) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    for (int s = 0; s < kStreamStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb + s)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](const StreamCursor& c, int stage) {
+    const int w = wave_of(c.q);
+    const int i = __ldg(wave_rows + __ldg(wave_start + w) + gw + c.m * nw);
+    unsigned char* dst = ring + (size_t)stage * kStreamRowBytes;
+    const unsigned mbar = smem_u32(mb + stage);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(kStreamRowBytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(L.H + (long long)i * 9 * kSlotPitch), "r"(9 * kSlotPitch * 8), "r"(mbar), "l"(policy)
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst + 9 * kSlotPitch * 8)),
+        "l"(L.cols + (long long)i * kSlotPitch), "r"(kSlotPitch * 4), "r"(mbar), "l"(policy)
+        : "memory");
+    return i;
+  };
+  // prologue: fill the ring
+  StreamCursor prod{0, 0};
+  settle(prod);
+  int rowid[kStreamStages];
+  for (int s = 0; s < kStreamStages; ++s) {
+    rowid[s] = -1;
+    if (prod.q < nq) {
+      int i = 0;
+      if (lane == 0) i = issue(prod, s);
+      rowid[s] = __shfl_sync(0xffffffffu, i, 0);
+      ++prod.m;
+      settle(prod);
+    }
+  }
+  int stage = 0;
+  unsigned phase_bits = 0;  // bit s: parity to wait for on stage s
+  for (int q = 0; q < nq; ++q) {
+    if (q > 0) sgs_grid_barrier(bar, (unsigned int)q);
+    const int cnt = count_of(q);
+    for (int r = gw; r < cnt; r += nw) {
+      const int i = rowid[stage];
+      mbar_wait(smem_u32(mb + stage), (phase_bits >> stage) & 1u);
+      phase_bits ^= 1u << stage;
+      const double* H = reinterpret_cast<const double*>(ring + (size_t)stage * kStreamRowBytes);
+      const int* cols = reinterpret_cast<const int*>(ring + (size_t)stage * kStreamRowBytes + 9 * kSlotPitch * 8);
+      int c[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) c[k] = cols[lane + 32 * k];
+      double xv[4][3];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double* xp = u + 3 * (c[k] >= 0 ? c[k] : 0);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) xv[k][a] = __ldcg(xp + a);
+      }
+      double D[9], rb[3], ub[3];
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) D[k] = __ldg(L.dinv + 9 * i + k);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          rb[a] = __ldg(b + 3 * i + a);
+          ub[a] = __ldcg(u + 3 * i + a);
+        }
+      }
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int s = lane + 32 * k;
+        double hv[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) hv[e] = H[e * kSlotPitch + s];
+        a0 += hv[0] * xv[k][0] + hv[1] * xv[k][1] + hv[2] * xv[k][2];
+        a1 += hv[3] * xv[k][0] + hv[4] * xv[k][1] + hv[5] * xv[k][2];
+        a2 += hv[6] * xv[k][0] + hv[7] * xv[k][1] + hv[8] * xv[k][2];
+      }
+      __syncwarp();  // all lanes are done with this stage's shared memory
+      if (prod.q < nq) {
+        int ni = 0;
+        if (lane == 0) ni = issue(prod, stage);
+        rowid[stage] = __shfl_sync(0xffffffffu, ni, 0);
+        ++prod.m;
+        settle(prod);
+      }
+      const double y0 = wsum(a0), y1 = wsum(a1), y2 = wsum(a2);
+      if (lane == 0) {
+        const double r0 = rb[0] - y0, r1 = rb[1] - y1, r2 = rb[2] - y2;
+        u[3 * i] = ub[0] + (D[0] * r0 + D[1] * r1 + D[2] * r2);
+        u[3 * i + 1] = ub[1] + (D[3] * r0 + D[4] * r1 + D[5] * r2);
+        u[3 * i + 2] = ub[2] + (D[6] * r0 + D[7] * r1 + D[8] * r2);
+      }
+      stage = stage + 1 == kStreamStages ? 0 : stage + 1;
     }
   }
 }
@@ -678,26 +915,10 @@ void launch_mark_parents(LevelView fine, DenseMap cmap, uint8_t* flags, cudaStre
 void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaStream_t s) {
   if (fine.n) { k_coarse_dirichlet<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, cdir); count_launches(1); }
 }
-void launch_galerkin(LevelView fine, LevelView coarse, cudaStream_t s) {
-  static bool ready = false;
-  if (!ready) {
-    signed char di[5][9] = {}, dl[5][9] = {};
-    int n[5] = {0, 0, 0, 0, 0};
-    for (int O = -2; O <= 2; ++O)
-      for (int a = -1; a <= 1; ++a)
-        for (int b = -1; b <= 1; ++b) {
-          const int fo = 2 * O + b - a;
-          if (fo < -2 || fo > 2) continue;
-          di[O + 2][n[O + 2]] = (signed char)a;
-          dl[O + 2][n[O + 2]] = (signed char)b;
-          ++n[O + 2];
-        }
-    cudaMemcpyToSymbol(c_gpair_di, di, sizeof(di));
-    cudaMemcpyToSymbol(c_gpair_dl, dl, sizeof(dl));
-    cudaMemcpyToSymbol(c_gpair_n, n, sizeof(n));
-    ready = true;
-  }
-  if (coarse.n) { k_galerkin<<<mgrid((long long)coarse.n * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse); count_launches(1); }
+void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s) {
+  if (coarse.n == 0) return;
+  { k_galerkin_x<<<mgrid((long long)fine.n * 32, kGalXWarps * 32), kGalXWarps * 32, 0, s>>>(fine, X); count_launches(1); }
+  { k_galerkin_c<<<mgrid((long long)coarse.n * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X); count_launches(1); }
 }
 void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
                            cudaStream_t s) {
@@ -734,14 +955,49 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
   void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &trace, &pf, &bar};
   { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, kSgsSmem, s); count_launches(1); }
 }
+
+int sgs_stream_blocks() {
+  static int blocks = 0;
+  if (!blocks) {
+    cudaFuncSetAttribute((const void*)k_sgs_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_sgs_stream, kStreamWarps * 32, kStreamSmem);
+    blocks = std::max(1, per_sm) * num_sms();
+  }
+  return blocks;
+}
+
+void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
+                       const double* b, cudaStream_t s) {
+  if (L.n == 0 || nwaves == 0) return;
+  static unsigned int* bar = nullptr;
+  if (!bar) cudaMalloc(&bar, 2 * sizeof(unsigned int));
+  cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
+  int grid = sgs_stream_blocks();
+  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar};
+  { cudaLaunchCooperativeKernel((const void*)k_sgs_stream, grid, kStreamWarps * 32, args, kStreamSmem, s); count_launches(1); }
+}
+
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s) {
+  static const int pdl = std::getenv("HOT_SGS_NOPDL") ? 0 : 1;
   for (int pass = 0; pass < 2; ++pass)
     for (int k = 0; k < nwaves; ++k) {
       const int w = pass == 0 ? k : nwaves - 1 - k;
       const int cnt = wave_start_host[w + 1] - wave_start_host[w];
       if (cnt == 0) continue;
-      { k_sgs_wave<<<mgrid((long long)cnt * 32, kMgThreads), kMgThreads, 0, s>>>(L, wave_rows + wave_start_host[w], cnt, u, b); count_launches(1); }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)((cnt + kWaveThreads / 32 - 1) / (kWaveThreads / 32)));
+      cfg.blockDim = dim3(kWaveThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl ? 1 : 0;
+      const int* rw = wave_rows + wave_start_host[w];
+      cudaLaunchKernelEx(&cfg, k_sgs_wave, L, rw, cnt, u, b, pdl);
+      count_launches(1);
     }
 }
 

@@ -132,10 +132,13 @@ def test_hierarchy_and_vcycle():
         assert rel_err(u, uo) < 1e-9
 
 
-def test_vcycle_streaming_wave_schedule(monkeypatch):
-    """Same V-cycle parity with every SGS level run as one launch per wave (the schedule the
-    large level 0 of the benchmark uses)."""
+@pytest.mark.parametrize("schedule", ["stream", "waves"])
+def test_vcycle_streaming_wave_schedule(monkeypatch, schedule):
+    """Same V-cycle parity with every SGS level run on the large-wave schedules the benchmark's
+    level 0 uses: the persistent bulk-copy streaming kernel, or one launch per wave.  Both
+    compute every row with the same arithmetic, so they agree bit for bit."""
     monkeypatch.setenv("HOT_SGS_STREAM_MIN", "0")
+    monkeypatch.setenv("HOT_SGS_LEVEL0", schedule)
     pr = _stretched_block_pair(seed=12, cells=6, youngs=1e6)
     n = pr.prepare(0.01)
     pr.gpu.assemble()
@@ -146,6 +149,9 @@ def test_vcycle_streaming_wave_schedule(monkeypatch):
     u, it = pr.gpu.vcycle(b)
     uo, ito = pr.orc.vcycle(b)
     assert it == ito and rel_err(u, uo) < 1e-9
+    monkeypatch.setenv("HOT_SGS_LEVEL0", "waves" if schedule == "stream" else "stream")
+    u2, it2 = pr.gpu.vcycle(b)
+    assert it2 == it and np.array_equal(u, u2)
 
 
 def test_single_level_vcycle_is_coarse_solve():
