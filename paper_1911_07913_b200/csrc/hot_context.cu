@@ -618,7 +618,7 @@ struct Context {
     Level& l0 = L[0];
     alloc_level(l0);
     int h = prof_begin(P_TENSORS);
-    Tu.ensure(sizeof(double) * 162 * std::max<long long>(np, 1));
+    Tu.ensure(sizeof(double) * 126 * std::max<long long>(np, 1));
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, project ? 1 : 0, Tu.as<double>(),
                             flag_bad(), stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 45 * 8));

@@ -11,6 +11,10 @@
 //   projection (objective.hpp:133-144) are fused into the write-out.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
+#include "hot_async.cuh"
 #include "hot_internal.h"
 #include "hot_particle.cuh"
 
@@ -21,7 +25,10 @@ namespace {
 constexpr int kAsmWarps = 4;
 constexpr int kUpper = 63;  // slots 62..124
 
-constexpr int kTensorStride = 162;  // per particle (bin order): kappa*T (81, full symmetric), W (27 x 3): W_k = F^nT grad w_k (0 where w_k = 0)
+/// Per particle (bin order): kappa*T as its 45-entry upper triangle (row-major, T is symmetric),
+/// then W (27 x 3): W_k = F^nT grad w_k (0 where w_k = 0).  1008 B = 63 x 16 B.
+constexpr int kTPacked = 45;
+constexpr int kTensorStride = kTPacked + 81;
 
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
                                    const DevMaterial* __restrict__ mats, const double* __restrict__ dv, int project,
@@ -40,17 +47,8 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
     double T[45];
     fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
     double* out = Tu + p * kTensorStride;
-    {
-      int q = 0;
 #pragma unroll
-      for (int r = 0; r < 9; ++r)
-#pragma unroll
-        for (int c = r; c < 9; ++c) {
-          out[r * 9 + c] = T[q];
-          out[c * 9 + r] = T[q];
-          ++q;
-        }
-    }
+    for (int q = 0; q < kTPacked; ++q) out[q] = T[q];
     // W_k = F^nT grad w_k for the 27 stencil nodes (grid.hpp:58-73, objective.hpp:337-339); nodes
     // with zero weight get W = 0, which is how the reference skips them (transfer.hpp:36-37)
     Axis3 ax[3];
@@ -70,7 +68,7 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
         for (int q = 0; q < 3; ++q) W[q] = Fn.m[q] * g0 + Fn.m[3 + q] * g1 + Fn.m[6 + q] * g2;
       }
 #pragma unroll
-      for (int q = 0; q < 3; ++q) out[81 + 3 * k + q] = W[q];
+      for (int q = 0; q < 3; ++q) out[kTPacked + 3 * k + q] = W[q];
     }
   }
 }
@@ -87,86 +85,196 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
   }
 }
 
-/// Row gather (objective.hpp:331-357).  Per (row a, particle p) the warp first forms
-/// M[c][e][g] = sum_f wa_f T[(3c+f),(3e+g)] (27 lanes, 3 FMA each), then every lane owning an
-/// upper-triangle stencil position kb contracts C[c][e] = sum_g M[c][e][g] wb_g (27 FMA).
-/// A bin's particles are contiguous (bin order), so they are staged in chunks with cp.async,
-/// and within a bin a lane's target slot is fixed: its block accumulates in registers and is
-/// folded into the row's shared-memory accumulator once per bin.
-constexpr int kAsmChunk = 4;
+/// Row gather (objective.hpp:331-357), one warp per row i.  For a particle p of a bin whose
+/// stencil holds i at position a, the warp forms M[c][e][g] = sum_f W_a[f] T[(3c+f),(3e+g)]
+/// (lane (c,e,g) < 27, 3 FMA) and a lane owning stencil position k contracts the upper-triangle
+/// block C[c][e] += sum_g M[c][e][g] W_k[g] (27 FMA).
+///
+/// Lane utilisation: in one bin only about half of the 27 stencil positions are upper-triangle
+/// slots of row i.  Bin offset o and its mirror 2-o are complementary: position k is lower in
+/// bin o exactly when position 26-k is upper in bin 2-o (slot s -> 124-s).  So the warp walks
+/// the 13 mirror pairs (+ the centre bin): lane k works on bin o if its slot is upper, else on
+/// the mirror bin at 26-k; lane 27 takes the mirror bin's diagonal block (both bins own one).
+/// Both bins' particles are staged together by the bulk-copy engine (one cp.async.bulk per bin
+/// chunk, mbarrier completion, double buffered one chunk ahead).  Each (pair, lane) block
+/// accumulates in registers and is folded into the row's shared accumulator once per pair
+/// (bin o's lanes, then the mirror's: fixed order, no atomics).
+constexpr int kAsmChunk = 2;                                  // particles per bin per stage
+constexpr int kAsmStage = 2 * kAsmChunk * kTensorStride;       // doubles: [bin of pair][particle][...]
+constexpr int kAsmWarpDoubles = 2 * kAsmStage + 2 * 2 * 28 + kUpper * 9 + 1 + 2;  // + 2 mbarriers; even
+constexpr int kAsmSmem = kAsmWarps * kAsmWarpDoubles * 8;
+constexpr unsigned kParticleBytes = kTensorStride * 8;  // 1008 = 63 x 16
+static_assert(kAsmWarpDoubles % 2 == 0, "16-byte aligned per-warp smem");
 
-__device__ __forceinline__ void asm_cp16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ int tpack(int r, int c) {  // index of T[r][c] in the packed upper triangle
+  if (r > c) {
+    const int t = r;
+    r = c;
+    c = t;
+  }
+  return r * 9 - r * (r - 1) / 2 + (c - r);
 }
 
 __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
                                                                    const double* __restrict__ Tu) {
-  __shared__ double acc_s[kAsmWarps][kUpper * 9];
-  __shared__ __align__(16) double S_s[kAsmWarps][kAsmChunk * kTensorStride];  // T | w | dw/dx | F per particle
-  __shared__ __align__(16) double M_s[kAsmWarps][36];                          // M[ce][g], g padded to 4
+  extern __shared__ __align__(16) double asm_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* acc = acc_s[wid];
-  double* Ms = M_s[wid];
-  const int kb0 = lane / 9, kb1 = (lane / 3) % 3, kb2 = lane % 3;
-  const int tb = 27 * kb0 + 3 * kb1 + kb2;  // lane's M entry (c,e,g) reads T[(3c+f)*9 + 3e+g]
-  const int mslot = 4 * (3 * kb0 + kb1) + kb2;
+  // per warp: staging [2 buffers][kAsmStage] | M [2 parity][2 bins][28] | acc [kUpper*9] | mbarriers [2]
+  double* base = asm_smem + (size_t)wid * kAsmWarpDoubles;
+  double* Sbuf = base;
+  double* Mbuf = base + 2 * kAsmStage;
+  double* acc = Mbuf + 2 * 2 * 28;
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(acc + kUpper * 9 + 1);
+  if (lane == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(mbar + 1, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  unsigned phase = 0;  // bit b: parity of the next completion of buffer b
+  // lane's M entry (c,e,g) = lane: packed T indices of T[(3c+f),(3e+g)], f = 0..2
+  const int lc = lane / 9, le = (lane / 3) % 3, lg = lane % 3;
+  const int tp0 = lane < 27 ? tpack(3 * lc, 3 * le + lg) : 0;
+  const int tp1 = lane < 27 ? tpack(3 * lc + 1, 3 * le + lg) : 0;
+  const int tp2 = lane < 27 ? tpack(3 * lc + 2, 3 * le + lg) : 0;
   const int nwarps = gridDim.x * kAsmWarps;
   for (int i = blockIdx.x * kAsmWarps + wid; i < L.n; i += nwarps) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
     const int ci0 = L.coords[3 * i], ci1 = L.coords[3 * i + 1], ci2 = L.coords[3 * i + 2];
-    for (int o = 0; o < 27; ++o) {
-      const int o0 = o / 9, o1 = (o / 3) % 3, o2 = o % 3;
-      const int j = dense_lookup(L.map, ci0 + o0 - 1, ci1 + o1 - 1, ci2 + o2 - 1);
-      if (j < 0) continue;
-      const int ka3 = 3 * (9 * (2 - o0) + 3 * (2 - o1) + (2 - o2));
-      const int s = 25 * (kb0 + o0) + 5 * (kb1 + o1) + (kb2 + o2);
-      const bool mine = lane < 27 && s >= kDiagSlot;
-      double Cr[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) Cr[k] = 0.0;
-      const int pb = bins.start[j], pe = bins.start[j + 1];
-      for (int c0 = pb; c0 < pe; c0 += kAsmChunk) {
-        const int cnt = min(kAsmChunk, pe - c0);
-        __syncwarp();
-        {
-          const char* src = reinterpret_cast<const char*>(Tu + (long long)c0 * kTensorStride);
-          char* dst = reinterpret_cast<char*>(S_s[wid]);
-          const int chunks = cnt * kTensorStride * 8 / 16;
-          for (int q = lane; q < chunks; q += 32) asm_cp16(dst + 16 * q, src + 16 * q);
-          asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        }
-        __syncwarp();
-        for (int t = 0; t < cnt; ++t) {
-          const double* Ts = S_s[wid] + t * kTensorStride;
-          const double* Ws = Ts + 81;
-          const double wA0 = Ws[ka3], wA1 = Ws[ka3 + 1], wA2 = Ws[ka3 + 2];  // zero when w_a = 0
-          __syncwarp();
-          if (lane < 27) Ms[mslot] = wA0 * Ts[tb] + wA1 * Ts[tb + 9] + wA2 * Ts[tb + 18];
-          __syncwarp();
-          if (mine) {
-            const double wB0 = Ws[3 * lane], wB1 = Ws[3 * lane + 1], wB2 = Ws[3 * lane + 2];
-#pragma unroll
-            for (int ce = 0; ce < 9; ++ce) {
-              const double2 m01 = *reinterpret_cast<const double2*>(Ms + 4 * ce);
-              const double m2 = Ms[4 * ce + 2];
-              Cr[ce] += m01.x * wB0 + m01.y * wB1 + m2 * wB2;
-            }
-          }
-        }
-      }
-      if (mine) {
-        if (s == kDiagSlot) {  // symmetrise the diagonal contribution (objective.hpp:349-351)
-          const double t01 = 0.5 * (Cr[1] + Cr[3]), t02 = 0.5 * (Cr[2] + Cr[6]), t12 = 0.5 * (Cr[5] + Cr[7]);
-          Cr[1] = Cr[3] = t01;
-          Cr[2] = Cr[6] = t02;
-          Cr[5] = Cr[7] = t12;
-        }
-        double* ap = acc + (s - kDiagSlot) * 9;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) ap[k] += Cr[k];
+    // lane o < 27 resolves bin offset o (bin node = i + o - 1): first particle and count
+    int my_pb = 0, my_np = 0;
+    if (lane < 27) {
+      const int j = dense_lookup(L.map, ci0 + lane / 9 - 1, ci1 + (lane / 3) % 3 - 1, ci2 + lane % 3 - 1);
+      if (j >= 0) {
+        my_pb = __ldg(bins.start + j);
+        my_np = __ldg(bins.start + j + 1) - my_pb;
       }
     }
+    // pair q = lane < 14: bins q and 26-q (q = 13: the centre bin alone); chunk schedule
+    const int q_pb1 = my_pb, q_n1 = my_np;
+    const int q_pb2 = __shfl_sync(0xffffffffu, my_pb, 26 - min(lane, 26));
+    const int q_n2_all = __shfl_sync(0xffffffffu, my_np, 26 - min(lane, 26));
+    const int q_n2 = lane < 13 ? q_n2_all : 0;
+    const int q_nch = lane < 14 ? (max(q_n1, q_n2) + kAsmChunk - 1) / kAsmChunk : 0;
+    int incl = q_nch;
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int q_cstart = incl - q_nch;
+    const int nchunks = __shfl_sync(0xffffffffu, incl, 13);
+    const unsigned has = __ballot_sync(0xffffffffu, q_nch > 0);
+    auto chunk_pair = [&](int f) {  // pair of flat chunk f
+      const unsigned m = __ballot_sync(0xffffffffu, q_nch > 0 && q_cstart <= f) & has;
+      return 31 - __clz(m);
+    };
+    auto issue = [&](int f, int buf) {  // lane 0: bulk-copy chunk f into buffer buf
+      const int q = chunk_pair(f);
+      const int c0 = (f - __shfl_sync(0xffffffffu, q_cstart, q)) * kAsmChunk;
+      const int pb1 = __shfl_sync(0xffffffffu, q_pb1, q), n1 = __shfl_sync(0xffffffffu, q_n1, q);
+      const int pb2 = __shfl_sync(0xffffffffu, q_pb2, q), n2 = __shfl_sync(0xffffffffu, q_n2, q);
+      if (lane == 0) {
+        const int k1 = max(0, min(kAsmChunk, n1 - c0)), k2 = max(0, min(kAsmChunk, n2 - c0));
+        const unsigned mb = smem_u32(mbar + buf);
+        double* dst = Sbuf + buf * kAsmStage;
+        mbar_expect_tx(mb, (k1 + k2) * kParticleBytes);
+        if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0) * kTensorStride, k1 * kParticleBytes, mb);
+        if (k2)
+          bulk_g2s(dst + kAsmChunk * kTensorStride, Tu + (long long)(pb2 + c0) * kTensorStride, k2 * kParticleBytes,
+                   mb);
+      }
+    };
+    if (nchunks > 0) issue(0, 0);
+    int cur_q = -1, n1 = 0, n2 = 0, mpar = 0;
+    double Cr[9];
+    int job_bin = 0, job_k = 0, job_slot = 0;
+    bool job = false;
+    auto flush = [&]() {  // fold the pair's register blocks into the row accumulator, bin by bin
+#pragma unroll
+      for (int phase_b = 0; phase_b < 2; ++phase_b) {
+        if (job && job_bin == phase_b) {
+          if (job_slot == kDiagSlot) {  // symmetrise the diagonal contribution (objective.hpp:349-351)
+            const double t01 = 0.5 * (Cr[1] + Cr[3]), t02 = 0.5 * (Cr[2] + Cr[6]), t12 = 0.5 * (Cr[5] + Cr[7]);
+            Cr[1] = Cr[3] = t01;
+            Cr[2] = Cr[6] = t02;
+            Cr[5] = Cr[7] = t12;
+          }
+          double* ap = acc + (job_slot - kDiagSlot) * 9;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) ap[k] += Cr[k];
+        }
+        __syncwarp();
+      }
+    };
+    for (int f = 0; f < nchunks; ++f) {
+      const int buf = f & 1;
+      if (f + 1 < nchunks) issue(f + 1, buf ^ 1);
+      const int pq = chunk_pair(f);
+      const int pc0 = (f - __shfl_sync(0xffffffffu, q_cstart, pq)) * kAsmChunk;
+      if (pq != cur_q) {
+        if (cur_q >= 0) flush();
+        cur_q = pq;
+        n1 = __shfl_sync(0xffffffffu, q_n1, pq);
+        n2 = __shfl_sync(0xffffffffu, q_n2, pq);
+        // this lane's job in the pair: its stencil position in bin pq if that slot is upper,
+        // else position 26-lane in the mirror bin; lane 27: the mirror bin's diagonal
+        const int o0 = pq / 9, o1 = (pq / 3) % 3, o2 = pq % 3;
+        job = false;
+        if (lane < 27) {
+          const int s = 25 * (lc + o0) + 5 * (le + o1) + (lg + o2);
+          if (s >= kDiagSlot) {
+            job = true, job_bin = 0, job_k = lane, job_slot = s;
+          } else if (pq != 13) {
+            job = true, job_bin = 1, job_k = 26 - lane, job_slot = kSlots - 1 - s;
+          }
+        } else if (lane == 27 && pq != 13) {
+          job = true, job_bin = 1, job_k = pq, job_slot = kDiagSlot;
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Cr[k] = 0.0;
+      }
+      mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      const int ka1 = 26 - pq, ka2 = pq;  // row i's stencil position in bin pq / in the mirror bin
+      const double* S = Sbuf + buf * kAsmStage;
+      const int tcount = min(kAsmChunk, max(n1, n2) - pc0);
+      for (int t = 0; t < tcount; ++t) {
+        const bool v1 = pc0 + t < n1, v2 = pc0 + t < n2;
+        const double* P1 = S + t * kTensorStride;
+        const double* P2 = S + (kAsmChunk + t) * kTensorStride;
+        double* M = Mbuf + mpar * 56;
+        if (lane < 27) {
+          if (v1) {
+            const double* Wa = P1 + kTPacked + 3 * ka1;
+            M[lane] = Wa[0] * P1[tp0] + Wa[1] * P1[tp1] + Wa[2] * P1[tp2];
+          }
+          if (v2) {
+            const double* Wa = P2 + kTPacked + 3 * ka2;
+            M[28 + lane] = Wa[0] * P2[tp0] + Wa[1] * P2[tp1] + Wa[2] * P2[tp2];
+          }
+        }
+        __syncwarp();
+        if (job && (job_bin == 0 ? v1 : v2)) {
+          const double* P = job_bin == 0 ? P1 : P2;
+          const double* Ms = M + 28 * job_bin;
+          const double wB0 = P[kTPacked + 3 * job_k], wB1 = P[kTPacked + 3 * job_k + 1],
+                       wB2 = P[kTPacked + 3 * job_k + 2];
+          double m[28];
+#pragma unroll
+          for (int u = 0; u < 14; ++u) {
+            const double2 v = reinterpret_cast<const double2*>(Ms)[u];
+            m[2 * u] = v.x;
+            m[2 * u + 1] = v.y;
+          }
+#pragma unroll
+          for (int ce = 0; ce < 9; ++ce) Cr[ce] += m[3 * ce] * wB0 + m[3 * ce + 1] * wB1 + m[3 * ce + 2] * wB2;
+        }
+        mpar ^= 1;  // M is double buffered: the next particle's M may be written before stragglers read
+      }
+      __syncwarp();  // buffer buf is refilled by the next iteration's issue
+    }
+    if (cur_q >= 0) flush();
     __syncwarp();
     // write-out: upper slots + transposed mirror, mass diagonal, Dirichlet projection
     const bool di = g.dir[i] != 0;
@@ -238,7 +346,12 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
   long long blocks = (L.n + kAsmWarps - 1) / kAsmWarps;
   const long long cap = (long long)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, 0, s>>>(bins, g, L, Tu); count_launches(1); }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem);
+    attr = true;
+  }
+  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, kAsmSmem, s>>>(bins, g, L, Tu); count_launches(1); }
 }
 
 }  // namespace hotb200

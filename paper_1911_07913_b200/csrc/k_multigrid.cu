@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#include "hot_async.cuh"
 #include "hot_internal.h"
 
 namespace cg = cooperative_groups;
@@ -607,20 +608,6 @@ constexpr int kStreamStages = 2;
 constexpr int kStreamRowBytes = 9 * kSlotPitch * 8 + kSlotPitch * 4;  // 9728
 constexpr int kStreamSmem = kStreamWarps * kStreamStages * kStreamRowBytes + kStreamWarps * kStreamStages * 8;
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  }
-}
-
 struct StreamCursor {  // position in a warp's flat (wave, row) sequence
   int q, m;           // q: 0..2*nwaves-1 (forward then backward), m: this warp's m-th row of wave w(q)
 };
@@ -650,11 +637,9 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   };
   unsigned long long policy = 0;
   if (lane == 0) {
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-    for (int s = 0; s < kStreamStages; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb + s)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    policy = l2_evict_first_policy();
+    for (int s = 0; s < kStreamStages; ++s) mbar_init(mb + s, 1);
+    mbar_fence_init();
   }
   __syncwarp();
   auto issue = [&](const StreamCursor& c, int stage) {
@@ -662,18 +647,9 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     const int i = __ldg(wave_rows + __ldg(wave_start + w) + gw + c.m * nw);
     unsigned char* dst = ring + (size_t)stage * kStreamRowBytes;
     const unsigned mbar = smem_u32(mb + stage);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(kStreamRowBytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(L.H + (long long)i * 9 * kSlotPitch), "r"(9 * kSlotPitch * 8), "r"(mbar), "l"(policy)
-        : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst + 9 * kSlotPitch * 8)),
-        "l"(L.cols + (long long)i * kSlotPitch), "r"(kSlotPitch * 4), "r"(mbar), "l"(policy)
-        : "memory");
+    mbar_expect_tx(mbar, kStreamRowBytes);
+    bulk_g2s_hint(dst, L.H + (long long)i * 9 * kSlotPitch, 9 * kSlotPitch * 8, mbar, policy);
+    bulk_g2s_hint(dst + 9 * kSlotPitch * 8, L.cols + (long long)i * kSlotPitch, kSlotPitch * 4, mbar, policy);
     return i;
   };
   // prologue: fill the ring
