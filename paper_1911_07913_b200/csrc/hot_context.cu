@@ -172,6 +172,7 @@ struct Context {
   double dt = 0;
   DBuf gmass, gvel, gmom, gbc, gcn;
   DBuf bin_of, bin_counts, bin_start, bin_cursor, bin_pid, scan_tmp;
+  DBuf pbin, nb27, node_u;  // per-slot bin node, 27-neighbour table, nodal velocity of virtual_F
   DBuf mats_d, cols_d;
 
   // solver vectors
@@ -211,6 +212,7 @@ struct Context {
     P.mass = pmass.as<double>();
     P.vol = pvol.as<double>();
     P.mat = pmat.as<int>();
+    P.bin = pbin.as<int>();
     P.n = np;
     return P;
   }
@@ -225,6 +227,7 @@ struct Context {
     G.dir = L[0].dir.as<uint8_t>();
     G.bc_vel = gbc.as<double>();
     G.cn_scale = gcn.as<double>();
+    G.nb27 = nb27.as<int>();
     return G;
   }
   BinsView bview() const {
@@ -274,7 +277,7 @@ struct Context {
     HOT_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
     HOT_CUDA(cudaMallocHost(&host_int, sizeof(int) * 64));
-    nred = 2 * num_sms();
+    nred = 8 * num_sms();
     partials.ensure(sizeof(double) * (6 * nred + std::max(pcg_max_blocks(), sgs_max_blocks()) + 64));
     scal.ensure(sizeof(double) * 64);
     iflags.ensure(sizeof(int) * 64);
@@ -526,7 +529,9 @@ struct Context {
     Q.mass = qmass.as<double>();
     Q.vol = qvol.as<double>();
     Q.mat = qmat.as<int>();
-    launch_reorder_particles(P, Q, bin_pid.as<int>(), porig.as<int>(), qorig.as<int>(), stream);
+    pbin.ensure(sizeof(int) * std::max<long long>(np, 1));
+    Q.bin = pbin.as<int>();
+    launch_reorder_particles(P, Q, bin_pid.as<int>(), bin_of.as<int>(), porig.as<int>(), qorig.as<int>(), stream);
     px.swap(qx);
     pv.swap(qv);
     pF.swap(qF);
@@ -535,6 +540,8 @@ struct Context {
     pvol.swap(qvol);
     pmat.swap(qmat);
     porig.swap(qorig);
+    nb27.ensure(sizeof(int) * 27 * std::max(n, 1));
+    launch_fill_nb27(gview(), nb27.as<int>(), stream);
     prof_end(h, (double)np * 24 * 3 + 5.0 * len);
     nlevels = 0;
     have_H = false;
@@ -577,7 +584,9 @@ struct Context {
   void energy_async(const double* dvp, const double* p, double alpha, bool want_stress) {
     int h = prof_begin(P_ENERGY);
     double* part = partials.as<double>();
-    launch_particle_energy(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, p, alpha,
+    node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
+    launch_node_u(gview(), dvp, p, alpha, node_u.as<double>(), stream);
+    launch_particle_energy(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
                            want_stress ? stress.as<double>() : nullptr, part, nred, flag_bad(), stream);
     launch_node_energy(gview(), dt, grav, dvp, p, alpha, part + nred, nred, stream);
     launch_sum_partials(part, 2 * nred, scal.as<double>() + 0, stream);
@@ -619,7 +628,9 @@ struct Context {
     alloc_level(l0);
     int h = prof_begin(P_TENSORS);
     Tu.ensure(sizeof(double) * 126 * std::max<long long>(np, 1));
-    launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), dvp, project ? 1 : 0, Tu.as<double>(),
+    node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
+    launch_node_u(gview(), dvp, nullptr, 0.0, node_u.as<double>(), stream);
+    launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(), project ? 1 : 0, Tu.as<double>(),
                             flag_bad(), stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 45 * 8));
     h = prof_begin(P_ASSEMBLE);

@@ -150,6 +150,11 @@ struct Rot {
   double c, s;
 };
 
+template <int I>
+struct IdxC {
+  static constexpr int value = I;
+};
+
 // rows (p,q) of A <- J (x,y) = (c x + s y, -s x + c y)
 template <int P, int Q>
 __device__ __forceinline__ void rot_rows(double* A, Rot j) {
@@ -255,31 +260,37 @@ __device__ __forceinline__ void svd3(const M3& F, M3& Uo, double s[3], M3& Vo) {
   }
 #pragma unroll
   for (int i = 0; i < 3; ++i) s[i] *= scale;
-  // selection sort, descending, first maximum wins
+  // selection sort, descending, first maximum wins (static indices: stays in registers)
+  auto swap_cols = [&](auto X, auto Y) {
+    constexpr int x = decltype(X)::value, y = decltype(Y)::value;
+    const double ts = s[x];
+    s[x] = s[y];
+    s[y] = ts;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    int pos = i;
-    double mx = s[i];
-#pragma unroll
-    for (int k = i + 1; k < 3; ++k)
-      if (s[k] > mx) {
-        mx = s[k];
-        pos = k;
-      }
-    if (mx == 0.0) break;
-    if (pos != i) {
-      const double ts = s[i];
-      s[i] = s[pos];
-      s[pos] = ts;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        double t0 = U[r * 3 + i];
-        U[r * 3 + i] = U[r * 3 + pos];
-        U[r * 3 + pos] = t0;
-        t0 = V[r * 3 + i];
-        V[r * 3 + i] = V[r * 3 + pos];
-        V[r * 3 + pos] = t0;
-      }
+    for (int r = 0; r < 3; ++r) {
+      double t0 = U[r * 3 + x];
+      U[r * 3 + x] = U[r * 3 + y];
+      U[r * 3 + y] = t0;
+      t0 = V[r * 3 + x];
+      V[r * 3 + x] = V[r * 3 + y];
+      V[r * 3 + y] = t0;
+    }
+  };
+  {
+    int pos = 0;
+    double mx = s[0];
+    if (s[1] > mx) {
+      mx = s[1];
+      pos = 1;
+    }
+    if (s[2] > mx) {
+      mx = s[2];
+      pos = 2;
+    }
+    if (mx != 0.0) {
+      if (pos == 1) swap_cols(IdxC<0>{}, IdxC<1>{});
+      if (pos == 2) swap_cols(IdxC<0>{}, IdxC<2>{});
+      if (s[2] > s[1]) swap_cols(IdxC<1>{}, IdxC<2>{});  // max of s[1..2] is s[2] > 0 here
     }
   }
 #pragma unroll

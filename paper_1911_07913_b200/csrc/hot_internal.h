@@ -19,6 +19,7 @@ struct ParticlesView {
   double* mass;
   double* vol;
   int* mat;
+  int* bin;  // stencil-centre node (bin) of each particle slot; valid after activation (bin order)
   long long n;
 };
 
@@ -52,6 +53,7 @@ struct GridView {
   uint8_t* dir;
   double* bc_vel;  // 3n
   double* cn_scale;
+  const int* nb27;  // per node: the 27 nodes at offsets {-1,0,1}^3 (lexicographic), -1 if inactive
 };
 
 struct DevCollider {
@@ -74,7 +76,9 @@ void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n
                           int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s);
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
                 double dt, cudaStream_t s);
-void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* orig_src,
+/// Also writes dst.bin[t] = bin_of[pid[t]].
+void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* bin_of,
+                              const int* orig_src,
                               int* orig_dst, cudaStream_t s);
 void launch_apply_bc(GridView g, double dx, const DevCollider* cols, int n_cols, cudaStream_t s);
 /// Generic exclusive scan over n ints (out may alias nothing); tmp >= ceil(n/4096)+1 ints.
@@ -83,9 +87,13 @@ void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, int* total_
 // ---------------------------------------------------------------- objective (k_objective.cu)
 /// Per-particle pass at nodal increment dv + alpha*p (p may be null): V_p psi partial sums
 /// into partials[blockIdx] and, when stress != null, stores V_p * P F^T (9 per particle).
+/// 27-neighbour table of every active node (g.nb27 must point to n*27 ints).
+void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s);
+/// u = vel + (dv + alpha p) per node (p may be null): the nodal velocity the virtual F sees.
+void launch_node_u(GridView g, const double* dv, const double* p, double alpha, double* u, cudaStream_t s);
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                            const double* dv, const double* p, double alpha, double* stress, double* partials,
-                            int nblocks, int* bad_flag, cudaStream_t s);
+                            const double* u, double* stress, double* partials, int nblocks, int* bad_flag,
+                            cudaStream_t s);
 void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
                         double* partials, int nblocks, cudaStream_t s);
 /// g_i = dt * sum_p (V P F^T) grad w + m_i (dv_i - dt*grav); 0 on Dirichlet; partial sums of
@@ -116,7 +124,7 @@ void launch_final_velocity(GridView g, const double* dv, double* out, cudaStream
 
 // ---------------------------------------------------------------- assembly (k_assembly.cu)
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                             const double* dv, int project, double* Tu, int* bad_flag, cudaStream_t s);
+                             const double* u, int project, double* Tu, int* bad_flag, cudaStream_t s);
 void launch_fill_cols(LevelView L, cudaStream_t s);
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, cudaStream_t s);

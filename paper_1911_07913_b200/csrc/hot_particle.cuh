@@ -5,10 +5,11 @@
 
 namespace hotb200 {
 
-/// Virtual deformation gradient (objective.hpp:218-230) at dv + alpha * p.
+/// Virtual deformation gradient (objective.hpp:218-230) from precomputed nodal velocities
+/// u = vel + (dv + alpha p) (launch_node_u).  The particle's stencil nodes come from its bin's
+/// 27-neighbour table (P.bin, g.nb27): no lattice lookups per particle.
 __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, const GridView& g, double dx, double dt,
-                                          const double* __restrict__ dv, const double* __restrict__ pd, double alpha,
-                                          M3& F, M3& Fn) {
+                                          const double* __restrict__ u, M3& F, M3& Fn) {
   const long long n = P.n;
   double c[3];
   int base[3];
@@ -19,6 +20,7 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
     base[a] = stencil_base_1d(c[a]);
     axis_weights(c[a], base[a], ax[a]);
   }
+  const int* nb = g.nb27 + 27LL * P.bin[p];
   double G[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) G[k] = 0.0;
@@ -30,23 +32,20 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
       for (int k = 0; k < 3; ++k) {
         const double w = ax[0].w[i] * ax[1].w[j] * ax[2].w[k];
         if (w <= 0.0) continue;
-        const int node = dense_lookup(g.map, base[0] + i, base[1] + j, base[2] + k);
+        const int node = __ldg(nb + 9 * i + 3 * j + k);
         const double gr0 = ax[0].dw[i] / dx * ax[1].w[j] * ax[2].w[k];
         const double gr1 = ax[1].dw[j] / dx * ax[0].w[i] * ax[2].w[k];
         const double gr2 = ax[2].dw[k] / dx * ax[0].w[i] * ax[1].w[j];
-        double u[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          double d = dv[3 * node + a];
-          if (pd) d = __dadd_rn(d, __dmul_rn(alpha, pd[3 * node + a]));
-          u[a] = g.vel[3 * node + a] + d;
-        }
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          G[a * 3] += u[a] * gr0;
-          G[a * 3 + 1] += u[a] * gr1;
-          G[a * 3 + 2] += u[a] * gr2;
-        }
+        const double u0 = __ldg(u + 3 * node), u1 = __ldg(u + 3 * node + 1), u2 = __ldg(u + 3 * node + 2);
+        G[0] += u0 * gr0;
+        G[1] += u0 * gr1;
+        G[2] += u0 * gr2;
+        G[3] += u1 * gr0;
+        G[4] += u1 * gr1;
+        G[5] += u1 * gr2;
+        G[6] += u2 * gr0;
+        G[7] += u2 * gr1;
+        G[8] += u2 * gr2;
       }
 #pragma unroll
   for (int k = 0; k < 9; ++k) Fn.m[k] = P.F[k * n + p];
@@ -55,6 +54,49 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
   for (int k = 0; k < 9; ++k) A.m[k] = ((k % 4 == 0) ? 1.0 : 0.0) + dt * G[k];
   F = m3_mul(A, Fn);
   return m3_finite(F);
+}
+
+/// Warp-cooperative node gather: calls body(p) for every particle slot p in the 27 bins
+/// around node i (the bins of g.nb27, lexicographic), lanes striding over the concatenated
+/// slot list, so consecutive lanes read consecutive particles.  All 32 lanes must call it.
+template <class Body>
+__device__ __forceinline__ void warp_node_gather(const GridView& g, const BinsView& bins, int i, int lane, Body body) {
+  int st = 0, cnt = 0;
+  if (lane < 27) {
+    const int j = __ldg(g.nb27 + 27LL * i + lane);
+    if (j >= 0) {
+      st = __ldg(bins.start + j);
+      cnt = __ldg(bins.start + j + 1) - st;
+    }
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 26);
+  for (int base = 0; base < total; base += 32) {
+    const int f = base + lane;
+    int o = 0;  // first bin whose inclusive count exceeds f
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const int probe = min(o + s - 1, 26);
+      const int v = __shfl_sync(0xffffffffu, incl, probe);
+      if (o + s - 1 <= 26 && v <= f) o += s;
+    }
+    o = min(o, 26);
+    const int so = __shfl_sync(0xffffffffu, st, o);
+    const int eo = __shfl_sync(0xffffffffu, incl - cnt, o);
+    if (f < total) body(so + (f - eo));
+  }
+}
+
+/// Deterministic warp sum (xor butterfly); lane 0's value is the result.
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 }  // namespace hotb200

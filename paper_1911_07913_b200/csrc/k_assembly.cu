@@ -31,12 +31,12 @@ constexpr int kTPacked = 45;
 constexpr int kTensorStride = kTPacked + 81;
 
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
-                                   const DevMaterial* __restrict__ mats, const double* __restrict__ dv, int project,
+                                   const DevMaterial* __restrict__ mats, const double* __restrict__ u, int project,
                                    double* __restrict__ Tu, int* bad) {
   const long long n = P.n;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
     M3 F, Fn;
-    if (!virtual_F(P, p, g, dx, dt, dv, nullptr, 0.0, F, Fn)) {
+    if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
       atomicExch(bad, 1);
       continue;
     }
@@ -329,9 +329,9 @@ int agrid(long long n, int threads) {
 }  // namespace
 
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                             const double* dv, int project, double* Tu, int* bad_flag, cudaStream_t s) {
+                             const double* u, int project, double* Tu, int* bad_flag, cudaStream_t s) {
   if (P.n == 0) return;
-  { k_particle_tensors<<<agrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, dv, project, Tu, bad_flag); count_launches(1); }
+  { k_particle_tensors<<<agrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, u, project, Tu, bad_flag); count_launches(1); }
 }
 
 void launch_fill_cols(LevelView L, cudaStream_t s) {

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include "hot_internal.h"
+#include "hot_particle.cuh"
 
 namespace hotb200 {
 
@@ -240,53 +241,57 @@ __global__ void k_bin_sort(const int* __restrict__ start, int n_nodes, int* pid)
 }
 
 /// APIC P2G gather (transfer.hpp:46-64) fused with the node characteristic norm
-/// (objective.hpp:450-473).  One thread per node; neighbour bins visited lexicographically.
-__global__ void k_p2g(ParticlesView P, BinsView bins, GridView g, double dx, const DevMaterial* __restrict__ mats,
-                      double ell, double dt) {
+/// (objective.hpp:450-473).  One warp per node: lanes stride over the particles of the 27
+/// neighbouring bins (contiguous in bin order), partial sums reduced in a fixed tree.
+__global__ void __launch_bounds__(256) k_p2g(ParticlesView P, BinsView bins, GridView g, double dx,
+                                             const DevMaterial* __restrict__ mats, double ell, double dt) {
   const long long n = P.n;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < g.n; i += nw) {
     const int ci0 = g.coords[3 * i], ci1 = g.coords[3 * i + 1], ci2 = g.coords[3 * i + 2];
     const double xi0 = (double)ci0 * dx, xi1 = (double)ci1 * dx, xi2 = (double)ci2 * dx;
     double m = 0.0, mom0 = 0.0, mom1 = 0.0, mom2 = 0.0, num = 0.0;
-    for (int o = 0; o < 27; ++o) {
-      const int j = dense_lookup(g.map, ci0 + o / 9 - 1, ci1 + (o / 3) % 3 - 1, ci2 + o % 3 - 1);
-      if (j < 0) continue;
-      const int e = bins.start[j + 1];
-      for (int t = bins.start[j]; t < e; ++t) {
-        const int p = t;  // particles are stored in bin order
-        const double px0 = P.x[p], px1 = P.x[n + p], px2 = P.x[2 * n + p];
-        const double w = bspline_w(px0 / dx - (double)ci0) * bspline_w(px1 / dx - (double)ci1) *
-                         bspline_w(px2 / dx - (double)ci2);
-        if (w <= 0.0) continue;
-        const double mp = P.mass[p];
-        const double wm = w * mp;
-        const double d0 = xi0 - px0, d1 = xi1 - px1, d2 = xi2 - px2;
-        const double* C = P.C;
-        const double a0 = P.v[p] + (C[p] * d0 + C[n + p] * d1 + C[2 * n + p] * d2);
-        const double a1 = P.v[n + p] + (C[3 * n + p] * d0 + C[4 * n + p] * d1 + C[5 * n + p] * d2);
-        const double a2 = P.v[2 * n + p] + (C[6 * n + p] * d0 + C[7 * n + p] * d1 + C[8 * n + p] * d2);
-        m += wm;
-        mom0 += wm * a0;
-        mom1 += wm * a1;
-        mom2 += wm * a2;
-        num += w * (mp * mats[P.mat[p]].xi);
+    warp_node_gather(g, bins, i, lane, [&](int p) {
+      const double px0 = P.x[p], px1 = P.x[n + p], px2 = P.x[2 * n + p];
+      const double w = bspline_w(px0 / dx - (double)ci0) * bspline_w(px1 / dx - (double)ci1) *
+                       bspline_w(px2 / dx - (double)ci2);
+      if (w <= 0.0) return;
+      const double mp = P.mass[p];
+      const double wm = w * mp;
+      const double d0 = xi0 - px0, d1 = xi1 - px1, d2 = xi2 - px2;
+      const double* C = P.C;
+      const double a0 = P.v[p] + (C[p] * d0 + C[n + p] * d1 + C[2 * n + p] * d2);
+      const double a1 = P.v[n + p] + (C[3 * n + p] * d0 + C[4 * n + p] * d1 + C[5 * n + p] * d2);
+      const double a2 = P.v[2 * n + p] + (C[6 * n + p] * d0 + C[7 * n + p] * d1 + C[8 * n + p] * d2);
+      m += wm;
+      mom0 += wm * a0;
+      mom1 += wm * a1;
+      mom2 += wm * a2;
+      num += w * (mp * mats[P.mat[p]].xi);
+    });
+    m = warp_sum_d(m);
+    mom0 = warp_sum_d(mom0);
+    mom1 = warp_sum_d(mom1);
+    mom2 = warp_sum_d(mom2);
+    num = warp_sum_d(num);
+    if (lane == 0) {
+      g.mass[i] = m;
+      g.mom[3 * i] = mom0;
+      g.mom[3 * i + 1] = mom1;
+      g.mom[3 * i + 2] = mom2;
+      if (m > 0.0) {
+        g.vel[3 * i] = mom0 / m;
+        g.vel[3 * i + 1] = mom1 / m;
+        g.vel[3 * i + 2] = mom2 / m;
+      } else {
+        g.vel[3 * i] = g.vel[3 * i + 1] = g.vel[3 * i + 2] = 0.0;
       }
+      const double xi = m > 0.0 ? num / m : 0.0;
+      g.cn_scale[i] = ell * xi * dt;
+      g.dir[i] = 0;
+      g.bc_vel[3 * i] = g.bc_vel[3 * i + 1] = g.bc_vel[3 * i + 2] = 0.0;
     }
-    g.mass[i] = m;
-    g.mom[3 * i] = mom0;
-    g.mom[3 * i + 1] = mom1;
-    g.mom[3 * i + 2] = mom2;
-    if (m > 0.0) {
-      g.vel[3 * i] = mom0 / m;
-      g.vel[3 * i + 1] = mom1 / m;
-      g.vel[3 * i + 2] = mom2 / m;
-    } else {
-      g.vel[3 * i] = g.vel[3 * i + 1] = g.vel[3 * i + 2] = 0.0;
-    }
-    const double xi = m > 0.0 ? num / m : 0.0;
-    g.cn_scale[i] = ell * xi * dt;
-    g.dir[i] = 0;
-    g.bc_vel[3 * i] = g.bc_vel[3 * i + 1] = g.bc_vel[3 * i + 2] = 0.0;
   }
 }
 
@@ -355,7 +360,8 @@ __global__ void k_apply_bc(GridView g, double dx, const DevCollider* __restrict_
 /// Gathers every particle array into bin order (stable, ascending ids inside a bin) so each
 /// bin is a contiguous range: the node-centric gathers then stream contiguous particle data.
 __global__ void k_reorder(ParticlesView src, ParticlesView dst, const int* __restrict__ pid,
-                          const int* __restrict__ orig_src, int* __restrict__ orig_dst) {
+                          const int* __restrict__ bin_of, const int* __restrict__ orig_src,
+                          int* __restrict__ orig_dst) {
   const long long n = src.n;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     const long long p = pid[t];
@@ -372,7 +378,29 @@ __global__ void k_reorder(ParticlesView src, ParticlesView dst, const int* __res
     dst.mass[t] = src.mass[p];
     dst.vol[t] = src.vol[p];
     dst.mat[t] = src.mat[p];
+    dst.bin[t] = bin_of[p];
     orig_dst[t] = orig_src[p];
+  }
+}
+
+__global__ void k_fill_nb27(GridView g, int* __restrict__ nb27) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)g.n * 27;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / 27), k = (int)(t - 27LL * i);
+    nb27[t] = dense_lookup(g.map, g.coords[3 * i] + k / 9 - 1, g.coords[3 * i + 1] + (k / 3) % 3 - 1,
+                           g.coords[3 * i + 2] + k % 3 - 1);
+  }
+}
+
+/// The nodal velocity of virtual_F (objective.hpp:218-230): vel + (dv + alpha p), rounded
+/// exactly as the per-particle expression it replaces.
+__global__ void k_node_u(GridView g, const double* __restrict__ dv, const double* __restrict__ pd, double alpha,
+                         double* __restrict__ u) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < 3LL * g.n;
+       t += (long long)gridDim.x * blockDim.x) {
+    double d = dv[t];
+    if (pd) d = __dadd_rn(d, __dmul_rn(alpha, pd[t]));
+    u[t] = g.vel[t] + d;
   }
 }
 
@@ -442,13 +470,24 @@ void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
                 double dt, cudaStream_t s) {
   if (g.n == 0) return;
-  { k_p2g<<<grid_for(g.n, 128), 128, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
+  { k_p2g<<<grid_for(32LL * g.n, 256), 256, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
 }
 
-void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* orig_src,
+void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s) {
+  if (g.n == 0) return;
+  { k_fill_nb27<<<grid_for(27LL * g.n, 256), 256, 0, s>>>(g, nb27); count_launches(1); }
+}
+
+void launch_node_u(GridView g, const double* dv, const double* p, double alpha, double* u, cudaStream_t s) {
+  if (g.n == 0) return;
+  { k_node_u<<<grid_for(3LL * g.n, 256), 256, 0, s>>>(g, dv, p, alpha, u); count_launches(1); }
+}
+
+void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* bin_of,
+                              const int* orig_src,
                               int* orig_dst, cudaStream_t s) {
   if (src.n == 0) return;
-  { k_reorder<<<grid_for(src.n, 256), 256, 0, s>>>(src, dst, pid, orig_src, orig_dst); count_launches(1); }
+  { k_reorder<<<grid_for(src.n, 256), 256, 0, s>>>(src, dst, pid, bin_of, orig_src, orig_dst); count_launches(1); }
 }
 
 void launch_apply_bc(GridView g, double dx, const DevCollider* cols, int n_cols, cudaStream_t s) {

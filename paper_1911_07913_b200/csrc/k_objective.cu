@@ -37,17 +37,18 @@ __device__ __forceinline__ double block_sum(double v) {
   return r;
 }
 
-__global__ void __launch_bounds__(kRedThreads) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
+constexpr int kEnergyThreads = 128;  // ~146 registers: 3 blocks (12 warps) per SM
+
+__global__ void __launch_bounds__(kEnergyThreads) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
                                                                  const DevMaterial* __restrict__ mats,
-                                                                 const double* __restrict__ dv,
-                                                                 const double* __restrict__ pd, double alpha,
+                                                                 const double* __restrict__ u,
                                                                  double* __restrict__ stress,
                                                                  double* __restrict__ partials, int* bad) {
   double acc = 0.0;
   const long long n = P.n;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
     M3 F, Fn;
-    if (!virtual_F(P, p, g, dx, dt, dv, pd, alpha, F, Fn)) {
+    if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
       atomicExch(bad, 1);
       continue;
     }
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kRedThreads) k_particle_energy(ParticlesView P
       for (int k = 0; k < 9; ++k) stress[k * n + p] = vol * PFt.m[k];
     }
   }
-  const double b = block_sum<kRedThreads>(acc);
+  const double b = block_sum<kEnergyThreads>(acc);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
 }
 
@@ -89,45 +90,49 @@ __global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, double 
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
 }
 
+/// Node gradient (objective.hpp:260-287): one warp per node gathers V P F^T grad w over the
+/// particles of its 27 bins (lanes over the contiguous slots, fixed-tree warp sum), fused
+/// with the scaled-norm residual (objective.hpp:476-486).
 __global__ void __launch_bounds__(kRedThreads) k_node_gradient(ParticlesView P, BinsView bins, GridView g, double dx,
                                                                double dt, double g0, double g1, double g2,
                                                                const double* __restrict__ stress,
                                                                const double* __restrict__ dv, double* __restrict__ gout,
                                                                double* __restrict__ partials, int* bad) {
   const long long n = P.n;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
   double acc_norm = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < g.n; i += nw) {
     const int ci0 = g.coords[3 * i], ci1 = g.coords[3 * i + 1], ci2 = g.coords[3 * i + 2];
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    for (int o = 0; o < 27; ++o) {
-      const int j = dense_lookup(g.map, ci0 + o / 9 - 1, ci1 + (o / 3) % 3 - 1, ci2 + o % 3 - 1);
-      if (j < 0) continue;
-      const int e = bins.start[j + 1];
-      for (int t = bins.start[j]; t < e; ++t) {
-        const int p = t;  // bin order
-        const double o0 = P.x[p] / dx - (double)ci0;
-        const double o1 = P.x[n + p] / dx - (double)ci1;
-        const double o2 = P.x[2 * n + p] / dx - (double)ci2;
-        const double w0 = bspline_w(o0), w1 = bspline_w(o1), w2 = bspline_w(o2);
-        if (w0 * w1 * w2 <= 0.0) continue;
-        const double gr0 = bspline_dw(o0) / dx * w1 * w2;
-        const double gr1 = bspline_dw(o1) / dx * w0 * w2;
-        const double gr2 = bspline_dw(o2) / dx * w0 * w1;
-        const double* Q = stress;
-        f0 += Q[p] * gr0 + Q[n + p] * gr1 + Q[2 * n + p] * gr2;
-        f1 += Q[3 * n + p] * gr0 + Q[4 * n + p] * gr1 + Q[5 * n + p] * gr2;
-        f2 += Q[6 * n + p] * gr0 + Q[7 * n + p] * gr1 + Q[8 * n + p] * gr2;
-      }
-    }
-    const double m = g.mass[i];
-    double gi[3] = {dt * f0 + m * (dv[3 * i] - dt * g0), dt * f1 + m * (dv[3 * i + 1] - dt * g1),
-                    dt * f2 + m * (dv[3 * i + 2] - dt * g2)};
-    if (g.dir[i]) gi[0] = gi[1] = gi[2] = 0.0;
+    warp_node_gather(g, bins, i, lane, [&](int p) {
+      const double o0 = P.x[p] / dx - (double)ci0;
+      const double o1 = P.x[n + p] / dx - (double)ci1;
+      const double o2 = P.x[2 * n + p] / dx - (double)ci2;
+      const double w0 = bspline_w(o0), w1 = bspline_w(o1), w2 = bspline_w(o2);
+      if (w0 * w1 * w2 <= 0.0) return;
+      const double gr0 = bspline_dw(o0) / dx * w1 * w2;
+      const double gr1 = bspline_dw(o1) / dx * w0 * w2;
+      const double gr2 = bspline_dw(o2) / dx * w0 * w1;
+      const double* Q = stress;
+      f0 += Q[p] * gr0 + Q[n + p] * gr1 + Q[2 * n + p] * gr2;
+      f1 += Q[3 * n + p] * gr0 + Q[4 * n + p] * gr1 + Q[5 * n + p] * gr2;
+      f2 += Q[6 * n + p] * gr0 + Q[7 * n + p] * gr1 + Q[8 * n + p] * gr2;
+    });
+    f0 = warp_sum_d(f0);
+    f1 = warp_sum_d(f1);
+    f2 = warp_sum_d(f2);
+    if (lane == 0) {
+      const double m = g.mass[i];
+      double gi[3] = {dt * f0 + m * (dv[3 * i] - dt * g0), dt * f1 + m * (dv[3 * i + 1] - dt * g1),
+                      dt * f2 + m * (dv[3 * i + 2] - dt * g2)};
+      if (g.dir[i]) gi[0] = gi[1] = gi[2] = 0.0;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) gout[3 * i + a] = gi[a];
-    const double sc = g.cn_scale[i];
-    if (!(sc > 0.0)) atomicExch(bad, 2);
-    acc_norm += (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
+      for (int a = 0; a < 3; ++a) gout[3 * i + a] = gi[a];
+      const double sc = g.cn_scale[i];
+      if (!(sc > 0.0)) atomicExch(bad, 2);
+      acc_norm += (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
+    }
   }
   const double b = block_sum<kRedThreads>(acc_norm);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
@@ -250,9 +255,9 @@ int vgrid(long long n) {
 }  // namespace
 
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                            const double* dv, const double* p, double alpha, double* stress, double* partials,
-                            int nblocks, int* bad_flag, cudaStream_t s) {
-  { k_particle_energy<<<nblocks, kRedThreads, 0, s>>>(P, g, dx, dt, mats, dv, p, alpha, stress, partials, bad_flag); count_launches(1); }
+                            const double* u, double* stress, double* partials, int nblocks, int* bad_flag,
+                            cudaStream_t s) {
+  { k_particle_energy<<<nblocks, kEnergyThreads, 0, s>>>(P, g, dx, dt, mats, u, stress, partials, bad_flag); count_launches(1); }
 }
 
 void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
