@@ -89,6 +89,8 @@ struct Level {
   int lo[3] = {0, 0, 0}, ext[3] = {0, 0, 0};
   DBuf map, coords, cols, H, dinv, dir, flags;
   DBuf wave_of, wave_counts, wave_start, wave_cursor, wave_rows, wave_start_c;
+  DBuf sgs_flag;      // per-row epoch flags of the dataflow smoother
+  int sgs_epoch = 1;
   int nwaves = 0, max_wave = 0;
   std::vector<int> wave_start_h;
   long long active_slots = 0;
@@ -680,6 +682,9 @@ struct Context {
     starts.push_back(acc);
     l.nwaves = (int)starts.size() - 1;
     l.wave_start_h = starts;
+    l.sgs_flag.ensure(sizeof(int) * std::max(l.n, 1));
+    HOT_CUDA(cudaMemsetAsync(l.sgs_flag.p, 0, sizeof(int) * std::max(l.n, 1), stream));
+    l.sgs_epoch = 1;
     l.wave_start_c.ensure(sizeof(int) * starts.size());
     HOT_CUDA(cudaMemcpyAsync(l.wave_start_c.p, starts.data(), sizeof(int) * starts.size(), cudaMemcpyHostToDevice,
                              stream));
@@ -755,7 +760,13 @@ struct Context {
     const int stream_min = env ? std::atoi(env) : 8 * 1024;
     const char* sched = std::getenv("HOT_SGS_LEVEL0");  // "waves" | "stream" (default)
     const bool per_wave = sched && std::strcmp(sched, "waves") == 0;
-    if (l.max_wave >= stream_min && !per_wave)
+    const char* coarse_sched = std::getenv("HOT_SGS_COARSE");  // "flow" (default) | "barrier"
+    const bool flow = !(coarse_sched && std::strcmp(coarse_sched, "barrier") == 0);
+    if (l.max_wave < stream_min && flow) {
+      launch_sgs_flow(l.view(), l.wave_rows.as<int>(), l.wave_of.as<int>(), u, b, l.sgs_flag.as<int>(), l.sgs_epoch,
+                      stream);
+      l.sgs_epoch += 2;
+    } else if (l.max_wave >= stream_min && !per_wave)
       launch_sgs_stream(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
     else if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)
       launch_sgs_waves(l.view(), l.wave_start_h.data(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);

@@ -152,6 +152,10 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s);
 /// The same sweep as one streaming launch per wave (large levels; waves given on the host).
+/// Coarse smoother: both passes as a dataflow kernel with per-row epoch flags (flag must hold
+/// values < epoch; the kernel leaves epoch+1 in every row).
+void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* u, const double* b, int* flag,
+                     int epoch, cudaStream_t s);
 /// Level-0 smoother: both passes, all waves, one persistent kernel with bulk-copy row streaming.
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
                        const double* b, cudaStream_t s);

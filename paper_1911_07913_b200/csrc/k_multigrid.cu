@@ -16,6 +16,7 @@
 //   coarse_solve/pcg   Jacobi-PCG from zero as one cooperative kernel (3 grid barriers per
 //                      iteration, deterministic block reductions).
 #include <cooperative_groups.h>
+#include <climits>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -594,6 +595,94 @@ __global__ void __launch_bounds__(kWaveThreads) k_sgs_wave(LevelView L, const in
   }
 }
 
+/// Coarse-level symmetric Gauss-Seidel as a dataflow kernel (exact reference order,
+/// multigrid.hpp:296-320).  Rows are dealt round-robin, in wave order (a topological order of
+/// the sweep's dependency graph), to co-resident CTAs of 128 threads (one per slot).  A row
+/// starts as soon as its own predecessors are done -- the coupled rows earlier in the pass
+/// order (lower wave forward, higher wave backward; plus, backward, the row's own forward
+/// update) -- tracked by per-row epoch flags (st.release / ld.acquire), instead of a grid
+/// barrier after every wave.  The rows later in the pass order wait for this row, so they
+/// still hold their old values when it reads them: exactly the sequential sweep.  Progress:
+/// the lowest unfinished row in pass order always has all predecessors done and its CTA has
+/// reached it (each CTA walks its rows in order).
+__global__ void __launch_bounds__(kSgsThreads) k_sgs_flow(LevelView L, const int* __restrict__ order, int n,
+                                                         const int* __restrict__ wave_of, double* u,
+                                                         const double* __restrict__ b, int* flag, int epoch) {
+  __shared__ double red[kSgsThreads / 32][3];
+  const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int e = epoch + pass;
+    for (int k = blockIdx.x; k < n; k += gridDim.x) {
+      const int i = __ldg(order + (pass == 0 ? k : n - 1 - k));
+      int c = -1;
+      double h[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) h[q] = 0.0;
+      if (s < kSlots) {
+        c = __ldg(L.cols + (long long)i * kSlotPitch + s);
+        const double* hp = L.H + (long long)i * 9 * kSlotPitch + s;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) h[q] = __ldcs(hp + q * kSlotPitch);
+      }
+      double D[9], rb[3];
+      if (s == 0) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] = __ldg(L.dinv + 9 * (long long)i + q);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) rb[a] = __ldg(b + 3 * (long long)i + a);
+      }
+      if (c >= 0) {  // wait for this row's predecessors in the pass order
+        const int wi = __ldg(wave_of + i), wc = __ldg(wave_of + c);
+        int need = INT_MIN;
+        if (pass == 0 ? wc < wi : wc > wi) need = e;
+        if (pass == 1 && c == i) need = e - 1;  // own forward update
+        if (need != INT_MIN) {
+          int v;
+          do {
+            asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(v) : "l"(flag + c) : "memory");
+          } while (v < need);
+        }
+      }
+      __syncthreads();
+      double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+      if (s < kSlots) {
+        const double* xp = u + 3 * (c >= 0 ? c : 0);  // inactive slots: zero block
+        x0 = __ldcg(xp);
+        x1 = __ldcg(xp + 1);
+        x2 = __ldcg(xp + 2);
+      }
+      double a0 = h[0] * x0 + h[1] * x1 + h[2] * x2;
+      double a1 = h[3] * x0 + h[4] * x1 + h[5] * x2;
+      double a2 = h[6] * x0 + h[7] * x1 + h[8] * x2;
+      a0 = wsum(a0);
+      a1 = wsum(a1);
+      a2 = wsum(a2);
+      if (lane == 0) {
+        red[wid][0] = a0;
+        red[wid][1] = a1;
+        red[wid][2] = a2;
+      }
+      __syncthreads();
+      if (s == 0) {
+        double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < kSgsThreads / 32; ++q) {
+          y0 += red[q][0];
+          y1 += red[q][1];
+          y2 += red[q][2];
+        }
+        const double uo0 = __ldcg(u + 3 * i), uo1 = __ldcg(u + 3 * i + 1), uo2 = __ldcg(u + 3 * i + 2);
+        const double r0 = rb[0] - y0, r1 = rb[1] - y1, r2 = rb[2] - y2;
+        u[3 * i] = uo0 + (D[0] * r0 + D[1] * r1 + D[2] * r2);
+        u[3 * i + 1] = uo1 + (D[3] * r0 + D[4] * r1 + D[5] * r2);
+        u[3 * i + 2] = uo2 + (D[6] * r0 + D[7] * r1 + D[8] * r2);
+        asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(flag + i), "r"(e) : "memory");
+      }
+      __syncthreads();
+    }
+  }
+}
+
 /// Level-0 symmetric Gauss-Seidel, all waves of both passes in ONE persistent cooperative
 /// kernel (one CTA per SM).  Each warp owns a ring of kStreamStages row buffers in shared memory
 /// filled by the bulk-copy engine (cp.async.bulk, completion on an mbarrier): a row's blocks
@@ -873,6 +962,21 @@ int coop_blocks(const void* fn, int threads, int smem = 0) {
 }
 
 }  // namespace
+
+int sgs_flow_blocks() {
+  static int v = 0;
+  if (!v) v = coop_blocks((const void*)k_sgs_flow, kSgsThreads, 0);
+  return v;
+}
+
+void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* u, const double* b, int* flag,
+                     int epoch, cudaStream_t s) {
+  if (L.n == 0) return;
+  int n = L.n;
+  int grid = std::min(sgs_flow_blocks(), n);
+  void* args[] = {&L, (void*)&order, &n, (void*)&wave_of, &u, (void*)&b, &flag, &epoch};
+  { cudaLaunchCooperativeKernel((const void*)k_sgs_flow, grid, kSgsThreads, args, 0, s); count_launches(1); }
+}
 
 int sgs_max_blocks() {
   static int v = 0;

@@ -132,6 +132,27 @@ def test_hierarchy_and_vcycle():
         assert rel_err(u, uo) < 1e-9
 
 
+@pytest.mark.parametrize("coarse", ["flow", "barrier"])
+def test_vcycle_coarse_smoother_schedules(monkeypatch, coarse):
+    """The coarse levels' smoother runs as a dataflow kernel (per-row epoch flags) or as a
+    persistent kernel with a grid barrier per wave; both follow the reference's sequential
+    sweep exactly and compute each row identically, so they agree bit for bit."""
+    monkeypatch.setenv("HOT_SGS_COARSE", coarse)
+    pr = _stretched_block_pair(seed=14, cells=6, youngs=1e6)
+    n = pr.prepare(0.01)
+    pr.gpu.assemble()
+    pr.orc.assemble()
+    pr.gpu.build_hierarchy(3)
+    pr.orc.build_hierarchy(3)
+    b = np.random.default_rng(15).uniform(-1, 1, 3 * n)
+    u, it = pr.gpu.vcycle(b)
+    uo, ito = pr.orc.vcycle(b)
+    assert it == ito and rel_err(u, uo) < 1e-9
+    monkeypatch.setenv("HOT_SGS_COARSE", "barrier" if coarse == "flow" else "flow")
+    u2, it2 = pr.gpu.vcycle(b)
+    assert it2 == it and np.array_equal(u, u2)
+
+
 @pytest.mark.parametrize("schedule", ["stream", "waves"])
 def test_vcycle_streaming_wave_schedule(monkeypatch, schedule):
     """Same V-cycle parity with every SGS level run on the large-wave schedules the benchmark's
