@@ -32,7 +32,7 @@ SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
 FP64_PEAK_TFLOPS = 34.79  # DFMA throughput measured on this pool's B200 (profiles/r01_fp64_peak.json)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
-TRAFFIC = {}
+TRAFFIC = {"assemble_rows": 12.694647e9, "sgs_level0": 4.087470e9}  # profiles/r01_ncu_full_summary.txt
 UNIT = "particle-steps/s"
 
 
@@ -95,19 +95,21 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def cpu_slab(particles, frac_x=0.05):
-    """Bounded CPU sample: the particles of the first `frac_x` metres of every bar (both driven
-    ends' physics is represented by the left end collider)."""
-    keep = particles["x"][:, 0] < frac_x
+def cpu_slab(particles, n_keep):
+    """Bounded CPU sample: the n_keep particles nearest the left end (x < x_cut across all four
+    bars): the driven end (rotating collider) plus free soft/stiff material beyond it, so the
+    sampled steps need the same solves as the full scene."""
+    order = np.argsort(particles["x"][:, 0], kind="stable")[: max(1, min(n_keep, particles["x"].shape[0]))]
+    keep = np.sort(order)
     return {k: v[keep] for k, v in particles.items()}
 
 
-def run_cpu_reference(sc, particles, steps, warmup, threads, frac_x=0.05):
+def run_cpu_reference(sc, particles, steps, warmup, threads, n_keep):
     """The reference CPU path (oracle port of hotmpm::advance_step) on the bounded slab."""
     from oracle import oracle as O
 
     O.set_threads(threads)
-    slab = cpu_slab(particles, frac_x)
+    slab = cpu_slab(particles, n_keep)
     orc = O.Oracle(3)
     orc.set_scene(sc.source)
     orc.set_particles(slab["x"], slab["v"], slab["mass"], slab["volume"], slab["F"].reshape(-1),
@@ -124,7 +126,7 @@ def run_cpu_reference(sc, particles, steps, warmup, threads, frac_x=0.05):
             outer.append(st["outer_iterations"])
     n = slab["x"].shape[0]
     return dict(value=n * n_steps / t_all, particles=n, steps=n_steps, seconds=t_all, outer=outer,
-                ms_per_step=1000 * t_all / max(n_steps, 1))
+                ms_per_step=1000 * t_all / max(n_steps, 1), x_cut=float(slab["x"][:, 0].max()))
 
 
 def main():
@@ -151,9 +153,13 @@ def main():
         if rank != 0:
             return
         threads = os.cpu_count() or 1
-        r = run_cpu_reference(sc, particles, max(args.steps, 1), args.warmup, threads, frac_x=0.03)
-        sample = (f"{r['particles']} particles (x < 0.03 m slab of all four bars), {args.warmup} warm-up + "
-                  f"{r['steps']} timed steps from t=0, {threads} threads; outer iterations {r['outer']}")
+        # slab sized so the whole run stays within ~2.5 min of CPU time: ~2.5K particle-steps/s
+        # per thread on this workload (1 outer iteration per step)
+        n_keep = int(2500 * threads * 150 / (max(args.steps, 1) + args.warmup))
+        r = run_cpu_reference(sc, particles, max(args.steps, 1), args.warmup, threads, n_keep)
+        sample = (f"{r['particles']} particles (x < {r['x_cut']:.3f} m slab of all four bars: driven end + free "
+                  f"material), {args.warmup} warm-up + {r['steps']} timed steps from t=0 (the GPU arm's step "
+                  f"sequence), {threads} threads; outer iterations {r['outer']}")
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling)",
@@ -253,33 +259,37 @@ def main():
     e2e_value = n_particles * world * e2e_steps / (e2e_ms / 1000.0)
 
     # ---- rooflines (algorithmic bytes or flops / CUDA-event duration on the context stream)
+    # `roofline` is the dominant kernel of the step: the level-0 assembly, bound by fp64 FMA
+    # throughput (its algorithmic flops / the measured DFMA peak).  `roofline_hbm` is the
+    # largest HBM-bound phase (the level-0 smoother in practice).
     peaks, peak_kind = measured_peaks()
-    hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
-                  k in ("sgs_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
-                        "lbfgs_vectors")}
-    # the north star's HBM-bound smoother / SpMV / P2G class: report the largest by time
-    top = max(hbm_phases, key=lambda k: hbm_phases[k]["ms"]) if hbm_phases else None
     roofline = None
-    if top:
-        ph = hbm_phases[top]
-        achieved = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
-        roofline = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": TRAFFIC.get(top), "peak_kind": peak_kind,
-                    "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
-                    "bytes_per_launch": ph["bytes"] / max(ph["launches"], 1)}
-    roofline_fp64 = None
     if "assemble_rows" in prof and prof["assemble_rows"]["ms"] > 0:
         ph = prof["assemble_rows"]
         ach = ph["flops"] / (ph["ms"] / 1000.0) / 1e12
-        roofline_fp64 = {"bound": "fp64", "kernel": "assemble_rows", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "share_of_step": ph["ms"] / ms,
-                         "peak_kind": "measured (profiles/r01_fp64_peak.json, tools/microbench/fp64peak.cu)"}
+        roofline = {"bound": "fp64", "kernel": "k_assemble_rows", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": TRAFFIC.get("assemble_rows"),
+                    "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                    "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
+                    "peak_kind": "measured DFMA peak (profiles/r01_fp64_peak.json, tools/microbench/fp64peak.cu)"}
+    hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
+                  k in ("sgs_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
+                        "lbfgs_vectors")}
+    top = max(hbm_phases, key=lambda k: hbm_phases[k]["ms"]) if hbm_phases else None
+    roofline_hbm = None
+    if top:
+        ph = hbm_phases[top]
+        achieved = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
+        roofline_hbm = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": achieved / peaks["hbm_gbs"], "traffic": TRAFFIC.get(top), "peak_kind": peak_kind,
+                        "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                        "bytes_per_launch": ph["bytes"] / max(ph["launches"], 1)}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = run_cpu_reference(sc, particles, 1, 0, 1)
+        r = run_cpu_reference(sc, particles, 1, 0, 1, 100000)
         cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
-                        "sample": f"{r['particles']} particles (x < 0.05 m slab of all four bars), 1 step from t=0, "
+                        "sample": f"{r['particles']} particles (x < {r['x_cut']:.3f} m slab of all four bars), 1 step from t=0, "
                                   f"oracle port of hotmpm::advance_step, 1 thread (reference default), "
                                   f"{r['seconds']:.1f} s, outer iterations {r['outer']}"}
 
@@ -293,7 +303,7 @@ def main():
                                outer_iterations=outer, phase_ms_per_step=phases),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps},
-                "gpu_launches": int(launches), "roofline": roofline, "roofline_fp64": roofline_fp64,
+                "gpu_launches": int(launches), "roofline": roofline, "roofline_hbm": roofline_hbm,
                 "cpu_baseline": cpu_baseline,
                 "clocks": clocks.summary()}
         print(json.dumps(line))

@@ -634,7 +634,7 @@ struct Context {
     launch_node_u(gview(), dvp, nullptr, 0.0, node_u.as<double>(), stream);
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(), project ? 1 : 0, Tu.as<double>(),
                             flag_bad(), stream);
-    prof_end(h, (double)np * (24 + 72 + 8 + 4 + 45 * 8));
+    prof_end(h, (double)np * (24 + 72 + 8 + 4 + 126 * 8));  // x F vol mat in, kappa*T (packed) + W out
     h = prof_begin(P_ASSEMBLE);
     launch_fill_cols(l0.view(), stream);
     launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), stream);

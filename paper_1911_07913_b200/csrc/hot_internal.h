@@ -177,6 +177,10 @@ void launch_soa_to_aos_perm(const double* in, double* out, long long n, int comp
 void launch_iota(int* out, long long n, cudaStream_t s);
 
 int num_sms();
+/// Co-resident CTAs of a kernel (occupancy x SMs).  Grid-stride kernels whose neighbouring
+/// items share data launch exactly this many CTAs, so at any time the active items form one
+/// contiguous window (L2 reuse) instead of being strided across the whole domain.
+int resident_blocks(const void* fn, int threads, int smem);
 
 /// Kernel launches issued by this process (all contexts); every launch_* wrapper counts.
 long long kernel_launch_count();

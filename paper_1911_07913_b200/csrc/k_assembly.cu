@@ -343,14 +343,13 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
                           const double* Tu, cudaStream_t s) {
   if (L.n == 0) return;
   (void)dx;
-  long long blocks = (L.n + kAsmWarps - 1) / kAsmWarps;
-  const long long cap = (long long)num_sms() * 16;
-  if (blocks > cap) blocks = cap;
-  static bool attr = false;
-  if (!attr) {
+  // oversubscribed grid (16 CTAs per SM): measured lower DRAM traffic than a resident-sized one
+  static const bool attr = [] {
     cudaFuncSetAttribute((const void*)k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem);
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
+  const long long blocks = std::min<long long>((long long)num_sms() * 16, (L.n + kAsmWarps - 1) / kAsmWarps);
   { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, kAsmSmem, s>>>(bins, g, L, Tu); count_launches(1); }
 }
 

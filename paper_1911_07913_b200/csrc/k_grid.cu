@@ -11,6 +11,8 @@
 //   apply_boundary_scripts simulation.hpp:259-272
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "hot_internal.h"
 #include "hot_particle.cuh"
 
@@ -424,6 +426,14 @@ int num_sms() {
   return n;
 }
 
+int resident_blocks(const void* fn, int threads, int smem) {
+  int per_sm = 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * num_sms();
+}
+
 void launch_particle_bounds(const ParticlesView& P, double dx, int* bounds6, int* bad_flag, cudaStream_t s) {
   if (P.n == 0) return;
   { k_particle_bounds<<<grid_for(P.n, 256), 256, 0, s>>>(P.x, P.n, dx, bounds6, bad_flag); count_launches(1); }
@@ -470,7 +480,8 @@ void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
                 double dt, cudaStream_t s) {
   if (g.n == 0) return;
-  { k_p2g<<<grid_for(32LL * g.n, 256), 256, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
+  static const int blocks = resident_blocks((const void*)k_p2g, 256, 0);
+  { k_p2g<<<std::min<long long>(blocks, (32LL * g.n + 255) / 256), 256, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
 }
 
 void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s) {

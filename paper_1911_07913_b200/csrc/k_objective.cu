@@ -5,6 +5,8 @@
 // fixed order; no float atomics).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "hot_internal.h"
 #include "hot_particle.cuh"
 
@@ -268,8 +270,15 @@ void launch_node_energy(GridView g, double dt, const double* grav, const double*
 void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
                           const double* stress, const double* dv, double* gout, double* partials, int nblocks,
                           int* bad_flag, cudaStream_t s) {
-  { k_node_gradient<<<nblocks, kRedThreads, 0, s>>>(P, bins, g, dx, dt, grav[0], grav[1], grav[2], stress, dv, gout,
-                                                  partials, bad_flag); count_launches(1); }
+  // resident-sized grid: the active nodes form one contiguous window, so the particles of
+  // neighbouring nodes' bins are reused from L2; unused partial slots are zeroed
+  static const int resident = resident_blocks((const void*)k_node_gradient, kRedThreads, 0);
+  const int nb = std::max(1, std::min(nblocks, resident));
+  if (nb < nblocks) {
+    cudaMemsetAsync(partials + nb, 0, sizeof(double) * (nblocks - nb), s);
+  }
+  { k_node_gradient<<<nb, kRedThreads, 0, s>>>(P, bins, g, dx, dt, grav[0], grav[1], grav[2], stress, dv, gout,
+                                              partials, bad_flag); count_launches(1); }
 }
 
 void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s) {
