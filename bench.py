@@ -32,7 +32,7 @@ SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
 FP64_PEAK_TFLOPS = 34.79  # DFMA throughput measured on this pool's B200 (profiles/r01_fp64_peak.json)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
-TRAFFIC = {"assemble_rows": 12.694647e9, "sgs_level0": 4.087470e9}  # profiles/r01_ncu_full_summary.txt
+TRAFFIC = {"assemble_rows": 12.694647e9, "sgs_level0": 4.087470e9}  # per launch, from profiles/r01_ncu_full_summary.txt
 UNIT = "particle-steps/s"
 
 
