@@ -174,7 +174,8 @@ struct Context {
   double dt = 0;
   DBuf gmass, gvel, gmom, gbc, gcn;
   DBuf bin_of, bin_counts, bin_start, bin_cursor, bin_pid, scan_tmp;
-  DBuf pbin, nb27, node_u;  // per-slot bin node, 27-neighbour table, nodal velocity of virtual_F
+  DBuf pbin, nb27, node_u;
+  DBuf svd;  // U s V of every particle's virtual F at the solve's initial dv (21 doubles SoA)  // per-slot bin node, 27-neighbour table, nodal velocity of virtual_F
   DBuf mats_d, cols_d;
 
   // solver vectors
@@ -583,13 +584,15 @@ struct Context {
   int* flag_bad() { return iflags.as<int>() + 0; }
 
   /// E(dv + alpha p) with stress stored for the gradient; returns through scal[0].
-  void energy_async(const double* dvp, const double* p, double alpha, bool want_stress) {
+  void energy_async(const double* dvp, const double* p, double alpha, bool want_stress, bool store_svd = false) {
     int h = prof_begin(P_ENERGY);
     double* part = partials.as<double>();
     node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
     launch_node_u(gview(), dvp, p, alpha, node_u.as<double>(), stream);
+    if (store_svd) svd.ensure(sizeof(double) * 21 * std::max<long long>(np, 1));
     launch_particle_energy(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
-                           want_stress ? stress.as<double>() : nullptr, part, nred, flag_bad(), stream);
+                           want_stress ? stress.as<double>() : nullptr, store_svd ? svd.as<double>() : nullptr, part,
+                           nred, flag_bad(), stream);
     launch_node_energy(gview(), dt, grav, dvp, p, alpha, part + nred, nred, stream);
     launch_sum_partials(part, 2 * nred, scal.as<double>() + 0, stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 27 * 28) + (want_stress ? 72.0 * np : 0.0));
@@ -625,15 +628,18 @@ struct Context {
     l.wave_rows.ensure(sizeof(int) * n);
   }
 
-  void assemble(const double* dvp, bool project) {
+  /// reuse_svd: the last energy evaluation stored the SVD at exactly this dv (solve_qn start).
+  void assemble(const double* dvp, bool project, bool reuse_svd = false) {
     Level& l0 = L[0];
     alloc_level(l0);
     int h = prof_begin(P_TENSORS);
     Tu.ensure(sizeof(double) * 126 * std::max<long long>(np, 1));
-    node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
-    launch_node_u(gview(), dvp, nullptr, 0.0, node_u.as<double>(), stream);
-    launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(), project ? 1 : 0, Tu.as<double>(),
-                            flag_bad(), stream);
+    if (!reuse_svd) {
+      node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
+      launch_node_u(gview(), dvp, nullptr, 0.0, node_u.as<double>(), stream);
+    }
+    launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
+                            reuse_svd ? svd.as<double>() : nullptr, project ? 1 : 0, Tu.as<double>(), flag_bad(), stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 126 * 8));  // x F vol mat in, kappa*T (packed) + W out
     h = prof_begin(P_ASSEMBLE);
     launch_fill_cols(l0.view(), stream);
@@ -898,7 +904,7 @@ struct Context {
     const double target = cfg.epsilon * std::sqrt((double)n);
     HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
     HOT_CUDA(cudaMemsetAsync(iflags.p, 0, sizeof(int) * 8, stream));
-    energy_async(dv.as<double>(), nullptr, 0.0, true);
+    energy_async(dv.as<double>(), nullptr, 0.0, true, /*store_svd=*/true);
     gradient_async(dv.as<double>(), g.as<double>());
     read_scalars(3, 2);
     check_flags();
@@ -908,7 +914,7 @@ struct Context {
       out.converged = true;
       return out;
     }
-    assemble(dv.as<double>(), true);
+    assemble(dv.as<double>(), true, /*reuse_svd=*/true);
     build_hierarchy(levels, cfg.embedding);
     for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
     if (std::getenv("HOT_VERBOSE"))

@@ -92,8 +92,8 @@ void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s);
 /// u = vel + (dv + alpha p) per node (p may be null): the nodal velocity the virtual F sees.
 void launch_node_u(GridView g, const double* dv, const double* p, double alpha, double* u, cudaStream_t s);
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                            const double* u, double* stress, double* partials, int nblocks, int* bad_flag,
-                            cudaStream_t s);
+                            const double* u, double* stress, double* svd_out, double* partials, int nblocks,
+                            int* bad_flag, cudaStream_t s);
 void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
                         double* partials, int nblocks, cudaStream_t s);
 /// g_i = dt * sum_p (V P F^T) grad w + m_i (dv_i - dt*grav); 0 on Dirichlet; partial sums of
@@ -124,7 +124,8 @@ void launch_final_velocity(GridView g, const double* dv, double* out, cudaStream
 
 // ---------------------------------------------------------------- assembly (k_assembly.cu)
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                             const double* u, int project, double* Tu, int* bad_flag, cudaStream_t s);
+                             const double* u, const double* svd_in, int project, double* Tu, int* bad_flag,
+                             cudaStream_t s);
 void launch_fill_cols(LevelView L, cudaStream_t s);
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, cudaStream_t s);

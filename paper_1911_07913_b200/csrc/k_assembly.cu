@@ -31,19 +31,30 @@ constexpr int kTPacked = 45;
 constexpr int kTensorStride = kTPacked + 81;
 
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
-                                   const DevMaterial* __restrict__ mats, const double* __restrict__ u, int project,
-                                   double* __restrict__ Tu, int* bad) {
+                                   const DevMaterial* __restrict__ mats, const double* __restrict__ u,
+                                   const double* __restrict__ svd_in, int project, double* __restrict__ Tu, int* bad) {
   const long long n = P.n;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-    M3 F, Fn;
-    if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
-      atomicExch(bad, 1);
-      continue;
+    M3 U, V, Fn;
+    double s[3];
+    if (svd_in) {  // SVD of the virtual F at this dv, stored by the energy evaluation
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        U.m[k] = svd_in[k * n + p];
+        V.m[k] = svd_in[(12 + k) * n + p];
+        Fn.m[k] = P.F[k * n + p];
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) s[k] = svd_in[(9 + k) * n + p];
+    } else {
+      M3 F;
+      if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
+        atomicExch(bad, 1);
+        continue;
+      }
+      svd3(F, U, s, V);
     }
     const DevMaterial mt = mats[P.mat[p]];
-    M3 U, V;
-    double s[3];
-    svd3(F, U, s, V);
     double T[45];
     fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
     double* out = Tu + p * kTensorStride;
@@ -329,9 +340,10 @@ int agrid(long long n, int threads) {
 }  // namespace
 
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                             const double* u, int project, double* Tu, int* bad_flag, cudaStream_t s) {
+                             const double* u, const double* svd_in, int project, double* Tu, int* bad_flag,
+                             cudaStream_t s) {
   if (P.n == 0) return;
-  { k_particle_tensors<<<agrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, u, project, Tu, bad_flag); count_launches(1); }
+  { k_particle_tensors<<<agrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag); count_launches(1); }
 }
 
 void launch_fill_cols(LevelView L, cudaStream_t s) {

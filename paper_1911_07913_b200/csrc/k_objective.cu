@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kEnergyThreads) k_particle_energy(ParticlesVie
                                                                  const DevMaterial* __restrict__ mats,
                                                                  const double* __restrict__ u,
                                                                  double* __restrict__ stress,
+                                                                 double* __restrict__ svd_out,
                                                                  double* __restrict__ partials, int* bad) {
   double acc = 0.0;
   const long long n = P.n;
@@ -58,6 +59,15 @@ __global__ void __launch_bounds__(kEnergyThreads) k_particle_energy(ParticlesVie
     M3 U, V;
     double s[3];
     svd3(F, U, s, V);
+    if (svd_out) {  // kept for the assembly at the same dv (k_particle_tensors)
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        svd_out[k * n + p] = U.m[k];
+        svd_out[(12 + k) * n + p] = V.m[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) svd_out[(9 + k) * n + p] = s[k];
+    }
     const double vol = P.vol[p];
     acc += vol * fcr_psi(s, mt.mu, mt.lambda);
     if (stress) {
@@ -257,9 +267,9 @@ int vgrid(long long n) {
 }  // namespace
 
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                            const double* u, double* stress, double* partials, int nblocks, int* bad_flag,
-                            cudaStream_t s) {
-  { k_particle_energy<<<nblocks, kEnergyThreads, 0, s>>>(P, g, dx, dt, mats, u, stress, partials, bad_flag); count_launches(1); }
+                            const double* u, double* stress, double* svd_out, double* partials, int nblocks,
+                            int* bad_flag, cudaStream_t s) {
+  { k_particle_energy<<<nblocks, kEnergyThreads, 0, s>>>(P, g, dx, dt, mats, u, stress, svd_out, partials, bad_flag); count_launches(1); }
 }
 
 void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
