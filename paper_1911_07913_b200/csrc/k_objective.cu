@@ -41,7 +41,7 @@ __device__ __forceinline__ double block_sum(double v) {
 
 constexpr int kEnergyThreads = 128;  // ~146 registers: 3 blocks (12 warps) per SM
 
-__global__ void __launch_bounds__(kEnergyThreads) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
+__global__ void __launch_bounds__(kEnergyThreads, 4) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
                                                                  const DevMaterial* __restrict__ mats,
                                                                  const double* __restrict__ u,
                                                                  double* __restrict__ stress,
