@@ -112,10 +112,19 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
 /// (bin o's lanes, then the mirror's: fixed order, no atomics).
 constexpr int kAsmChunk = 2;                                  // particles per bin per stage
 constexpr int kAsmStage = 2 * kAsmChunk * kTensorStride;       // doubles: [bin of pair][particle][...]
-constexpr int kAsmWarpDoubles = 2 * kAsmStage + 2 * 2 * 28 + kUpper * 9 + 1 + 2;  // + 2 mbarriers; even
+constexpr int kAsmM = 36;  // M[ce*4 + g] of one bin, g = 3 padded with zero (the DMMA K = 4)
+constexpr int kAsmWarpDoubles = 2 * kAsmStage + 2 * 2 * kAsmM + kUpper * 9 + 1 + 2 + 28;  // + pad + 2 mbarriers + pair table; even
 constexpr int kAsmSmem = kAsmWarps * kAsmWarpDoubles * 8;
 constexpr unsigned kParticleBytes = kTensorStride * 8;  // 1008 = 63 x 16
 static_assert(kAsmWarpDoubles % 2 == 0, "16-byte aligned per-warp smem");
+
+/// D = A B + D on the fp64 tensor cores: m8n8k4, A row-major (lane: row lane/4, col lane%4),
+/// B column-major (lane: row lane%4, col lane/4), C/D (lane: row lane/4, cols 2(lane%4)+{0,1}).
+__device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 
 __device__ __forceinline__ int tpack(int r, int c) {  // index of T[r][c] in the packed upper triangle
   if (r > c) {
@@ -134,8 +143,9 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
   double* base = asm_smem + (size_t)wid * kAsmWarpDoubles;
   double* Sbuf = base;
   double* Mbuf = base + 2 * kAsmStage;
-  double* acc = Mbuf + 2 * 2 * 28;
+  double* acc = Mbuf + 2 * 2 * kAsmM;
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(acc + kUpper * 9 + 1);
+  int* PT = reinterpret_cast<int*>(acc + kUpper * 9 + 1 + 2);  // [14][pb1, n1, pb2, n2]
   if (lane == 0) {
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
@@ -143,11 +153,14 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
   }
   __syncwarp();
   unsigned phase = 0;  // bit b: parity of the next completion of buffer b
+  for (int q = lane; q < 2 * 2 * kAsmM; q += 32) Mbuf[q] = 0.0;  // the g = 3 pads stay zero
+  __syncwarp();
   // lane's M entry (c,e,g) = lane: packed T indices of T[(3c+f),(3e+g)], f = 0..2
   const int lc = lane / 9, le = (lane / 3) % 3, lg = lane % 3;
   const int tp0 = lane < 27 ? tpack(3 * lc, 3 * le + lg) : 0;
   const int tp1 = lane < 27 ? tpack(3 * lc + 1, 3 * le + lg) : 0;
   const int tp2 = lane < 27 ? tpack(3 * lc + 2, 3 * le + lg) : 0;
+  const int mi = (3 * lc + le) * 4 + lg;  // lane's M entry in M[ce*4 + g]
   const int nwarps = gridDim.x * kAsmWarps;
   for (int i = blockIdx.x * kAsmWarps + wid; i < L.n; i += nwarps) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
@@ -161,132 +174,152 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
         my_np = __ldg(bins.start + j + 1) - my_pb;
       }
     }
-    // pair q = lane < 14: bins q and 26-q (q = 13: the centre bin alone); chunk schedule
-    const int q_pb1 = my_pb, q_n1 = my_np;
-    const int q_pb2 = __shfl_sync(0xffffffffu, my_pb, 26 - min(lane, 26));
-    const int q_n2_all = __shfl_sync(0xffffffffu, my_np, 26 - min(lane, 26));
-    const int q_n2 = lane < 13 ? q_n2_all : 0;
-    const int q_nch = lane < 14 ? (max(q_n1, q_n2) + kAsmChunk - 1) / kAsmChunk : 0;
-    int incl = q_nch;
-#pragma unroll
-    for (int d = 1; d < 16; d <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
+    // pair q < 14: bins q and 26-q (q = 13: the centre bin alone); its table row in shared memory
+    {
+      const int pb2 = __shfl_sync(0xffffffffu, my_pb, 26 - min(lane, 26));
+      const int n2 = __shfl_sync(0xffffffffu, my_np, 26 - min(lane, 26));
+      if (lane < 14) {
+        PT[4 * lane] = my_pb;
+        PT[4 * lane + 1] = my_np;
+        PT[4 * lane + 2] = pb2;
+        PT[4 * lane + 3] = lane < 13 ? n2 : 0;
+      }
+      __syncwarp();
     }
-    const int q_cstart = incl - q_nch;
-    const int nchunks = __shfl_sync(0xffffffffu, incl, 13);
-    const unsigned has = __ballot_sync(0xffffffffu, q_nch > 0);
-    auto chunk_pair = [&](int f) {  // pair of flat chunk f
-      const unsigned m = __ballot_sync(0xffffffffu, q_nch > 0 && q_cstart <= f) & has;
-      return 31 - __clz(m);
-    };
-    auto issue = [&](int f, int buf) {  // lane 0: bulk-copy chunk f into buffer buf
-      const int q = chunk_pair(f);
-      const int c0 = (f - __shfl_sync(0xffffffffu, q_cstart, q)) * kAsmChunk;
-      const int pb1 = __shfl_sync(0xffffffffu, q_pb1, q), n1 = __shfl_sync(0xffffffffu, q_n1, q);
-      const int pb2 = __shfl_sync(0xffffffffu, q_pb2, q), n2 = __shfl_sync(0xffffffffu, q_n2, q);
-      if (lane == 0) {
-        const int k1 = max(0, min(kAsmChunk, n1 - c0)), k2 = max(0, min(kAsmChunk, n2 - c0));
-        const unsigned mb = smem_u32(mbar + buf);
-        double* dst = Sbuf + buf * kAsmStage;
-        mbar_expect_tx(mb, (k1 + k2) * kParticleBytes);
-        if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0) * kTensorStride, k1 * kParticleBytes, mb);
-        if (k2)
-          bulk_g2s(dst + kAsmChunk * kTensorStride, Tu + (long long)(pb2 + c0) * kTensorStride, k2 * kParticleBytes,
-                   mb);
+    // lane 0 runs the bulk-copy producer one chunk ahead along (pair, c0)
+    int pq_n = 0, c0_n = 0;  // next chunk to issue (lane 0)
+    auto advance = [&]() {   // lane 0: move (pq_n, c0_n) to the next non-empty chunk
+      c0_n += kAsmChunk;
+      while (pq_n < 14 && c0_n >= max(PT[4 * pq_n + 1], PT[4 * pq_n + 3])) {
+        ++pq_n;
+        c0_n = 0;
       }
     };
-    if (nchunks > 0) issue(0, 0);
-    int cur_q = -1, n1 = 0, n2 = 0, mpar = 0;
-    double Cr[9];
-    int job_bin = 0, job_k = 0, job_slot = 0;
-    bool job = false;
-    auto flush = [&]() {  // fold the pair's register blocks into the row accumulator, bin by bin
+    auto issue = [&](int buf) {  // lane 0
+      const int pb1 = PT[4 * pq_n], n1 = PT[4 * pq_n + 1], pb2 = PT[4 * pq_n + 2], n2 = PT[4 * pq_n + 3];
+      const int k1 = max(0, min(kAsmChunk, n1 - c0_n)), k2 = max(0, min(kAsmChunk, n2 - c0_n));
+      const unsigned mb = smem_u32(mbar + buf);
+      double* dst = Sbuf + buf * kAsmStage;
+      mbar_expect_tx(mb, (k1 + k2) * kParticleBytes);
+      if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0_n) * kTensorStride, k1 * kParticleBytes, mb);
+      if (k2)
+        bulk_g2s(dst + kAsmChunk * kTensorStride, Tu + (long long)(pb2 + c0_n) * kTensorStride, k2 * kParticleBytes,
+                 mb);
+    };
+    if (lane == 0) {
+      pq_n = 0;
+      c0_n = -kAsmChunk;
+      advance();
+      if (pq_n < 14) issue(0);
+      advance();
+    }
+    int buf = 0, mpar = 0;
+    const int qk = lane & 3, qm = lane >> 2;
+    for (int pq = 0; pq < 14; ++pq) {
+      const int n1 = PT[4 * pq + 1], n2 = PT[4 * pq + 3];
+      const int nmax = max(n1, n2);
+      if (nmax == 0) continue;
+      // bin b's upper stencil positions: the suffix k >= kmin_b (slot S(k) + S(o_b) >= 62,
+      // S(v) = 25 v0 + 5 v1 + v2); o_0 = pq, o_1 = 26 - pq (S(o_1) = 62 - S(o_0))
+      const int So0 = 25 * (pq / 9) + 5 * ((pq / 3) % 3) + pq % 3, So1 = 62 - So0;
+      int kmin0 = 27, kmin1 = 27;
+      for (int k = 26; k >= 0; --k) {
+        const int Sk = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3;
+        if (Sk + So0 >= kDiagSlot) kmin0 = k;
+        if (Sk + So1 >= kDiagSlot) kmin1 = k;
+      }
+      if (pq == 13) kmin1 = 27;  // the centre bin has no mirror
+      // C_b[k - kmin_b][ce] += sum_g W_t[k][g] M_b[ce][g]: per particle a rank-3 update on the
+      // fp64 tensor cores (DMMA m8n8k4): M = upper positions (<= 4 tiles), N = ce (2), K = g (3 -> 4)
+      double C0[4][2][2], C1[4][2][2];
 #pragma unroll
-      for (int phase_b = 0; phase_b < 2; ++phase_b) {
-        if (job && job_bin == phase_b) {
-          if (job_slot == kDiagSlot) {  // symmetrise the diagonal contribution (objective.hpp:349-351)
-            const double t01 = 0.5 * (Cr[1] + Cr[3]), t02 = 0.5 * (Cr[2] + Cr[6]), t12 = 0.5 * (Cr[5] + Cr[7]);
-            Cr[1] = Cr[3] = t01;
-            Cr[2] = Cr[6] = t02;
-            Cr[5] = Cr[7] = t12;
-          }
-          double* ap = acc + (job_slot - kDiagSlot) * 9;
+      for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-          for (int k = 0; k < 9; ++k) ap[k] += Cr[k];
+        for (int nt = 0; nt < 2; ++nt) C0[mt][nt][0] = C0[mt][nt][1] = C1[mt][nt][0] = C1[mt][nt][1] = 0.0;
+      for (int c0 = 0; c0 < nmax; c0 += kAsmChunk) {
+        if (lane == 0) {
+          if (pq_n < 14) issue(buf ^ 1);
+          advance();
         }
-        __syncwarp();
-      }
-    };
-    for (int f = 0; f < nchunks; ++f) {
-      const int buf = f & 1;
-      if (f + 1 < nchunks) issue(f + 1, buf ^ 1);
-      const int pq = chunk_pair(f);
-      const int pc0 = (f - __shfl_sync(0xffffffffu, q_cstart, pq)) * kAsmChunk;
-      if (pq != cur_q) {
-        if (cur_q >= 0) flush();
-        cur_q = pq;
-        n1 = __shfl_sync(0xffffffffu, q_n1, pq);
-        n2 = __shfl_sync(0xffffffffu, q_n2, pq);
-        // this lane's job in the pair: its stencil position in bin pq if that slot is upper,
-        // else position 26-lane in the mirror bin; lane 27: the mirror bin's diagonal
-        const int o0 = pq / 9, o1 = (pq / 3) % 3, o2 = pq % 3;
-        job = false;
-        if (lane < 27) {
-          const int s = 25 * (lc + o0) + 5 * (le + o1) + (lg + o2);
-          if (s >= kDiagSlot) {
-            job = true, job_bin = 0, job_k = lane, job_slot = s;
-          } else if (pq != 13) {
-            job = true, job_bin = 1, job_k = 26 - lane, job_slot = kSlots - 1 - s;
+        mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+        const double* S = Sbuf + buf * kAsmStage;
+        const int tcount = min(kAsmChunk, nmax - c0);
+        for (int t = 0; t < tcount; ++t) {
+          const bool v1 = c0 + t < n1, v2 = c0 + t < n2;
+          const double* P1 = S + t * kTensorStride;
+          const double* P2 = S + (kAsmChunk + t) * kTensorStride;
+          double* M = Mbuf + mpar * 2 * kAsmM;
+          if (lane < 27) {  // lane (c,e,g): M_b[ce][g] = sum_f W_a[f] T[(3c+f),(3e+g)]
+            if (v1) {
+              const double* Wa = P1 + kTPacked + 3 * (26 - pq);
+              M[mi] = Wa[0] * P1[tp0] + Wa[1] * P1[tp1] + Wa[2] * P1[tp2];
+            }
+            if (v2) {
+              const double* Wa = P2 + kTPacked + 3 * pq;
+              M[kAsmM + mi] = Wa[0] * P2[tp0] + Wa[1] * P2[tp1] + Wa[2] * P2[tp2];
+            }
           }
-        } else if (lane == 27 && pq != 13) {
-          job = true, job_bin = 1, job_k = pq, job_slot = kDiagSlot;
-        }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) Cr[k] = 0.0;
-      }
-      mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-      const int ka1 = 26 - pq, ka2 = pq;  // row i's stencil position in bin pq / in the mirror bin
-      const double* S = Sbuf + buf * kAsmStage;
-      const int tcount = min(kAsmChunk, max(n1, n2) - pc0);
-      for (int t = 0; t < tcount; ++t) {
-        const bool v1 = pc0 + t < n1, v2 = pc0 + t < n2;
-        const double* P1 = S + t * kTensorStride;
-        const double* P2 = S + (kAsmChunk + t) * kTensorStride;
-        double* M = Mbuf + mpar * 56;
-        if (lane < 27) {
+          __syncwarp();
           if (v1) {
-            const double* Wa = P1 + kTPacked + 3 * ka1;
-            M[lane] = Wa[0] * P1[tp0] + Wa[1] * P1[tp1] + Wa[2] * P1[tp2];
-          }
-          if (v2) {
-            const double* Wa = P2 + kTPacked + 3 * ka2;
-            M[28 + lane] = Wa[0] * P2[tp0] + Wa[1] * P2[tp1] + Wa[2] * P2[tp2];
-          }
-        }
-        __syncwarp();
-        if (job && (job_bin == 0 ? v1 : v2)) {
-          const double* P = job_bin == 0 ? P1 : P2;
-          const double* Ms = M + 28 * job_bin;
-          const double wB0 = P[kTPacked + 3 * job_k], wB1 = P[kTPacked + 3 * job_k + 1],
-                       wB2 = P[kTPacked + 3 * job_k + 2];
-          double m[28];
+            const double bf0 = M[qm * 4 + qk], bf1 = qm == 0 ? M[32 + qk] : 0.0;
 #pragma unroll
-          for (int u = 0; u < 14; ++u) {
-            const double2 v = reinterpret_cast<const double2*>(Ms)[u];
-            m[2 * u] = v.x;
-            m[2 * u + 1] = v.y;
+            for (int mt = 0; mt < 4; ++mt) {
+              const int kk = kmin0 + 8 * mt + qm;
+              if (kmin0 + 8 * mt > 26) break;
+              const double af = (kk <= 26 && qk < 3) ? P1[kTPacked + 3 * kk + qk] : 0.0;
+              dmma_f64(C0[mt][0], af, bf0);
+              dmma_f64(C0[mt][1], af, bf1);
+            }
           }
+          if (v2 && kmin1 <= 26) {
+            const double bf0 = M[kAsmM + qm * 4 + qk], bf1 = qm == 0 ? M[kAsmM + 32 + qk] : 0.0;
 #pragma unroll
-          for (int ce = 0; ce < 9; ++ce) Cr[ce] += m[3 * ce] * wB0 + m[3 * ce + 1] * wB1 + m[3 * ce + 2] * wB2;
+            for (int mt = 0; mt < 4; ++mt) {
+              const int kk = kmin1 + 8 * mt + qm;
+              if (kmin1 + 8 * mt > 26) break;
+              const double af = (kk <= 26 && qk < 3) ? P2[kTPacked + 3 * kk + qk] : 0.0;
+              dmma_f64(C1[mt][0], af, bf0);
+              dmma_f64(C1[mt][1], af, bf1);
+            }
+          }
+          mpar ^= 1;  // M is double buffered: the next particle's M may be written before stragglers read
         }
-        mpar ^= 1;  // M is double buffered: the next particle's M may be written before stragglers read
+        __syncwarp();  // buffer buf is refilled by the next iteration's issue
+        buf ^= 1;
       }
-      __syncwarp();  // buffer buf is refilled by the next iteration's issue
+      // fold the pair's accumulators into the row: bin 0, then the mirror bin
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int k = kmin0 + 8 * mt + qm;
+        if (k <= 26) {
+          const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 + So0 - kDiagSlot;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int n = 8 * nt + 2 * qk + v;
+              if (n < 9) acc[su * 9 + n] += C0[mt][nt][v];
+            }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int k = kmin1 + 8 * mt + qm;
+        if (k <= 26) {
+          const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 + So1 - kDiagSlot;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int n = 8 * nt + 2 * qk + v;
+              if (n < 9) acc[su * 9 + n] += C1[mt][nt][v];
+            }
+        }
+      }
+      __syncwarp();
     }
-    if (cur_q >= 0) flush();
-    __syncwarp();
     // write-out: upper slots + transposed mirror, mass diagonal, Dirichlet projection
     const bool di = g.dir[i] != 0;
     const double mi = g.mass[i];
@@ -307,7 +340,11 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
         if (di) {
 #pragma unroll
           for (int k = 0; k < 9; ++k) C[k] = (k % 4 == 0) ? 1.0 : 0.0;
-        } else {
+        } else {  // symmetrise (objective.hpp:349-351), then the mass diagonal
+          const double t01 = 0.5 * (C[1] + C[3]), t02 = 0.5 * (C[2] + C[6]), t12 = 0.5 * (C[5] + C[7]);
+          C[1] = C[3] = t01;
+          C[2] = C[6] = t02;
+          C[5] = C[7] = t12;
           C[0] += mi;
           C[4] += mi;
           C[8] += mi;
