@@ -88,21 +88,47 @@ __global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, uint8_t* __restri
 constexpr int kGalX = 64 * 9;  // doubles of X per fine row
 constexpr int kGalXWarps = 4;
 
+constexpr int kGalXStages = 2;
+constexpr int kGalXRowBytes = 9 * kSlotPitch * 8;  // 9216: one fine row's blocks, contiguous
+constexpr int kGalXSmem = kGalXWarps * (kGalXStages * kGalXRowBytes + kGalXStages * 8);
+
+/// Stage 1 of the Galerkin product, HBM-streaming: each warp keeps kGalXStages fine rows in
+/// flight through the bulk-copy engine (one 9 KB cp.async.bulk per row, mbarrier completion)
+/// while it contracts the previous row into its 64 coarse targets.
 __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, double* __restrict__ X) {
-  __shared__ double hs[kGalXWarps][9 * kSlotPitch];
+  extern __shared__ __align__(128) unsigned char gx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  double* H = hs[wib];
+  unsigned char* ring = gx_smem + (size_t)wib * kGalXStages * kGalXRowBytes;
+  unsigned long long* mb =
+      reinterpret_cast<unsigned long long*>(gx_smem + (size_t)kGalXWarps * kGalXStages * kGalXRowBytes) +
+      wib * kGalXStages;
+  unsigned long long policy = 0;
+  if (lane == 0) {
+    policy = l2_evict_first_policy();
+    for (int s = 0; s < kGalXStages; ++s) mbar_init(mb + s, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](int row, int s) {  // lane 0
+    const unsigned bar = smem_u32(mb + s);
+    mbar_expect_tx(bar, kGalXRowBytes);
+    bulk_g2s_hint(ring + (size_t)s * kGalXRowBytes, f.H + (long long)row * 9 * kSlotPitch, kGalXRowBytes, bar, policy);
+  };
+  if (lane == 0)
+    for (int s = 0; s < kGalXStages; ++s)
+      if (gw + s * nw < f.n) issue(gw + s * nw, s);
+  unsigned phase_bits = 0;
+  int s = 0;
   for (int i = gw; i < f.n; i += nw) {
-    const double* src = f.H + (long long)i * 9 * kSlotPitch;
-    __syncwarp();
-    for (int q = lane; q < 9 * kSlotPitch; q += 32) H[q] = __ldcs(src + q);
-    __syncwarp();
+    mbar_wait(smem_u32(mb + s), (phase_bits >> s) & 1u);
+    phase_bits ^= 1u << s;
+    const double* H = reinterpret_cast<const double*>(ring + (size_t)s * kGalXRowBytes);
     int base[3];  // 2*(floor(c/2)-1) - c: -2 (even) or -3 (odd)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const int c = f.coords[3 * i + a];
+      const int c = __ldg(f.coords + 3 * i + a);
       base[a] = 2 * ((c >> 1) - 1) - c;
     }
     for (int tq = lane; tq < 64; tq += 32) {
@@ -123,9 +149,9 @@ __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, dou
             const int f2 = 2 * t2 + d2 + base[2];
             if (f2 < -2 || f2 > 2) continue;
             const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
-            const int s = 25 * (f0 + 2) + 5 * (f1 + 2) + (f2 + 2);
+            const int sl = 25 * (f0 + 2) + 5 * (f1 + 2) + (f2 + 2);
 #pragma unroll
-            for (int k = 0; k < 9; ++k) acc[k] += w * H[k * kSlotPitch + s];  // zero when l is inactive
+            for (int k = 0; k < 9; ++k) acc[k] += w * H[k * kSlotPitch + sl];  // zero when l is inactive
           }
         }
       }
@@ -133,6 +159,9 @@ __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, dou
 #pragma unroll
       for (int k = 0; k < 9; ++k) dst[k] = acc[k];
     }
+    __syncwarp();  // the stage is refilled below
+    if (lane == 0 && i + kGalXStages * nw < f.n) issue(i + kGalXStages * nw, s);
+    s = s + 1 == kGalXStages ? 0 : s + 1;
   }
 }
 
@@ -997,7 +1026,12 @@ void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaS
 }
 void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s) {
   if (coarse.n == 0) return;
-  { k_galerkin_x<<<mgrid((long long)fine.n * 32, kGalXWarps * 32), kGalXWarps * 32, 0, s>>>(fine, X); count_launches(1); }
+  static const int gx_blocks = coop_blocks((const void*)k_galerkin_x, kGalXWarps * 32, kGalXSmem);
+  {
+    const int blocks = (int)std::min<long long>(gx_blocks, ((long long)fine.n + kGalXWarps - 1) / kGalXWarps);
+    k_galerkin_x<<<std::max(1, blocks), kGalXWarps * 32, kGalXSmem, s>>>(fine, X);
+    count_launches(1);
+  }
   { k_galerkin_c<<<mgrid((long long)coarse.n * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X); count_launches(1); }
 }
 void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
