@@ -181,6 +181,7 @@ struct Context {
   // solver vectors
   DBuf dv, g, gnew, pdir, q, stress, Tu, vout, hist_s[kMaxWindow + 1], hist_y[kMaxWindow + 1];
   DBuf pcg_r, pcg_z, pcg_p, pcg_Ap, sgs_trace, gal_x;
+  DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
   int* host_int = nullptr;      // pinned
@@ -632,6 +633,19 @@ struct Context {
   void assemble(const double* dvp, bool project, bool reuse_svd = false) {
     Level& l0 = L[0];
     alloc_level(l0);
+    particle_tensors(dvp, project, reuse_svd);
+    const int h = prof_begin(P_ASSEMBLE);
+    launch_fill_cols(l0.view(), stream);
+    launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), stream);
+    // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
+    prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
+    have_H = true;
+    nlevels = 1;
+  }
+
+  /// Per-particle kappa * dP/dF (projected) and the 27 W_k vectors at dv (assemble_hessian's
+  /// particle half, objective.hpp:322-340).
+  void particle_tensors(const double* dvp, bool project, bool reuse_svd) {
     int h = prof_begin(P_TENSORS);
     Tu.ensure(sizeof(double) * 126 * std::max<long long>(np, 1));
     if (!reuse_svd) {
@@ -641,13 +655,6 @@ struct Context {
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
                             reuse_svd ? svd.as<double>() : nullptr, project ? 1 : 0, Tu.as<double>(), flag_bad(), stream);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 126 * 8));  // x F vol mat in, kappa*T (packed) + W out
-    h = prof_begin(P_ASSEMBLE);
-    launch_fill_cols(l0.view(), stream);
-    launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), stream);
-    // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
-    prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
-    have_H = true;
-    nlevels = 1;
   }
 
   /// Diag inverse + wave schedule for level m (multigrid.hpp:227-251).
@@ -894,6 +901,34 @@ struct Context {
     bool converged = false;
   };
 
+  /// accept()'s line search (solvers.hpp:66-78, 169-175): g.p, then Armijo backtracking from
+  /// alpha = 1 on E(dv + alpha p).  Returns alpha; e_trial = E at it.  host_int[0..2] hold the
+  /// flags after the first trial (iflags[2]: inner iterations of the direction).
+  double line_search(const double* pd, double e_curr, double& e_trial) {
+    const long long n3 = 3LL * L[0].n;
+    const int hv = prof_begin(P_VEC);
+    launch_dot_partials(g.as<double>(), pd, n3, partials.as<double>() + 3 * nred, nred, stream);
+    launch_sum_partials(partials.as<double>() + 3 * nred, nred, scal.as<double>() + 1, stream);
+    prof_end(hv, 16.0 * n3);
+    double alpha = 1.0;
+    energy_async(dv.as<double>(), pd, alpha, true);
+    read_scalars(2, 3);
+    check_flags();
+    const double gdotp = host_scal[1];
+    if (!(gdotp < 0.0)) throw SolverFailure("line_search: not a descent direction");
+    e_trial = host_scal[0];
+    int k = 0;
+    while (!(e_trial <= e_curr + cfg.ls_armijo * alpha * gdotp)) {
+      if (++k >= cfg.ls_max_steps) throw SolverFailure("line_search: no acceptable step (gradient/Hessian inconsistency)");
+      alpha *= cfg.ls_shrink;
+      energy_async(dv.as<double>(), pd, alpha, true);
+      read_scalars(1, 1);
+      check_flags();
+      e_trial = host_scal[0];
+    }
+    return alpha;
+  }
+
   /// solve_quasi_newton (solvers.hpp:191-231); dv result in this->dv.
   SolveOut solve_qn(int levels, int frame_no, long long step_no) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -932,26 +967,8 @@ struct Context {
       HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 2, 0, sizeof(int), stream));
       lbfgs_direction(hist, pdir.as<double>());
       // accept(): g.p then the Armijo backtracking (solvers.hpp:66-78, 169-186)
-      const int hv = prof_begin(P_VEC);
-      launch_dot_partials(g.as<double>(), pdir.as<double>(), n3, partials.as<double>() + 3 * nred, nred, stream);
-      launch_sum_partials(partials.as<double>() + 3 * nred, nred, scal.as<double>() + 1, stream);
-      prof_end(hv, 16.0 * n3);
-      double alpha = 1.0;
-      energy_async(dv.as<double>(), pdir.as<double>(), alpha, true);
-      read_scalars(2, 3);
-      check_flags();
-      const double gdotp = host_scal[1];
-      if (!(gdotp < 0.0)) throw SolverFailure("line_search: not a descent direction");
-      double e_trial = host_scal[0];
-      int k = 0;
-      while (!(e_trial <= e_curr + cfg.ls_armijo * alpha * gdotp)) {
-        if (++k >= cfg.ls_max_steps) throw SolverFailure("line_search: no acceptable step (gradient/Hessian inconsistency)");
-        alpha *= cfg.ls_shrink;
-        energy_async(dv.as<double>(), pdir.as<double>(), alpha, true);
-        read_scalars(1, 1);
-        check_flags();
-        e_trial = host_scal[0];
-      }
+      double e_trial = 0.0;
+      const double alpha = line_search(pdir.as<double>(), e_curr, e_trial);
       // s = alpha p ; dv += s ; g_new ; y = g_new - g
       const int slot = next_slot(hist);
       const int hv3 = prof_begin(P_VEC);
@@ -1016,10 +1033,178 @@ struct Context {
     return 0;
   }
 
+  /// Host-driven PCG on level 0 (pcg.hpp:17-46): x = 0, stop on sqrt(r.z) <= rel sqrt(r0.z0).
+  /// apply_a(in, out), apply_p(in, out) are device operators.  Returns the iteration count.
+  template <class ApplyA, class ApplyP>
+  int pcg_level0(ApplyA&& apply_a, ApplyP&& apply_p, const double* b, double* x, double rel, int cap) {
+    const int n = L[0].n;
+    const long long n3 = 3LL * n;
+    double* r = pn_r.as<double>();
+    double* z = pn_z.as<double>();
+    double* p = pn_p.as<double>();
+    double* Ap = pn_Ap.as<double>();
+    double* part = partials.as<double>() + 3 * nred;
+    auto dot = [&](const double* a, const double* bb) {
+      launch_dot_partials(a, bb, n3, part, nred, stream);
+      launch_sum_partials(part, nred, scal.as<double>() + 7, stream);
+      HOT_CUDA(cudaMemcpyAsync(host_scal + 7, scal.as<double>() + 7, sizeof(double), cudaMemcpyDeviceToHost, stream));
+      sync();
+      check_launch();
+      return host_scal[7];
+    };
+    HOT_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n3, stream));
+    HOT_CUDA(cudaMemcpyAsync(r, b, sizeof(double) * n3, cudaMemcpyDeviceToDevice, stream));
+    apply_p(r, z);
+    double rho = dot(r, z);
+    if (!(rho > 0.0)) {
+      if (rho < 0.0) throw SolverFailure("pcg: preconditioner is not positive definite");
+      return 0;  // b == 0
+    }
+    const double threshold = rel * rel * rho;
+    HOT_CUDA(cudaMemcpyAsync(p, z, sizeof(double) * n3, cudaMemcpyDeviceToDevice, stream));
+    int its = 0;
+    for (int it = 0; it < cap; ++it) {
+      apply_a(p, Ap);
+      const double pAp = dot(p, Ap);
+      if (!(pAp > 0.0)) throw SolverFailure("pcg: system matrix is not positive definite");
+      const double alpha = rho / pAp;
+      launch_pcg_xr(x, r, p, Ap, alpha, n3, stream);
+      apply_p(r, z);
+      const double rho_new = dot(r, z);
+      its = it + 1;
+      if (rho_new <= threshold) break;
+      launch_pcg_p(p, z, rho_new / rho, n3, stream);
+      rho = rho_new;
+    }
+    return its;
+  }
+
+  /// solve_projected_newton (solvers.hpp:235-300): variant 0 assembled Jacobi-PCG (pn-pcg),
+  /// 1 matrix-free Jacobi-PCG (pn-pcg-mf), 2 V-cycle-preconditioned PCG (pn-mgpcg).  The
+  /// Newton model (projected Hessian, its block diagonal, the hierarchy) is rebuilt at every
+  /// outer iterate; the inner tolerance is adaptive (solvers.hpp:62-64).
+  SolveOut solve_pn(int variant, int frame_no, long long step_no) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = L[0].n;
+    const long long n3 = 3LL * n;
+    SolveOut out;
+    const double target = cfg.epsilon * std::sqrt((double)n);
+    HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
+    HOT_CUDA(cudaMemsetAsync(iflags.p, 0, sizeof(int) * 8, stream));
+    energy_async(dv.as<double>(), nullptr, 0.0, true);
+    gradient_async(dv.as<double>(), g.as<double>());
+    read_scalars(3, 2);
+    check_flags();
+    double e_curr = host_scal[0];
+    double residual = std::sqrt(host_scal[2]);
+    if (residual <= target) {
+      out.converged = true;
+      return out;
+    }
+    const size_t vb = sizeof(double) * std::max<long long>(n3, 1);
+    for (DBuf* d : {&pn_b, &pn_x, &pn_r, &pn_z, &pn_p, &pn_Ap}) d->ensure(vb);
+    long long work = 0;
+    for (int outer = 1; outer <= cfg.outer_cap; ++outer) {
+      HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 2, 0, sizeof(int), stream));
+      const double* Dinv = nullptr;
+      if (variant == 1) {
+        particle_tensors(dv.as<double>(), true, false);
+        pn_dinv.ensure(sizeof(double) * 9 * std::max(n, 1));
+        launch_mf_block_diag_inv(pview(), bview(), gview(), Tu.as<double>(), pn_dinv.as<double>(), stream);
+        Dinv = pn_dinv.as<double>();
+      } else {
+        assemble(dv.as<double>(), true);
+        build_hierarchy(variant == 2 ? cfg.levels : 1, cfg.embedding);
+        for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
+        Dinv = L[0].dinv.as<double>();
+      }
+      // gpg = g^T D^-1 g (solvers.hpp:263-268); k = adaptive_cg_tolerance
+      launch_block_apply(Dinv, g.as<double>(), pn_z.as<double>(), n, stream);
+      launch_dot_partials(g.as<double>(), pn_z.as<double>(), n3, partials.as<double>() + 3 * nred, nred, stream);
+      launch_sum_partials(partials.as<double>() + 3 * nred, nred, scal.as<double>() + 7, stream);
+      HOT_CUDA(cudaMemcpyAsync(host_scal + 7, scal.as<double>() + 7, sizeof(double), cudaMemcpyDeviceToHost, stream));
+      sync();
+      const double gpg = host_scal[7];
+      const double k = std::min(0.5, std::sqrt(std::max(std::sqrt(gpg), cfg.tau)));
+      launch_neg_copy(g.as<double>(), pn_b.as<double>(), n3, stream);
+      long long inner_this = 0;
+      const int hp = prof_begin(P_PCG);
+      if (variant == 0) {  // Jacobi-PCG on the assembled matrix: the cooperative kernel
+        launch_pcg(L[0].view(), pn_b.as<double>(), pn_x.as<double>(), pn_r.as<double>(), pn_z.as<double>(),
+                   pn_p.as<double>(), pn_Ap.as<double>(), k, cfg.cg_cap, partials.as<double>() + 6 * nred,
+                   iflags.as<int>() + 4, iflags.as<int>() + 2, coop_grid(pcg_max_blocks(), n, 8, 4), stream);
+        copy_status();
+        read_scalars(0, 3);
+        check_flags();
+        inner_this = host_int[2];
+      } else if (variant == 1) {
+        pn_dP.ensure(sizeof(double) * 9 * std::max<long long>(np, 1));
+        inner_this = pcg_level0(
+            [&](const double* in, double* o) {
+              launch_mf_multiply(pview(), bview(), gview(), Tu.as<double>(), in, pn_dP.as<double>(), o, stream);
+            },
+            [&](const double* in, double* o) { launch_block_apply(Dinv, in, o, n, stream); }, pn_b.as<double>(),
+            pn_x.as<double>(), k, cfg.cg_cap);
+      } else {
+        int its = pcg_level0([&](const double* in, double* o) { launch_spmv(L[0].view(), in, o, stream); },
+                             [&](const double* in, double* o) {
+                               vcycle(in, o, true, cfg.pinned_coarse_iterations);
+                             },
+                             pn_b.as<double>(), pn_x.as<double>(), k, cfg.cg_cap);
+        read_scalars(0, 3);
+        check_flags();
+        inner_this = its + host_int[2];  // + the pinned coarse solves' iterations
+      }
+      prof_end(hp);
+      double e_trial = 0.0;
+      const double alpha = line_search(pn_x.as<double>(), e_curr, e_trial);
+      launch_add_scaled(dv.as<double>(), pn_x.as<double>(), alpha, dv.as<double>(), n3, stream);
+      gradient_async(dv.as<double>(), g.as<double>());
+      read_scalars(3, 2);
+      check_flags();
+      residual = std::sqrt(host_scal[2]);
+      e_curr = e_trial;
+      work += inner_this;
+      hot_diag_row row;
+      row.frame = frame_no;
+      row.step = step_no;
+      row.outer_iteration = outer;
+      row.scaled_residual = residual;
+      row.energy = e_curr;
+      row.step_length = alpha;
+      row.inner_iterations = inner_this;
+      row.work_units = work;
+      row.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      diag.push_back(row);
+      out.outer = outer;
+      out.inner += inner_this;
+      if (residual <= target) {
+        out.converged = true;
+        break;
+      }
+    }
+    if (!out.converged) {
+      char buf[128];
+      std::snprintf(buf, sizeof(buf), "projected newton solve: outer iteration cap reached (residual %f)", residual);
+      throw SolverFailure(buf);
+    }
+    return out;
+  }
+
   SolveOut step_grid(int frame_no, long long step_no) {
-    if (cfg.kind == 4) return solve_qn(1, frame_no, step_no);
-    if (cfg.kind != 0) throw Unsupported("projected-Newton solvers are not built for the device path (SURVEY 8f)");
-    return solve_qn(cfg.levels, frame_no, step_no);
+    switch (cfg.kind) {  // solvers.hpp:360-372
+      case 0:
+        return solve_qn(cfg.levels, frame_no, step_no);  // hot
+      case 1:
+        return solve_pn(0, frame_no, step_no);  // pn-pcg
+      case 2:
+        return solve_pn(1, frame_no, step_no);  // pn-pcg-mf
+      case 3:
+        return solve_pn(2, frame_no, step_no);  // pn-mgpcg
+      case 4:
+        return solve_qn(1, frame_no, step_no);  // lbfgs-h
+    }
+    throw std::invalid_argument("unknown solver kind");
   }
 
   // ------------------------------------------------------------------ advance_step

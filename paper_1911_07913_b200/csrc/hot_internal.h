@@ -87,6 +87,16 @@ void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, int* total_
 // ---------------------------------------------------------------- objective (k_objective.cu)
 /// Per-particle pass at nodal increment dv + alpha*p (p may be null): V_p psi partial sums
 /// into partials[blockIdx] and, when stress != null, stores V_p * P F^T (9 per particle).
+// ---- projected-Newton baselines (k_pn.cu)
+void launch_block_apply(const double* dinv, const double* r, double* z, int n, cudaStream_t s);
+void launch_pcg_xr(double* x, double* r, const double* p, const double* Ap, double alpha, long long n, cudaStream_t s);
+void launch_pcg_p(double* p, const double* z, double beta, long long n, cudaStream_t s);
+/// y = H u without H (objective.hpp:396-440) from the particle tensors Tu; dP: 9 * np scratch.
+void launch_mf_multiply(const ParticlesView& P, BinsView bins, GridView g, const double* Tu, const double* u,
+                        double* dP, double* y, cudaStream_t s);
+/// Inverse block diagonal of the projected system (objective.hpp:366-392) into dinv (9 per node).
+void launch_mf_block_diag_inv(const ParticlesView& P, BinsView bins, GridView g, const double* Tu, double* dinv,
+                              cudaStream_t s);
 /// 27-neighbour table of every active node (g.nb27 must point to n*27 ints).
 void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s);
 /// u = vel + (dv + alpha p) per node (p may be null): the nodal velocity the virtual F sees.

@@ -1,6 +1,8 @@
 // Shared per-particle device helpers (virtual deformation gradient).
 #pragma once
 
+#include <type_traits>
+
 #include "hot_internal.h"
 
 namespace hotb200 {
@@ -56,9 +58,11 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
   return m3_finite(F);
 }
 
-/// Warp-cooperative node gather: calls body(p) for every particle slot p in the 27 bins
-/// around node i (the bins of g.nb27, lexicographic), lanes striding over the concatenated
-/// slot list, so consecutive lanes read consecutive particles.  All 32 lanes must call it.
+/// Warp-cooperative node gather: calls body(p) -- or body(p, o) with o the bin offset index
+/// (bin node = i + o - 1, lexicographic in {0,1,2}^3; node i is stencil position 26 - o of
+/// that bin) -- for every particle slot p in the 27 bins around node i, lanes striding over
+/// the concatenated slot list, so consecutive lanes read consecutive particles.  All 32 lanes
+/// must call it.
 template <class Body>
 __device__ __forceinline__ void warp_node_gather(const GridView& g, const BinsView& bins, int i, int lane, Body body) {
   int st = 0, cnt = 0;
@@ -88,7 +92,12 @@ __device__ __forceinline__ void warp_node_gather(const GridView& g, const BinsVi
     o = min(o, 26);
     const int so = __shfl_sync(0xffffffffu, st, o);
     const int eo = __shfl_sync(0xffffffffu, incl - cnt, o);
-    if (f < total) body(so + (f - eo));
+    if (f < total) {
+      if constexpr (std::is_invocable_v<Body, int, int>)
+        body(so + (f - eo), o);
+      else
+        body(so + (f - eo));
+    }
   }
 }
 

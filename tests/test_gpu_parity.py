@@ -188,8 +188,11 @@ def test_single_level_vcycle_is_coarse_solve():
     assert it == ito and rel_err(u, uo) < 1e-9
 
 
-@pytest.mark.parametrize("kind", ["hot", "lbfgs-h"])
+@pytest.mark.parametrize("kind", ["hot", "lbfgs-h", "pn-pcg", "pn-pcg-mf", "pn-mgpcg"])
 def test_step_grid(kind):
+    """step_grid (solvers.hpp:354-381) for every solver kind: HOT and LBFGS-H (L-BFGS), and the
+    projected-Newton baselines (solvers.hpp:235-300): assembled Jacobi-PCG, matrix-free
+    Jacobi-PCG, and V-cycle-preconditioned PCG."""
     pr = _stretched_block_pair(seed=10, cells=6)
     pr.prepare(1.0 / 24)
     pr.set_solver(kind=kind, epsilon=1e-7)
@@ -201,6 +204,8 @@ def test_step_grid(kind):
     dirm = pr.orc.grid()["dirichlet"] == 1
     bc = pr.orc.grid()["bc_velocity"].reshape(-1, 3)
     assert np.array_equal(r["velocity"].reshape(-1, 3)[dirm], bc[dirm])  # exact scripted velocities
+    if kind.startswith("pn"):
+        assert abs(r["inner_total"] - ro["inner_total"]) <= max(2, 0.1 * ro["inner_total"])
 
 
 def test_rest_state_zero_iterations():
