@@ -279,3 +279,35 @@ def test_empty_and_single_particle():
     # eps*sqrt(n) in the CN norm bounds the HOT iterate only to ~3e-5 with 2.5e-4 kg fringe nodes
     # (see tests/test_oracle_solvers.py::test_ballistic_single_particle)
     assert np.abs(r["velocity"].reshape(-1, 3) - np.array([0, -9.8, 0]) / 24).max() < 3e-5
+
+
+def test_deterministic_reruns_are_byte_identical(tmp_path):
+    """cli.cpp:120-121 / SPEC --deterministic: the frame loop's output directory (HOTP
+    snapshots, text tables, diagnostics.csv with zeroed wall times) is byte-identical across
+    reruns, and the last frame agrees with the oracle's frame loop."""
+    from paper_1911_07913_b200 import io
+
+    sc = scene("cfg1_cube")
+    logs = []
+    for run in ("a", "b"):
+        io.run_simulation(sc, tmp_path / run, deterministic=True, frames=2, log=logs.append)
+    files = sorted(p.name for p in (tmp_path / "a").iterdir())
+    assert files == sorted(p.name for p in (tmp_path / "b").iterdir())
+    assert {"frame_0000.bin", "frame_0002.txt", "diagnostics.csv"} <= set(files)
+    for f in files:
+        assert (tmp_path / "a" / f).read_bytes() == (tmp_path / "b" / f).read_bytes(), f
+    # the oracle's frame loop for the same scene and frames
+    from oracle.oracle import Oracle
+    from paper_1911_07913_b200 import sample_scene_particles
+
+    orc = Oracle(3)
+    orc.set_scene(sc.source)
+    p = sample_scene_particles(sc)
+    orc.set_particles(p["x"], p["v"], p["mass"], p["volume"], p["F"], p["C"], p["material"])
+    for frame in (1, 2):
+        orc.set_sim_state(orc.sim_state()["time"], orc.sim_state()["step"], frame)
+        while orc.sim_state()["time"] < frame / sc.fps - 1e-12:
+            orc.advance_step(frame / sc.fps)
+    snap = io.read_snapshot(tmp_path / "a" / "frame_0002.bin")
+    xo = orc.get_particles()["x"].reshape(-1)
+    assert rel_err(snap["positions"], xo) < STATE_TOL
