@@ -118,6 +118,33 @@ constexpr int kAsmSmem = kAsmWarps * kAsmWarpDoubles * 8;
 constexpr unsigned kParticleBytes = kTensorStride * 8;  // 1008 = 63 x 16
 static_assert(kAsmWarpDoubles % 2 == 0, "16-byte aligned per-warp smem");
 
+/// S(o) = 25 o0 + 5 o1 + o2 of a stencil position, and kmin(o): the first stencil position k of
+/// the bin at offset o whose slot S(k) + S(o) is in the row's upper triangle (>= 62).
+struct Kmin27 {
+  int S[27], kmin[27];
+  constexpr Kmin27() : S(), kmin() {
+    for (int o = 0; o < 27; ++o) S[o] = 25 * (o / 9) + 5 * ((o / 3) % 3) + o % 3;
+    for (int o = 0; o < 27; ++o) {
+      int k = 0;
+      while (k < 27 && S[k] + S[o] < kDiagSlot) ++k;
+      kmin[o] = k;
+    }
+  }
+};
+constexpr Kmin27 kKmin27{};
+__constant__ int c_S27[27] = {
+#define HOT_S(o) (25 * ((o) / 9) + 5 * (((o) / 3) % 3) + (o) % 3)
+    HOT_S(0),  HOT_S(1),  HOT_S(2),  HOT_S(3),  HOT_S(4),  HOT_S(5),  HOT_S(6),  HOT_S(7),  HOT_S(8),
+    HOT_S(9),  HOT_S(10), HOT_S(11), HOT_S(12), HOT_S(13), HOT_S(14), HOT_S(15), HOT_S(16), HOT_S(17),
+    HOT_S(18), HOT_S(19), HOT_S(20), HOT_S(21), HOT_S(22), HOT_S(23), HOT_S(24), HOT_S(25), HOT_S(26)};
+#undef HOT_S
+__constant__ int c_kmin27[27] = {
+    kKmin27.kmin[0],  kKmin27.kmin[1],  kKmin27.kmin[2],  kKmin27.kmin[3],  kKmin27.kmin[4],  kKmin27.kmin[5],
+    kKmin27.kmin[6],  kKmin27.kmin[7],  kKmin27.kmin[8],  kKmin27.kmin[9],  kKmin27.kmin[10], kKmin27.kmin[11],
+    kKmin27.kmin[12], kKmin27.kmin[13], kKmin27.kmin[14], kKmin27.kmin[15], kKmin27.kmin[16], kKmin27.kmin[17],
+    kKmin27.kmin[18], kKmin27.kmin[19], kKmin27.kmin[20], kKmin27.kmin[21], kKmin27.kmin[22], kKmin27.kmin[23],
+    kKmin27.kmin[24], kKmin27.kmin[25], kKmin27.kmin[26]};
+
 /// D = A B + D on the fp64 tensor cores: m8n8k4, A row-major (lane: row lane/4, col lane%4),
 /// B column-major (lane: row lane%4, col lane/4), C/D (lane: row lane/4, cols 2(lane%4)+{0,1}).
 __device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
@@ -221,14 +248,8 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
       if (nmax == 0) continue;
       // bin b's upper stencil positions: the suffix k >= kmin_b (slot S(k) + S(o_b) >= 62,
       // S(v) = 25 v0 + 5 v1 + v2); o_0 = pq, o_1 = 26 - pq (S(o_1) = 62 - S(o_0))
-      const int So0 = 25 * (pq / 9) + 5 * ((pq / 3) % 3) + pq % 3, So1 = 62 - So0;
-      int kmin0 = 27, kmin1 = 27;
-      for (int k = 26; k >= 0; --k) {
-        const int Sk = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3;
-        if (Sk + So0 >= kDiagSlot) kmin0 = k;
-        if (Sk + So1 >= kDiagSlot) kmin1 = k;
-      }
-      if (pq == 13) kmin1 = 27;  // the centre bin has no mirror
+      const int So0 = c_S27[pq], So1 = 62 - So0;
+      const int kmin0 = c_kmin27[pq], kmin1 = pq == 13 ? 27 : c_kmin27[26 - pq];  // the centre bin has no mirror
       // C_b[k - kmin_b][ce] += sum_g W_t[k][g] M_b[ce][g]: per particle a rank-3 update on the
       // fp64 tensor cores (DMMA m8n8k4): M = upper positions (<= 4 tiles), N = ce (2), K = g (3 -> 4)
       double C0[4][2][2], C1[4][2][2];
