@@ -26,18 +26,22 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
   double G[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) G[k] = 0.0;
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
+  // The x-axis loop stays rolled (select instead of indexing) to keep the kernels that inline
+  // this small enough for the instruction cache; the 9 (y, z) nodes per x-plane are unrolled.
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+    const double wi = i == 0 ? ax[0].w[0] : (i == 1 ? ax[0].w[1] : ax[0].w[2]);
+    const double dwi = i == 0 ? ax[0].dw[0] : (i == 1 ? ax[0].dw[1] : ax[0].dw[2]);
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const double w = ax[0].w[i] * ax[1].w[j] * ax[2].w[k];
+        const double w = wi * ax[1].w[j] * ax[2].w[k];
         if (w <= 0.0) continue;
         const int node = __ldg(nb + 9 * i + 3 * j + k);
-        const double gr0 = ax[0].dw[i] / dx * ax[1].w[j] * ax[2].w[k];
-        const double gr1 = ax[1].dw[j] / dx * ax[0].w[i] * ax[2].w[k];
-        const double gr2 = ax[2].dw[k] / dx * ax[0].w[i] * ax[1].w[j];
+        const double gr0 = dwi / dx * ax[1].w[j] * ax[2].w[k];
+        const double gr1 = ax[1].dw[j] / dx * wi * ax[2].w[k];
+        const double gr2 = ax[2].dw[k] / dx * wi * ax[1].w[j];
         const double u0 = __ldg(u + 3 * node), u1 = __ldg(u + 3 * node + 1), u2 = __ldg(u + 3 * node + 2);
         G[0] += u0 * gr0;
         G[1] += u0 * gr1;
@@ -49,6 +53,7 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
         G[7] += u2 * gr1;
         G[8] += u2 * gr2;
       }
+  }
 #pragma unroll
   for (int k = 0; k < 9; ++k) Fn.m[k] = P.F[k * n + p];
   M3 A;
