@@ -68,18 +68,23 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
       const double c = P.x[a * n + p] / dx;
       axis_weights(c, stencil_base_1d(c), ax[a]);
     }
+#pragma unroll 1
+    for (int k0 = 0; k0 < 3; ++k0) {  // rolled x axis (select, not indexing): instruction-cache size
+      const double w0 = k0 == 0 ? ax[0].w[0] : (k0 == 1 ? ax[0].w[1] : ax[0].w[2]);
+      const double dw0 = k0 == 0 ? ax[0].dw[0] : (k0 == 1 ? ax[0].dw[1] : ax[0].dw[2]);
 #pragma unroll
-    for (int k = 0; k < 27; ++k) {
-      const int k0 = k / 9, k1 = (k / 3) % 3, k2 = k % 3;
-      const double w0 = ax[0].w[k0], w1 = ax[1].w[k1], w2 = ax[2].w[k2];
-      double W[3] = {0.0, 0.0, 0.0};
-      if (w0 * w1 * w2 > 0.0) {
-        const double g0 = ax[0].dw[k0] / dx * w1 * w2, g1 = ax[1].dw[k1] / dx * w0 * w2, g2 = ax[2].dw[k2] / dx * w0 * w1;
+      for (int kk = 0; kk < 9; ++kk) {
+        const int k1 = kk / 3, k2 = kk % 3, k = 9 * k0 + kk;
+        const double w1 = ax[1].w[k1], w2 = ax[2].w[k2];
+        double W[3] = {0.0, 0.0, 0.0};
+        if (w0 * w1 * w2 > 0.0) {
+          const double g0 = dw0 / dx * w1 * w2, g1 = ax[1].dw[k1] / dx * w0 * w2, g2 = ax[2].dw[k2] / dx * w0 * w1;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) W[q] = Fn.m[q] * g0 + Fn.m[3 + q] * g1 + Fn.m[6 + q] * g2;
+          for (int q = 0; q < 3; ++q) W[q] = Fn.m[q] * g0 + Fn.m[3 + q] * g1 + Fn.m[6 + q] * g2;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) out[kTPacked + 3 * k + q] = W[q];
       }
-#pragma unroll
-      for (int q = 0; q < 3; ++q) out[kTPacked + 3 * k + q] = W[q];
     }
   }
 }

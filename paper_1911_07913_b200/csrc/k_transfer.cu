@@ -28,20 +28,25 @@ __global__ void k_g2p_strain_advect(ParticlesView P, GridView g, double dx, doub
     double v[3] = {0.0, 0.0, 0.0}, B[9], G[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) B[k] = G[k] = 0.0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
+    // stencil nodes from the bin's 27-neighbour table; the x-axis loop stays rolled (select, not
+    // indexing) so the kernel fits the instruction cache
+    const int* nb = g.nb27 + 27LL * P.bin[p];
+#pragma unroll 1
+    for (int i = 0; i < 3; ++i) {
+      const double wi = i == 0 ? ax[0].w[0] : (i == 1 ? ax[0].w[1] : ax[0].w[2]);
+      const double dwi = i == 0 ? ax[0].dw[0] : (i == 1 ? ax[0].dw[1] : ax[0].dw[2]);
 #pragma unroll
       for (int j = 0; j < 3; ++j)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const double w = ax[0].w[i] * ax[1].w[j] * ax[2].w[k];
+          const double w = wi * ax[1].w[j] * ax[2].w[k];
           if (w <= 0.0) continue;
-          const int node = dense_lookup(g.map, base[0] + i, base[1] + j, base[2] + k);
+          const int node = __ldg(nb + 9 * i + 3 * j + k);
           const double vi[3] = {g.vel[3 * node], g.vel[3 * node + 1], g.vel[3 * node + 2]};
           const double d[3] = {(double)(base[0] + i) * dx - xp[0], (double)(base[1] + j) * dx - xp[1],
                                (double)(base[2] + k) * dx - xp[2]};
-          const double gr[3] = {ax[0].dw[i] / dx * ax[1].w[j] * ax[2].w[k], ax[1].dw[j] / dx * ax[0].w[i] * ax[2].w[k],
-                                ax[2].dw[k] / dx * ax[0].w[i] * ax[1].w[j]};
+          const double gr[3] = {dwi / dx * ax[1].w[j] * ax[2].w[k], ax[1].dw[j] / dx * wi * ax[2].w[k],
+                                ax[2].dw[k] / dx * wi * ax[1].w[j]};
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const double wv = w * vi[a];
@@ -53,6 +58,7 @@ __global__ void k_g2p_strain_advect(ParticlesView P, GridView g, double dx, doub
             }
           }
         }
+    }
     M3 Fn, A;
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
