@@ -247,6 +247,35 @@ def test_cfg1_drop_steps_with_floor():
     assert pr.gpu.grid is not None
 
 
+@pytest.mark.parametrize("plasticity", [
+    {"kind": "von_mises", "yield_stress": 2.0e3},
+    {"kind": "snow_clamp", "lo": 0.975, "hi": 1.0075},
+])
+def test_plastic_return_map_steps(plasticity):
+    """The strain update's return map (constitutive.hpp:224-251) on the device: von Mises with a
+    yield stress low enough that most particles yield, and the snow clamp with a tight band,
+    over several steps from a pre-stretched, moving block; x, v, F against the oracle."""
+    d = block_scene_dict(youngs=2e5, extra={"fps": 48})
+    d["materials"][0]["plasticity"] = dict(plasticity)
+    sc = scene_from_dict(d)
+    p = random_block_particles(np.random.default_rng(21), 0.02, 6, f_spread=0.05, v_spread=0.5)
+    pr = Pair(sc, p)
+    for k in range(3):
+        frame_end = (k + 1) / sc.fps
+        s = pr.gpu.advance_step(frame_end)
+        so = pr.orc.advance_step(frame_end)
+        assert s["node_count"] == so["node_count"]
+        assert abs(s["outer_iterations"] - so["outer_iterations"]) <= 1, (k, s, so)
+        gp, op = pr.gpu.particles(), pr.orc.get_particles()
+        for key in ("x", "v", "F"):
+            assert rel_err(gp[key], op[key]) < STATE_TOL, (k, key)
+    # the map did act: F left the elastic trial state somewhere (det or singular values clamped)
+    F = pr.gpu.particles()["F"]
+    sv = np.linalg.svd(F, compute_uv=False)
+    if plasticity["kind"] == "snow_clamp":
+        assert sv.min() >= 0.975 - 1e-12 and sv.max() <= 1.0075 + 1e-12
+
+
 def test_solver_failure_leaves_particles_unmodified():
     pr = Pair(scene("cfg1_stretched"))
     pr.set_solver(outer_cap=1)
