@@ -410,29 +410,24 @@ struct Context {
     qvol.ensure(sizeof(double) * std::max<long long>(n, 1));
     qmat.ensure(sizeof(int) * std::max<long long>(n, 1));
     qorig.ensure(sizeof(int) * std::max<long long>(n, 1));
-    stage.ensure(n9);
+    // one staging region per interleaved field, so the host->device copies run back to back
+    // (no DMA gaps for the transposes) and the transposes follow
+    stage.ensure(sizeof(double) * 24 * std::max<long long>(n, 1));
     launch_iota(porig.as<int>(), n, stream);
-    auto soa = [&](const double* src, DBuf& dst, int comps, double fill_diag) {
-      if (src) {
-        HOT_CUDA(cudaMemcpyAsync(stage.p, src, sizeof(double) * comps * n, cudaMemcpyHostToDevice, stream));
-        launch_aos_to_soa(stage.as<double>(), dst.as<double>(), n, comps, stream);
-        // the staging buffer is reused by the next component: order on the stream suffices
-      } else {
-        HOT_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(double) * comps * n, stream));
-        if (fill_diag != 0.0) {
-          std::vector<double> eye(9 * n, 0.0);
-          for (long long p = 0; p < n; ++p) eye[0 * n + p] = eye[4 * n + p] = eye[8 * n + p] = 1.0;
-          HOT_CUDA(cudaMemcpyAsync(dst.p, eye.data(), sizeof(double) * 9 * n, cudaMemcpyHostToDevice, stream));
-          sync();
-        }
-      }
-    };
     if (n > 0) {
       if (!x) throw std::invalid_argument("positions are required");
-      soa(x, px, 3, 0.0);
-      soa(v, pv, 3, 0.0);
-      soa(F, pF, 9, 1.0);
-      soa(C, pC, 9, 0.0);
+      double* sx = stage.as<double>();
+      double* sv = sx + 3 * n;
+      double* sF = sv + 3 * n;
+      double* sC = sF + 9 * n;
+      struct Field {
+        const double* src;
+        double* st;
+        DBuf* dst;
+        int comps;
+      } fields[4] = {{x, sx, &px, 3}, {v, sv, &pv, 3}, {F, sF, &pF, 9}, {C, sC, &pC, 9}};
+      for (const Field& f : fields)
+        if (f.src) HOT_CUDA(cudaMemcpyAsync(f.st, f.src, sizeof(double) * f.comps * n, cudaMemcpyHostToDevice, stream));
       if (mass)
         HOT_CUDA(cudaMemcpyAsync(pmass.p, mass, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
       else
@@ -445,28 +440,55 @@ struct Context {
         HOT_CUDA(cudaMemcpyAsync(pmat.p, mat, sizeof(int) * n, cudaMemcpyHostToDevice, stream));
       else
         HOT_CUDA(cudaMemsetAsync(pmat.p, 0, sizeof(int) * n, stream));
+      for (const Field& f : fields) {
+        if (f.src) {
+          launch_aos_to_soa(f.st, f.dst->as<double>(), n, f.comps, stream);
+        } else {
+          HOT_CUDA(cudaMemsetAsync(f.dst->p, 0, sizeof(double) * f.comps * n, stream));
+          if (f.dst == &pF) {  // default F = I
+            std::vector<double> eye(9 * n, 0.0);
+            for (long long p = 0; p < n; ++p) eye[0 * n + p] = eye[4 * n + p] = eye[8 * n + p] = 1.0;
+            HOT_CUDA(cudaMemcpyAsync(pF.p, eye.data(), sizeof(double) * 9 * n, cudaMemcpyHostToDevice, stream));
+            sync();
+          }
+        }
+      }
+      if (mat) {  // material ids checked on the device
+        HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 7, 0, sizeof(int), stream));
+        launch_check_ids(pmat.as<int>(), n, (int)mats_h.size(), iflags.as<int>() + 7, stream);
+      }
     }
     prof_end(h, (double)n * (3 + 3 + 9 + 9 + 2) * 8 + 4.0 * n);
     have_state = false;
-    sync();
     if (mat && n) {
-      for (long long p = 0; p < n; ++p)
-        if (mat[p] < 0 || mat[p] >= (int)mats_h.size()) throw std::invalid_argument("particle material id out of range");
+      int bad = 0;
+      HOT_CUDA(cudaMemcpyAsync(&bad, iflags.as<int>() + 7, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      sync();
+      if (bad) throw std::invalid_argument("particle material id out of range");
+    } else {
+      sync();
     }
   }
 
   void download(double* x, double* v, double* F, double* C) {
     const int h = prof_begin(P_IO);
-    stage.ensure(sizeof(double) * 9 * std::max<long long>(np, 1));
-    auto aos = [&](const DBuf& src, double* dst, int comps) {
-      if (!dst || np == 0) return;
-      launch_soa_to_aos_perm(src.as<double>(), stage.as<double>(), np, comps, porig.as<int>(), stream);
-      HOT_CUDA(cudaMemcpyAsync(dst, stage.p, sizeof(double) * comps * np, cudaMemcpyDeviceToHost, stream));
-    };
-    aos(px, x, 3);
-    aos(pv, v, 3);
-    aos(pF, F, 9);
-    aos(pC, C, 9);
+    stage.ensure(sizeof(double) * 24 * std::max<long long>(np, 1));
+    struct Field {
+      const DBuf* src;
+      double* dst;
+      int comps;
+      long long off;
+    } fields[4] = {{&px, x, 3, 0}, {&pv, v, 3, 3}, {&pF, F, 9, 6}, {&pC, C, 9, 15}};
+    if (np > 0) {  // un-permute every field, then the device->host copies back to back
+      for (const Field& f : fields)
+        if (f.dst)
+          launch_soa_to_aos_perm(f.src->as<double>(), stage.as<double>() + f.off * np, np, f.comps, porig.as<int>(),
+                                 stream);
+      for (const Field& f : fields)
+        if (f.dst)
+          HOT_CUDA(cudaMemcpyAsync(f.dst, stage.as<double>() + f.off * np, sizeof(double) * f.comps * np,
+                                   cudaMemcpyDeviceToHost, stream));
+    }
     prof_end(h, (double)np * 24 * 8);
     sync();
   }

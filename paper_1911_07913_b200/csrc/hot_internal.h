@@ -180,6 +180,8 @@ int pcg_max_blocks();
 void launch_g2p_strain_advect(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
                               int* inverted, cudaStream_t s);
 void launch_vmax(const ParticlesView& P, unsigned long long* vmax_bits, cudaStream_t s);
+/// *bad = 1 if any id is outside [0, limit).
+void launch_check_ids(const int* ids, long long n, int limit, int* bad, cudaStream_t s);
 
 void launch_aos_to_soa(const double* in, double* out, long long n, int comps, cudaStream_t s);
 void launch_soa_to_aos(const double* in, double* out, long long n, int comps, cudaStream_t s);

@@ -4,6 +4,8 @@
 // converged grid velocity, so fusing them changes no value.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "hot_internal.h"
 
 namespace hotb200 {
@@ -86,6 +88,11 @@ __global__ void k_g2p_strain_advect(ParticlesView P, GridView g, double dx, doub
   }
 }
 
+__global__ void k_check_ids(const int* __restrict__ ids, long long n, int limit, int* bad) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    if (ids[p] < 0 || ids[p] >= limit) atomicExch(bad, 1);
+}
+
 __global__ void k_vmax(const double* __restrict__ v, long long n, unsigned long long* vmax_bits) {
   double m = 0.0;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
@@ -111,6 +118,10 @@ void launch_g2p_strain_advect(const ParticlesView& P, GridView g, double dx, dou
                               int* inverted, cudaStream_t s) {
   if (P.n == 0) return;
   { k_g2p_strain_advect<<<tgrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, inverted); count_launches(1); }
+}
+
+void launch_check_ids(const int* ids, long long n, int limit, int* bad, cudaStream_t s) {
+  if (n) { k_check_ids<<<(int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8), 256, 0, s>>>(ids, n, limit, bad); count_launches(1); }
 }
 
 void launch_vmax(const ParticlesView& P, unsigned long long* vmax_bits, cudaStream_t s) {
