@@ -308,16 +308,6 @@ __device__ __forceinline__ void row_product(const LevelView& L, int i, const dou
   y2 = wsum(a2);
 }
 
-/// L2 prefetch of one row's block storage (9 x 1 KB) and column ids (512 B).
-__device__ __forceinline__ void prefetch_row(const LevelView& L, int i, int lane) {
-  const char* h = reinterpret_cast<const char*>(L.H + (long long)i * 9 * kSlotPitch);
-  const char* c = reinterpret_cast<const char*>(L.cols + (long long)i * kSlotPitch);
-  for (int line = lane; line < 76; line += 32) {
-    const char* p = line < 72 ? h + 128 * line : c + 128 * (line - 72);
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-  }
-}
-
 __global__ void __launch_bounds__(kMgThreads) k_spmv(LevelView L, const double* __restrict__ x, double* __restrict__ y,
                                                      const double* __restrict__ b) {
   const int lane = threadIdx.x & 31;
@@ -386,43 +376,9 @@ __global__ void k_prolong_add(LevelView f, LevelView c, const double* __restrict
   }
 }
 
-// ---- staged row access: cp.async the row's 9 KB block storage + column ids (+ D^-1 and b)
-// into a per-warp shared-memory buffer, double-buffered so the next row (also across the
-// grid barrier into the next wave) streams in while the current one is consumed.
-constexpr int kRowBytesH = 9 * kSlotPitch * 8;       // 9216
-constexpr int kRowBytesC = kSlotPitch * 4;            // 512
-constexpr int kRowStage = kRowBytesH + kRowBytesC + 96;  // + dinv (72) + b (24)
 constexpr int kMaxSgsWaves = 4096;
 constexpr int kSgsSmem = 4 * (kMaxSgsWaves + 1);
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-__device__ __forceinline__ void stage_row(const LevelView& L, const double* __restrict__ b, int i, char* buf,
-                                          int lane) {
-  const char* h = reinterpret_cast<const char*>(L.H + (long long)i * 9 * kSlotPitch);
-  const char* c = reinterpret_cast<const char*>(L.cols + (long long)i * kSlotPitch);
-#pragma unroll
-  for (int k = 0; k < kRowBytesH / 16 / 32; ++k) cp_async16(buf + 16 * (lane + 32 * k), h + 16 * (lane + 32 * k));
-  cp_async16(buf + kRowBytesH + 16 * lane, c + 16 * lane);
-  if (lane < 9) cp_async8(buf + kRowBytesH + kRowBytesC + 8 * lane, L.dinv + 9 * (long long)i + lane);
-  else if (lane < 12) cp_async8(buf + kRowBytesH + kRowBytesC + 8 * lane, b + 3 * (long long)i + (lane - 9));
-}
-
-/// One symmetric Gauss-Seidel sweep (multigrid.hpp:298-316) over the wave schedule: a row of
-/// wave w reads only neighbours of earlier waves (already updated) or later waves (still
-/// old), exactly as the serial colour-ordered sweep does.  Persistent cooperative kernel for
-/// the small coarse-level waves: after the wave's rows are updated each warp issues L2
-/// prefetches (fire-and-forget, so they do not queue ahead of the next gathers in the SM's
-/// load FIFO) for its row of the next wave, then the grid barrier.
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -480,9 +436,13 @@ __device__ __forceinline__ void sgs_grid_barrier(unsigned int* bar, unsigned int
   __syncthreads();
 }
 
+/// One symmetric Gauss-Seidel sweep (multigrid.hpp:298-316) over the wave schedule, barrier
+/// variant (HOT_SGS_COARSE=barrier; the dataflow k_sgs_flow is the default): a row of wave w
+/// reads only neighbours of earlier waves (already updated) or later waves (still old),
+/// exactly as the serial colour-ordered sweep does, with a grid barrier after every wave.
 __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __restrict__ wave_start,
                                                     const int* __restrict__ wave_rows, int nwaves, double* u,
-                                                    const double* __restrict__ b, long long* trace, int prefetch,
+                                                    const double* __restrict__ b, long long* trace,
                                                     unsigned int* bar) {
   // One CTA (128 threads = one per diagonal-storage slot) per row; after the barrier only the
   // gather of the neighbours' u (one L2 round trip), the FMA and the CTA reduction remain.
@@ -494,7 +454,6 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __r
   int* ws = reinterpret_cast<int*>(sgs_smem);
   for (int k2 = threadIdx.x; k2 <= nwaves; k2 += blockDim.x) ws[k2] = wave_start[k2];
   __syncthreads();
-  (void)prefetch;
   SgsRow R;
   bool have = false;
   {
@@ -1061,12 +1020,10 @@ void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, doub
 void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
                 int grid_blocks, cudaStream_t s, long long* trace) {
   if (L.n == 0 || nwaves == 0) return;
-  static const int prefetch = std::getenv("HOT_SGS_NOPREFETCH") ? 0 : 1;
-  int pf = prefetch;
   static unsigned int* bar = nullptr;
   if (!bar) cudaMalloc(&bar, 2 * sizeof(unsigned int));
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
-  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &trace, &pf, &bar};
+  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &trace, &bar};
   { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, kSgsSmem, s); count_launches(1); }
 }
 
