@@ -973,8 +973,10 @@ struct Context {
     }
     assemble(dv.as<double>(), true, /*reuse_svd=*/true);
     build_hierarchy(levels, cfg.embedding);
-    for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
-    if (std::getenv("HOT_VERBOSE"))
+    static const bool verbose = std::getenv("HOT_VERBOSE") != nullptr;
+    if (prof || verbose)  // active-slot counts only feed the profile's algorithmic bytes
+      for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
+    if (verbose)
       for (int m = 0; m < nlevels; ++m)
         std::fprintf(stderr, "[hot] level %d: rows=%d waves=%d max_wave=%d active_slots=%lld (%.1f/row) bbox=%dx%dx%d\n",
                      m, L[m].n, L[m].nwaves, L[m].max_wave, L[m].active_slots, L[m].n ? (double)L[m].active_slots / L[m].n : 0.0,
@@ -1137,7 +1139,8 @@ struct Context {
       } else {
         assemble(dv.as<double>(), true);
         build_hierarchy(variant == 2 ? cfg.levels : 1, cfg.embedding);
-        for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
+        if (prof)
+          for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
         Dinv = L[0].dinv.as<double>();
       }
       // gpg = g^T D^-1 g (solvers.hpp:263-268); k = adaptive_cg_tolerance
