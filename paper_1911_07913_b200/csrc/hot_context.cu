@@ -181,6 +181,10 @@ struct Context {
   // solver vectors
   DBuf dv, g, gnew, pdir, q, stress, Tu, vout, hist_s[kMaxWindow + 1], hist_y[kMaxWindow + 1];
   DBuf pcg_r, pcg_z, pcg_p, pcg_Ap, sgs_trace, gal_x;
+  // second stream for the hierarchy's structure half (overlaps the level-0 assembly)
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DBuf scan_tmp2, struct_flags;
   DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
@@ -203,6 +207,9 @@ struct Context {
     for (auto e : event_pool) cudaEventDestroy(e);
     if (host_scal) cudaFreeHost(host_scal);
     if (host_int) cudaFreeHost(host_int);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -279,6 +286,10 @@ struct Context {
     device = dev;
     HOT_CUDA(cudaSetDevice(dev));
     HOT_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    HOT_CUDA(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
+    HOT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    HOT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    struct_flags.ensure(sizeof(int) * 16);
     HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
     HOT_CUDA(cudaMallocHost(&host_int, sizeof(int) * 64));
     nred = 8 * num_sms();
@@ -679,32 +690,36 @@ struct Context {
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 126 * 8));  // x F vol mat in, kappa*T (packed) + W out
   }
 
-  /// Diag inverse + wave schedule for level m (multigrid.hpp:227-251).
-  void finalize(int m) {
+  /// Wave schedule of level m (multigrid.hpp:241-250 as waves), structure
+  /// only (coordinates), on stream st with scan scratch tmp and count scratch cnt.
+  void level_waves(int m, cudaStream_t st, DBuf& tmp) {
     Level& l = L[m];
-    int mm[2] = {INT_MAX, INT_MIN};
-    HOT_CUDA(cudaMemcpyAsync(iflags.as<int>() + 10, mm, sizeof(mm), cudaMemcpyHostToDevice, stream));
-    HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 12, 0, sizeof(int), stream));
-    launch_finalize_level(l.view(), m > 0 ? 1 : 0, l.wave_of.as<int>(), iflags.as<int>() + 10, iflags.as<int>() + 12,
-                          stream);
-    int hb[3];
-    HOT_CUDA(cudaMemcpyAsync(hb, iflags.as<int>() + 10, sizeof(hb), cudaMemcpyDeviceToHost, stream));
-    sync();
-    if (hb[2]) throw std::logic_error("multigrid: singular diagonal block");
     if (l.n == 0) {
       l.nwaves = 0;
+      l.max_wave = 0;
+      l.wave_start_h.assign(1, 0);
       return;
     }
-    const int wmin = hb[0], nw = hb[1] - hb[0] + 1;
+    int off[3] = {0, 0, 0};
+    int nw = 27;
+    if (m > 0) {
+      int span[3];
+      for (int a = 0; a < 3; ++a) {
+        off[a] = l.lo[a] >> 1;
+        span[a] = ((l.lo[a] + l.ext[a] - 1) >> 1) - off[a] + 1;
+      }
+      nw = 8 * 7 + 4 * (span[0] - 1) + 2 * (span[1] - 1) + (span[2] - 1) + 1;
+    }
+    launch_level_waves(l.view(), m > 0 ? 1 : 0, off, l.wave_of.as<int>(), st);
     l.wave_counts.ensure(sizeof(int) * (nw + 2));
     l.wave_start.ensure(sizeof(int) * (nw + 2));
     l.wave_cursor.ensure(sizeof(int) * (nw + 2));
-    scan_tmp.ensure(sizeof(int) * (nw / 4096 + 64));
-    launch_bucket_rows(l.wave_of.as<int>(), l.n, wmin, l.wave_counts.as<int>(), l.wave_start.as<int>(),
-                       l.wave_cursor.as<int>(), l.wave_rows.as<int>(), nw, scan_tmp.as<int>(), stream);
+    tmp.ensure(sizeof(int) * (nw / 4096 + 64));
+    launch_bucket_rows(l.wave_of.as<int>(), l.n, 0, l.wave_counts.as<int>(), l.wave_start.as<int>(),
+                       l.wave_cursor.as<int>(), l.wave_rows.as<int>(), nw, tmp.as<int>(), st);
     std::vector<int> counts(nw);
-    HOT_CUDA(cudaMemcpyAsync(counts.data(), l.wave_counts.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, stream));
-    sync();
+    HOT_CUDA(cudaMemcpyAsync(counts.data(), l.wave_counts.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, st));
+    HOT_CUDA(cudaStreamSynchronize(st));
     std::vector<int> starts;
     int acc = 0;
     l.max_wave = 0;
@@ -718,22 +733,23 @@ struct Context {
     l.nwaves = (int)starts.size() - 1;
     l.wave_start_h = starts;
     l.sgs_flag.ensure(sizeof(int) * std::max(l.n, 1));
-    HOT_CUDA(cudaMemsetAsync(l.sgs_flag.p, 0, sizeof(int) * std::max(l.n, 1), stream));
+    HOT_CUDA(cudaMemsetAsync(l.sgs_flag.p, 0, sizeof(int) * std::max(l.n, 1), st));
     l.sgs_epoch = 1;
     l.wave_start_c.ensure(sizeof(int) * starts.size());
     HOT_CUDA(cudaMemcpyAsync(l.wave_start_c.p, starts.data(), sizeof(int) * starts.size(), cudaMemcpyHostToDevice,
-                             stream));
-    sync();
+                             st));
+    HOT_CUDA(cudaStreamSynchronize(st));  // `starts` is a host temporary
   }
 
-  /// build_hierarchy (multigrid.hpp:258-294), linear node embedding.
-  void build_hierarchy(int levels, int embedding) {
-    if (levels < 1) throw std::invalid_argument("build_hierarchy: need at least one level");
-    if (levels > kMaxLevels) throw std::invalid_argument("build_hierarchy: too many levels");
-    if (embedding != 1 && levels > 1) throw Unsupported("quadratic embedding is not built for the device path");
-    const int h = prof_begin(P_HIER);
-    finalize(0);
-    nlevels = 1;
+  /// build_hierarchy, structure half (multigrid.hpp:127-158, 241-250, 275-284): coarse node
+  /// sets, Dirichlet flags, column ids and every level's wave schedule.  Depends only on the
+  /// level-0 coordinates and Dirichlet flags, so the solve runs it on a second stream while
+  /// the level-0 assembly occupies the GPU.  Returns the number of levels built.
+  int build_structure(int levels, cudaStream_t st) {
+    DBuf& tmp = scan_tmp2;
+    int* cnt = struct_flags.as<int>();
+    level_waves(0, st, tmp);
+    int built = 1;
     for (int m = 1; m < levels; ++m) {
       Level& f = L[m - 1];
       Level& c = L[m];
@@ -746,26 +762,42 @@ struct Context {
       c.flags.ensure(len + 16);
       c.map.ensure(sizeof(int) * len);
       c.coords.ensure(sizeof(int) * 3 * std::min<long long>(len, 8LL * f.n));
-      scan_tmp.ensure(sizeof(int) * (len / 4096 + 64));
-      HOT_CUDA(cudaMemsetAsync(c.flags.p, 0, len + 16, stream));
-      launch_mark_parents(f.view(), c.dmap(), c.flags.as<uint8_t>(), stream);
+      tmp.ensure(sizeof(int) * (len / 4096 + 64));
+      HOT_CUDA(cudaMemsetAsync(c.flags.p, 0, len + 16, st));
+      launch_mark_parents(f.view(), c.dmap(), c.flags.as<uint8_t>(), st);
       launch_flags_to_index(c.flags.as<uint8_t>(), len, c.ext, c.lo, c.map.as<int>(), c.coords.as<int>(),
-                            scan_tmp.as<int>(), iflags.as<int>() + 8, stream);
+                            tmp.as<int>(), cnt, st);
       int nc = 0;
-      HOT_CUDA(cudaMemcpyAsync(&nc, iflags.as<int>() + 8, sizeof(int), cudaMemcpyDeviceToHost, stream));
-      sync();
+      HOT_CUDA(cudaMemcpyAsync(&nc, cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+      HOT_CUDA(cudaStreamSynchronize(st));
       if (nc == 0) break;  // truncated hierarchy (multigrid.hpp:281-284)
       c.n = nc;
       alloc_level(c);
       c.dir.ensure(std::max(nc, 1));
-      HOT_CUDA(cudaMemsetAsync(c.dir.p, 0, nc, stream));
-      launch_coarse_dirichlet(f.view(), c.dmap(), c.dir.as<uint8_t>(), stream);
-      launch_fill_cols(c.view(), stream);
+      HOT_CUDA(cudaMemsetAsync(c.dir.p, 0, nc, st));
+      launch_coarse_dirichlet(f.view(), c.dmap(), c.dir.as<uint8_t>(), st);
+      launch_fill_cols(c.view(), st);
+      level_waves(m, st, tmp);
+      built = m + 1;
+    }
+    return built;
+  }
+
+  /// build_hierarchy, values half: D^-1 of level 0, then per coarse level the Galerkin
+  /// product (multigrid.hpp:162-202) with the fused Dirichlet projection and its D^-1; one
+  /// readback for the singular-block check of every level (multigrid.hpp:236-238).
+  void build_values(int built) {
+    const int h = prof_begin(P_HIER);
+    HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 12, 0, sizeof(int), stream));
+    launch_level_dinv(L[0].view(), iflags.as<int>() + 12, stream);
+    nlevels = 1;
+    for (int m = 1; m < built; ++m) {
+      Level& f = L[m - 1];
+      Level& c = L[m];
       gal_x.ensure(sizeof(double) * 64 * 9 * std::max(f.n, 1));
       launch_galerkin(f.view(), c.view(), gal_x.as<double>(), stream);
-      check_launch();
+      launch_level_dinv(c.view(), iflags.as<int>() + 12, stream);
       nlevels = m + 1;
-      finalize(m);
     }
     // PCG scratch on the coarsest level
     const Level& bot = L[nlevels - 1];
@@ -774,8 +806,36 @@ struct Context {
     pcg_z.ensure(v);
     pcg_p.ensure(v);
     pcg_Ap.ensure(v);
+    int singular = 0;
+    HOT_CUDA(cudaMemcpyAsync(&singular, iflags.as<int>() + 12, sizeof(int), cudaMemcpyDeviceToHost, stream));
     prof_end(h);
+    sync();
     check_launch();
+    if (singular) throw std::logic_error("multigrid: singular diagonal block");
+  }
+
+  /// build_hierarchy (multigrid.hpp:258-294), linear node embedding, in stream order.
+  void build_hierarchy(int levels, int embedding) {
+    if (levels < 1) throw std::invalid_argument("build_hierarchy: need at least one level");
+    if (levels > kMaxLevels) throw std::invalid_argument("build_hierarchy: too many levels");
+    if (embedding != 1 && levels > 1) throw Unsupported("quadratic embedding is not built for the device path");
+    build_values(build_structure(levels, stream));
+  }
+
+  /// build_hierarchy overlapped with the level-0 assembly: the structure half runs on the
+  /// second stream (its host round trips wait on that stream only) while the main stream
+  /// assembles; the values half joins after both.
+  void assemble_and_build_hierarchy(const double* dvp, int levels, int embedding, bool reuse_svd) {
+    if (levels < 1) throw std::invalid_argument("build_hierarchy: need at least one level");
+    if (levels > kMaxLevels) throw std::invalid_argument("build_hierarchy: too many levels");
+    if (embedding != 1 && levels > 1) throw Unsupported("quadratic embedding is not built for the device path");
+    HOT_CUDA(cudaEventRecord(ev_fork, stream));  // level-0 coords and Dirichlet flags are final
+    assemble(dvp, true, reuse_svd);
+    HOT_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
+    const int built = build_structure(levels, stream2);
+    HOT_CUDA(cudaEventRecord(ev_join, stream2));
+    HOT_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+    build_values(built);
   }
 
   /// Few, fat CTAs for the cooperative kernels: the grid barrier costs grow with the number of
@@ -971,8 +1031,7 @@ struct Context {
       out.converged = true;
       return out;
     }
-    assemble(dv.as<double>(), true, /*reuse_svd=*/true);
-    build_hierarchy(levels, cfg.embedding);
+    assemble_and_build_hierarchy(dv.as<double>(), levels, cfg.embedding, /*reuse_svd=*/true);
     static const bool verbose = std::getenv("HOT_VERBOSE") != nullptr;
     if (prof || verbose)  // active-slot counts only feed the profile's algorithmic bytes
       for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);

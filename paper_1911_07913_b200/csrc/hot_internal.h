@@ -146,8 +146,9 @@ void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaS
 /// X: scratch of 64*9 doubles per fine row.
 void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s);
 /// diag inverse, singular check, wave id per row (level 0: colour mod 3; coarse: wavefront).
-void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
-                           cudaStream_t s);
+/// D^-1 per row (+ singular flag) and the wave id per row (coarse: offsets = bbox min >> 1).
+void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s);
+void launch_level_waves(LevelView L, int coarse, const int* off, int* wave_of, cudaStream_t s);
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
                         int nwaves, int* scan_tmp, cudaStream_t s);
 void launch_spmv(LevelView L, const double* x, double* y, cudaStream_t s);

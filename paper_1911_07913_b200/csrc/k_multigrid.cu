@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin_c(LevelView f, LevelVie
   }
 }
 
-__global__ void k_finalize_level(LevelView L, int coarse, int* __restrict__ wave_of, int* minmax, int* singular) {
-  int wmin = INT_MAX, wmax = INT_MIN;
+/// Level diagonal inverse (multigrid.hpp:233-240) with the singular-block check.
+__global__ void k_level_dinv(LevelView L, int* singular) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
     M3 D;
 #pragma unroll
@@ -242,26 +242,22 @@ __global__ void k_finalize_level(LevelView L, int coarse, int* __restrict__ wave
     if (!(fabs(det) > 0.0)) atomicExch(singular, 1);
 #pragma unroll
     for (int k = 0; k < 9; ++k) L.dinv[9 * i + k] = Di.m[k];
+  }
+}
+
+/// Wave id of every row (§4.1 of DESIGN.md): level 0 the mod-3 colour; coarse levels
+/// 8 * colour + 4 (x>>1) + 2 (y>>1) + (z>>1), offset by the bounding box so ids start near 0.
+__global__ void k_level_waves(LevelView L, int coarse, int off0, int off1, int off2, int* __restrict__ wave_of) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
     const int c0 = L.coords[3 * i], c1 = L.coords[3 * i + 1], c2 = L.coords[3 * i + 2];
     int w;
     if (!coarse) {
       w = (((c0 % 3) + 3) % 3 * 3 + ((c1 % 3) + 3) % 3) * 3 + ((c2 % 3) + 3) % 3;
     } else {
       const int col = ((c0 & 1) * 2 + (c1 & 1)) * 2 + (c2 & 1);
-      w = 8 * col + 4 * (c0 >> 1) + 2 * (c1 >> 1) + (c2 >> 1);
+      w = 8 * col + 4 * ((c0 >> 1) - off0) + 2 * ((c1 >> 1) - off1) + ((c2 >> 1) - off2);
     }
     wave_of[i] = w;
-    wmin = min(wmin, w);
-    wmax = max(wmax, w);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
-    wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(minmax, wmin);
-    atomicMax(minmax + 1, wmax);
   }
 }
 
@@ -993,9 +989,11 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
   }
   { k_galerkin_c<<<mgrid((long long)coarse.n * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X); count_launches(1); }
 }
-void launch_finalize_level(LevelView L, int coarse, int* wave_of, int* wave_minmax, int* singular_flag,
-                           cudaStream_t s) {
-  if (L.n) { k_finalize_level<<<mgrid(L.n, 256), 256, 0, s>>>(L, coarse, wave_of, wave_minmax, singular_flag); count_launches(1); }
+void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s) {
+  if (L.n) { k_level_dinv<<<mgrid(L.n, 256), 256, 0, s>>>(L, singular_flag); count_launches(1); }
+}
+void launch_level_waves(LevelView L, int coarse, const int* off, int* wave_of, cudaStream_t s) {
+  if (L.n) { k_level_waves<<<mgrid(L.n, 256), 256, 0, s>>>(L, coarse, off[0], off[1], off[2], wave_of); count_launches(1); }
 }
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
                         int nwaves, int* scan_tmp, cudaStream_t s) {
