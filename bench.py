@@ -30,9 +30,9 @@ import numpy as np  # noqa: E402
 
 SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
-FP64_PEAK_TFLOPS = 34.79  # DFMA throughput measured on this pool's B200 (profiles/r01_fp64_peak.json)
+FP64_PEAK_TFLOPS = 37.06  # fp64 peak measured on this pool's B200: DMMA m8n8k4 37.06, DFMA 34.79 (profiles/r01_fp64_peak.json)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
-TRAFFIC = {"assemble_rows": 12.694647e9, "sgs_level0": 4.087470e9}  # per launch, from profiles/r01_ncu_full_summary.txt
+TRAFFIC = {"assemble_rows": 11.156031e9, "sgs_level0": 4.087060e9}  # per launch, from profiles/r01_ncu_full_summary.txt
 UNIT = "particle-steps/s"
 
 
@@ -271,7 +271,7 @@ def main():
                     "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": TRAFFIC.get("assemble_rows"),
                     "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
                     "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
-                    "peak_kind": "measured DFMA peak (profiles/r01_fp64_peak.json, tools/microbench/fp64peak.cu)"}
+                    "peak_kind": "measured fp64 tensor (DMMA) peak, the higher of DMMA/DFMA (profiles/r01_fp64_peak.json, tools/microbench/dmma.cu)"}
     hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
                   k in ("sgs_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
                         "lbfgs_vectors")}
