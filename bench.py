@@ -260,7 +260,7 @@ def main():
 
     # ---- rooflines (algorithmic bytes or flops / CUDA-event duration on the context stream)
     # `roofline` is the dominant kernel of the step: the level-0 assembly, bound by fp64 FMA
-    # throughput (its algorithmic flops / the measured DFMA peak).  `roofline_hbm` is the
+    # throughput (its algorithmic flops / the measured fp64 peak).  `roofline_hbm` is the
     # largest HBM-bound phase (the level-0 smoother in practice).
     peaks, peak_kind = measured_peaks()
     roofline = None
@@ -273,9 +273,13 @@ def main():
                     "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
                     "peak_kind": "measured fp64 tensor (DMMA) peak, the higher of DMMA/DFMA (profiles/r01_fp64_peak.json, tools/microbench/dmma.cu)"}
     hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
-                  k in ("sgs_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
+                  k in ("sgs_level0", "spmv_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
                         "lbfgs_vectors")}
     top = max(hbm_phases, key=lambda k: hbm_phases[k]["ms"]) if hbm_phases else None
+    # every HBM-class phase of the step: algorithmic GB/s and fraction of the measured peak
+    hbm_all = {k: {"GBps": round(v["bytes"] / (v["ms"] / 1000.0) / 1e9, 1),
+                   "frac": round(v["bytes"] / (v["ms"] / 1000.0) / 1e9 / peaks["hbm_gbs"], 3),
+                   "ms_per_step": round(v["ms"] / args.steps, 3)} for k, v in hbm_phases.items()}
     roofline_hbm = None
     if top:
         ph = hbm_phases[top]
@@ -303,7 +307,7 @@ def main():
                                outer_iterations=outer, phase_ms_per_step=phases),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps},
-                "gpu_launches": int(launches), "roofline": roofline, "roofline_hbm": roofline_hbm,
+                "gpu_launches": int(launches), "roofline": roofline, "roofline_hbm": roofline_hbm, "hbm_phases": hbm_all,
                 "cpu_baseline": cpu_baseline,
                 "clocks": clocks.summary()}
         print(json.dumps(line))

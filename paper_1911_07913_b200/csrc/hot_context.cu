@@ -124,7 +124,8 @@ struct ProfEvent {
 
 const char* kPhaseNames[] = {"activate_bin", "p2g_bc", "particle_energy", "node_gradient", "particle_tensors",
                              "assemble_rows", "hierarchy", "sgs_level0", "sgs_coarse", "residual_restrict",
-                             "coarse_pcg", "prolong", "lbfgs_vectors", "g2p_strain_advect", "upload_download"};
+                             "coarse_pcg", "prolong", "lbfgs_vectors", "g2p_strain_advect", "upload_download",
+                             "spmv_level0"};
 constexpr int kPhases = sizeof(kPhaseNames) / sizeof(kPhaseNames[0]);
 enum Phase {
   P_ACTIVATE,
@@ -141,7 +142,8 @@ enum Phase {
   P_PROLONG,
   P_VEC,
   P_G2P,
-  P_IO
+  P_IO,
+  P_SPMV0
 };
 
 }  // namespace
@@ -904,10 +906,13 @@ struct Context {
       Level& l = L[m];
       HOT_CUDA(cudaMemsetAsync(l.u.p, 0, sizeof(double) * 3 * l.n, stream));
       sgs(m, l.u.as<double>(), l.b.as<double>());
-      const int h = prof_begin(P_RESID);
+      // residual r = b - H u: the level's block-sparse SpMV (H, column ids, u b r)
+      const int hs = prof_begin(m == 0 ? P_SPMV0 : P_RESID);
       launch_residual(l.view(), l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
+      prof_end(hs, 72.0 * l.active_slots + 4.0 * kSlotPitch * l.n + 72.0 * l.n);
+      const int h = prof_begin(P_RESID);
       launch_restrict(l.view(), L[m + 1].view(), l.r.as<double>(), L[m + 1].b.as<double>(), stream);
-      prof_end(h, 72.0 * l.active_slots + 72.0 * l.n + 48.0 * L[m + 1].n);  // H, u b r (3 x 24 R), restrict
+      prof_end(h, 24.0 * l.n + 24.0 * L[m + 1].n);  // r in, coarse b out
     }
     Level& bot = L[M - 1];
     {
