@@ -187,6 +187,7 @@ struct Context {
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DBuf scan_tmp2, struct_flags;
+  DBuf grid_bar;  // 2 words: the persistent smoothers' grid barrier (per context, per device)
   DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
@@ -292,6 +293,7 @@ struct Context {
     HOT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     HOT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     struct_flags.ensure(sizeof(int) * 16);
+    grid_bar.ensure(sizeof(unsigned int) * 16);
     HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
     HOT_CUDA(cudaMallocHost(&host_int, sizeof(int) * 64));
     nred = 8 * num_sms();
@@ -864,7 +866,8 @@ struct Context {
                       stream);
       l.sgs_epoch += 2;
     } else if (l.max_wave >= stream_min && !per_wave)
-      launch_sgs_stream(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
+      launch_sgs_stream(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
+                        grid_bar.as<unsigned int>(), stream);
     else if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)
       launch_sgs_waves(l.view(), l.wave_start_h.data(), l.wave_rows.as<int>(), l.nwaves, u, b, stream);
     else
@@ -876,7 +879,7 @@ struct Context {
         trace = sgs_trace.as<long long>();
       }
       launch_sgs(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
-                 std::max(1, std::min(sgs_max_blocks(), l.max_wave)), stream, trace);
+                 std::max(1, std::min(sgs_max_blocks(), l.max_wave)), grid_bar.as<unsigned int>(), stream, trace);
       if (trace) {
         std::vector<long long> t(4 * 1025);
         HOT_CUDA(cudaMemcpy(t.data(), trace, sizeof(long long) * t.size(), cudaMemcpyDeviceToHost));

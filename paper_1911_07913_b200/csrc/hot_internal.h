@@ -157,8 +157,9 @@ void launch_restrict(LevelView fine, LevelView coarse, const double* rf, double*
 void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, double* uf, cudaStream_t s);
 /// One symmetric Gauss-Seidel sweep (forward + backward over the wave schedule), as a
 /// cooperative persistent kernel with a grid barrier between waves.
+/// bar: 2 device words of the caller's (the grid barrier's counter and release flag).
 void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
-                int grid_blocks, cudaStream_t s, long long* trace = nullptr);
+                int grid_blocks, unsigned int* bar, cudaStream_t s, long long* trace = nullptr);
 /// Jacobi-PCG from zero (pcg.hpp:17-46) as one cooperative kernel; writes x, iterations,
 /// status (0 ok, 1 rho<0, 2 pAp<=0) into stat[0..1] and accumulates iterations into *iter_acc.
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
@@ -170,7 +171,7 @@ void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* 
                      int epoch, cudaStream_t s);
 /// Level-0 smoother: both passes, all waves, one persistent kernel with bulk-copy row streaming.
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                       const double* b, cudaStream_t s);
+                       const double* b, unsigned int* bar, cudaStream_t s);
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s);
 int sgs_max_blocks();

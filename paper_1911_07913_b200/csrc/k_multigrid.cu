@@ -1016,10 +1016,8 @@ void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, doub
   if (fine.n) { k_prolong_add<<<mgrid(fine.n, 128), 128, 0, s>>>(fine, coarse, uc, uf); count_launches(1); }
 }
 void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
-                int grid_blocks, cudaStream_t s, long long* trace) {
+                int grid_blocks, unsigned int* bar, cudaStream_t s, long long* trace) {
   if (L.n == 0 || nwaves == 0) return;
-  static unsigned int* bar = nullptr;
-  if (!bar) cudaMalloc(&bar, 2 * sizeof(unsigned int));
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
   void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &trace, &bar};
   { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, kSgsSmem, s); count_launches(1); }
@@ -1037,10 +1035,8 @@ int sgs_stream_blocks() {
 }
 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                       const double* b, cudaStream_t s) {
+                       const double* b, unsigned int* bar, cudaStream_t s) {
   if (L.n == 0 || nwaves == 0) return;
-  static unsigned int* bar = nullptr;
-  if (!bar) cudaMalloc(&bar, 2 * sizeof(unsigned int));
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
   int grid = sgs_stream_blocks();
   void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar};
