@@ -1,18 +1,14 @@
 // Node-embedding Galerkin multigrid on B200 (multigrid.hpp:14-392, pcg.hpp:17-46).
 //
 //   build_restriction  dense coarse flags + scan (same lexicographic order as the
-//                      reference's sort/unique); the linear embedding weights are implicit.
-//   galerkin_coarsen   one warp per coarse row: every upper-triangle coarse block
-//                      H_c(A,B) = sum_{i in ch(A), l in ch(B)} w_iA w_lB H_f(i,l) is gathered
-//                      (deterministic, no atomics) and mirrored, so H_c is exactly symmetric.
+//                      reference's sort/unique); the embedding weights are implicit.
+//   galerkin_coarsen   two gathers, each fine block read once: X = H_f P^T per fine row
+//                      (rows streamed by bulk copy), then H_c = P X per upper coarse block,
+//                      written with its transpose (exactly symmetric), Dirichlet projection fused.
 //   smooth_sgs         the reference's serial colour-ordered symmetric Gauss-Seidel
-//                      (multigrid.hpp:298-316) reproduced exactly by a wave schedule: level 0
-//                      uses its 27 mod-3 colours (same-colour nodes never couple at radius 2);
-//                      coarse levels (mod-2 colours, radius 2) use t = 8*colour + 4a + 2b + c on
-//                      the colour sub-lattice, which is strictly increasing along every coupled
-//                      predecessor of the serial order, so rows of one wave are independent and
-//                      every row sees exactly the neighbour values the serial sweep sees.  One
-//                      cooperative persistent kernel per sweep, grid barrier between waves.
+//                      (multigrid.hpp:298-316) reproduced exactly by a wave schedule (DESIGN.md
+//                      §4.1): level 0 streams all 54 waves through one persistent bulk-copy
+//                      kernel; coarse levels run as a dataflow kernel with per-row epoch flags.
 //   coarse_solve/pcg   Jacobi-PCG from zero as one cooperative kernel (3 grid barriers per
 //                      iteration, deterministic block reductions).
 #include <cooperative_groups.h>
