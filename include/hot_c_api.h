@@ -170,7 +170,8 @@ int hot_stage_assemble(hot_ctx* ctx, const double* dv, int project);
 int hot_stage_build_hierarchy(hot_ctx* ctx, int levels, int embedding);
 int hot_stage_level_count(hot_ctx* ctx, int* levels);
 int hot_stage_level_shape(hot_ctx* ctx, int level, int* rows, int* slots);
-/* blocks: rows*125*9 doubles (row-major 3x3 per slot, zero where cols == -1); cols rows*125. */
+/* blocks: rows*slots*9 doubles (row-major 3x3 per slot, zero where cols == -1); cols rows*slots; slots from
+ * hot_stage_level_shape: 125 (radius 2) or 343 (radius 3, quadratic-embedding coarse levels). */
 int hot_stage_level_matrix(hot_ctx* ctx, int level, double* blocks, int* cols, int* coords, unsigned char* dirichlet);
 int hot_stage_matvec(hot_ctx* ctx, int level, const double* x, double* y);
 int hot_stage_vcycle(hot_ctx* ctx, const double* b, double* u, int* coarse_iterations);

@@ -94,7 +94,8 @@ struct Level {
   int nwaves = 0, max_wave = 0;
   std::vector<int> wave_start_h;
   long long active_slots = 0;
-  DBuf b, u, r;  // V-cycle vectors
+  int radius = 2;  // diagonal-storage radius (3 on quadratic-embedding coarse levels)
+  DBuf b, u, r;    // V-cycle vectors
   DenseMap dmap() const {
     DenseMap m;
     for (int a = 0; a < 3; ++a) {
@@ -113,8 +114,11 @@ struct Level {
     v.H = H.as<double>();
     v.dinv = dinv.as<double>();
     v.dir = dir.as<uint8_t>();
+    v.radius = radius;
     return v;
   }
+  int pitch() const { return level_pitch(radius); }
+  int slots() const { return level_slots(radius); }
 };
 
 struct ProfEvent {
@@ -656,8 +660,8 @@ struct Context {
   // ------------------------------------------------------------------ matrix + hierarchy
   void alloc_level(Level& l) {
     const long long n = std::max(l.n, 1);
-    l.cols.ensure(sizeof(int) * n * kSlotPitch);
-    l.H.ensure(sizeof(double) * n * 9 * kSlotPitch);
+    l.cols.ensure(sizeof(int) * n * l.pitch());
+    l.H.ensure(sizeof(double) * n * 9 * l.pitch());
     l.dinv.ensure(sizeof(double) * 9 * n);
     l.b.ensure(sizeof(double) * 3 * n);
     l.u.ensure(sizeof(double) * 3 * n);
@@ -706,15 +710,17 @@ struct Context {
     }
     int off[3] = {0, 0, 0};
     int nw = 27;
+    const int q = l.radius == 3 ? 3 : 2;  // coarse colour modulus (multigrid.hpp:275)
     if (m > 0) {
+      auto fl = [](int v, int k) { return v >= 0 ? v / k : -((-v + k - 1) / k); };
       int span[3];
       for (int a = 0; a < 3; ++a) {
-        off[a] = l.lo[a] >> 1;
-        span[a] = ((l.lo[a] + l.ext[a] - 1) >> 1) - off[a] + 1;
+        off[a] = fl(l.lo[a], q);
+        span[a] = fl(l.lo[a] + l.ext[a] - 1, q) - off[a] + 1;
       }
-      nw = 8 * 7 + 4 * (span[0] - 1) + 2 * (span[1] - 1) + (span[2] - 1) + 1;
+      nw = 8 * (q * q * q - 1) + 4 * (span[0] - 1) + 2 * (span[1] - 1) + (span[2] - 1) + 1;
     }
-    launch_level_waves(l.view(), m > 0 ? 1 : 0, off, l.wave_of.as<int>(), st);
+    launch_level_waves(l.view(), m > 0 ? 1 : 0, q, off, l.wave_of.as<int>(), st);
     l.wave_counts.ensure(sizeof(int) * (nw + 2));
     l.wave_start.ensure(sizeof(int) * (nw + 2));
     l.wave_cursor.ensure(sizeof(int) * (nw + 2));
@@ -749,7 +755,8 @@ struct Context {
   /// sets, Dirichlet flags, column ids and every level's wave schedule.  Depends only on the
   /// level-0 coordinates and Dirichlet flags, so the solve runs it on a second stream while
   /// the level-0 assembly occupies the GPU.  Returns the number of levels built.
-  int build_structure(int levels, cudaStream_t st) {
+  int build_structure(int levels, int embedding, cudaStream_t st) {
+    const int quad = embedding == 1 ? 0 : 1;
     DBuf& tmp = scan_tmp2;
     int* cnt = struct_flags.as<int>();
     level_waves(0, st, tmp);
@@ -758,17 +765,18 @@ struct Context {
       Level& f = L[m - 1];
       Level& c = L[m];
       if (f.n == 0) break;
-      for (int a = 0; a < 3; ++a) {
-        c.lo[a] = f.lo[a] >> 1;
+      for (int a = 0; a < 3; ++a) {  // parents span floor(x/2) (- 1 quadratic) .. floor(x/2) + 1
+        c.lo[a] = (f.lo[a] >> 1) - quad;
         c.ext[a] = ((f.lo[a] + f.ext[a] - 1) >> 1) + 1 - c.lo[a] + 1;
       }
+      c.radius = quad ? 3 : 2;  // coarse diagonal-storage radius (multigrid.hpp:274)
       const long long len = (long long)c.ext[0] * c.ext[1] * c.ext[2];
       c.flags.ensure(len + 16);
       c.map.ensure(sizeof(int) * len);
       c.coords.ensure(sizeof(int) * 3 * std::min<long long>(len, 8LL * f.n));
       tmp.ensure(sizeof(int) * (len / 4096 + 64));
       HOT_CUDA(cudaMemsetAsync(c.flags.p, 0, len + 16, st));
-      launch_mark_parents(f.view(), c.dmap(), c.flags.as<uint8_t>(), st);
+      launch_mark_parents(f.view(), c.dmap(), quad, c.flags.as<uint8_t>(), st);
       launch_flags_to_index(c.flags.as<uint8_t>(), len, c.ext, c.lo, c.map.as<int>(), c.coords.as<int>(),
                             tmp.as<int>(), cnt, st);
       int nc = 0;
@@ -779,7 +787,7 @@ struct Context {
       alloc_level(c);
       c.dir.ensure(std::max(nc, 1));
       HOT_CUDA(cudaMemsetAsync(c.dir.p, 0, nc, st));
-      launch_coarse_dirichlet(f.view(), c.dmap(), c.dir.as<uint8_t>(), st);
+      launch_coarse_dirichlet(f.view(), c.dmap(), quad, c.dir.as<uint8_t>(), st);
       launch_fill_cols(c.view(), st);
       level_waves(m, st, tmp);
       built = m + 1;
@@ -798,7 +806,8 @@ struct Context {
     for (int m = 1; m < built; ++m) {
       Level& f = L[m - 1];
       Level& c = L[m];
-      gal_x.ensure(sizeof(double) * 64 * 9 * std::max(f.n, 1));
+      const int span = f.radius + 3;  // quadratic X targets per axis
+      gal_x.ensure(sizeof(double) * 9 * (c.radius == 3 ? span * span * span : 64) * std::max(f.n, 1));
       launch_galerkin(f.view(), c.view(), gal_x.as<double>(), stream);
       launch_level_dinv(c.view(), iflags.as<int>() + 12, stream);
       nlevels = m + 1;
@@ -822,8 +831,7 @@ struct Context {
   void build_hierarchy(int levels, int embedding) {
     if (levels < 1) throw std::invalid_argument("build_hierarchy: need at least one level");
     if (levels > kMaxLevels) throw std::invalid_argument("build_hierarchy: too many levels");
-    if (embedding != 1 && levels > 1) throw Unsupported("quadratic embedding is not built for the device path");
-    build_values(build_structure(levels, stream));
+    build_values(build_structure(levels, embedding, stream));
   }
 
   /// build_hierarchy overlapped with the level-0 assembly: the structure half runs on the
@@ -832,11 +840,10 @@ struct Context {
   void assemble_and_build_hierarchy(const double* dvp, int levels, int embedding, bool reuse_svd) {
     if (levels < 1) throw std::invalid_argument("build_hierarchy: need at least one level");
     if (levels > kMaxLevels) throw std::invalid_argument("build_hierarchy: too many levels");
-    if (embedding != 1 && levels > 1) throw Unsupported("quadratic embedding is not built for the device path");
     HOT_CUDA(cudaEventRecord(ev_fork, stream));  // level-0 coords and Dirichlet flags are final
     assemble(dvp, true, reuse_svd);
     HOT_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-    const int built = build_structure(levels, stream2);
+    const int built = build_structure(levels, embedding, stream2);
     HOT_CUDA(cudaEventRecord(ev_join, stream2));
     HOT_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
     build_values(built);
@@ -861,7 +868,7 @@ struct Context {
     const bool per_wave = sched && std::strcmp(sched, "waves") == 0;
     const char* coarse_sched = std::getenv("HOT_SGS_COARSE");  // "flow" (default) | "barrier"
     const bool flow = !(coarse_sched && std::strcmp(coarse_sched, "barrier") == 0);
-    if (l.max_wave < stream_min && flow) {
+    if (l.radius != 2 || (l.max_wave < stream_min && flow)) {  // radius-3 levels: dataflow kernel only
       launch_sgs_flow(l.view(), l.wave_rows.as<int>(), l.wave_of.as<int>(), u, b, l.sgs_flag.as<int>(), l.sgs_epoch,
                       stream);
       l.sgs_epoch += 2;
@@ -912,7 +919,7 @@ struct Context {
       // residual r = b - H u: the level's block-sparse SpMV (H, column ids, u b r)
       const int hs = prof_begin(m == 0 ? P_SPMV0 : P_RESID);
       launch_residual(l.view(), l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
-      prof_end(hs, 72.0 * l.active_slots + 4.0 * kSlotPitch * l.n + 72.0 * l.n);
+      prof_end(hs, 72.0 * l.active_slots + 4.0 * l.pitch() * l.n + 72.0 * l.n);
       const int h = prof_begin(P_RESID);
       launch_restrict(l.view(), L[m + 1].view(), l.r.as<double>(), L[m + 1].b.as<double>(), stream);
       prof_end(h, 24.0 * l.n + 24.0 * L[m + 1].n);  // r in, coarse b out
@@ -1368,7 +1375,7 @@ long long Context::count_active_slots(int m) {
   if (l.n == 0) return 0;
   unsigned long long* d = reinterpret_cast<unsigned long long*>(scal.as<double>() + 12);
   HOT_CUDA(cudaMemsetAsync(d, 0, 8, stream));
-  { k_count_active<<<num_sms() * 4, 256, 0, stream>>>(l.cols.as<int>(), (long long)l.n * kSlotPitch, d); count_launches(1); }
+  { k_count_active<<<num_sms() * 4, 256, 0, stream>>>(l.cols.as<int>(), (long long)l.n * l.pitch(), d); count_launches(1); }
   unsigned long long h = 0;
   HOT_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, stream));
   sync();
@@ -1633,7 +1640,7 @@ int hot_stage_level_shape(hot_ctx* ctx, int level, int* rows, int* slots) {
   return guard(ctx, [&] {
     if (level < 0 || level >= ctx->c.nlevels) throw std::logic_error("no such level");
     *rows = ctx->c.L[level].n;
-    *slots = hotb200::kSlots;
+    *slots = ctx->c.L[level].slots();
   });
 }
 
@@ -1643,20 +1650,20 @@ int hot_stage_level_matrix(hot_ctx* ctx, int level, double* blocks, int* cols, i
     if (level < 0 || level >= c.nlevels) throw std::logic_error("no such level");
     const hotb200::Level& l = c.L[level];
     const long long n = l.n;
-    std::vector<int> cl(n * hotb200::kSlotPitch);
-    std::vector<double> H(n * 9 * hotb200::kSlotPitch);
+    const int pitch = l.pitch(), ns = l.slots();
+    std::vector<int> cl(n * pitch);
+    std::vector<double> H(n * 9 * pitch);
     HOT_CUDA(cudaMemcpyAsync(cl.data(), l.cols.p, sizeof(int) * cl.size(), cudaMemcpyDeviceToHost, c.stream));
     HOT_CUDA(cudaMemcpyAsync(H.data(), l.H.p, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, c.stream));
     if (coords) HOT_CUDA(cudaMemcpyAsync(coords, l.coords.p, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
     if (dirichlet) HOT_CUDA(cudaMemcpyAsync(dirichlet, l.dir.p, n, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     for (long long i = 0; i < n; ++i)
-      for (int s = 0; s < hotb200::kSlots; ++s) {
-        const int col = cl[i * hotb200::kSlotPitch + s];
-        if (cols) cols[i * hotb200::kSlots + s] = col;
+      for (int s = 0; s < ns; ++s) {
+        const int col = cl[i * pitch + s];
+        if (cols) cols[i * ns + s] = col;
         if (blocks)
-          for (int e = 0; e < 9; ++e)
-            blocks[(i * hotb200::kSlots + s) * 9 + e] = col < 0 ? 0.0 : H[(i * 9 + e) * hotb200::kSlotPitch + s];
+          for (int e = 0; e < 9; ++e) blocks[(i * ns + s) * 9 + e] = col < 0 ? 0.0 : H[(i * 9 + e) * pitch + s];
       }
   });
 }

@@ -31,8 +31,10 @@ struct BinsView {
 };
 
 /// One multigrid level in diagonal storage, component-major per row:
-/// H[(row*9 + e)*kSlotPitch + slot], e = 3*r + c of the 3x3 block, slot lexicographic in
-/// {-2..2}^3 (objective.hpp:24-32).  cols[row*kSlotPitch + slot] = -1 when inactive.
+/// H[(row*9 + e)*pitch + slot], e = 3*r + c of the 3x3 block, slot lexicographic in
+/// {-R..R}^3 (objective.hpp:24-32).  cols[row*pitch + slot] = -1 when inactive.  R = 2
+/// (125 slots, pitch 128) on level 0 and on linear-embedding coarse levels; R = 3 (343 slots,
+/// pitch 352) on quadratic-embedding coarse levels (multigrid.hpp:274-275).
 struct LevelView {
   int n;
   const int* coords;  // 3*n, lexicographic
@@ -41,7 +43,13 @@ struct LevelView {
   double* H;
   double* dinv;       // 9*n row-major
   const uint8_t* dir;
+  int radius;         // diagonal-storage radius R
 };
+
+__host__ __device__ constexpr int level_slots(int radius) { return (2 * radius + 1) * (2 * radius + 1) * (2 * radius + 1); }
+__host__ __device__ constexpr int level_pitch(int radius) { return radius == 2 ? 128 : 352; }
+static_assert(level_pitch(2) == kSlotPitch && level_slots(2) == kSlots, "radius-2 layout");
+static_assert(level_pitch(3) >= level_slots(3) && level_pitch(3) % 32 == 0, "radius-3 layout");
 
 struct GridView {
   int n;
@@ -141,14 +149,15 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
                           const double* Tu, cudaStream_t s);
 
 // ---------------------------------------------------------------- multigrid (k_multigrid.cu)
-void launch_mark_parents(LevelView fine, DenseMap cmap, uint8_t* flags, cudaStream_t s);
-void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaStream_t s);
-/// X: scratch of 64*9 doubles per fine row.
+/// quad: quadratic node embedding (multigrid.hpp:72-90).
+void launch_mark_parents(LevelView fine, DenseMap cmap, int quad, uint8_t* flags, cudaStream_t s);
+void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, int quad, uint8_t* cdir, cudaStream_t s);
+/// X: scratch per fine row of 64*9 doubles (linear) or (R_f+3)^3 * 9 (quadratic: coarse.radius == 3).
 void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s);
 /// diag inverse, singular check, wave id per row (level 0: colour mod 3; coarse: wavefront).
 /// D^-1 per row (+ singular flag) and the wave id per row (coarse: offsets = bbox min >> 1).
 void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s);
-void launch_level_waves(LevelView L, int coarse, const int* off, int* wave_of, cudaStream_t s);
+void launch_level_waves(LevelView L, int coarse, int modulus, const int* off, int* wave_of, cudaStream_t s);
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
                         int nwaves, int* scan_tmp, cudaStream_t s);
 void launch_spmv(LevelView L, const double* x, double* y, cudaStream_t s);

@@ -90,13 +90,14 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
 }
 
 __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)L.n * kSlotPitch;
+  const int R = L.radius, P = level_pitch(R), S = level_slots(R), W = 2 * R + 1;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)L.n * P;
        t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t / kSlotPitch), s = (int)(t % kSlotPitch);
+    const int i = (int)(t / P), s = (int)(t % P);
     int c = -1;
-    if (s < kSlots)
-      c = dense_lookup(L.map, L.coords[3 * i] + s / 25 - 2, L.coords[3 * i + 1] + (s / 5) % 5 - 2,
-                       L.coords[3 * i + 2] + s % 5 - 2);
+    if (s < S)
+      c = dense_lookup(L.map, L.coords[3 * i] + s / (W * W) - R, L.coords[3 * i + 1] + (s / W) % W - R,
+                       L.coords[3 * i + 2] + s % W - R);
     cols[t] = c;
   }
 }
@@ -411,7 +412,7 @@ void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, doub
 
 void launch_fill_cols(LevelView L, cudaStream_t s) {
   if (L.n == 0) return;
-  { k_fill_cols<<<agrid((long long)L.n * kSlotPitch, 256), 256, 0, s>>>(L, const_cast<int*>(L.cols)); count_launches(1); }
+  { k_fill_cols<<<agrid((long long)L.n * level_pitch(L.radius), 256), 256, 0, s>>>(L, const_cast<int*>(L.cols)); count_launches(1); }
 }
 
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,

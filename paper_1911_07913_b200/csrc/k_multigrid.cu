@@ -38,15 +38,42 @@ __device__ __forceinline__ double wsum(double v) {
 
 __device__ __forceinline__ int floor_div2(int x) { return x >> 1; }  // arithmetic shift = floor
 
-__global__ void k_mark_parents(LevelView f, DenseMap cmap, uint8_t* __restrict__ flags) {
+/// Coarse parents of a fine lattice coordinate along one axis and their embedding weights
+/// (multigrid.hpp:63-93, embedding_entries_1d): linear: even c -> c/2 (1); odd -> floor(c/2),
+/// +1 (1/2 each).  Quadratic: even c -> c/2-1, c/2, c/2+1 (1/8, 3/4, 1/8); odd -> floor(c/2),
+/// +1 (1/2 each).
+__device__ __forceinline__ void parents_1d(int c, int quad, int& lo, int& cnt, double w[3]) {
+  if (c & 1) {
+    lo = floor_div2(c);
+    cnt = 2;
+    w[0] = w[1] = 0.5;
+  } else if (quad) {
+    lo = c / 2 - 1;
+    cnt = 3;
+    w[0] = 0.125;
+    w[1] = 0.75;
+    w[2] = 0.125;
+  } else {
+    lo = c / 2;
+    cnt = 1;
+    w[0] = 1.0;
+  }
+}
+
+/// Weight of the fine child 2J + d of coarse node J along one axis (0 outside the embedding).
+__device__ __forceinline__ double child_w(int d, int quad) {
+  if (d == 0) return quad ? 0.75 : 1.0;
+  if (d == 1 || d == -1) return 0.5;
+  if (quad && (d == 2 || d == -2)) return 0.125;
+  return 0.0;
+}
+
+__global__ void k_mark_parents(LevelView f, DenseMap cmap, int quad, uint8_t* __restrict__ flags) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < f.n; i += gridDim.x * blockDim.x) {
     int lo[3], cnt[3];
+    double w[3][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const int c = f.coords[3 * i + a];
-      lo[a] = floor_div2(c);
-      cnt[a] = (c & 1) ? 2 : 1;
-    }
+    for (int a = 0; a < 3; ++a) parents_1d(f.coords[3 * i + a], quad, lo[a], cnt[a], w[a]);
     for (int x = 0; x < cnt[0]; ++x)
       for (int y = 0; y < cnt[1]; ++y)
         for (int z = 0; z < cnt[2]; ++z) {
@@ -56,16 +83,14 @@ __global__ void k_mark_parents(LevelView f, DenseMap cmap, uint8_t* __restrict__
   }
 }
 
-__global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, uint8_t* __restrict__ cdir) {
+/// A coarse node is Dirichlet when a fine Dirichlet node embeds into it (multigrid.hpp:151).
+__global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, int quad, uint8_t* __restrict__ cdir) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < f.n; i += gridDim.x * blockDim.x) {
     if (!f.dir[i]) continue;
     int lo[3], cnt[3];
+    double w[3][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const int c = f.coords[3 * i + a];
-      lo[a] = floor_div2(c);
-      cnt[a] = (c & 1) ? 2 : 1;
-    }
+    for (int a = 0; a < 3; ++a) parents_1d(f.coords[3 * i + a], quad, lo[a], cnt[a], w[a]);
     for (int x = 0; x < cnt[0]; ++x)
       for (int y = 0; y < cnt[1]; ++y)
         for (int z = 0; z < cnt[2]; ++z) cdir[dense_lookup(cmap, lo[0] + x, lo[1] + y, lo[2] + z)] = 1;
@@ -227,12 +252,142 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin_c(LevelView f, LevelVie
   }
 }
 
+/// Galerkin product for the QUADRATIC node embedding (coarse radius 3, multigrid.hpp:274),
+/// the same two gathers as the linear kernels:
+///   X[i][t] = sum_{l in row i, B parent of l} w_lB H_f(i,l), B = base(i) + t, t in [0, RF+3)^3,
+///             base_a = floor((c_a - RF) / 2) - 1      (one warp per fine row, row in smem)
+///   H_c(A,B) = sum_{i = 2A + d, |d| <= 2} w_iA X[i][B - base(i)]   (one lane per upper block)
+/// Children weights per axis (1/8, 1/2, 3/4, 1/2, 1/8) for d = -2..2.  A contribution always
+/// lands within radius 3 (|B - A| <= |l - i| / 2 + 2 <= 3), as the reference's overflow check
+/// requires (multigrid.hpp:186-188).
+constexpr int kGqWarps = 4;
+
+template <int RF>
+__global__ void __launch_bounds__(kGqWarps * 32) k_galerkin_qx(LevelView f, double* __restrict__ X) {
+  constexpr int P = level_pitch(RF), NSL = 2 * RF + 1, SP = RF + 3, NT = SP * SP * SP;
+  extern __shared__ __align__(16) double gq_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  double* H = gq_smem + (size_t)wib * 9 * P;
+  for (int i = gw; i < f.n; i += nw) {
+    const double* src = f.H + (long long)i * 9 * P;
+    __syncwarp();
+    for (int q = lane; q < 9 * P; q += 32) H[q] = __ldcs(src + q);
+    __syncwarp();
+    int c[3], base[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      c[a] = f.coords[3 * i + a];
+      base[a] = ((c[a] - RF) >> 1) - 1;
+    }
+    for (int t = lane; t < NT; t += 32) {
+      const int B0 = base[0] + t / (SP * SP), B1 = base[1] + (t / SP) % SP, B2 = base[2] + t % SP;
+      double acc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+      for (int d0 = -2; d0 <= 2; ++d0) {
+        const int f0 = 2 * B0 + d0 - c[0];
+        if (f0 < -RF || f0 > RF) continue;
+        const double w0 = child_w(d0, 1);
+        for (int d1 = -2; d1 <= 2; ++d1) {
+          const int f1 = 2 * B1 + d1 - c[1];
+          if (f1 < -RF || f1 > RF) continue;
+          const double w01 = w0 * child_w(d1, 1);
+          for (int d2 = -2; d2 <= 2; ++d2) {
+            const int f2 = 2 * B2 + d2 - c[2];
+            if (f2 < -RF || f2 > RF) continue;
+            const double w = w01 * child_w(d2, 1);
+            const int sl = ((f0 + RF) * NSL + (f1 + RF)) * NSL + (f2 + RF);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[k] += w * H[k * P + sl];  // zero when l is inactive
+          }
+        }
+      }
+      double* dst = X + ((long long)i * NT + t) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) dst[k] = acc[k];
+    }
+  }
+}
+
+template <int RF>
+__global__ void __launch_bounds__(kMgThreads) k_galerkin_qc(LevelView f, LevelView c, const double* __restrict__ X) {
+  constexpr int SP = RF + 3, NT = SP * SP * SP;
+  constexpr int PC = level_pitch(3), SC = level_slots(3), DC = SC / 2, UPC = SC - DC;  // 352, 343, 171, 172
+  __shared__ int ch_s[kMgWarps][125];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  int* ch = ch_s[wib];
+  for (int A = gw; A < c.n; A += nw) {
+    const int A0 = c.coords[3 * A], A1 = c.coords[3 * A + 1], A2 = c.coords[3 * A + 2];
+    const bool dA = c.dir[A] != 0;
+    __syncwarp();
+    for (int t = lane; t < 125; t += 32)
+      ch[t] = dense_lookup(f.map, 2 * A0 + t / 25 - 2, 2 * A1 + (t / 5) % 5 - 2, 2 * A2 + t % 5 - 2);
+    __syncwarp();
+    for (int s = lane; s < PC; s += 32)
+      if (s >= SC || c.cols[(long long)A * PC + s] < 0)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) __stcs(c.H + ((long long)A * 9 + k) * PC + s, 0.0);
+    for (int u = lane; u < UPC; u += 32) {
+      const int s = DC + u;
+      const int B = c.cols[(long long)A * PC + s];
+      if (B < 0) continue;
+      const int O0 = s / 49 - 3, O1 = (s / 7) % 7 - 3, O2 = s % 7 - 3;
+      double acc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+      for (int t = 0; t < 125; ++t) {
+        const int i = ch[t];
+        if (i < 0) continue;
+        const int d0 = t / 25 - 2, d1 = (t / 5) % 5 - 2, d2 = t % 5 - 2;
+        // B - base(i), base_a = floor((2A + d - RF) / 2) - 1
+        const int q0 = A0 + O0 - ((((2 * A0 + d0) - RF) >> 1) - 1);
+        const int q1 = A1 + O1 - ((((2 * A1 + d1) - RF) >> 1) - 1);
+        const int q2 = A2 + O2 - ((((2 * A2 + d2) - RF) >> 1) - 1);
+        if ((unsigned)q0 >= (unsigned)SP || (unsigned)q1 >= (unsigned)SP || (unsigned)q2 >= (unsigned)SP) continue;
+        const double w = child_w(d0, 1) * child_w(d1, 1) * child_w(d2, 1);
+        const double* x = X + ((long long)i * NT + (q0 * SP + q1) * SP + q2) * 9;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] += w * __ldg(x + k);
+      }
+      double C[9];
+      if (s == DC) {
+        C[0] = acc[0];
+        C[4] = acc[4];
+        C[8] = acc[8];
+        C[1] = C[3] = acc[1];
+        C[2] = C[6] = acc[2];
+        C[5] = C[7] = acc[5];
+        if (dA) {
+#pragma unroll
+          for (int k = 0; k < 9; ++k) C[k] = (k % 4 == 0) ? 1.0 : 0.0;
+        }
+      } else {
+        const bool zero = dA || c.dir[B] != 0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) C[k] = zero ? 0.0 : acc[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) __stcs(c.H + ((long long)A * 9 + k) * PC + s, C[k]);
+      if (s != DC) {
+        const int sm = SC - 1 - s;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int q = 0; q < 3; ++q) __stcs(c.H + ((long long)B * 9 + 3 * r + q) * PC + sm, C[3 * q + r]);
+      }
+    }
+  }
+}
+
 /// Level diagonal inverse (multigrid.hpp:233-240) with the singular-block check.
 __global__ void k_level_dinv(LevelView L, int* singular) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
     M3 D;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) D.m[k] = L.H[((long long)i * 9 + k) * kSlotPitch + kDiagSlot];
+    for (int k = 0; k < 9; ++k)
+      D.m[k] = L.H[((long long)i * 9 + k) * level_pitch(L.radius) + level_slots(L.radius) / 2];
     double det;
     const M3 Di = m3_inverse(D, &det);
     if (!(fabs(det) > 0.0)) atomicExch(singular, 1);
@@ -243,15 +398,19 @@ __global__ void k_level_dinv(LevelView L, int* singular) {
 
 /// Wave id of every row (§4.1 of DESIGN.md): level 0 the mod-3 colour; coarse levels
 /// 8 * colour + 4 (x>>1) + 2 (y>>1) + (z>>1), offset by the bounding box so ids start near 0.
-__global__ void k_level_waves(LevelView L, int coarse, int off0, int off1, int off2, int* __restrict__ wave_of) {
+__global__ void k_level_waves(LevelView L, int coarse, int q, int off0, int off1, int off2, int* __restrict__ wave_of) {
+  // level 0: the mod-3 colour; coarse levels, colour modulus q (2 linear, 3 quadratic) and
+  // radius <= q: t = 8 * colour + 4 X + 2 Y + Z on the colour sub-lattice (X = floor(x / q))
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
     const int c0 = L.coords[3 * i], c1 = L.coords[3 * i + 1], c2 = L.coords[3 * i + 2];
+    auto md = [](int v, int k) { return ((v % k) + k) % k; };
+    auto fl = [](int v, int k) { return v >= 0 ? v / k : -((-v + k - 1) / k); };
     int w;
     if (!coarse) {
-      w = (((c0 % 3) + 3) % 3 * 3 + ((c1 % 3) + 3) % 3) * 3 + ((c2 % 3) + 3) % 3;
+      w = (md(c0, 3) * 3 + md(c1, 3)) * 3 + md(c2, 3);
     } else {
-      const int col = ((c0 & 1) * 2 + (c1 & 1)) * 2 + (c2 & 1);
-      w = 8 * col + 4 * ((c0 >> 1) - off0) + 2 * ((c1 >> 1) - off1) + ((c2 >> 1) - off2);
+      const int col = (md(c0, q) * q + md(c1, q)) * q + md(c2, q);
+      w = 8 * col + 4 * (fl(c0, q) - off0) + 2 * (fl(c1, q) - off1) + (fl(c2, q) - off2);
     }
     wave_of[i] = w;
   }
@@ -270,27 +429,29 @@ __global__ void k_wave_scatter(const int* __restrict__ wave_of, int n, int wmin,
 /// all 36 block entries a lane needs are requested before any is consumed (memory-level
 /// parallelism); inactive slots hold zeros (written by assembly / Galerkin), so they are
 /// multiplied by 0 instead of branched around.
+template <int R>
 __device__ __forceinline__ void row_product(const LevelView& L, int i, const double* __restrict__ x, int lane,
                                             double& y0, double& y1, double& y2, bool cg_load) {
-  const int* cols = L.cols + (long long)i * kSlotPitch;
-  const double* h = L.H + (long long)i * 9 * kSlotPitch;
-  int c[4];
+  constexpr int P = level_pitch(R), NS = P / 32;
+  const int* cols = L.cols + (long long)i * P;
+  const double* h = L.H + (long long)i * 9 * P;
+  int c[NS];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) c[k] = __ldg(cols + lane + 32 * k);
-  double xv[4][3];
+  for (int k = 0; k < NS; ++k) c[k] = __ldg(cols + lane + 32 * k);
+  double xv[NS][3];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < NS; ++k) {
     const double* xp = x + 3 * (c[k] >= 0 ? c[k] : 0);  // inactive slots: zero block, any finite x
 #pragma unroll
     for (int a = 0; a < 3; ++a) xv[k][a] = cg_load ? __ldcg(xp + a) : __ldg(xp + a);
   }
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < NS; ++k) {
     const int s = lane + 32 * k;
     double hv[9];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) hv[e] = __ldcs(h + e * kSlotPitch + s);
+    for (int e = 0; e < 9; ++e) hv[e] = __ldcs(h + e * P + s);
     a0 += hv[0] * xv[k][0] + hv[1] * xv[k][1] + hv[2] * xv[k][2];
     a1 += hv[3] * xv[k][0] + hv[4] * xv[k][1] + hv[5] * xv[k][2];
     a2 += hv[6] * xv[k][0] + hv[7] * xv[k][1] + hv[8] * xv[k][2];
@@ -300,6 +461,7 @@ __device__ __forceinline__ void row_product(const LevelView& L, int i, const dou
   y2 = wsum(a2);
 }
 
+template <int R>
 __global__ void __launch_bounds__(kMgThreads) k_spmv(LevelView L, const double* __restrict__ x, double* __restrict__ y,
                                                      const double* __restrict__ b) {
   const int lane = threadIdx.x & 31;
@@ -307,7 +469,7 @@ __global__ void __launch_bounds__(kMgThreads) k_spmv(LevelView L, const double* 
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int i = gw; i < L.n; i += nw) {
     double y0, y1, y2;
-    row_product(L, i, x, lane, y0, y1, y2, false);
+    row_product<R>(L, i, x, lane, y0, y1, y2, false);
     if (lane == 0) {
       if (b) {
         y[3 * i] = b[3 * i] - y0;
@@ -322,16 +484,19 @@ __global__ void __launch_bounds__(kMgThreads) k_spmv(LevelView L, const double* 
   }
 }
 
-__global__ void k_restrict(LevelView f, LevelView c, const double* __restrict__ rf, double* __restrict__ bc) {
+/// b_c = R r_f (multigrid.hpp:24-31) as a gather over each coarse node's fine children 2J + d
+/// (|d| <= 1 linear, <= 2 quadratic), Dirichlet coarse rows zeroed (multigrid.hpp:372-376).
+__global__ void k_restrict(LevelView f, LevelView c, int quad, const double* __restrict__ rf, double* __restrict__ bc) {
+  const int r = quad ? 2 : 1, w1 = 2 * r + 1;
   for (int J = blockIdx.x * blockDim.x + threadIdx.x; J < c.n; J += gridDim.x * blockDim.x) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     if (!c.dir[J]) {
       const int J0 = c.coords[3 * J], J1 = c.coords[3 * J + 1], J2 = c.coords[3 * J + 2];
-      for (int t = 0; t < 27; ++t) {
-        const int d0 = t / 9 - 1, d1 = (t / 3) % 3 - 1, d2 = t % 3 - 1;
+      for (int t = 0; t < w1 * w1 * w1; ++t) {
+        const int d0 = t / (w1 * w1) - r, d1 = (t / w1) % w1 - r, d2 = t % w1 - r;
         const int i = dense_lookup(f.map, 2 * J0 + d0, 2 * J1 + d1, 2 * J2 + d2);
         if (i < 0) continue;
-        const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
+        const double w = child_w(d0, quad) * child_w(d1, quad) * child_w(d2, quad);
         a0 += w * rf[3 * i];
         a1 += w * rf[3 * i + 1];
         a2 += w * rf[3 * i + 2];
@@ -343,24 +508,23 @@ __global__ void k_restrict(LevelView f, LevelView c, const double* __restrict__ 
   }
 }
 
-__global__ void k_prolong_add(LevelView f, LevelView c, const double* __restrict__ uc, double* __restrict__ uf) {
+/// u_f += P u_c (multigrid.hpp:33-39): each fine node's embedding parents.
+__global__ void k_prolong_add(LevelView f, LevelView c, int quad, const double* __restrict__ uc,
+                              double* __restrict__ uf) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < f.n; i += gridDim.x * blockDim.x) {
     int lo[3], cnt[3];
+    double w[3][3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const int cc = f.coords[3 * i + a];
-      lo[a] = floor_div2(cc);
-      cnt[a] = (cc & 1) ? 2 : 1;
-    }
-    const double w = (cnt[0] == 2 ? 0.5 : 1.0) * (cnt[1] == 2 ? 0.5 : 1.0) * (cnt[2] == 2 ? 0.5 : 1.0);
+    for (int a = 0; a < 3; ++a) parents_1d(f.coords[3 * i + a], quad, lo[a], cnt[a], w[a]);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int x = 0; x < cnt[0]; ++x)
       for (int y = 0; y < cnt[1]; ++y)
         for (int z = 0; z < cnt[2]; ++z) {
           const int J = dense_lookup(c.map, lo[0] + x, lo[1] + y, lo[2] + z);
-          a0 += w * uc[3 * J];
-          a1 += w * uc[3 * J + 1];
-          a2 += w * uc[3 * J + 2];
+          const double ww = w[0][x] * w[1][y] * w[2][z];
+          a0 += ww * uc[3 * J];
+          a1 += ww * uc[3 * J + 1];
+          a2 += ww * uc[3 * J + 2];
         }
     uf[3 * i] += a0;
     uf[3 * i + 1] += a1;
@@ -585,10 +749,12 @@ __global__ void __launch_bounds__(kWaveThreads) k_sgs_wave(LevelView L, const in
 /// still hold their old values when it reads them: exactly the sequential sweep.  Progress:
 /// the lowest unfinished row in pass order always has all predecessors done and its CTA has
 /// reached it (each CTA walks its rows in order).
-__global__ void __launch_bounds__(kSgsThreads) k_sgs_flow(LevelView L, const int* __restrict__ order, int n,
+template <int R>
+__global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const int* __restrict__ order, int n,
                                                          const int* __restrict__ wave_of, double* u,
                                                          const double* __restrict__ b, int* flag, int epoch) {
-  __shared__ double red[kSgsThreads / 32][3];
+  constexpr int T = level_pitch(R), S = level_slots(R);  // one thread per diagonal-storage slot
+  __shared__ double red[T / 32][3];
   const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
   for (int pass = 0; pass < 2; ++pass) {
     const int e = epoch + pass;
@@ -598,11 +764,11 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs_flow(LevelView L, const int
       double h[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) h[q] = 0.0;
-      if (s < kSlots) {
-        c = __ldg(L.cols + (long long)i * kSlotPitch + s);
-        const double* hp = L.H + (long long)i * 9 * kSlotPitch + s;
+      if (s < S) {
+        c = __ldg(L.cols + (long long)i * T + s);
+        const double* hp = L.H + (long long)i * 9 * T + s;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) h[q] = __ldcs(hp + q * kSlotPitch);
+        for (int q = 0; q < 9; ++q) h[q] = __ldcs(hp + q * T);
       }
       double D[9], rb[3];
       if (s == 0) {
@@ -625,7 +791,7 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs_flow(LevelView L, const int
       }
       __syncthreads();
       double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-      if (s < kSlots) {
+      if (s < S) {
         const double* xp = u + 3 * (c >= 0 ? c : 0);  // inactive slots: zero block
         x0 = __ldcg(xp);
         x1 = __ldcg(xp + 1);
@@ -646,7 +812,7 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs_flow(LevelView L, const int
       if (s == 0) {
         double y0 = 0.0, y1 = 0.0, y2 = 0.0;
 #pragma unroll
-        for (int q = 0; q < kSgsThreads / 32; ++q) {
+        for (int q = 0; q < T / 32; ++q) {
           y0 += red[q][0];
           y1 += red[q][1];
           y2 += red[q][2];
@@ -832,6 +998,7 @@ __device__ __forceinline__ void block_partial(double v, double* partials) {
   __syncthreads();
 }
 
+template <int R>
 __global__ void __launch_bounds__(kMgThreads) k_pcg(LevelView L, const double* __restrict__ b, double* x, double* r,
                                                     double* z, double* p, double* Ap, double rel, int cap,
                                                     double* partials, int* stat, int* iter_acc) {
@@ -872,7 +1039,7 @@ __global__ void __launch_bounds__(kMgThreads) k_pcg(LevelView L, const double* _
       loc = 0.0;
       for (int i = gw; i < L.n; i += nw) {
         double y0, y1, y2;
-        row_product(L, i, p, lane, y0, y1, y2, true);
+        row_product<R>(L, i, p, lane, y0, y1, y2, true);
         if (lane == 0) {
           Ap[3 * i] = y0;
           Ap[3 * i + 1] = y1;
@@ -943,9 +1110,10 @@ int coop_blocks(const void* fn, int threads, int smem = 0) {
 
 }  // namespace
 
+template <int R>
 int sgs_flow_blocks() {
   static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_sgs_flow, kSgsThreads, 0);
+  if (!v) v = coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
   return v;
 }
 
@@ -953,9 +1121,15 @@ void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* 
                      int epoch, cudaStream_t s) {
   if (L.n == 0) return;
   int n = L.n;
-  int grid = std::min(sgs_flow_blocks(), n);
   void* args[] = {&L, (void*)&order, &n, (void*)&wave_of, &u, (void*)&b, &flag, &epoch};
-  { cudaLaunchCooperativeKernel((const void*)k_sgs_flow, grid, kSgsThreads, args, 0, s); count_launches(1); }
+  if (L.radius == 2) {
+    const int grid = std::min(sgs_flow_blocks<2>(), n);
+    cudaLaunchCooperativeKernel((const void*)k_sgs_flow<2>, grid, level_pitch(2), args, 0, s);
+  } else {
+    const int grid = std::min(sgs_flow_blocks<3>(), n);
+    cudaLaunchCooperativeKernel((const void*)k_sgs_flow<3>, grid, level_pitch(3), args, 0, s);
+  }
+  count_launches(1);
 }
 
 int sgs_max_blocks() {
@@ -965,18 +1139,43 @@ int sgs_max_blocks() {
 }
 int pcg_max_blocks() {
   static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_pcg, kMgThreads);
+  if (!v) v = std::min(coop_blocks((const void*)k_pcg<2>, kMgThreads), coop_blocks((const void*)k_pcg<3>, kMgThreads));
   return v;
 }
 
-void launch_mark_parents(LevelView fine, DenseMap cmap, uint8_t* flags, cudaStream_t s) {
-  if (fine.n) { k_mark_parents<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, flags); count_launches(1); }
+void launch_mark_parents(LevelView fine, DenseMap cmap, int quad, uint8_t* flags, cudaStream_t s) {
+  if (fine.n) { k_mark_parents<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, quad, flags); count_launches(1); }
 }
-void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, uint8_t* cdir, cudaStream_t s) {
-  if (fine.n) { k_coarse_dirichlet<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, cdir); count_launches(1); }
+void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, int quad, uint8_t* cdir, cudaStream_t s) {
+  if (fine.n) { k_coarse_dirichlet<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, quad, cdir); count_launches(1); }
 }
 void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s) {
   if (coarse.n == 0) return;
+  if (coarse.radius == 3) {  // quadratic embedding
+    const int fr = fine.radius;
+    const int smem = kGqWarps * 9 * level_pitch(fr) * 8;
+    const void* fx = fr == 2 ? (const void*)k_galerkin_qx<2> : (const void*)k_galerkin_qx<3>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute((const void*)k_galerkin_qx<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kGqWarps * 9 * level_pitch(2) * 8);
+      cudaFuncSetAttribute((const void*)k_galerkin_qx<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kGqWarps * 9 * level_pitch(3) * 8);
+      attr = true;
+    }
+    (void)fx;
+    const int bx = mgrid((long long)fine.n * 32, kGqWarps * 32);
+    const int bc = mgrid((long long)coarse.n * 32, kMgThreads);
+    if (fr == 2) {
+      k_galerkin_qx<2><<<bx, kGqWarps * 32, smem, s>>>(fine, X);
+      k_galerkin_qc<2><<<bc, kMgThreads, 0, s>>>(fine, coarse, X);
+    } else {
+      k_galerkin_qx<3><<<bx, kGqWarps * 32, smem, s>>>(fine, X);
+      k_galerkin_qc<3><<<bc, kMgThreads, 0, s>>>(fine, coarse, X);
+    }
+    count_launches(2);
+    return;
+  }
   static const int gx_blocks = coop_blocks((const void*)k_galerkin_x, kGalXWarps * 32, kGalXSmem);
   {
     const int blocks = (int)std::min<long long>(gx_blocks, ((long long)fine.n + kGalXWarps - 1) / kGalXWarps);
@@ -988,8 +1187,8 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
 void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s) {
   if (L.n) { k_level_dinv<<<mgrid(L.n, 256), 256, 0, s>>>(L, singular_flag); count_launches(1); }
 }
-void launch_level_waves(LevelView L, int coarse, const int* off, int* wave_of, cudaStream_t s) {
-  if (L.n) { k_level_waves<<<mgrid(L.n, 256), 256, 0, s>>>(L, coarse, off[0], off[1], off[2], wave_of); count_launches(1); }
+void launch_level_waves(LevelView L, int coarse, int modulus, const int* off, int* wave_of, cudaStream_t s) {
+  if (L.n) { k_level_waves<<<mgrid(L.n, 256), 256, 0, s>>>(L, coarse, modulus, off[0], off[1], off[2], wave_of); count_launches(1); }
 }
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
                         int nwaves, int* scan_tmp, cudaStream_t s) {
@@ -1000,16 +1199,28 @@ void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* s
   if (n) { k_wave_scatter<<<mgrid(n, 256), 256, 0, s>>>(wave_of, n, wmin, cursor, rows); count_launches(1); }
 }
 void launch_spmv(LevelView L, const double* x, double* y, cudaStream_t s) {
-  if (L.n) { k_spmv<<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr); count_launches(1); }
+  if (!L.n) return;
+  if (L.radius == 2)
+    k_spmv<2><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr);
+  else
+    k_spmv<3><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr);
+  count_launches(1);
 }
 void launch_residual(LevelView L, const double* b, const double* u, double* r, cudaStream_t s) {
-  if (L.n) { k_spmv<<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b); count_launches(1); }
+  if (!L.n) return;
+  if (L.radius == 2)
+    k_spmv<2><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b);
+  else
+    k_spmv<3><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b);
+  count_launches(1);
 }
 void launch_restrict(LevelView fine, LevelView coarse, const double* rf, double* bc, cudaStream_t s) {
-  if (coarse.n) { k_restrict<<<mgrid(coarse.n, 128), 128, 0, s>>>(fine, coarse, rf, bc); count_launches(1); }
+  const int quad = coarse.radius == 3;  // quadratic-embedding coarse levels carry radius 3
+  if (coarse.n) { k_restrict<<<mgrid(coarse.n, 128), 128, 0, s>>>(fine, coarse, quad, rf, bc); count_launches(1); }
 }
 void launch_prolong_add(LevelView fine, LevelView coarse, const double* uc, double* uf, cudaStream_t s) {
-  if (fine.n) { k_prolong_add<<<mgrid(fine.n, 128), 128, 0, s>>>(fine, coarse, uc, uf); count_launches(1); }
+  const int quad = coarse.radius == 3;
+  if (fine.n) { k_prolong_add<<<mgrid(fine.n, 128), 128, 0, s>>>(fine, coarse, quad, uc, uf); count_launches(1); }
 }
 void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u, const double* b,
                 int grid_blocks, unsigned int* bar, cudaStream_t s, long long* trace) {
@@ -1065,7 +1276,8 @@ void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_r
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s) {
   void* args[] = {&L, (void*)&b, &x, &r, &z, &p, &Ap, &rel, &cap, &partials, &stat, &iter_acc};
-  { cudaLaunchCooperativeKernel((const void*)k_pcg, grid_blocks, kMgThreads, args, 0, s); count_launches(1); }
+  const void* fn = L.radius == 2 ? (const void*)k_pcg<2> : (const void*)k_pcg<3>;
+  { cudaLaunchCooperativeKernel(fn, grid_blocks, kMgThreads, args, 0, s); count_launches(1); }
 }
 
 }  // namespace hotb200

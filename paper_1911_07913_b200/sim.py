@@ -62,13 +62,13 @@ class Simulation:
     # ---------------------------------------------------------------- configuration
     def set_solver(self, epsilon=None, tau=None, levels=None, window=None, kind=None, ls_shrink=0.5, ls_armijo=1e-4,
                    ls_max_steps=30, cg_cap=10000, outer_cap=1000, pinned_coarse_iterations=256,
-                   cn_length_factor=None):
+                   cn_length_factor=None, embedding=None):
         sc = self.scene
         cfg = capi.hot_solver_config(
             sc.epsilon if epsilon is None else epsilon, sc.tau if tau is None else tau,
             sc.levels if levels is None else levels, sc.window if window is None else window, ls_shrink, ls_armijo,
             ls_max_steps, cg_cap, outer_cap, capi.SOLVER_KINDS[sc.solver if kind is None else kind],
-            1 if sc.embedding == "linear" else 0, pinned_coarse_iterations,
+            1 if (sc.embedding if embedding is None else embedding) == "linear" else 0, pinned_coarse_iterations,
             sc.cn_length_factor if cn_length_factor is None else cn_length_factor)
         self._check(self._lib.hot_set_solver(self._h, C.byref(cfg)))
 

@@ -117,12 +117,13 @@ def test_non_finite_dv_rejected():
 
 def _sym_err(m):
     b, c = m["blocks"], m["cols"]
+    ns = c.shape[1]  # 125 (radius 2) or 343 (radius 3): slot s and ns-1-s are mirror offsets
     err = 0.0
     for r in range(b.shape[0]):
-        for s in range(125):
+        for s in range(ns):
             j = c[r, s]
             if j >= 0:
-                err = max(err, np.abs(b[r, s] - b[j, 124 - s].T).max())
+                err = max(err, np.abs(b[r, s] - b[j, ns - 1 - s].T).max())
     return err
 
 
@@ -164,6 +165,48 @@ def test_hierarchy_and_vcycle():
         uo, ito = pr.orc.vcycle(b)
         assert it == ito
         assert rel_err(u, uo) < 1e-9
+
+
+def test_quadratic_embedding_hierarchy_and_vcycle():
+    """Quadratic node embedding (multigrid.hpp:72-90, 274-275): coarse levels of radius 3
+    (343 slots) with colour modulus 3; coarse indexing and column ids bit-exact, Galerkin
+    blocks, exact symmetry, and V-cycles against the oracle."""
+    from oracle.oracle import QUADRATIC
+
+    pr = _stretched_block_pair(seed=16, cells=6, youngs=1e6)
+    n = pr.prepare(0.01)
+    pr.gpu.assemble()
+    pr.orc.assemble()
+    assert pr.gpu.build_hierarchy(3, embedding="quadratic") == pr.orc.build_hierarchy(3, QUADRATIC)
+    for lvl in range(pr.orc.level_count()):
+        m = pr.gpu.level_matrix(lvl)
+        info = pr.orc.level_info(lvl)
+        ob, oc = pr.orc.level_matrix(lvl)
+        assert m["cols"].shape == oc.shape  # 125 slots on level 0, 343 on the coarse levels
+        assert np.array_equal(m["coords"], info["coords"])
+        assert np.array_equal(m["dirichlet"], info["dirichlet"])
+        assert np.array_equal(m["cols"], oc)
+        assert rel_err(m["blocks"], ob) < STAGE_TOL
+        assert _sym_err(m) == 0.0
+    rng = np.random.default_rng(17)
+    for _ in range(2):
+        b = rng.uniform(-1, 1, 3 * n)
+        u, it = pr.gpu.vcycle(b)
+        uo, ito = pr.orc.vcycle(b)
+        assert it == ito
+        assert rel_err(u, uo) < 1e-9
+
+
+def test_quadratic_embedding_step_grid():
+    """HOT step_grid with the quadratic embedding (the paper's embedding ablation)."""
+    pr = _stretched_block_pair(seed=18, cells=6)
+    pr.prepare(1.0 / 24)
+    pr.set_solver(kind="hot", epsilon=1e-7, embedding="quadratic")
+    r = pr.gpu.step_grid()
+    ro = pr.orc.step_grid()
+    assert r["converged"] and ro["converged"]
+    assert abs(r["outer_iterations"] - ro["outer_iterations"]) <= 1
+    assert rel_err(r["velocity"], ro["velocity"]) < STATE_TOL
 
 
 @pytest.mark.parametrize("coarse", ["flow", "barrier"])
