@@ -35,7 +35,7 @@ enum hot_status {
   HOT_E_LOGIC = 3,            /* std::logic_error */
   HOT_E_DOMAIN = 4,           /* std::domain_error */
   HOT_E_CUDA = 5,             /* CUDA runtime / device failure */
-  HOT_E_UNSUPPORTED = 6       /* feature not built for the device path (2D, quadratic embedding) */
+  HOT_E_UNSUPPORTED = 6       /* feature not built for the device path (2D) */
 };
 
 typedef struct hot_ctx hot_ctx;
