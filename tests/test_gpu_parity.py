@@ -315,6 +315,12 @@ def test_cfg1_cube_steps():
     _run_steps("cfg1_cube", 5)
 
 
+def test_cfg1_cube_full_20_steps():
+    """BASELINE config 1 as specified: the elastic cube, 20 steps, parity after every step
+    (x, v, F to 1e-6 relative, node counts equal, outer iterations within 1)."""
+    _run_steps("cfg1_cube", 20)
+
+
 def test_cfg1_stretched_steps():
     _run_steps("cfg1_stretched", 3)
 
