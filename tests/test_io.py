@@ -78,3 +78,38 @@ def test_text_formatting_matches_cpp_ostream(tmp_path):
                            [0.0, -0.0, 1.0, 0.1, 1e-5, 123456789.0, 1e22, 5e-324, np.inf, -np.inf]])
     out = subprocess.run([str(exe)], input=vals.astype("<f8").tobytes(), capture_output=True, check=True).stdout
     assert out.decode().splitlines() == [io._g17(v) for v in vals]
+
+
+def test_kernel_sweep_particle_sets():
+    """tools/kernel_sweep.py (BASELINE config 5): 8 ppc in the ball, random F with singular
+    values in [0.5, 2]."""
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "kernel_sweep.py")
+    spec = importlib.util.spec_from_file_location("kernel_sweep", path)
+    ks = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ks)
+    p = ks.particles_for(16)
+    n = p["x"].shape[0]
+    assert n % 8 == 0 and n > 0
+    assert np.all(np.linalg.norm(p["x"] - 0.5, axis=1) < 0.45 + 2.0 / 16)
+    s = np.linalg.svd(p["F"], compute_uv=False)
+    assert s.min() >= 0.5 - 1e-12 and s.max() <= 2.0 + 1e-12
+    R = ks.rotations(np.random.default_rng(0), 50)
+    assert np.allclose(np.einsum("nij,nkj->nik", R, R), np.eye(3)) and np.allclose(np.linalg.det(R), 1.0)
+
+
+def test_bench_cpu_slab_keeps_the_left_end():
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py")
+    spec = importlib.util.spec_from_file_location("bench_mod", path)
+    bm = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bm)
+    rng = np.random.default_rng(1)
+    parts = dict(x=rng.uniform(0, 1, (100, 3)), v=np.zeros((100, 3)), mass=np.ones(100))
+    s = bm.cpu_slab(parts, 10)
+    assert s["x"].shape[0] == 10
+    assert s["x"][:, 0].max() <= np.sort(parts["x"][:, 0])[9] + 1e-15
