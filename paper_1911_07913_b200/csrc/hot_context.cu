@@ -191,7 +191,7 @@ struct Context {
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DBuf scan_tmp2, struct_flags;
-  DBuf grid_bar;  // 2 words: the persistent smoothers' grid barrier (per context, per device)
+  DBuf grid_bar;  // words 0-1: the persistent smoothers' grid barrier; word 8: the assembly's row counter
   DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
@@ -677,7 +677,7 @@ struct Context {
     particle_tensors(dvp, project, reuse_svd);
     const int h = prof_begin(P_ASSEMBLE);
     launch_fill_cols(l0.view(), stream);
-    launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), stream);
+    launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), grid_bar.as<unsigned int>() + 8, stream);
     // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
     prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
     have_H = true;

@@ -146,7 +146,7 @@ void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, doub
                              cudaStream_t s);
 void launch_fill_cols(LevelView L, cudaStream_t s);
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
-                          const double* Tu, cudaStream_t s);
+                          const double* Tu, unsigned int* row_counter, cudaStream_t s);
 
 // ---------------------------------------------------------------- multigrid (k_multigrid.cu)
 /// quad: quadratic node embedding (multigrid.hpp:72-90).

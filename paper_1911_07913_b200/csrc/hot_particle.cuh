@@ -7,6 +7,29 @@
 
 namespace hotb200 {
 
+/// A particle's tensor record (k_particle_tensors; 1008 B = 63 x 16 B): W_k[g] = (F^nT grad w_k)[g]
+/// at kRecW + 3k + g for the 27 stencil positions, then kappa*T (45 packed entries) at
+/// kRecT + tslot(r, c).  W comes first so that the suffix a row gather needs (positions k >= kmin,
+/// and T) is one contiguous range.
+constexpr int kRecW = 0;
+constexpr int kRecT = 81;
+constexpr int kRecStride = 126;
+
+/// Slot of kappa*T[r][c] (symmetric 9x9) in the record's T part (k_particle_tensors,
+/// read by k_assemble_rows and the matrix-free PN kernels): the packed upper-triangle index,
+/// permuted so that the assembly's B-fragment loads (for each f, the lanes' T[3c+f][3e+g] and
+/// T[6+f][6+g]) fall on distinct shared-memory bank pairs within each half-warp.  The
+/// permutation came from a small backtracking search; any bijection of 0..44 is correct.
+__host__ __device__ constexpr int tperm(int q) {
+  constexpr int perm[45] = {44, 2, 26, 23, 25, 3, 24, 22, 29, 31, 6, 36, 42, 37, 12, 16, 43, 18, 33, 39, 20, 9, 30, 15, 35, 34, 10, 0, 7, 38, 17, 40, 4, 27, 19, 28, 1, 21, 41, 5, 14, 32, 8, 13, 11};
+  return perm[q];
+}
+__host__ __device__ constexpr int tpack_index(int r, int c) {
+  return r > c ? c * 9 - c * (c - 1) / 2 + (r - c) : r * 9 - r * (r - 1) / 2 + (c - r);
+}
+__host__ __device__ constexpr int tslot(int r, int c) { return tperm(tpack_index(r, c)); }
+static_assert(tslot(0, 0) != tslot(8, 8) && tslot(3, 5) == tslot(5, 3), "record slot table");
+
 /// Virtual deformation gradient (objective.hpp:218-230) from precomputed nodal velocities
 /// u = vel + (dv + alpha p) (launch_node_u).  The particle's stencil nodes come from its bin's
 /// 27-neighbour table (P.bin, g.nb27): no lattice lookups per particle.

@@ -1,18 +1,21 @@
 // Level-0 system matrix H = M + dt^2 d2Phi/dx2 on B200 (objective.hpp:318-363).
 //
 // Stage 1 (one thread per particle): virtual F -> SVD -> dP/dF projected in the diagonal
-//   space -> kappa * T stored as the 45-entry upper triangle (SoA, coalesced).
-// Stage 2 (one warp per row): gather over the 27 neighbouring particle bins.  Lane l owns
-//   stencil position kb = l of the current particle and accumulates the 3x3 pair block into
-//   the row's upper-triangle slot in shared memory (distinct slots per particle, so no
-//   atomics).  Each unordered block pair is computed once by the row with the smaller
-//   index and written together with its transpose, so block (i,j) == block(j,i)^T exactly
-//   (the reference's symmetry_error() == 0 invariant).  The mass diagonal and the Dirichlet
-//   projection (objective.hpp:133-144) are fused into the write-out.
+//   space -> one 1008-byte record per particle: the 27 W_k = F^nT grad w_k, then kappa*T as
+//   its 45 unique entries (hot_particle.cuh: kRecW, kRecT, tslot).
+// Stage 2 (one warp per row, rows from a work counter): gather over the 27 neighbouring
+//   particle bins, records staged by the bulk-copy engine, the per-particle rank-3 block
+//   updates on the fp64 tensor cores (DMMA), accumulated into the row's upper-triangle slots
+//   in shared memory (fixed order, no atomics).  Each unordered block pair is computed once by
+//   the row with the smaller index and written together with its transpose, so block (i,j) ==
+//   block(j,i)^T exactly (the reference's symmetry_error() == 0 invariant).  The mass diagonal
+//   and the Dirichlet projection (objective.hpp:133-144) are fused into the write-out.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
+#include <type_traits>
 
 #include "hot_async.cuh"
 #include "hot_internal.h"
@@ -25,10 +28,10 @@ namespace {
 constexpr int kAsmWarps = 4;
 constexpr int kUpper = 63;  // slots 62..124
 
-/// Per particle (bin order): kappa*T as its 45-entry upper triangle (row-major, T is symmetric),
-/// then W (27 x 3): W_k = F^nT grad w_k (0 where w_k = 0).  1008 B = 63 x 16 B.
+/// Per particle (bin order) one record of kRecStride doubles (1008 B = 63 x 16 B): W (27 x 3),
+/// W_k = F^nT grad w_k (0 where w_k = 0), then kappa*T's 45 unique entries (T is symmetric).
 constexpr int kTPacked = 45;
-constexpr int kTensorStride = kTPacked + 81;
+constexpr int kTensorStride = kRecStride;
 
 __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
                                    const DevMaterial* __restrict__ mats, const double* __restrict__ u,
@@ -59,7 +62,7 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
     fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
     double* out = Tu + p * kTensorStride;
 #pragma unroll
-    for (int q = 0; q < kTPacked; ++q) out[q] = T[q];
+    for (int q = 0; q < kTPacked; ++q) out[kRecT + tperm(q)] = T[q];  // record slot kRecT + tslot(r, c)
     // W_k = F^nT grad w_k for the 27 stencil nodes (grid.hpp:58-73, objective.hpp:337-339); nodes
     // with zero weight get W = 0, which is how the reference skips them (transfer.hpp:36-37)
     Axis3 ax[3];
@@ -83,7 +86,7 @@ __global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, doubl
           for (int q = 0; q < 3; ++q) W[q] = Fn.m[q] * g0 + Fn.m[3 + q] * g1 + Fn.m[6 + q] * g2;
         }
 #pragma unroll
-        for (int q = 0; q < 3; ++q) out[kTPacked + 3 * k + q] = W[q];
+        for (int q = 0; q < 3; ++q) out[kRecW + 3 * k + q] = W[q];
       }
     }
   }
@@ -102,24 +105,25 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
   }
 }
 
-/// Row gather (objective.hpp:331-357), one warp per row i.  For a particle p of a bin whose
-/// stencil holds i at position a, the warp forms M[c][e][g] = sum_f W_a[f] T[(3c+f),(3e+g)]
-/// (lane (c,e,g) < 27, 3 FMA) and a lane owning stencil position k contracts the upper-triangle
-/// block C[c][e] += sum_g M[c][e][g] W_k[g] (27 FMA).
+/// Row gather (objective.hpp:331-357), one warp per row i.  A particle p of a bin whose stencil
+/// holds i at position a contributes to the row's upper-triangle block at stencil position k
+///   C_k[c][e] += sum_g W_k[g] M[c][e][g],   M[c][e][g] = sum_f W_a[f] T[(3c+f),(3e+g)].
+/// Per particle that is a rank-3 update of the (upper positions) x (ce) block, which runs on the
+/// fp64 tensor cores (DMMA m8n8k4): M-dim = upper positions (tiles of 8), N-dim = ce 0..7, K = g
+/// (3, padded to 4 with a zero row of B).  The ninth column ce = 8 would waste a whole second
+/// N tile, so it goes to the FMA pipe instead: each lane accumulates A[k][g] * M[8][g] and the
+/// four g lanes are summed once per bin pair.  Every lane computes its own B-fragment entry
+/// M[ce][g] (3 FMA from the staged T and W_a), so M never goes through shared memory.
 ///
-/// Lane utilisation: in one bin only about half of the 27 stencil positions are upper-triangle
-/// slots of row i.  Bin offset o and its mirror 2-o are complementary: position k is lower in
-/// bin o exactly when position 26-k is upper in bin 2-o (slot s -> 124-s).  So the warp walks
-/// the 13 mirror pairs (+ the centre bin): lane k works on bin o if its slot is upper, else on
-/// the mirror bin at 26-k; lane 27 takes the mirror bin's diagonal block (both bins own one).
-/// Both bins' particles are staged together by the bulk-copy engine (one cp.async.bulk per bin
-/// chunk, mbarrier completion, double buffered one chunk ahead).  Each (pair, lane) block
-/// accumulates in registers and is folded into the row's shared accumulator once per pair
-/// (bin o's lanes, then the mirror's: fixed order, no atomics).
+/// Bin offset o and its mirror 26-o are walked together (their upper position counts add up to
+/// 28), both bins' particles staged by the bulk-copy engine (one cp.async.bulk per bin chunk,
+/// mbarrier completion, double buffered one chunk ahead).  The tile counts of a pair are
+/// template constants, so the per-particle loop has no tile branches.  Each (pair, lane) block
+/// accumulates in registers and is folded into the row's shared accumulator once per pair (bin
+/// o's lanes, then the mirror's: fixed order, no atomics).
 constexpr int kAsmChunk = 2;                                  // particles per bin per stage
 constexpr int kAsmStage = 2 * kAsmChunk * kTensorStride;       // doubles: [bin of pair][particle][...]
-constexpr int kAsmM = 36;  // M[ce*4 + g] of one bin, g = 3 padded with zero (the DMMA K = 4)
-constexpr int kAsmWarpDoubles = 2 * kAsmStage + 2 * 2 * kAsmM + kUpper * 9 + 1 + 2 + 28;  // + pad + 2 mbarriers + pair table; even
+constexpr int kAsmWarpDoubles = 2 * kAsmStage + kUpper * 9 + 1 + 2 + 28;  // + pad + 2 mbarriers + pair table; even
 constexpr int kAsmSmem = kAsmWarps * kAsmWarpDoubles * 8;
 constexpr unsigned kParticleBytes = kTensorStride * 8;  // 1008 = 63 x 16
 static_assert(kAsmWarpDoubles % 2 == 0, "16-byte aligned per-warp smem");
@@ -159,44 +163,106 @@ __device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ int tpack(int r, int c) {  // index of T[r][c] in the packed upper triangle
-  if (r > c) {
-    const int t = r;
-    r = c;
-    c = t;
+/// One bin of a pair, one particle: B-fragment entries from the staged T and W_a, then the
+/// DMMA tiles (ce 0..7) and the FMA column (ce 8).  Lanes g < 3 form M[ce = qm][g]; the g = 3
+/// pad lanes qm < 3 form M[8][qm] in the same loads, and a shuffle hands M[8][g] to the lanes of
+/// column g.  `valid` = the slot holds a particle of this bin (stale slots hold finite data of an
+/// earlier particle and get B = 0).
+template <int NT>
+__device__ __forceinline__ void asm_particle(const double* __restrict__ P, int wa, const int (&tb)[3], int src8,
+                                             bool valid, const int (&oA)[4], double (&C)[4][2], double (&E)[4]) {
+  const double w0 = P[wa], w1 = P[wa + 1], w2 = P[wa + 2];
+  const double raw = w0 * P[tb[0]] + w1 * P[tb[1]] + w2 * P[tb[2]];
+  const double m8raw = __shfl_sync(0xffffffffu, raw, src8);
+  const double b = valid ? raw : 0.0;
+  const double m8 = valid ? m8raw : 0.0;
+#pragma unroll
+  for (int mt = 0; mt < NT; ++mt) {
+    const double a = P[oA[mt]];
+    dmma_f64(C[mt], a, b);
+    E[mt] = fma(a, m8, E[mt]);
   }
-  return r * 9 - r * (r - 1) / 2 + (c - r);
+}
+
+/// Fold one bin's register blocks into the row accumulator (upper slots su = S(k) + S(o) - 62).
+template <int NT>
+__device__ __forceinline__ void asm_fold(double* acc, int kmin, int So, int qm, int qk, double (&C)[4][2],
+                                         double (&E)[4]) {
+#pragma unroll
+  for (int mt = 0; mt < NT; ++mt) {
+    double e = E[mt];
+    e += __shfl_xor_sync(0xffffffffu, e, 1);
+    e += __shfl_xor_sync(0xffffffffu, e, 2);
+    const int k = kmin + 8 * mt + qm;
+    if (k <= 26) {
+      const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 + So - kDiagSlot;
+      acc[su * 9 + 2 * qk] += C[mt][0];
+      acc[su * 9 + 2 * qk + 1] += C[mt][1];
+      if (qk == 0) acc[su * 9 + 8] += e;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
-                                                                   const double* __restrict__ Tu) {
+                                                                   const double* __restrict__ Tu,
+                                                                   unsigned int* __restrict__ row_counter) {
   extern __shared__ __align__(16) double asm_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // per warp: staging [2 buffers][kAsmStage] | M [2 parity][2 bins][28] | acc [kUpper*9] | mbarriers [2]
+  // per warp: staging [2 buffers][kAsmStage] | acc [kUpper*9] | pad | mbarriers [2] | pair table
   double* base = asm_smem + (size_t)wid * kAsmWarpDoubles;
   double* Sbuf = base;
-  double* Mbuf = base + 2 * kAsmStage;
-  double* acc = Mbuf + 2 * 2 * kAsmM;
+  double* acc = base + 2 * kAsmStage;
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(acc + kUpper * 9 + 1);
   int* PT = reinterpret_cast<int*>(acc + kUpper * 9 + 1 + 2);  // [14][pb1, n1, pb2, n2]
+  for (int q = lane; q < 2 * kAsmStage; q += 32) Sbuf[q] = 0.0;  // stale slots must hold finite data
+  __syncwarp();
   if (lane == 0) {
     mbar_init(mbar, 1);
     mbar_init(mbar + 1, 1);
     mbar_fence_init();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before the bulk copies
   }
   __syncwarp();
   unsigned phase = 0;  // bit b: parity of the next completion of buffer b
-  for (int q = lane; q < 2 * 2 * kAsmM; q += 32) Mbuf[q] = 0.0;  // the g = 3 pads stay zero
-  __syncwarp();
-  // lane's M entry (c,e,g) = lane: packed T indices of T[(3c+f),(3e+g)], f = 0..2
-  const int lc = lane / 9, le = (lane / 3) % 3, lg = lane % 3;
-  const int tp0 = lane < 27 ? tpack(3 * lc, 3 * le + lg) : 0;
-  const int tp1 = lane < 27 ? tpack(3 * lc + 1, 3 * le + lg) : 0;
-  const int tp2 = lane < 27 ? tpack(3 * lc + 2, 3 * le + lg) : 0;
-  const int mi = (3 * lc + le) * 4 + lg;  // lane's M entry in M[ce*4 + g]
+  const int qk = lane & 3, qm = lane >> 2;
+  // lane's load f: M[ce = qm][g = qk] needs T[(3c+f),(3e+g)]; the g = 3 pad lanes qm < 3 load
+  // T[(6+f),(6+qm)] (the ce = 8 column), the other pad lanes repeat a neighbour's address
+  int tb[3];
+  {
+    const int c = qm / 3, e = qm % 3;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      if (qk < 3) tb[f] = kRecT + tslot(3 * c + f, 3 * e + qk);
+      else if (qm < 4) tb[f] = kRecT + tslot(6 + f, 6 + min(qm, 2));
+      else tb[f] = kRecT + tslot(3 * c + f, 3 * e + 2);
+    }
+  }
+  const bool lane_g = qk < 3;
+  const int src8 = 4 * min(qk, 2) + 3;  // the pad lane holding M[8][g]
   const int nwarps = gridDim.x * kAsmWarps;
-  for (int i = blockIdx.x * kAsmWarps + wid; i < L.n; i += nwarps) {
+  // rows are handed out in index order (a work counter, or a static stride without one), so the
+  // rows in flight stay a narrow band and their particle bins stay in L2
+  auto next_row = [&](int cur) {
+    if (!row_counter) return cur < 0 ? (int)(blockIdx.x * kAsmWarps + wid) : cur + nwarps;
+    int r = 0;
+    if (lane == 0) r = (int)atomicAdd(row_counter, 1u);
+    return __shfl_sync(0xffffffffu, r, 0);
+  };
+  for (int i = next_row(-1); i < L.n; i = next_row(i)) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
+    // the write-out's column ids and Dirichlet flags, loaded now so their latency hides under
+    // the gather: slot s = lane + 32 j (zero fill), upper slot 62 + lane + 32 j
+    const int* crow = L.cols + (long long)i * kSlotPitch;
+    int zc[kSlotPitch / 32], uc[2];
+    bool ud[2];
+#pragma unroll
+    for (int j = 0; j < kSlotPitch / 32; ++j) zc[j] = lane + 32 * j < kSlots ? __ldg(crow + lane + 32 * j) : -1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) uc[j] = lane + 32 * j < kUpper ? __ldg(crow + kDiagSlot + lane + 32 * j) : -1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) ud[j] = uc[j] >= 0 && g.dir[uc[j]] != 0;
+    const bool di = g.dir[i] != 0;
+    const double mi = g.mass[i];
     const int ci0 = L.coords[3 * i], ci1 = L.coords[3 * i + 1], ci2 = L.coords[3 * i + 2];
     // lane o < 27 resolves bin offset o (bin node = i + o - 1): first particle and count
     int my_pb = 0, my_np = 0;
@@ -228,16 +294,15 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
         c0_n = 0;
       }
     };
-    auto issue = [&](int buf) {  // lane 0
+    auto issue = [&](int buf) {  // lane 0: one bulk copy per bin and chunk
       const int pb1 = PT[4 * pq_n], n1 = PT[4 * pq_n + 1], pb2 = PT[4 * pq_n + 2], n2 = PT[4 * pq_n + 3];
       const int k1 = max(0, min(kAsmChunk, n1 - c0_n)), k2 = max(0, min(kAsmChunk, n2 - c0_n));
       const unsigned mb = smem_u32(mbar + buf);
       double* dst = Sbuf + buf * kAsmStage;
       mbar_expect_tx(mb, (k1 + k2) * kParticleBytes);
-      if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0_n) * kTensorStride, k1 * kParticleBytes, mb);
+      if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0_n) * kRecStride, k1 * kParticleBytes, mb);
       if (k2)
-        bulk_g2s(dst + kAsmChunk * kTensorStride, Tu + (long long)(pb2 + c0_n) * kTensorStride, k2 * kParticleBytes,
-                 mb);
+        bulk_g2s(dst + kAsmChunk * kRecStride, Tu + (long long)(pb2 + c0_n) * kRecStride, k2 * kParticleBytes, mb);
     };
     if (lane == 0) {
       pq_n = 0;
@@ -246,123 +311,79 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
       if (pq_n < 14) issue(0);
       advance();
     }
-    int buf = 0, mpar = 0;
-    const int qk = lane & 3, qm = lane >> 2;
+    int buf = 0;
     for (int pq = 0; pq < 14; ++pq) {
       const int n1 = PT[4 * pq + 1], n2 = PT[4 * pq + 3];
       const int nmax = max(n1, n2);
       if (nmax == 0) continue;
       // bin b's upper stencil positions: the suffix k >= kmin_b (slot S(k) + S(o_b) >= 62,
-      // S(v) = 25 v0 + 5 v1 + v2); o_0 = pq, o_1 = 26 - pq (S(o_1) = 62 - S(o_0))
+      // S(v) = 25 v0 + 5 v1 + v2); o_0 = pq, o_1 = 26 - pq (S(o_1) = 62 - S(o_0)); the row sits
+      // at stencil position 26 - o_b of the bin's particles
       const int So0 = c_S27[pq], So1 = 62 - So0;
       const int kmin0 = c_kmin27[pq], kmin1 = pq == 13 ? 27 : c_kmin27[26 - pq];  // the centre bin has no mirror
-      // C_b[k - kmin_b][ce] += sum_g W_t[k][g] M_b[ce][g]: per particle a rank-3 update on the
-      // fp64 tensor cores (DMMA m8n8k4): M = upper positions (<= 4 tiles), N = ce (2), K = g (3 -> 4)
-      double C0[4][2][2], C1[4][2][2];
+      const int wa0 = kRecW + 3 * (26 - pq), wa1 = kRecW + 3 * pq;
+      auto run = [&](auto nt0c, auto nt1c) {
+        constexpr int NT0 = decltype(nt0c)::value, NT1 = decltype(nt1c)::value;
+        double C0[4][2], C1[4][2], E0[4], E1[4];
+        int oA0[4], oA1[4];  // A fragment W_k[g]: k clamped to 26 (rows past 26 are never folded)
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) C0[mt][nt][0] = C0[mt][nt][1] = C1[mt][nt][0] = C1[mt][nt][1] = 0.0;
-      for (int c0 = 0; c0 < nmax; c0 += kAsmChunk) {
-        if (lane == 0) {
-          if (pq_n < 14) issue(buf ^ 1);
-          advance();
+        for (int mt = 0; mt < 4; ++mt) {
+          C0[mt][0] = C0[mt][1] = C1[mt][0] = C1[mt][1] = E0[mt] = E1[mt] = 0.0;
+          oA0[mt] = kRecW + 3 * min(kmin0 + 8 * mt + qm, 26) + min(qk, 2);
+          oA1[mt] = kRecW + 3 * min(kmin1 + 8 * mt + qm, 26) + min(qk, 2);
         }
-        mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
-        phase ^= 1u << buf;
-        const double* S = Sbuf + buf * kAsmStage;
-        const int tcount = min(kAsmChunk, nmax - c0);
-        for (int t = 0; t < tcount; ++t) {
-          const bool v1 = c0 + t < n1, v2 = c0 + t < n2;
-          const double* P1 = S + t * kTensorStride;
-          const double* P2 = S + (kAsmChunk + t) * kTensorStride;
-          double* M = Mbuf + mpar * 2 * kAsmM;
-          if (lane < 27) {  // lane (c,e,g): M_b[ce][g] = sum_f W_a[f] T[(3c+f),(3e+g)]
-            if (v1) {
-              const double* Wa = P1 + kTPacked + 3 * (26 - pq);
-              M[mi] = Wa[0] * P1[tp0] + Wa[1] * P1[tp1] + Wa[2] * P1[tp2];
-            }
-            if (v2) {
-              const double* Wa = P2 + kTPacked + 3 * pq;
-              M[kAsmM + mi] = Wa[0] * P2[tp0] + Wa[1] * P2[tp1] + Wa[2] * P2[tp2];
-            }
+        for (int c0 = 0; c0 < nmax; c0 += kAsmChunk) {
+          if (lane == 0) {
+            if (pq_n < 14) issue(buf ^ 1);
+            advance();
           }
-          __syncwarp();
-          if (v1) {
-            const double bf0 = M[qm * 4 + qk], bf1 = qm == 0 ? M[32 + qk] : 0.0;
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-              const int kk = kmin0 + 8 * mt + qm;
-              if (kmin0 + 8 * mt > 26) break;
-              const double af = (kk <= 26 && qk < 3) ? P1[kTPacked + 3 * kk + qk] : 0.0;
-              dmma_f64(C0[mt][0], af, bf0);
-              dmma_f64(C0[mt][1], af, bf1);
-            }
+          mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
+          phase ^= 1u << buf;
+          const double* S = Sbuf + buf * kAsmStage;
+#pragma unroll 1
+          for (int t = 0; t < kAsmChunk; ++t) {
+            asm_particle<NT0>(S + t * kTensorStride, wa0, tb, src8, lane_g && c0 + t < n1, oA0, C0, E0);
+            if (NT1 > 0)
+              asm_particle<NT1>(S + (kAsmChunk + t) * kTensorStride, wa1, tb, src8, lane_g && c0 + t < n2, oA1,
+                                C1, E1);
           }
-          if (v2 && kmin1 <= 26) {
-            const double bf0 = M[kAsmM + qm * 4 + qk], bf1 = qm == 0 ? M[kAsmM + 32 + qk] : 0.0;
-#pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-              const int kk = kmin1 + 8 * mt + qm;
-              if (kmin1 + 8 * mt > 26) break;
-              const double af = (kk <= 26 && qk < 3) ? P2[kTPacked + 3 * kk + qk] : 0.0;
-              dmma_f64(C1[mt][0], af, bf0);
-              dmma_f64(C1[mt][1], af, bf1);
-            }
-          }
-          mpar ^= 1;  // M is double buffered: the next particle's M may be written before stragglers read
+          __syncwarp();  // buffer buf is refilled by the next iteration's issue
+          buf ^= 1;
         }
-        __syncwarp();  // buffer buf is refilled by the next iteration's issue
-        buf ^= 1;
-      }
-      // fold the pair's accumulators into the row: bin 0, then the mirror bin
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int k = kmin0 + 8 * mt + qm;
-        if (k <= 26) {
-          const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 + So0 - kDiagSlot;
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              const int n = 8 * nt + 2 * qk + v;
-              if (n < 9) acc[su * 9 + n] += C0[mt][nt][v];
-            }
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int k = kmin1 + 8 * mt + qm;
-        if (k <= 26) {
-          const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 + So1 - kDiagSlot;
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              const int n = 8 * nt + 2 * qk + v;
-              if (n < 9) acc[su * 9 + n] += C1[mt][nt][v];
-            }
-        }
-      }
-      __syncwarp();
+        // fold the pair's accumulators into the row: bin 0, then the mirror bin
+        asm_fold<NT0>(acc, kmin0, So0, qm, qk, C0, E0);
+        __syncwarp();
+        if (NT1 > 0) asm_fold<NT1>(acc, kmin1, So1, qm, qk, C1, E1);
+        __syncwarp();
+      };
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I3 = std::integral_constant<int, 3>;
+      using I4 = std::integral_constant<int, 4>;
+      // tile counts ceil((27 - kmin) / 8) per bin: (1,4) pq 0-2, (1,3) 3-7, (2,3) 8-10, (2,2) 11-12, (2,0) 13
+      if (pq < 3) run(I1{}, I4{});
+      else if (pq < 8) run(I1{}, I3{});
+      else if (pq < 11) run(I2{}, I3{});
+      else if (pq < 13) run(I2{}, I2{});
+      else run(I2{}, I0{});
     }
     // write-out: upper slots + transposed mirror, mass diagonal, Dirichlet projection
-    const bool di = g.dir[i] != 0;
-    const double mi = g.mass[i];
-    for (int s = lane; s < kSlotPitch; s += 32) {  // inactive / pad slots hold zeros
-      if (s >= kSlots || L.cols[(long long)i * kSlotPitch + s] < 0)
 #pragma unroll
-        for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + s, 0.0);
+    for (int j = 0; j < kSlotPitch / 32; ++j) {  // inactive / pad slots hold zeros
+      if (zc[j] < 0)
+#pragma unroll
+        for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + lane + 32 * j, 0.0);
     }
-    for (int u = lane; u < kUpper; u += 32) {
-      const int s = kDiagSlot + u;
-      const int col = L.cols[(long long)i * kSlotPitch + s];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int u = lane + 32 * j, s = kDiagSlot + u;
+      const int col = uc[j];
       if (col < 0) continue;
       double C[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) C[k] = acc[u * 9 + k];
-      const bool zero = di || g.dir[col] != 0;
+      const bool zero = di || ud[j];
       if (s == kDiagSlot) {
         if (di) {
 #pragma unroll
@@ -416,17 +437,25 @@ void launch_fill_cols(LevelView L, cudaStream_t s) {
 }
 
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
-                          const double* Tu, cudaStream_t s) {
+                          const double* Tu, unsigned int* row_counter, cudaStream_t s) {
   if (L.n == 0) return;
   (void)dx;
-  // oversubscribed grid (16 CTAs per SM): measured lower DRAM traffic than a resident-sized one
-  static const bool attr = [] {
-    cudaFuncSetAttribute((const void*)k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, kAsmSmem);
-    return true;
+  static const int resident = resident_blocks((const void*)k_assemble_rows, kAsmWarps * 32, kAsmSmem);
+  static const bool dynamic = [] {
+    const char* e = std::getenv("HOT_ASM_ROWS");
+    return !(e && std::string(e) == "static");
   }();
-  (void)attr;
-  const long long blocks = std::min<long long>((long long)num_sms() * 16, (L.n + kAsmWarps - 1) / kAsmWarps);
-  { k_assemble_rows<<<(int)blocks, kAsmWarps * 32, kAsmSmem, s>>>(bins, g, L, Tu); count_launches(1); }
+  long long blocks;
+  if (dynamic) {  // resident grid, rows from the work counter
+    cudaMemsetAsync(row_counter, 0, sizeof(unsigned int), s);
+    blocks = resident;
+  } else {  // oversubscribed grid (16 CTAs per SM), static row stride
+    row_counter = nullptr;
+    blocks = (long long)num_sms() * 16;
+  }
+  blocks = std::min<long long>(blocks, (L.n + kAsmWarps - 1) / kAsmWarps);
+  k_assemble_rows<<<(int)blocks, kAsmWarps * 32, kAsmSmem, s>>>(bins, g, L, Tu, row_counter);
+  count_launches(1);
 }
 
 }  // namespace hotb200

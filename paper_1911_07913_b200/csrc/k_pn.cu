@@ -14,17 +14,7 @@ namespace hotb200 {
 
 namespace {
 
-constexpr int kTP = 45;        // packed kappa*T entries per particle (k_assembly.cu)
-constexpr int kTS = kTP + 81;  // per-particle tensor stride
-
-__device__ __forceinline__ int tpk(int r, int c) {  // packed upper-triangle index of a symmetric 9x9
-  if (r > c) {
-    const int t = r;
-    r = c;
-    c = t;
-  }
-  return r * 9 - r * (r - 1) / 2 + (c - r);
-}
+constexpr int kTS = kRecStride;  // per-particle tensor record (hot_particle.cuh)
 
 int pgrid(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
@@ -76,7 +66,7 @@ __global__ void __launch_bounds__(128) k_mf_particle(ParticlesView P, GridView g
       const int node = __ldg(nb + k);
       if (node < 0) continue;  // outside the active set: zero weight (W_k = 0)
       if (g.dir[node]) continue;
-      const double w0 = T[kTP + 3 * k], w1 = T[kTP + 3 * k + 1], w2 = T[kTP + 3 * k + 2];
+      const double w0 = T[kRecW + 3 * k], w1 = T[kRecW + 3 * k + 1], w2 = T[kRecW + 3 * k + 2];
       const double u0 = __ldg(u + 3 * node), u1 = __ldg(u + 3 * node + 1), u2 = __ldg(u + 3 * node + 2);
       dF[0] += u0 * w0;
       dF[1] += u0 * w1;
@@ -92,7 +82,7 @@ __global__ void __launch_bounds__(128) k_mf_particle(ParticlesView P, GridView g
     for (int r = 0; r < 9; ++r) {
       double s = 0.0;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) s += T[tpk(r, c)] * dF[c];
+      for (int c = 0; c < 9; ++c) s += T[kRecT + tslot(r, c)] * dF[c];
       dP[r * n + p] = s;
     }
   }
@@ -109,7 +99,7 @@ __global__ void __launch_bounds__(256) k_mf_node(ParticlesView P, BinsView bins,
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < g.n; i += nw) {
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     warp_node_gather(g, bins, i, lane, [&](int p, int o) {
-      const double* W = Tu + (long long)p * kTS + kTP + 3 * (26 - o);
+      const double* W = Tu + (long long)p * kTS + kRecW + 3 * (26 - o);
       const double w0 = W[0], w1 = W[1], w2 = W[2];
       y0 += dP[p] * w0 + dP[n + p] * w1 + dP[2 * n + p] * w2;
       y1 += dP[3 * n + p] * w0 + dP[4 * n + p] * w1 + dP[5 * n + p] * w2;
@@ -145,7 +135,7 @@ __global__ void __launch_bounds__(256) k_mf_diag(ParticlesView P, BinsView bins,
     for (int q = 0; q < 9; ++q) D[q] = 0.0;
     warp_node_gather(g, bins, i, lane, [&](int p, int o) {
       const double* T = Tu + (long long)p * kTS;
-      const double* W = T + kTP + 3 * (26 - o);
+      const double* W = T + kRecW + 3 * (26 - o);
       const double w[3] = {W[0], W[1], W[2]};
       double C[9];
 #pragma unroll
@@ -156,7 +146,7 @@ __global__ void __launch_bounds__(256) k_mf_diag(ParticlesView P, BinsView bins,
 #pragma unroll
           for (int f = 0; f < 3; ++f)
 #pragma unroll
-            for (int gg = 0; gg < 3; ++gg) s += w[f] * T[tpk(3 * c + f, 3 * e + gg)] * w[gg];
+            for (int gg = 0; gg < 3; ++gg) s += w[f] * T[kRecT + tslot(3 * c + f, 3 * e + gg)] * w[gg];
           C[3 * c + e] = s;
         }
 #pragma unroll
