@@ -192,6 +192,7 @@ struct Context {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DBuf scan_tmp2, struct_flags;
   DBuf grid_bar;  // words 0-1: the persistent smoothers' grid barrier; word 8: the assembly's row counter
+  DBuf bin_part;  // per (bin, stencil position) particle sums feeding the node gathers (P2G, gradient)
   DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
   double* host_scal = nullptr;  // pinned
@@ -586,6 +587,7 @@ struct Context {
     pmat.swap(qmat);
     porig.swap(qorig);
     nb27.ensure(sizeof(int) * 27 * std::max(n, 1));
+    bin_part.ensure(sizeof(double) * 135 * std::max(n, 1));  // per (bin, stencil position): P2G 5, gradient 3
     launch_fill_nb27(gview(), nb27.as<int>(), stream);
     prof_end(h, (double)np * 24 * 3 + 5.0 * len);
     nlevels = 0;
@@ -594,7 +596,8 @@ struct Context {
 
   void p2g_bc(double time_now) {
     const int h = prof_begin(P_P2G);
-    launch_p2g(pview(), bview(), gview(), dx, mats_d.as<DevMaterial>(), cn_factor * dx * dx, dt, stream);
+    launch_p2g(pview(), bview(), gview(), dx, mats_d.as<DevMaterial>(), cn_factor * dx * dx, dt, bin_part.as<double>(),
+               stream);
     launch_apply_bc(gview(), dx, cols_d.as<DevCollider>(), (int)cols_h.size(), stream);
     (void)time_now;
     prof_end(h, (double)np * 136 + (double)L[0].n * 88);  // x v C m mat | mass mom vel cn dir bc
@@ -644,10 +647,10 @@ struct Context {
   void gradient_async(const double* dvp, double* gout) {
     const int h = prof_begin(P_GRADIENT);
     double* part = partials.as<double>() + 2 * nred;
-    launch_node_gradient(pview(), bview(), gview(), dx, dt, grav, stress.as<double>(), dvp, gout, part, nred,
-                         flag_bad(), stream);
+    launch_node_gradient(pview(), bview(), gview(), dx, dt, grav, stress.as<double>(), dvp, gout, bin_part.as<double>(),
+                         part, nred, flag_bad(), stream);
     launch_sum_partials(part, nred, scal.as<double>() + 2, stream);
-    prof_end(h, (double)L[0].n * (27 * 8 * 96.0 / 8) + 72.0 * np);
+    prof_end(h, 96.0 * np + 64.0 * L[0].n);  // x, V P F^T | dv, mass, g
   }
 
   void check_flags() {

@@ -83,7 +83,7 @@ void launch_flags_to_index(const uint8_t* flags, long long len, const int* ext, 
 void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n_nodes, int* bin_of, int* counts,
                           int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s);
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
-                double dt, cudaStream_t s);
+                double dt, double* bin_part, cudaStream_t s);
 /// Also writes dst.bin[t] = bin_of[pid[t]].
 void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* bin_of,
                               const int* orig_src,
@@ -117,8 +117,8 @@ void launch_node_energy(GridView g, double dt, const double* grav, const double*
 /// g_i = dt * sum_p (V P F^T) grad w + m_i (dv_i - dt*grav); 0 on Dirichlet; partial sums of
 /// |g_i|^2 / scale_i^2 into partials.
 void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
-                          const double* stress, const double* dv, double* gout, double* partials, int nblocks,
-                          int* bad_flag, cudaStream_t s);
+                          const double* stress, const double* dv, double* gout, double* bin_part, double* partials,
+                          int nblocks, int* bad_flag, cudaStream_t s);
 void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s);
 
 // vector helpers (deterministic block partials + fixed-order final sums)

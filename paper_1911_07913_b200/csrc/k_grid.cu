@@ -242,58 +242,117 @@ __global__ void k_bin_sort(const int* __restrict__ start, int n_nodes, int* pid)
   }
 }
 
-/// APIC P2G gather (transfer.hpp:46-64) fused with the node characteristic norm
-/// (objective.hpp:450-473).  One warp per node: lanes stride over the particles of the 27
-/// neighbouring bins (contiguous in bin order), partial sums reduced in a fixed tree.
-__global__ void __launch_bounds__(256) k_p2g(ParticlesView P, BinsView bins, GridView g, double dx,
-                                             const DevMaterial* __restrict__ mats, double ell, double dt) {
+/// P2G, particle half (transfer.hpp:46-64, objective.hpp:445-463): for bin j and stencil
+/// position k, the sums over the bin's particles (bin order) of w m, w m (v + C (x_i - x_p)) and
+/// w m xi, into B[j][k][0..4].  One warp per bin, lane k < 27, particle data broadcast.  Every
+/// (bin, k) pair feeds exactly one node.  Empty bins write zeros.
+constexpr int kBinWarps = 8;
+__global__ void __launch_bounds__(kBinWarps * 32) k_bin_p2g(ParticlesView P, BinsView bins, GridView g, double dx,
+                                                           const DevMaterial* __restrict__ mats,
+                                                           double* __restrict__ B) {
+  // per warp: the current chunk of <= 32 bin particles, [field][slot] (x 3, v 3, C 9, m, m xi),
+  // loaded coalesced (lanes over particles) and read back as broadcasts by the stencil lanes
+  __shared__ double stage[kBinWarps][17][32];
   const long long n = P.n;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < g.n; i += nw) {
-    const int ci0 = g.coords[3 * i], ci1 = g.coords[3 * i + 1], ci2 = g.coords[3 * i + 2];
+  double(*sm)[32] = stage[wib];
+  // 1D weights: lane 9u + 3a + k (< 27) evaluates axis a, node k of particle t + u, so one
+  // division serves three particles; the stencil lanes (lane = 9 k0 + 3 k1 + k2) take theirs by
+  // shuffle
+  const int wu = min(lane / 9, 2), la = (lane % 9) / 3, lk = lane % 3;
+  const int s0 = lane / 9, s1 = 3 + (lane / 3) % 3, s2 = 6 + lane % 3;
+  const int k0 = lane / 9 - 1, k1 = (lane / 3) % 3 - 1, k2 = lane % 3 - 1;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < g.n; j += nw) {
+    const int pb = __ldg(bins.start + j), pe = __ldg(bins.start + j + 1);
+    const int ci0 = g.coords[3 * j] + k0, ci1 = g.coords[3 * j + 1] + k1, ci2 = g.coords[3 * j + 2] + k2;
     const double xi0 = (double)ci0 * dx, xi1 = (double)ci1 * dx, xi2 = (double)ci2 * dx;
+    const double ca = (double)(g.coords[3 * j + la] + lk - 1);
     double m = 0.0, mom0 = 0.0, mom1 = 0.0, mom2 = 0.0, num = 0.0;
-    warp_node_gather(g, bins, i, lane, [&](int p) {
-      const double px0 = P.x[p], px1 = P.x[n + p], px2 = P.x[2 * n + p];
-      const double w = bspline_w(px0 / dx - (double)ci0) * bspline_w(px1 / dx - (double)ci1) *
-                       bspline_w(px2 / dx - (double)ci2);
-      if (w <= 0.0) return;
-      const double mp = P.mass[p];
-      const double wm = w * mp;
-      const double d0 = xi0 - px0, d1 = xi1 - px1, d2 = xi2 - px2;
-      const double* C = P.C;
-      const double a0 = P.v[p] + (C[p] * d0 + C[n + p] * d1 + C[2 * n + p] * d2);
-      const double a1 = P.v[n + p] + (C[3 * n + p] * d0 + C[4 * n + p] * d1 + C[5 * n + p] * d2);
-      const double a2 = P.v[2 * n + p] + (C[6 * n + p] * d0 + C[7 * n + p] * d1 + C[8 * n + p] * d2);
-      m += wm;
-      mom0 += wm * a0;
-      mom1 += wm * a1;
-      mom2 += wm * a2;
-      num += w * (mp * mats[P.mat[p]].xi);
-    });
-    m = warp_sum_d(m);
-    mom0 = warp_sum_d(mom0);
-    mom1 = warp_sum_d(mom1);
-    mom2 = warp_sum_d(mom2);
-    num = warp_sum_d(num);
-    if (lane == 0) {
-      g.mass[i] = m;
-      g.mom[3 * i] = mom0;
-      g.mom[3 * i + 1] = mom1;
-      g.mom[3 * i + 2] = mom2;
-      if (m > 0.0) {
-        g.vel[3 * i] = mom0 / m;
-        g.vel[3 * i + 1] = mom1 / m;
-        g.vel[3 * i + 2] = mom2 / m;
-      } else {
-        g.vel[3 * i] = g.vel[3 * i + 1] = g.vel[3 * i + 2] = 0.0;
+    for (int c0 = pb; c0 < pe; c0 += 32) {
+      const int cnt = min(32, pe - c0);
+      __syncwarp();
+      if (lane < cnt) {
+        const long long p = c0 + lane;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          sm[a][lane] = __ldg(P.x + a * n + p);
+          sm[3 + a][lane] = __ldg(P.v + a * n + p);
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) sm[6 + q][lane] = __ldg(P.C + q * n + p);
+        const double mp = __ldg(P.mass + p);
+        sm[15][lane] = mp;
+        sm[16][lane] = mp * mats[__ldg(P.mat + p)].xi;
       }
-      const double xi = m > 0.0 ? num / m : 0.0;
-      g.cn_scale[i] = ell * xi * dt;
-      g.dir[i] = 0;
-      g.bc_vel[3 * i] = g.bc_vel[3 * i + 1] = g.bc_vel[3 * i + 2] = 0.0;
+      __syncwarp();
+      for (int t0 = 0; t0 < cnt; t0 += 3) {
+        const double wa = bspline_w(sm[la][min(t0 + wu, cnt - 1)] / dx - ca);
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int t = t0 + u;
+          if (t >= cnt) break;
+          const double w = __shfl_sync(0xffffffffu, wa, 9 * u + s0) * __shfl_sync(0xffffffffu, wa, 9 * u + s1) *
+                           __shfl_sync(0xffffffffu, wa, 9 * u + s2);
+          if (w <= 0.0) continue;
+          const double px0 = sm[0][t], px1 = sm[1][t], px2 = sm[2][t];
+          const double wm = w * sm[15][t];
+          const double d0 = xi0 - px0, d1 = xi1 - px1, d2 = xi2 - px2;
+          const double a0 = sm[3][t] + (sm[6][t] * d0 + sm[7][t] * d1 + sm[8][t] * d2);
+          const double a1 = sm[4][t] + (sm[9][t] * d0 + sm[10][t] * d1 + sm[11][t] * d2);
+          const double a2 = sm[5][t] + (sm[12][t] * d0 + sm[13][t] * d1 + sm[14][t] * d2);
+          m += wm;
+          mom0 += wm * a0;
+          mom1 += wm * a1;
+          mom2 += wm * a2;
+          num += w * sm[16][t];
+        }
+      }
     }
+    if (lane < 27) {  // [bin][stencil position][field]
+      double* out = B + 135LL * j + 5 * lane;
+      out[0] = m;
+      out[1] = mom0;
+      out[2] = mom1;
+      out[3] = mom2;
+      out[4] = num;
+    }
+  }
+}
+
+/// P2G, node half: one thread per node sums its 27 bins' contributions in offset order (bin at
+/// offset o - 1, where the node is stencil position 26 - o), then v = mom / m and the characteristic-norm scale
+/// (objective.hpp:445-463); resets the boundary fields.
+__global__ void __launch_bounds__(256) k_p2g(GridView g, const double* __restrict__ B, double ell, double dt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+    double m = 0.0, mom0 = 0.0, mom1 = 0.0, mom2 = 0.0, num = 0.0;
+    const int* nbi = g.nb27 + 27LL * i;
+#pragma unroll 9
+    for (int o = 0; o < 27; ++o) {
+      const int j = __ldg(nbi + o);
+      if (j < 0) continue;
+      const double* bv = B + 135LL * j + 5 * (26 - o);
+      m += __ldg(bv);
+      mom0 += __ldg(bv + 1);
+      mom1 += __ldg(bv + 2);
+      mom2 += __ldg(bv + 3);
+      num += __ldg(bv + 4);
+    }
+    g.mass[i] = m;
+    g.mom[3 * i] = mom0;
+    g.mom[3 * i + 1] = mom1;
+    g.mom[3 * i + 2] = mom2;
+    if (m > 0.0) {
+      g.vel[3 * i] = mom0 / m;
+      g.vel[3 * i + 1] = mom1 / m;
+      g.vel[3 * i + 2] = mom2 / m;
+    } else {
+      g.vel[3 * i] = g.vel[3 * i + 1] = g.vel[3 * i + 2] = 0.0;
+    }
+    const double xi = m > 0.0 ? num / m : 0.0;
+    g.cn_scale[i] = ell * xi * dt;
+    g.dir[i] = 0;
+    g.bc_vel[3 * i] = g.bc_vel[3 * i + 1] = g.bc_vel[3 * i + 2] = 0.0;
   }
 }
 
@@ -478,10 +537,15 @@ void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n
 }
 
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
-                double dt, cudaStream_t s) {
+                double dt, double* bin_part, cudaStream_t s) {
   if (g.n == 0) return;
   static const int blocks = resident_blocks((const void*)k_p2g, 256, 0);
-  { k_p2g<<<std::min<long long>(blocks, (32LL * g.n + 255) / 256), 256, 0, s>>>(P, bins, g, dx, mats, ell, dt); count_launches(1); }
+  const long long need = (32LL * g.n + 255) / 256;
+  static const int bin_blocks = resident_blocks((const void*)k_bin_p2g, kBinWarps * 32, 0);
+  k_bin_p2g<<<std::min<long long>(bin_blocks, (g.n + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
+      P, bins, g, dx, mats, bin_part);
+  k_p2g<<<std::min<long long>(blocks, (g.n + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt);
+  count_launches(2);
 }
 
 void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s) {

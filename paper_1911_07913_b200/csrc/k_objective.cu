@@ -102,49 +102,101 @@ __global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, double 
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
 }
 
-/// Node gradient (objective.hpp:260-287): one warp per node gathers V P F^T grad w over the
-/// particles of its 27 bins (lanes over the contiguous slots, fixed-tree warp sum), fused
-/// with the scaled-norm residual (objective.hpp:476-486).
-__global__ void __launch_bounds__(kRedThreads) k_node_gradient(ParticlesView P, BinsView bins, GridView g, double dx,
-                                                               double dt, double g0, double g1, double g2,
-                                                               const double* __restrict__ stress,
+/// Gradient, particle half (objective.hpp:276-280): for bin j and stencil position k, the sum
+/// over the bin's particles (bin order) of (V P F^nT)_p grad w_k(x_p), into S[j][k][0..2].  One
+/// warp per bin, lane k < 27; the particle's data is a broadcast load.  Every (bin, k) pair
+/// feeds exactly one node, so each particle is read once per gradient instead of once per
+/// stencil node, and the node pass reads each S entry once.  Empty bins write zeros.
+constexpr int kBinWarps = 8;
+__global__ void __launch_bounds__(kBinWarps * 32) k_bin_force(ParticlesView P, BinsView bins, GridView g, double dx,
+                                                             const double* __restrict__ stress,
+                                                             double* __restrict__ S) {
+  // per warp: the current chunk of <= 32 bin particles, [field][slot] (x 3, V P F^T 9), loaded
+  // coalesced (lanes over particles) and read back as broadcasts by the stencil lanes
+  __shared__ double stage[kBinWarps][12][32];
+  const long long n = P.n;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  double(*sm)[32] = stage[wib];
+  // 1D weights: lane 9u + 3a + k (< 27) evaluates axis a, node k of particle t + u, so one
+  // division sequence serves three particles; the stencil lanes (lane = 9 k0 + 3 k1 + k2) take
+  // theirs by shuffle
+  const int wu = min(lane / 9, 2), la = (lane % 9) / 3, lk = lane % 3;
+  const int s0 = lane / 9, s1 = 3 + (lane / 3) % 3, s2 = 6 + lane % 3;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < g.n; j += nw) {
+    const int pb = __ldg(bins.start + j), pe = __ldg(bins.start + j + 1);
+    const double ca = (double)(g.coords[3 * j + la] + lk - 1);
+    double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+    for (int c0 = pb; c0 < pe; c0 += 32) {
+      const int cnt = min(32, pe - c0);
+      __syncwarp();
+      if (lane < cnt) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) sm[a][lane] = __ldg(P.x + a * n + c0 + lane);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) sm[3 + q][lane] = __ldg(stress + q * n + c0 + lane);
+      }
+      __syncwarp();
+      for (int t0 = 0; t0 < cnt; t0 += 3) {
+        const double o = sm[la][min(t0 + wu, cnt - 1)] / dx - ca;
+        const double wa = bspline_w(o), dwa = bspline_dw(o) / dx;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int t = t0 + u;
+          if (t >= cnt) break;
+          const double w0 = __shfl_sync(0xffffffffu, wa, 9 * u + s0), w1 = __shfl_sync(0xffffffffu, wa, 9 * u + s1),
+                       w2 = __shfl_sync(0xffffffffu, wa, 9 * u + s2);
+          const double d0 = __shfl_sync(0xffffffffu, dwa, 9 * u + s0),
+                       d1 = __shfl_sync(0xffffffffu, dwa, 9 * u + s1),
+                       d2 = __shfl_sync(0xffffffffu, dwa, 9 * u + s2);
+          if (w0 * w1 * w2 <= 0.0) continue;
+          const double gr0 = d0 * w1 * w2;
+          const double gr1 = d1 * w0 * w2;
+          const double gr2 = d2 * w0 * w1;
+          f0 += sm[3][t] * gr0 + sm[4][t] * gr1 + sm[5][t] * gr2;
+          f1 += sm[6][t] * gr0 + sm[7][t] * gr1 + sm[8][t] * gr2;
+          f2 += sm[9][t] * gr0 + sm[10][t] * gr1 + sm[11][t] * gr2;
+        }
+      }
+    }
+    if (lane < 27) {  // [bin][stencil position][field]
+      double* out = S + 81LL * j + 3 * lane;
+      out[0] = f0;
+      out[1] = f1;
+      out[2] = f2;
+    }
+  }
+}
+
+/// Node gradient (objective.hpp:260-287): one thread per node sums its 27 bins' contributions
+/// in offset order (bin at offset o - 1, where the node is stencil position 26 - o), fused with
+/// the scaled-norm residual (objective.hpp:476-486).
+__global__ void __launch_bounds__(kRedThreads) k_node_gradient(GridView g, double dt, double g0, double g1, double g2,
+                                                               const double* __restrict__ S,
                                                                const double* __restrict__ dv, double* __restrict__ gout,
                                                                double* __restrict__ partials, int* bad) {
-  const long long n = P.n;
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
   double acc_norm = 0.0;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < g.n; i += nw) {
-    const int ci0 = g.coords[3 * i], ci1 = g.coords[3 * i + 1], ci2 = g.coords[3 * i + 2];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
-    warp_node_gather(g, bins, i, lane, [&](int p) {
-      const double o0 = P.x[p] / dx - (double)ci0;
-      const double o1 = P.x[n + p] / dx - (double)ci1;
-      const double o2 = P.x[2 * n + p] / dx - (double)ci2;
-      const double w0 = bspline_w(o0), w1 = bspline_w(o1), w2 = bspline_w(o2);
-      if (w0 * w1 * w2 <= 0.0) return;
-      const double gr0 = bspline_dw(o0) / dx * w1 * w2;
-      const double gr1 = bspline_dw(o1) / dx * w0 * w2;
-      const double gr2 = bspline_dw(o2) / dx * w0 * w1;
-      const double* Q = stress;
-      f0 += Q[p] * gr0 + Q[n + p] * gr1 + Q[2 * n + p] * gr2;
-      f1 += Q[3 * n + p] * gr0 + Q[4 * n + p] * gr1 + Q[5 * n + p] * gr2;
-      f2 += Q[6 * n + p] * gr0 + Q[7 * n + p] * gr1 + Q[8 * n + p] * gr2;
-    });
-    f0 = warp_sum_d(f0);
-    f1 = warp_sum_d(f1);
-    f2 = warp_sum_d(f2);
-    if (lane == 0) {
-      const double m = g.mass[i];
-      double gi[3] = {dt * f0 + m * (dv[3 * i] - dt * g0), dt * f1 + m * (dv[3 * i + 1] - dt * g1),
-                      dt * f2 + m * (dv[3 * i + 2] - dt * g2)};
-      if (g.dir[i]) gi[0] = gi[1] = gi[2] = 0.0;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) gout[3 * i + a] = gi[a];
-      const double sc = g.cn_scale[i];
-      if (!(sc > 0.0)) atomicExch(bad, 2);
-      acc_norm += (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
+    const int* nbi = g.nb27 + 27LL * i;
+#pragma unroll 9
+    for (int o = 0; o < 27; ++o) {
+      const int j = __ldg(nbi + o);
+      if (j < 0) continue;
+      const double* sv = S + 81LL * j + 3 * (26 - o);
+      f0 += __ldg(sv);
+      f1 += __ldg(sv + 1);
+      f2 += __ldg(sv + 2);
     }
+    const double m = g.mass[i];
+    double gi[3] = {dt * f0 + m * (dv[3 * i] - dt * g0), dt * f1 + m * (dv[3 * i + 1] - dt * g1),
+                    dt * f2 + m * (dv[3 * i + 2] - dt * g2)};
+    if (g.dir[i]) gi[0] = gi[1] = gi[2] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gout[3 * i + a] = gi[a];
+    const double sc = g.cn_scale[i];
+    if (!(sc > 0.0)) atomicExch(bad, 2);
+    acc_norm += (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
   }
   const double b = block_sum<kRedThreads>(acc_norm);
   if (threadIdx.x == 0) partials[blockIdx.x] = b;
@@ -278,17 +330,21 @@ void launch_node_energy(GridView g, double dt, const double* grav, const double*
 }
 
 void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
-                          const double* stress, const double* dv, double* gout, double* partials, int nblocks,
-                          int* bad_flag, cudaStream_t s) {
-  // resident-sized grid: the active nodes form one contiguous window, so the particles of
-  // neighbouring nodes' bins are reused from L2; unused partial slots are zeroed
+                          const double* stress, const double* dv, double* gout, double* bin_part, double* partials,
+                          int nblocks, int* bad_flag, cudaStream_t s) {
+  if (g.n > 0) {
+    static const int bin_blocks = resident_blocks((const void*)k_bin_force, kBinWarps * 32, 0);
+    k_bin_force<<<std::min<long long>(bin_blocks, (g.n + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
+        P, bins, g, dx, stress, bin_part);
+    count_launches(1);
+  }
   static const int resident = resident_blocks((const void*)k_node_gradient, kRedThreads, 0);
   const int nb = std::max(1, std::min(nblocks, resident));
   if (nb < nblocks) {
     cudaMemsetAsync(partials + nb, 0, sizeof(double) * (nblocks - nb), s);
   }
-  { k_node_gradient<<<nb, kRedThreads, 0, s>>>(P, bins, g, dx, dt, grav[0], grav[1], grav[2], stress, dv, gout,
-                                              partials, bad_flag); count_launches(1); }
+  { k_node_gradient<<<nb, kRedThreads, 0, s>>>(g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, partials,
+                                              bad_flag); count_launches(1); }
 }
 
 void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s) {
