@@ -79,6 +79,13 @@ __device__ __forceinline__ void axis_weights(double c, int base, Axis3& ax) {
   }
 }
 
+/// dw/dx in place (the reference's kernel_gradient divides each 1D derivative by dx before the
+/// products, grid.hpp:58-73): 3 divisions per axis instead of one per stencil node.
+__device__ __forceinline__ void axis_dw_over_dx(Axis3& ax, double dx) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ax.dw[k] = ax.dw[k] / dx;
+}
+
 // ------------------------------------------------------------------------------------
 // 3x3 fp64 algebra, row-major m[i*3+j]
 // ------------------------------------------------------------------------------------

@@ -24,6 +24,12 @@ __host__ __device__ constexpr int tperm(int q) {
   constexpr int perm[45] = {44, 2, 26, 23, 25, 3, 24, 22, 29, 31, 6, 36, 42, 37, 12, 16, 43, 18, 33, 39, 20, 9, 30, 15, 35, 34, 10, 0, 7, 38, 17, 40, 4, 27, 19, 28, 1, 21, 41, 5, 14, 32, 8, 13, 11};
   return perm[q];
 }
+/// Inverse of tperm: the packed index stored at T slot t.
+__host__ __device__ constexpr int tperm_inv(int t) {
+  int q = 0;
+  while (q < 45 && tperm(q) != t) ++q;
+  return q;
+}
 __host__ __device__ constexpr int tpack_index(int r, int c) {
   return r > c ? c * 9 - c * (c - 1) / 2 + (r - c) : r * 9 - r * (r - 1) / 2 + (c - r);
 }
@@ -44,6 +50,7 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
     c[a] = P.x[a * n + p] / dx;
     base[a] = stencil_base_1d(c[a]);
     axis_weights(c[a], base[a], ax[a]);
+    axis_dw_over_dx(ax[a], dx);
   }
   const int* nb = g.nb27 + 27LL * P.bin[p];
   double G[9];
@@ -62,9 +69,9 @@ __device__ __forceinline__ bool virtual_F(const ParticlesView& P, long long p, c
         const double w = wi * ax[1].w[j] * ax[2].w[k];
         if (w <= 0.0) continue;
         const int node = __ldg(nb + 9 * i + 3 * j + k);
-        const double gr0 = dwi / dx * ax[1].w[j] * ax[2].w[k];
-        const double gr1 = ax[1].dw[j] / dx * wi * ax[2].w[k];
-        const double gr2 = ax[2].dw[k] / dx * wi * ax[1].w[j];
+        const double gr0 = dwi * ax[1].w[j] * ax[2].w[k];
+        const double gr1 = ax[1].dw[j] * wi * ax[2].w[k];
+        const double gr2 = ax[2].dw[k] * wi * ax[1].w[j];
         const double u0 = __ldg(u + 3 * node), u1 = __ldg(u + 3 * node + 1), u2 = __ldg(u + 3 * node + 2);
         G[0] += u0 * gr0;
         G[1] += u0 * gr1;

@@ -33,61 +33,111 @@ constexpr int kUpper = 63;  // slots 62..124
 constexpr int kTPacked = 45;
 constexpr int kTensorStride = kRecStride;
 
-__global__ void k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
-                                   const DevMaterial* __restrict__ mats, const double* __restrict__ u,
-                                   const double* __restrict__ svd_in, int project, double* __restrict__ Tu, int* bad) {
+/// Records are written through a per-warp shared-memory transpose: each lane computes its
+/// particle's values, then the warp writes the 32 records part by part, consecutive lanes on
+/// consecutive addresses (a thread-per-particle store pattern puts every lane on its own line).
+constexpr int kTWarps = 4;
+__global__ void __launch_bounds__(kTWarps * 32) k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
+                                                                   const DevMaterial* __restrict__ mats,
+                                                                   const double* __restrict__ u,
+                                                                   const double* __restrict__ svd_in, int project,
+                                                                   double* __restrict__ Tu, int* bad) {
+  __shared__ double stage[kTWarps][32][kTPacked];
   const long long n = P.n;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-    M3 U, V, Fn;
-    double s[3];
-    if (svd_in) {  // SVD of the virtual F at this dv, stored by the energy evaluation
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long nchunks = (n + 31) / 32;
+  for (long long ch = blockIdx.x * (long long)kTWarps + wib; ch < nchunks; ch += (long long)gridDim.x * kTWarps) {
+    const long long p = ch * 32 + lane;
+    if (p < n) {
+      const int mat = __ldg(P.mat + p);
+      const double vol = __ldg(P.vol + p);
+      M3 U, V, Fn;
+      double s[3];
+      bool ok = true;
+      if (svd_in) {  // SVD of the virtual F at this dv, stored by the energy evaluation
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        U.m[k] = svd_in[k * n + p];
-        V.m[k] = svd_in[(12 + k) * n + p];
-        Fn.m[k] = P.F[k * n + p];
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) s[k] = svd_in[(9 + k) * n + p];
-    } else {
-      M3 F;
-      if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
-        atomicExch(bad, 1);
-        continue;
-      }
-      svd3(F, U, s, V);
-    }
-    const DevMaterial mt = mats[P.mat[p]];
-    double T[45];
-    fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * P.vol[p], project != 0, T);
-    double* out = Tu + p * kTensorStride;
-#pragma unroll
-    for (int q = 0; q < kTPacked; ++q) out[kRecT + tperm(q)] = T[q];  // record slot kRecT + tslot(r, c)
-    // W_k = F^nT grad w_k for the 27 stencil nodes (grid.hpp:58-73, objective.hpp:337-339); nodes
-    // with zero weight get W = 0, which is how the reference skips them (transfer.hpp:36-37)
-    Axis3 ax[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double c = P.x[a * n + p] / dx;
-      axis_weights(c, stencil_base_1d(c), ax[a]);
-    }
-#pragma unroll 1
-    for (int k0 = 0; k0 < 3; ++k0) {  // rolled x axis (select, not indexing): instruction-cache size
-      const double w0 = k0 == 0 ? ax[0].w[0] : (k0 == 1 ? ax[0].w[1] : ax[0].w[2]);
-      const double dw0 = k0 == 0 ? ax[0].dw[0] : (k0 == 1 ? ax[0].dw[1] : ax[0].dw[2]);
-#pragma unroll
-      for (int kk = 0; kk < 9; ++kk) {
-        const int k1 = kk / 3, k2 = kk % 3, k = 9 * k0 + kk;
-        const double w1 = ax[1].w[k1], w2 = ax[2].w[k2];
-        double W[3] = {0.0, 0.0, 0.0};
-        if (w0 * w1 * w2 > 0.0) {
-          const double g0 = dw0 / dx * w1 * w2, g1 = ax[1].dw[k1] / dx * w0 * w2, g2 = ax[2].dw[k2] / dx * w0 * w1;
-#pragma unroll
-          for (int q = 0; q < 3; ++q) W[q] = Fn.m[q] * g0 + Fn.m[3 + q] * g1 + Fn.m[6 + q] * g2;
+        for (int k = 0; k < 9; ++k) {
+          U.m[k] = __ldg(svd_in + k * n + p);
+          V.m[k] = __ldg(svd_in + (12 + k) * n + p);
         }
 #pragma unroll
-        for (int q = 0; q < 3; ++q) out[kRecW + 3 * k + q] = W[q];
+        for (int k = 0; k < 3; ++k) s[k] = __ldg(svd_in + (9 + k) * n + p);
+      } else {
+        M3 F;
+        ok = virtual_F(P, p, g, dx, dt, u, F, Fn);
+        if (ok) svd3(F, U, s, V);
+        else atomicExch(bad, 1);
       }
+      if (ok) {
+        const DevMaterial mt = mats[mat];
+        double T[45];
+        fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * vol, project != 0, T);
+#pragma unroll
+        for (int q = 0; q < kTPacked; ++q) stage[wib][lane][tperm(q)] = T[q];  // T slot tslot(r, c)
+      }
+    }
+    __syncwarp();
+    const int cnt = (int)min(32LL, n - ch * 32);
+    for (int t = 0; t < cnt; ++t) {
+      double* out = Tu + (ch * 32 + t) * kTensorStride + kRecT;
+      out[lane] = stage[wib][t][lane];
+      if (lane < kTPacked - 32) out[32 + lane] = stage[wib][t][32 + lane];
+    }
+    __syncwarp();
+  }
+}
+
+/// The record's W part: W_k = F^nT grad w_k for the 27 stencil nodes (grid.hpp:58-73,
+/// objective.hpp:337-339); nodes with zero weight get W = 0, which is how the reference skips
+/// them (transfer.hpp:36-37).  A separate light kernel (the T kernel is register bound).
+constexpr int kWWarps = 4;
+__global__ void __launch_bounds__(kWWarps * 32) k_particle_W(ParticlesView P, double dx, double* __restrict__ Tu) {
+  __shared__ double stage[kWWarps][32][27 + 1];  // one x-plane (9 positions) of the warp's 32 records
+  const long long n = P.n;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long nchunks = (n + 31) / 32;
+  for (long long ch = blockIdx.x * (long long)kWWarps + wib; ch < nchunks; ch += (long long)gridDim.x * kWWarps) {
+    const long long p = ch * 32 + lane;
+    const bool live = p < n;
+    double Fn[9];
+    Axis3 ax[3];
+    if (live) {
+      double xs[3];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Fn[k] = __ldg(P.F + k * n + p);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) xs[a] = __ldg(P.x + a * n + p);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double c = xs[a] / dx;
+        axis_weights(c, stencil_base_1d(c), ax[a]);
+        axis_dw_over_dx(ax[a], dx);
+      }
+    }
+    const int cnt = (int)min(32LL, n - ch * 32);
+#pragma unroll 1
+    for (int k0 = 0; k0 < 3; ++k0) {
+      if (live) {
+        const double w0 = k0 == 0 ? ax[0].w[0] : (k0 == 1 ? ax[0].w[1] : ax[0].w[2]);
+        const double dw0 = k0 == 0 ? ax[0].dw[0] : (k0 == 1 ? ax[0].dw[1] : ax[0].dw[2]);
+#pragma unroll
+        for (int kk = 0; kk < 9; ++kk) {
+          const int k1 = kk / 3, k2 = kk % 3;
+          const double w1 = ax[1].w[k1], w2 = ax[2].w[k2];
+          double W[3] = {0.0, 0.0, 0.0};
+          if (w0 * w1 * w2 > 0.0) {
+            const double g0 = dw0 * w1 * w2, g1 = ax[1].dw[k1] * w0 * w2, g2 = ax[2].dw[k2] * w0 * w1;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) W[q] = Fn[q] * g0 + Fn[3 + q] * g1 + Fn[6 + q] * g2;
+          }
+#pragma unroll
+          for (int q = 0; q < 3; ++q) stage[wib][lane][3 * kk + q] = W[q];
+        }
+      }
+      __syncwarp();
+      for (int t = 0; t < cnt; ++t)
+        if (lane < 27) Tu[(ch * 32 + t) * kTensorStride + kRecW + 27 * k0 + lane] = stage[wib][t][lane];
+      __syncwarp();
     }
   }
 }
@@ -428,7 +478,12 @@ void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, doub
                              const double* u, const double* svd_in, int project, double* Tu, int* bad_flag,
                              cudaStream_t s) {
   if (P.n == 0) return;
-  { k_particle_tensors<<<agrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag); count_launches(1); }
+  const long long chunks = (P.n + 31) / 32;
+  k_particle_tensors<<<(int)std::min<long long>((chunks + kTWarps - 1) / kTWarps, 16LL * num_sms()), kTWarps * 32, 0,
+                       s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag);
+  k_particle_W<<<(int)std::min<long long>((chunks + kWWarps - 1) / kWWarps, 32LL * num_sms()), kWWarps * 32, 0, s>>>(
+      P, dx, Tu);
+  count_launches(2);
 }
 
 void launch_fill_cols(LevelView L, cudaStream_t s) {

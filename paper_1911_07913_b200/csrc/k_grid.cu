@@ -74,12 +74,23 @@ __global__ void k_particle_bounds(const double* __restrict__ x, long long n, dou
       mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
     }
   }
-  if ((threadIdx.x & 31) == 0) {
+  // block reduction, then one set of atomics per block (a few hundred blocks, not one per warp)
+  __shared__ int red[6][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (lane == 0) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      atomicMin(bounds6 + a, mn[a]);
-      atomicMax(bounds6 + 3 + a, mx[a]);
+      red[a][wid] = mn[a];
+      red[3 + a][wid] = mx[a];
     }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int a = threadIdx.x;
+    int v = red[a][0];
+    for (int w = 1; w < nwarp; ++w) v = a < 3 ? min(v, red[a][w]) : max(v, red[a][w]);
+    if (a < 3) atomicMin(bounds6 + a, v);
+    else atomicMax(bounds6 + a, v);
   }
 }
 
@@ -495,7 +506,7 @@ int resident_blocks(const void* fn, int threads, int smem) {
 
 void launch_particle_bounds(const ParticlesView& P, double dx, int* bounds6, int* bad_flag, cudaStream_t s) {
   if (P.n == 0) return;
-  { k_particle_bounds<<<grid_for(P.n, 256), 256, 0, s>>>(P.x, P.n, dx, bounds6, bad_flag); count_launches(1); }
+  { k_particle_bounds<<<std::min(grid_for(P.n, 256), 4 * num_sms()), 256, 0, s>>>(P.x, P.n, dx, bounds6, bad_flag); count_launches(1); }
 }
 
 void launch_mark_active(const ParticlesView& P, double dx, DenseMap map, uint8_t* flags, cudaStream_t s) {

@@ -26,6 +26,7 @@ __global__ void k_g2p_strain_advect(ParticlesView P, GridView g, double dx, doub
       c[a] = xp[a] / dx;
       base[a] = stencil_base_1d(c[a]);
       axis_weights(c[a], base[a], ax[a]);
+      axis_dw_over_dx(ax[a], dx);
     }
     double v[3] = {0.0, 0.0, 0.0}, B[9], G[9];
 #pragma unroll
@@ -47,8 +48,8 @@ __global__ void k_g2p_strain_advect(ParticlesView P, GridView g, double dx, doub
           const double vi[3] = {g.vel[3 * node], g.vel[3 * node + 1], g.vel[3 * node + 2]};
           const double d[3] = {(double)(base[0] + i) * dx - xp[0], (double)(base[1] + j) * dx - xp[1],
                                (double)(base[2] + k) * dx - xp[2]};
-          const double gr[3] = {dwi / dx * ax[1].w[j] * ax[2].w[k], ax[1].dw[j] / dx * wi * ax[2].w[k],
-                                ax[2].dw[k] / dx * wi * ax[1].w[j]};
+          const double gr[3] = {dwi * ax[1].w[j] * ax[2].w[k], ax[1].dw[j] * wi * ax[2].w[k],
+                                ax[2].dw[k] * wi * ax[1].w[j]};
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const double wv = w * vi[a];
@@ -101,8 +102,14 @@ __global__ void k_vmax(const double* __restrict__ v, long long n, unsigned long 
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  // non-negative doubles order like their bit patterns
-  if ((threadIdx.x & 31) == 0) atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(m));
+  // block maximum, then one atomic per block; non-negative doubles order like their bit patterns
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    atomicMax(vmax_bits, (unsigned long long)__double_as_longlong(m));
+  }
 }
 
 int tgrid(long long n, int threads) {
@@ -126,7 +133,7 @@ void launch_check_ids(const int* ids, long long n, int limit, int* bad, cudaStre
 
 void launch_vmax(const ParticlesView& P, unsigned long long* vmax_bits, cudaStream_t s) {
   if (P.n == 0) return;
-  { k_vmax<<<tgrid(P.n, 256), 256, 0, s>>>(P.v, P.n, vmax_bits); count_launches(1); }
+  { k_vmax<<<std::min(tgrid(P.n, 256), 4 * num_sms()), 256, 0, s>>>(P.v, P.n, vmax_bits); count_launches(1); }
 }
 
 }  // namespace hotb200
