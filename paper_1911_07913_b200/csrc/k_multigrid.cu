@@ -755,6 +755,7 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
                                                          const double* __restrict__ b, int* flag, int epoch) {
   constexpr int T = level_pitch(R), S = level_slots(R);  // one thread per diagonal-storage slot
   __shared__ double red[T / 32][3];
+  __shared__ double uold[3];  // u_i, from the diagonal slot's gather (no second L2 round trip)
   const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
   for (int pass = 0; pass < 2; ++pass) {
     const int e = epoch + pass;
@@ -796,6 +797,11 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
         x0 = __ldcg(xp);
         x1 = __ldcg(xp + 1);
         x2 = __ldcg(xp + 2);
+        if (s == S / 2) {
+          uold[0] = x0;
+          uold[1] = x1;
+          uold[2] = x2;
+        }
       }
       double a0 = h[0] * x0 + h[1] * x1 + h[2] * x2;
       double a1 = h[3] * x0 + h[4] * x1 + h[5] * x2;
@@ -817,7 +823,7 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
           y1 += red[q][1];
           y2 += red[q][2];
         }
-        const double uo0 = __ldcg(u + 3 * i), uo1 = __ldcg(u + 3 * i + 1), uo2 = __ldcg(u + 3 * i + 2);
+        const double uo0 = uold[0], uo1 = uold[1], uo2 = uold[2];
         const double r0 = rb[0] - y0, r1 = rb[1] - y1, r2 = rb[2] - y2;
         u[3 * i] = uo0 + (D[0] * r0 + D[1] * r1 + D[2] * r2);
         u[3 * i + 1] = uo1 + (D[3] * r0 + D[4] * r1 + D[5] * r2);
