@@ -11,8 +11,10 @@ corotated (the reference's only model), eps = 1e-5).  One step = one advance_ste
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 --impl reference times the reference CPU path (the oracle port, all host threads) on a
-bounded slab of the same workload.  Under torchrun (N > 1) each rank runs an independent
-replica of the workload (the slab-sharded path is not built yet), scaling "weak".
+bounded slab of the same workload.  Under torchrun (N > 1) the ranks share ONE copy of the
+workload and the solve is cut into slabs of lattice planes along axis 0 (NCCL inside the
+library): scaling "strong", value = the scene's particle-steps / the max over
+ranks of the device time.  --mode replicas runs N independent copies instead ("weak").
 """
 import argparse
 import json
@@ -137,6 +139,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scene", default=SCENE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="slabs", choices=["slabs", "replicas"], help="N > 1: slab-sharded or replicas")
     args = ap.parse_args()
 
     rank, world, local_rank = dist_env()
@@ -184,6 +187,17 @@ def main():
     sim = Simulation(sc, device=device)
     sim.set_particles(**particles)
     stream = torch.cuda.ExternalStream(sim.stream(), device=device)
+    slabbed = world > 1 and args.mode == "slabs"
+    slab_error = None
+    if slabbed:
+        from paper_1911_07913_b200 import slabs
+
+        try:
+            slabs.attach_nccl(sim)
+        except Exception as e:  # no NCCL transport: say so in the line and run replicas
+            slab_error = f"{type(e).__name__}: {e}"
+            slabbed = False
+    copies = 1 if slabbed else world  # scene copies processed per step by the whole job
 
     def barrier():
         if world > 1:
@@ -222,7 +236,12 @@ def main():
         t = torch.tensor([ms], device=f"cuda:{device}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = n_particles * world * args.steps / (ms / 1000.0)
+    value = n_particles * copies * args.steps / (ms / 1000.0)
+    shard = None
+    if slabbed:
+        si = slabs.shard_info(sim)
+        shard = {"rows": [si["row_lo"], si["row_hi"]], "planes": [si["plane_lo"], si["plane_hi"]],
+                 "halo_exchanges": si["halo_exchanges"], "row_gathers": si["gathers"]}
 
     # ---- end-to-end through the public API with host buffers (pinned)
     host = sim.particles()
@@ -256,7 +275,7 @@ def main():
         t = torch.tensor([e2e_ms], device=f"cuda:{device}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = n_particles * world * e2e_steps / (e2e_ms / 1000.0)
+    e2e_value = n_particles * copies * e2e_steps / (e2e_ms / 1000.0)
 
     # ---- rooflines (algorithmic bytes or flops / CUDA-event duration on the context stream)
     # `roofline` is the dominant kernel of the step: the level-0 assembly, bound by fp64 FMA
@@ -301,10 +320,13 @@ def main():
         phases = {k: round(v["ms"] / args.steps, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
                   if v["ms"] > 0}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong" if slabbed else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling, reference schema)",
-                "config": dict(config, parallelism=f"replicas x{world}" if world > 1 else "single GPU",
-                               outer_iterations=outer, phase_ms_per_step=phases),
+                "config": dict(config, parallelism=(f"slabs x{world} (axis-0 lattice planes, NCCL)" if slabbed else
+                                                    f"replicas x{world}" + (f" (slab transport failed: {slab_error})" if slab_error else "")
+                                                    if world > 1 else "single GPU"),
+                               outer_iterations=outer, phase_ms_per_step=phases, rank0_shard=shard),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps},
                 "gpu_launches": int(launches), "roofline": roofline, "roofline_hbm": roofline_hbm, "hbm_phases": hbm_all,

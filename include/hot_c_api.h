@@ -191,6 +191,61 @@ int hot_profile_read(hot_ctx* ctx, char* names /* cap*32 */, double* total_ms, l
 /* Kernel launches issued by this context since creation (all phases). */
 long long hot_kernel_launches(hot_ctx* ctx);
 
+/* ---- multi-GPU: spatial slabs along lattice axis 0 -------------
+ * The reference is single-process (its only parallelism is parallel_for over host threads,
+ * common.hpp:77-83); these entry points are new.  One context per GPU, one process per GPU.
+ * Every rank uploads the SAME particles; each step the ranks cut the level-0 rows into slabs
+ * of lattice planes (axis 0 is the most significant key of the reference order, common.hpp:41,
+ * so a slab is a contiguous range of global rows) and split the level-0 assembly, the level-1
+ * Galerkin product and the level-0 smoother / residual between them.  All other state stays
+ * replicated and every rank's result is bitwise identical to the single-GPU step.
+ * Only the HOT solver (kind 0) with the linear embedding and >= 2 levels shards; other solver
+ * configurations run replicated on every rank. */
+
+/* Caller-owned collectives (tests, or any transport the caller owns: gloo, MPI ...).  Every
+ * callback is collective (all ranks call it in the same order) and returns 0 on success.
+ * device_buffers = 0: buf is host memory (the library stages the ranges through pinned
+ * memory); 1: buf is the device buffer itself (the context stream is synchronised before the
+ * call, and the callback must have finished writing when it returns). */
+typedef struct {
+  void* user;
+  int rank, size;
+  /* rank r's byte range [off[r], off[r+1]) of buf is delivered to every rank (off: size+1). */
+  int (*allgather_ranges)(void* user, void* buf, const long long* off);
+  /* halo exchange: edges[4r..4r+3] = byte ranges [a,b) (rank r's first planes) and [c,d) (its
+   * last planes); rank r receives rank r-1's [c,d) and rank r+1's [a,b) into the same offsets. */
+  int (*halo)(void* user, void* buf, const long long* edges);
+  /* element-wise max over ranks of n ints (host memory), in place. */
+  int (*allreduce_max_i32)(void* user, int* v, int n);
+  int device_buffers;
+} hot_comm_host;
+
+int hot_set_comm_host(hot_ctx* ctx, const hot_comm_host* comm);
+/* NCCL transport (libnccl.so.2, loaded at run time): rank 0 calls hot_nccl_unique_id, the
+ * caller broadcasts the 128 bytes (e.g. torch.distributed), then every rank joins. */
+int hot_nccl_unique_id(unsigned char id[128]);
+int hot_set_comm_nccl(hot_ctx* ctx, const unsigned char id[128], int rank, int size);
+
+typedef struct {
+  int rank, size;
+  int sharded;              /* 1 when the last solve ran slab-sharded */
+  int plane_lo, plane_hi;   /* owned lattice planes [lo, hi) along axis 0 (absolute coordinates) */
+  int row_lo, row_hi;       /* owned level-0 rows */
+  int crow_lo, crow_hi;     /* owned level-1 rows */
+  int asm_lo, asm_hi;       /* level-0 rows this rank assembles (owned + the left extension) */
+  long long halo_exchanges; /* level-0 halo exchanges issued since creation */
+  long long gathers;        /* row-range allgathers issued since creation */
+} hot_shard_info_t;
+int hot_shard_info(hot_ctx* ctx, hot_shard_info_t* out);
+
+/* Slab planner (pure host function, no context): cut planes [plane_lo, plane_lo + nplanes)
+ * into `size` slabs of consecutive planes balancing weight[] (one weight per plane), every
+ * interior cut at a multiple of `align` (absolute coordinate) and every slab >= min_width
+ * planes.  bounds: size+1 absolute plane coordinates, bounds[0] = plane_lo,
+ * bounds[size] = plane_lo + nplanes.  HOT_E_INVALID_ARGUMENT when no such cut exists. */
+int hot_plan_slabs(int plane_lo, int nplanes, const long long* weight, int size, int align, int min_width,
+                   int* bounds);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,7 +116,26 @@ EXPORTS = [
     "hot_stage_gradient", "hot_stage_assemble", "hot_stage_build_hierarchy", "hot_stage_level_count",
     "hot_stage_level_shape", "hot_stage_level_matrix", "hot_stage_matvec", "hot_stage_vcycle",
     "hot_stage_step_grid", "hot_stream", "hot_profile_enable", "hot_profile_read", "hot_kernel_launches",
+    "hot_set_comm_host", "hot_nccl_unique_id", "hot_set_comm_nccl", "hot_shard_info", "hot_plan_slabs",
 ]
+
+# multi-GPU slabs (hot_c_api.h): host-staged collectives and the shard report
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_longlong))
+HALO_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_longlong))
+MAXI32_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int), C.c_int)
+
+
+class hot_comm_host(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("rank", C.c_int), ("size", C.c_int), ("allgather_ranges", ALLGATHER_FN),
+                ("halo", HALO_FN), ("allreduce_max_i32", MAXI32_FN), ("device_buffers", C.c_int)]
+
+
+class hot_shard_info_t(C.Structure):
+    _fields_ = [("rank", C.c_int), ("size", C.c_int), ("sharded", C.c_int), ("plane_lo", C.c_int),
+                ("plane_hi", C.c_int), ("row_lo", C.c_int), ("row_hi", C.c_int), ("crow_lo", C.c_int),
+                ("crow_hi", C.c_int), ("asm_lo", C.c_int), ("asm_hi", C.c_int), ("halo_exchanges", C.c_longlong),
+                ("gathers", C.c_longlong)]
+
 
 _lib = None
 
@@ -166,6 +185,11 @@ def lib():
     L.hot_profile_read.argtypes = [vp, C.c_char_p, dp, i64p, dp, C.c_int, ip]
     L.hot_kernel_launches.restype = C.c_longlong
     L.hot_kernel_launches.argtypes = [vp]
+    L.hot_set_comm_host.argtypes = [vp, C.POINTER(hot_comm_host)]
+    L.hot_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte)]
+    L.hot_set_comm_nccl.argtypes = [vp, C.POINTER(C.c_ubyte), C.c_int, C.c_int]
+    L.hot_shard_info.argtypes = [vp, C.POINTER(hot_shard_info_t)]
+    L.hot_plan_slabs.argtypes = [C.c_int, C.c_int, i64p, C.c_int, C.c_int, C.c_int, ip]
     _lib = L
     return L
 

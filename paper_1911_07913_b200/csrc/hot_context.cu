@@ -15,11 +15,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "../../include/hot_c_api.h"
+#include "hot_comm.h"
 #include "hot_internal.h"
 
 namespace hotb200 {
@@ -115,6 +117,8 @@ struct Level {
     v.dinv = dinv.as<double>();
     v.dir = dir.as<uint8_t>();
     v.radius = radius;
+    v.lo = 0;
+    v.hi = n;
     return v;
   }
   int pitch() const { return level_pitch(radius); }
@@ -129,7 +133,7 @@ struct ProfEvent {
 const char* kPhaseNames[] = {"activate_bin", "p2g_bc", "particle_energy", "node_gradient", "particle_tensors",
                              "assemble_rows", "hierarchy", "sgs_level0", "sgs_coarse", "residual_restrict",
                              "coarse_pcg", "prolong", "lbfgs_vectors", "g2p_strain_advect", "upload_download",
-                             "spmv_level0"};
+                             "spmv_level0", "slab_comm"};
 constexpr int kPhases = sizeof(kPhaseNames) / sizeof(kPhaseNames[0]);
 enum Phase {
   P_ACTIVATE,
@@ -147,7 +151,8 @@ enum Phase {
   P_VEC,
   P_G2P,
   P_IO,
-  P_SPMV0
+  P_SPMV0,
+  P_COMM
 };
 
 }  // namespace
@@ -198,6 +203,30 @@ struct Context {
   double* host_scal = nullptr;  // pinned
   int* host_int = nullptr;      // pinned
   int nred = 0;
+
+  // multi-GPU slabs: the transport, and this solve's cut
+  std::unique_ptr<Comm> comm;
+  struct Shard {
+    bool on = false;               // the current solve runs slab-sharded
+    int P = 0, Q = 0;              // owned lattice planes [P, Q) (axis 0, absolute)
+    int r_lo = 0, r_hi = 0;        // owned level-0 rows
+    int a_lo = 0;                  // assembled level-0 rows [a_lo, r_hi): owned + 7 planes to the left
+    int x_lo = 0;                  // Galerkin stage-1 fine rows [x_lo, r_hi): owned + 5 planes
+    long long p_lo = 0, p_hi = 0;  // particles of the bins the assembled rows read (planes [P-8, Q+1))
+    int c_lo = 0, c_hi = 0;        // owned level-1 rows (coarse planes [P/2, Q/2))
+    int gc_lo = 0;                 // Galerkin stage-2 coarse rows [gc_lo, c_hi): owned + 2 coarse planes
+    std::vector<int> bounds;       // size+1 plane cuts
+    std::vector<int> ps0;          // level-0 plane starts (rows), ext0+1
+    std::vector<long long> row_off;                 // level-0 row cuts per rank
+    std::vector<long long> crow_off;                // level-1 row cuts per rank
+    std::vector<long long> halo_edges[3];           // per axis-0 residue: byte ranges of the one edge plane a wave changes
+    std::vector<int> wave_counts_global;            // level-0 rows per colour (all ranks)
+    std::vector<int> wave_start;                    // this rank's rows per colour (27 + 1)
+    DBuf wave_rows, wave_counts, wave_starts, wave_cursor;
+    long long solves = 0;          // sharded solves so far
+    bool last = false;             // the last solve ran sharded
+  } sh;
+  DBuf plane_buf;
 
   // profiling
   bool prof = false;
@@ -625,6 +654,123 @@ struct Context {
     check_launch();
   }
 
+  // ------------------------------------------------------------------ slabs
+  /// The slab-sharded solve: HOT / LBFGS-H solves with a coarse level under the linear
+  /// embedding, when a transport with more than one rank is attached.
+  bool want_shard(int levels) const { return comm && comm->size > 1 && cfg.embedding == 1 && levels >= 2; }
+  /// First level-0 row at or after absolute lattice plane `plane` (axis 0).
+  int row_of(int plane) const {
+    const int k = std::min(std::max(plane - L[0].lo[0], 0), L[0].ext[0]);
+    return sh.ps0[k];
+  }
+  /// Cuts the level-0 rows into slabs of lattice planes.  Every input is replicated, so every
+  /// rank computes the same cut without communicating.  False: too few planes to cut (the
+  /// solve then runs replicated on every rank).
+  bool plan_shard() {
+    const Level& l0 = L[0];
+    const int R = comm->size, me = comm->rank;
+    const int np0 = l0.ext[0];
+    if (l0.n == 0) return false;
+    plane_buf.ensure(sizeof(int) * (np0 + 2));
+    launch_plane_starts(l0.coords.as<int>(), l0.n, l0.lo[0], np0, plane_buf.as<int>(), stream);
+    sh.ps0.resize(np0 + 1);
+    HOT_CUDA(cudaMemcpyAsync(sh.ps0.data(), plane_buf.p, sizeof(int) * (np0 + 1), cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::vector<long long> w(np0);
+    for (int k = 0; k < np0; ++k) w[k] = sh.ps0[k + 1] - sh.ps0[k];  // rows per plane
+    sh.bounds.assign(R + 1, 0);
+    // interior cuts at even planes (the level-1 cut is then exact: coarse plane = fine / 2) and
+    // at least 2 planes per slab (a row's coupling radius: halos come from one neighbour)
+    if (!plan_slabs(l0.lo[0], np0, w.data(), R, 2, 2, sh.bounds.data())) return false;
+    sh.P = sh.bounds[me];
+    sh.Q = sh.bounds[me + 1];
+    sh.r_lo = row_of(sh.P);
+    sh.r_hi = row_of(sh.Q);
+    // assembly writes each upper block and its transpose: a row's lower blocks come from rows up
+    // to 2 planes left.  Level-1 rows [P/2, Q/2) are complete when the coarse rows 2 coarse
+    // planes further left are computed too (their transposes), which read X of fine children
+    // from plane P-5 on, whose rows need the assembly from plane P-7 on, which reads the bins
+    // (particle tensors) from plane P-8 on.
+    sh.a_lo = row_of(sh.P - 7);
+    sh.x_lo = row_of(sh.P - 5);
+    const int prow[2] = {row_of(sh.P - 8), row_of(sh.Q + 1)};
+    int pb[2] = {0, 0};
+    for (int k = 0; k < 2; ++k)
+      HOT_CUDA(cudaMemcpyAsync(&pb[k], bin_start.as<int>() + prow[k], sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    sh.p_lo = pb[0];
+    sh.p_hi = pb[1];
+    sh.row_off.assign(R + 1, 0);
+    for (int r = 0; r <= R; ++r) sh.row_off[r] = row_of(sh.bounds[r]);
+    // halo after a wave of colour c: only the rows of the edge plane with axis-0 residue c / 9
+    // changed; each side sends that one plane (or nothing)
+    auto md3 = [](int v) { return ((v % 3) + 3) % 3; };
+    for (int m = 0; m < 3; ++m) {
+      std::vector<long long>& e = sh.halo_edges[m];
+      e.assign(4 * R, 0);
+      for (int r = 0; r < R; ++r) {
+        for (int pl = sh.bounds[r]; pl < sh.bounds[r] + 2; ++pl)
+          if (md3(pl) == m) e[4 * r] = 24LL * row_of(pl), e[4 * r + 1] = 24LL * row_of(pl + 1);
+        for (int pl = sh.bounds[r + 1] - 2; pl < sh.bounds[r + 1]; ++pl)
+          if (md3(pl) == m) e[4 * r + 2] = 24LL * row_of(pl), e[4 * r + 3] = 24LL * row_of(pl + 1);
+      }
+    }
+    return true;
+  }
+
+  /// Level-1 cut: coarse planes [P/2, Q/2) (interior cuts are even).
+  void plan_shard_coarse() {
+    const Level& l1 = L[1];
+    const int R = comm->size, me = comm->rank;
+    const int np1 = l1.ext[0];
+    plane_buf.ensure(sizeof(int) * (np1 + 2));
+    launch_plane_starts(l1.coords.as<int>(), l1.n, l1.lo[0], np1, plane_buf.as<int>(), stream);
+    std::vector<int> ps1(np1 + 1);
+    HOT_CUDA(cudaMemcpyAsync(ps1.data(), plane_buf.p, sizeof(int) * (np1 + 1), cudaMemcpyDeviceToHost, stream));
+    sync();
+    auto crow = [&](int plane) { return ps1[std::min(std::max(plane - l1.lo[0], 0), np1)]; };
+    sh.crow_off.assign(R + 1, 0);
+    for (int r = 1; r < R; ++r) sh.crow_off[r] = crow(sh.bounds[r] / 2);
+    sh.crow_off[R] = l1.n;
+    sh.c_lo = (int)sh.crow_off[me];
+    sh.c_hi = (int)sh.crow_off[me + 1];
+    sh.gc_lo = me == 0 ? 0 : crow(sh.bounds[me] / 2 - 2);
+  }
+
+  /// Rows [row_off[r], row_off[r+1]) of a level-0 node vector from their owners to every rank.
+  void gather_rows0(void* vec) {
+    const int h = prof_begin(P_COMM);
+    std::vector<long long> off(sh.row_off.size());
+    for (size_t r = 0; r < off.size(); ++r) off[r] = 24LL * sh.row_off[r];
+    comm->allgather_ranges(vec, off, stream);
+    prof_end(h, (double)off.back());
+  }
+
+  /// smooth_sgs on level 0 (multigrid.hpp:298-316) over this rank's rows: the 27 colour waves
+  /// forward then backward, exactly the single-GPU schedule; after each wave the changed edge
+  /// plane goes to the neighbour, so every row reads the values the serial sweep reads.
+  void sgs0_sharded(double* u, const double* b) {
+    const Level& l = L[0];
+    const LevelView v = l.view();
+    for (int pass = 0; pass < 2; ++pass)
+      for (int k = 0; k < 27; ++k) {
+        const int c = pass == 0 ? k : 26 - k;
+        if (sh.wave_counts_global[c] == 0) continue;  // replicated: every rank skips the same waves
+        const int h = prof_begin(P_SGS0);
+        launch_sgs_wave1(v, sh.wave_rows.as<int>() + sh.wave_start[c], sh.wave_start[c + 1] - sh.wave_start[c], u, b,
+                         stream);
+        prof_end(h, (double)(sh.wave_start[c + 1] - sh.wave_start[c]) * (72.0 * 125 + 72 + 24 + 48));
+        const std::vector<long long>& e = sh.halo_edges[c / 9];
+        bool any = false;
+        for (long long x : e) any |= x != 0;
+        if (any) {
+          const int hc = prof_begin(P_COMM);
+          comm->halo(u, e, stream);
+          prof_end(hc);
+        }
+      }
+  }
+
   // ------------------------------------------------------------------ objective
   int* flag_bad() { return iflags.as<int>() + 0; }
 
@@ -680,7 +826,12 @@ struct Context {
     particle_tensors(dvp, project, reuse_svd);
     const int h = prof_begin(P_ASSEMBLE);
     launch_fill_cols(l0.view(), stream);
-    launch_assemble_rows(pview(), bview(), gview(), l0.view(), dx, Tu.as<double>(), grid_bar.as<unsigned int>() + 8, stream);
+    LevelView v0 = l0.view();
+    if (sh.on) {  // this slab's rows and the rows whose transposes complete them
+      v0.lo = sh.a_lo;
+      v0.hi = sh.r_hi;
+    }
+    launch_assemble_rows(pview(), bview(), gview(), v0, dx, Tu.as<double>(), grid_bar.as<unsigned int>() + 8, stream);
     // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
     prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
     have_H = true;
@@ -697,7 +848,8 @@ struct Context {
       launch_node_u(gview(), dvp, nullptr, 0.0, node_u.as<double>(), stream);
     }
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
-                            reuse_svd ? svd.as<double>() : nullptr, project ? 1 : 0, Tu.as<double>(), flag_bad(), stream);
+                            reuse_svd ? svd.as<double>() : nullptr, project ? 1 : 0, Tu.as<double>(), flag_bad(), stream,
+                            sh.on ? sh.p_lo : 0, sh.on ? sh.p_hi : -1);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 126 * 8));  // x F vol mat in, kappa*T (packed) + W out
   }
 
@@ -732,7 +884,19 @@ struct Context {
                        l.wave_cursor.as<int>(), l.wave_rows.as<int>(), nw, tmp.as<int>(), st);
     std::vector<int> counts(nw);
     HOT_CUDA(cudaMemcpyAsync(counts.data(), l.wave_counts.p, sizeof(int) * nw, cudaMemcpyDeviceToHost, st));
+    if (m == 0 && sh.on) {  // this slab's rows per colour, in the same 27 colour buckets
+      sh.wave_counts.ensure(sizeof(int) * (nw + 2));
+      sh.wave_starts.ensure(sizeof(int) * (nw + 2));
+      sh.wave_cursor.ensure(sizeof(int) * (nw + 2));
+      sh.wave_rows.ensure(sizeof(int) * std::max(sh.r_hi - sh.r_lo, 1));
+      launch_bucket_rows(l.wave_of.as<int>(), sh.r_hi - sh.r_lo, 0, sh.wave_counts.as<int>(), sh.wave_starts.as<int>(),
+                         sh.wave_cursor.as<int>(), sh.wave_rows.as<int>(), nw, tmp.as<int>(), st, sh.r_lo);
+      sh.wave_start.resize(nw + 1);
+      HOT_CUDA(cudaMemcpyAsync(sh.wave_start.data(), sh.wave_starts.p, sizeof(int) * (nw + 1), cudaMemcpyDeviceToHost,
+                               st));
+    }
     HOT_CUDA(cudaStreamSynchronize(st));
+    if (m == 0 && sh.on) sh.wave_counts_global = counts;
     std::vector<int> starts;
     int acc = 0;
     l.max_wave = 0;
@@ -804,14 +968,36 @@ struct Context {
   void build_values(int built) {
     const int h = prof_begin(P_HIER);
     HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 12, 0, sizeof(int), stream));
-    launch_level_dinv(L[0].view(), iflags.as<int>() + 12, stream);
+    LevelView v0 = L[0].view();
+    if (sh.on) {  // D^-1 of this slab's rows (the only level-0 rows it smooths)
+      v0.lo = sh.r_lo;
+      v0.hi = sh.r_hi;
+    }
+    launch_level_dinv(v0, iflags.as<int>() + 12, stream);
     nlevels = 1;
     for (int m = 1; m < built; ++m) {
       Level& f = L[m - 1];
       Level& c = L[m];
       const int span = f.radius + 3;  // quadratic X targets per axis
       gal_x.ensure(sizeof(double) * 9 * (c.radius == 3 ? span * span * span : 64) * std::max(f.n, 1));
-      launch_galerkin(f.view(), c.view(), gal_x.as<double>(), stream);
+      if (m == 1 && sh.on) {
+        // this slab's level-1 rows (and the 2 coarse planes whose transposes complete them), then
+        // every rank's rows to every rank: levels >= 1 are replicated
+        plan_shard_coarse();
+        LevelView fv = f.view(), cv = c.view();
+        fv.lo = sh.x_lo;
+        fv.hi = sh.r_hi;
+        cv.lo = sh.gc_lo;
+        cv.hi = sh.c_hi;
+        launch_galerkin(fv, cv, gal_x.as<double>(), stream);
+        const int hc = prof_begin(P_COMM);
+        std::vector<long long> off(sh.crow_off.size());
+        for (size_t r = 0; r < off.size(); ++r) off[r] = sh.crow_off[r] * 9LL * c.pitch() * (long long)sizeof(double);
+        comm->allgather_ranges(c.H.p, off, stream);
+        prof_end(hc, (double)off.back());
+      } else {
+        launch_galerkin(f.view(), c.view(), gal_x.as<double>(), stream);
+      }
       launch_level_dinv(c.view(), iflags.as<int>() + 12, stream);
       nlevels = m + 1;
     }
@@ -827,6 +1013,13 @@ struct Context {
     prof_end(h);
     sync();
     check_launch();
+    if (sh.on) {  // flags of sharded kernels: every rank takes the same branch
+      int fl[2] = {singular, 0};
+      HOT_CUDA(cudaMemcpy(&fl[1], flag_bad(), sizeof(int), cudaMemcpyDeviceToHost));
+      comm->allreduce_max(fl, 2, stream);
+      singular = fl[0];
+      HOT_CUDA(cudaMemcpy(flag_bad(), &fl[1], sizeof(int), cudaMemcpyHostToDevice));
+    }
     if (singular) throw std::logic_error("multigrid: singular diagonal block");
   }
 
@@ -918,11 +1111,22 @@ struct Context {
     for (int m = 0; m < M - 1; ++m) {
       Level& l = L[m];
       HOT_CUDA(cudaMemsetAsync(l.u.p, 0, sizeof(double) * 3 * l.n, stream));
-      sgs(m, l.u.as<double>(), l.b.as<double>());
+      const bool slab = m == 0 && sh.on;
+      if (slab)
+        sgs0_sharded(l.u.as<double>(), l.b.as<double>());
+      else
+        sgs(m, l.u.as<double>(), l.b.as<double>());
       // residual r = b - H u: the level's block-sparse SpMV (H, column ids, u b r)
       const int hs = prof_begin(m == 0 ? P_SPMV0 : P_RESID);
-      launch_residual(l.view(), l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
-      prof_end(hs, 72.0 * l.active_slots + 4.0 * l.pitch() * l.n + 72.0 * l.n);
+      LevelView lv = l.view();
+      if (slab) {
+        lv.lo = sh.r_lo;
+        lv.hi = sh.r_hi;
+      }
+      launch_residual(lv, l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
+      const double frac = slab && l.n ? (double)(sh.r_hi - sh.r_lo) / l.n : 1.0;
+      prof_end(hs, frac * (72.0 * l.active_slots + 4.0 * l.pitch() * l.n + 72.0 * l.n));
+      if (slab) gather_rows0(l.r.p);  // restriction (replicated) reads every fine row
       const int h = prof_begin(P_RESID);
       launch_restrict(l.view(), L[m + 1].view(), l.r.as<double>(), L[m + 1].b.as<double>(), stream);
       prof_end(h, 24.0 * l.n + 24.0 * L[m + 1].n);  // r in, coarse b out
@@ -944,8 +1148,12 @@ struct Context {
       const int h = prof_begin(P_PROLONG);
       launch_prolong_add(l.view(), L[m + 1].view(), L[m + 1].u.as<double>(), l.u.as<double>(), stream);
       prof_end(h, 24.0 * L[m + 1].n + 48.0 * l.n);
-      sgs(m, l.u.as<double>(), l.b.as<double>());
+      if (m == 0 && sh.on)
+        sgs0_sharded(l.u.as<double>(), l.b.as<double>());
+      else
+        sgs(m, l.u.as<double>(), l.b.as<double>());
     }
+    if (sh.on && M > 1) gather_rows0(L[0].u.p);
     HOT_CUDA(cudaMemcpyAsync(out, L[0].u.p, sizeof(double) * 3 * L[0].n, cudaMemcpyDeviceToDevice, stream));
     check_launch();
   }
@@ -1035,6 +1243,7 @@ struct Context {
     const int n = L[0].n;
     const long long n3 = 3LL * n;
     SolveOut out;
+    sh.last = false;
     if (cfg.window > kMaxWindow) throw std::invalid_argument("L-BFGS window too large");
     const double target = cfg.epsilon * std::sqrt((double)n);
     HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
@@ -1049,6 +1258,13 @@ struct Context {
       out.converged = true;
       return out;
     }
+    struct ShardOff {  // the cut is per solve; taps and the other solvers run unsharded
+      Shard& s;
+      ~ShardOff() { s.on = false; }
+    } shard_off{sh};
+    sh.on = want_shard(levels) && plan_shard();
+    sh.last = sh.on;
+    if (sh.on) ++sh.solves;
     assemble_and_build_hierarchy(dv.as<double>(), levels, cfg.embedding, /*reuse_svd=*/true);
     static const bool verbose = std::getenv("HOT_VERBOSE") != nullptr;
     if (prof || verbose)  // active-slot counts only feed the profile's algorithmic bytes
@@ -1758,6 +1974,57 @@ int hot_profile_read(hot_ctx* ctx, char* names, double* total_ms, long long* lau
 long long hot_kernel_launches(hot_ctx* ctx) {
   (void)ctx;
   return hotb200::kernel_launch_count();
+}
+
+int hot_set_comm_host(hot_ctx* ctx, const hot_comm_host* ops) {
+  if (!ctx) return HOT_E_INVALID_ARGUMENT;
+  return guard(ctx, [&] {
+    if (!ops) {
+      ctx->c.comm.reset();
+      return;
+    }
+    ctx->c.comm.reset(hotb200::make_host_comm(*ops));
+  });
+}
+
+int hot_nccl_unique_id(unsigned char id[128]) {
+  if (!id) return HOT_E_INVALID_ARGUMENT;
+  return guard(nullptr, [&] { hotb200::nccl_unique_id(id); });
+}
+
+int hot_set_comm_nccl(hot_ctx* ctx, const unsigned char id[128], int rank, int size) {
+  if (!ctx || !id) return HOT_E_INVALID_ARGUMENT;
+  return guard(ctx, [&] {
+    HOT_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.comm.reset(hotb200::make_nccl_comm(id, rank, size));
+  });
+}
+
+int hot_shard_info(hot_ctx* ctx, hot_shard_info_t* out) {
+  if (!ctx || !out) return HOT_E_INVALID_ARGUMENT;
+  const Context& c = ctx->c;
+  *out = hot_shard_info_t{};
+  out->rank = c.comm ? c.comm->rank : 0;
+  out->size = c.comm ? c.comm->size : 1;
+  out->sharded = c.sh.last ? 1 : 0;
+  out->plane_lo = c.sh.P;
+  out->plane_hi = c.sh.Q;
+  out->row_lo = c.sh.r_lo;
+  out->row_hi = c.sh.r_hi;
+  out->crow_lo = c.sh.c_lo;
+  out->crow_hi = c.sh.c_hi;
+  out->asm_lo = c.sh.a_lo;
+  out->asm_hi = c.sh.r_hi;
+  out->halo_exchanges = c.comm ? c.comm->halos : 0;
+  out->gathers = c.comm ? c.comm->gathers : 0;
+  return HOT_OK;
+}
+
+int hot_plan_slabs(int plane_lo, int nplanes, const long long* weight, int size, int align, int min_width,
+                   int* bounds) {
+  if (!bounds) return HOT_E_INVALID_ARGUMENT;
+  return hotb200::plan_slabs(plane_lo, nplanes, weight, size, align, min_width, bounds) ? HOT_OK
+                                                                                      : HOT_E_INVALID_ARGUMENT;
 }
 
 }  // extern "C"

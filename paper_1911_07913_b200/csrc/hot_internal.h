@@ -44,6 +44,8 @@ struct LevelView {
   double* dinv;       // 9*n row-major
   const uint8_t* dir;
   int radius;         // diagonal-storage radius R
+  int lo, hi;         // row range [lo, hi) the range-aware kernels compute (assembly, Galerkin,
+                      // D^-1, SpMV / residual); [0, n) except in the slab-sharded solve
 };
 
 __host__ __device__ constexpr int level_slots(int radius) { return (2 * radius + 1) * (2 * radius + 1) * (2 * radius + 1); }
@@ -143,7 +145,7 @@ void launch_final_velocity(GridView g, const double* dv, double* out, cudaStream
 // ---------------------------------------------------------------- assembly (k_assembly.cu)
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
                              const double* u, const double* svd_in, int project, double* Tu, int* bad_flag,
-                             cudaStream_t s);
+                             cudaStream_t s, long long plo = 0, long long phi = -1);  // particles [plo, phi)
 void launch_fill_cols(LevelView L, cudaStream_t s);
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, unsigned int* row_counter, cudaStream_t s);
@@ -159,7 +161,10 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
 void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s);
 void launch_level_waves(LevelView L, int coarse, int modulus, const int* off, int* wave_of, cudaStream_t s);
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
-                        int nwaves, int* scan_tmp, cudaStream_t s);
+                        int nwaves, int* scan_tmp, cudaStream_t s, int row_base = 0);  // rows [row_base, +n)
+void launch_plane_starts(const int* coords, int n, int lo0, int nplanes, int* out, cudaStream_t s);
+/// One level-0 smoother wave (k_sgs_wave) over the given rows.
+void launch_sgs_wave1(LevelView L, const int* rows, int cnt, double* u, const double* b, cudaStream_t s);
 void launch_spmv(LevelView L, const double* x, double* y, cudaStream_t s);
 void launch_residual(LevelView L, const double* b, const double* u, double* r, cudaStream_t s);
 void launch_restrict(LevelView fine, LevelView coarse, const double* rf, double* bc, cudaStream_t s);

@@ -41,14 +41,15 @@ __global__ void __launch_bounds__(kTWarps * 32) k_particle_tensors(ParticlesView
                                                                    const DevMaterial* __restrict__ mats,
                                                                    const double* __restrict__ u,
                                                                    const double* __restrict__ svd_in, int project,
-                                                                   double* __restrict__ Tu, int* bad) {
+                                                                   double* __restrict__ Tu, int* bad, long long plo,
+                                                                   long long phi) {
   __shared__ double stage[kTWarps][32][kTPacked];
   const long long n = P.n;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const long long nchunks = (n + 31) / 32;
+  const long long nchunks = (phi - plo + 31) / 32;
   for (long long ch = blockIdx.x * (long long)kTWarps + wib; ch < nchunks; ch += (long long)gridDim.x * kTWarps) {
-    const long long p = ch * 32 + lane;
-    if (p < n) {
+    const long long p = plo + ch * 32 + lane;
+    if (p < phi) {
       const int mat = __ldg(P.mat + p);
       const double vol = __ldg(P.vol + p);
       M3 U, V, Fn;
@@ -77,9 +78,9 @@ __global__ void __launch_bounds__(kTWarps * 32) k_particle_tensors(ParticlesView
       }
     }
     __syncwarp();
-    const int cnt = (int)min(32LL, n - ch * 32);
+    const int cnt = (int)min(32LL, phi - plo - ch * 32);
     for (int t = 0; t < cnt; ++t) {
-      double* out = Tu + (ch * 32 + t) * kTensorStride + kRecT;
+      double* out = Tu + (plo + ch * 32 + t) * kTensorStride + kRecT;
       out[lane] = stage[wib][t][lane];
       if (lane < kTPacked - 32) out[32 + lane] = stage[wib][t][32 + lane];
     }
@@ -91,14 +92,15 @@ __global__ void __launch_bounds__(kTWarps * 32) k_particle_tensors(ParticlesView
 /// objective.hpp:337-339); nodes with zero weight get W = 0, which is how the reference skips
 /// them (transfer.hpp:36-37).  A separate light kernel (the T kernel is register bound).
 constexpr int kWWarps = 4;
-__global__ void __launch_bounds__(kWWarps * 32) k_particle_W(ParticlesView P, double dx, double* __restrict__ Tu) {
+__global__ void __launch_bounds__(kWWarps * 32) k_particle_W(ParticlesView P, double dx, double* __restrict__ Tu, long long plo,
+                                                             long long phi) {
   __shared__ double stage[kWWarps][32][27 + 1];  // one x-plane (9 positions) of the warp's 32 records
   const long long n = P.n;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const long long nchunks = (n + 31) / 32;
+  const long long nchunks = (phi - plo + 31) / 32;
   for (long long ch = blockIdx.x * (long long)kWWarps + wib; ch < nchunks; ch += (long long)gridDim.x * kWWarps) {
-    const long long p = ch * 32 + lane;
-    const bool live = p < n;
+    const long long p = plo + ch * 32 + lane;
+    const bool live = p < phi;
     double Fn[9];
     Axis3 ax[3];
     if (live) {
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_particle_W(ParticlesView P, do
         axis_dw_over_dx(ax[a], dx);
       }
     }
-    const int cnt = (int)min(32LL, n - ch * 32);
+    const int cnt = (int)min(32LL, phi - plo - ch * 32);
 #pragma unroll 1
     for (int k0 = 0; k0 < 3; ++k0) {
       if (live) {
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_particle_W(ParticlesView P, do
       }
       __syncwarp();
       for (int t = 0; t < cnt; ++t)
-        if (lane < 27) Tu[(ch * 32 + t) * kTensorStride + kRecW + 27 * k0 + lane] = stage[wib][t][lane];
+        if (lane < 27) Tu[(plo + ch * 32 + t) * kTensorStride + kRecW + 27 * k0 + lane] = stage[wib][t][lane];
       __syncwarp();
     }
   }
@@ -293,12 +295,12 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
   // rows are handed out in index order (a work counter, or a static stride without one), so the
   // rows in flight stay a narrow band and their particle bins stay in L2
   auto next_row = [&](int cur) {
-    if (!row_counter) return cur < 0 ? (int)(blockIdx.x * kAsmWarps + wid) : cur + nwarps;
+    if (!row_counter) return cur < 0 ? (int)(L.lo + blockIdx.x * kAsmWarps + wid) : cur + nwarps;
     int r = 0;
     if (lane == 0) r = (int)atomicAdd(row_counter, 1u);
-    return __shfl_sync(0xffffffffu, r, 0);
+    return L.lo + __shfl_sync(0xffffffffu, r, 0);
   };
-  for (int i = next_row(-1); i < L.n; i = next_row(i)) {
+  for (int i = next_row(-1); i < L.hi; i = next_row(i)) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
     // the write-out's column ids and Dirichlet flags, loaded now so their latency hides under
     // the gather: slot s = lane + 32 j (zero fill), upper slot 62 + lane + 32 j
@@ -476,13 +478,14 @@ int agrid(long long n, int threads) {
 
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
                              const double* u, const double* svd_in, int project, double* Tu, int* bad_flag,
-                             cudaStream_t s) {
-  if (P.n == 0) return;
-  const long long chunks = (P.n + 31) / 32;
+                             cudaStream_t s, long long plo, long long phi) {
+  if (phi < 0) phi = P.n;
+  if (phi <= plo) return;
+  const long long chunks = (phi - plo + 31) / 32;
   k_particle_tensors<<<(int)std::min<long long>((chunks + kTWarps - 1) / kTWarps, 16LL * num_sms()), kTWarps * 32, 0,
-                       s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag);
+                       s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi);
   k_particle_W<<<(int)std::min<long long>((chunks + kWWarps - 1) / kWWarps, 32LL * num_sms()), kWWarps * 32, 0, s>>>(
-      P, dx, Tu);
+      P, dx, Tu, plo, phi);
   count_launches(2);
 }
 
@@ -493,7 +496,7 @@ void launch_fill_cols(LevelView L, cudaStream_t s) {
 
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, unsigned int* row_counter, cudaStream_t s) {
-  if (L.n == 0) return;
+  if (L.hi <= L.lo) return;
   (void)dx;
   static const int resident = resident_blocks((const void*)k_assemble_rows, kAsmWarps * 32, kAsmSmem);
   static const bool dynamic = [] {
@@ -508,7 +511,7 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
     row_counter = nullptr;
     blocks = (long long)num_sms() * 16;
   }
-  blocks = std::min<long long>(blocks, (L.n + kAsmWarps - 1) / kAsmWarps);
+  blocks = std::min<long long>(blocks, ((long long)(L.hi - L.lo) + kAsmWarps - 1) / kAsmWarps);
   k_assemble_rows<<<(int)blocks, kAsmWarps * 32, kAsmSmem, s>>>(bins, g, L, Tu, row_counter);
   count_launches(1);
 }

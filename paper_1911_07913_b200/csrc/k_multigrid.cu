@@ -139,10 +139,10 @@ __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, dou
   };
   if (lane == 0)
     for (int s = 0; s < kGalXStages; ++s)
-      if (gw + s * nw < f.n) issue(gw + s * nw, s);
+      if (f.lo + gw + s * nw < f.hi) issue(f.lo + gw + s * nw, s);
   unsigned phase_bits = 0;
   int s = 0;
-  for (int i = gw; i < f.n; i += nw) {
+  for (int i = f.lo + gw; i < f.hi; i += nw) {
     mbar_wait(smem_u32(mb + s), (phase_bits >> s) & 1u);
     phase_bits ^= 1u << s;
     const double* H = reinterpret_cast<const double*>(ring + (size_t)s * kGalXRowBytes);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, dou
       for (int k = 0; k < 9; ++k) dst[k] = acc[k];
     }
     __syncwarp();  // the stage is refilled below
-    if (lane == 0 && i + kGalXStages * nw < f.n) issue(i + kGalXStages * nw, s);
+    if (lane == 0 && i + kGalXStages * nw < f.hi) issue(i + kGalXStages * nw, s);
     s = s + 1 == kGalXStages ? 0 : s + 1;
   }
 }
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin_c(LevelView f, LevelVie
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int A = gw; A < c.n; A += nw) {
+  for (int A = c.lo + gw; A < c.hi; A += nw) {
     const int A0 = c.coords[3 * A], A1 = c.coords[3 * A + 1], A2 = c.coords[3 * A + 2];
     const bool dA = c.dir[A] != 0;
     // children of A (fine nodes 2A + d) and their X base offsets
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin_qc(LevelView f, LevelVi
 
 /// Level diagonal inverse (multigrid.hpp:233-240) with the singular-block check.
 __global__ void k_level_dinv(LevelView L, int* singular) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += gridDim.x * blockDim.x) {
+  for (int i = L.lo + blockIdx.x * blockDim.x + threadIdx.x; i < L.hi; i += gridDim.x * blockDim.x) {
     M3 D;
 #pragma unroll
     for (int k = 0; k < 9; ++k)
@@ -420,9 +420,23 @@ __global__ void k_wave_count(const int* __restrict__ wave_of, int n, int wmin, i
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     atomicAdd(counts + (wave_of[i] - wmin), 1);
 }
-__global__ void k_wave_scatter(const int* __restrict__ wave_of, int n, int wmin, int* cursor, int* rows) {
+__global__ void k_wave_scatter(const int* __restrict__ wave_of, int n, int wmin, int* cursor, int* rows, int base) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    rows[atomicAdd(cursor + (wave_of[i] - wmin), 1)] = i;
+    rows[atomicAdd(cursor + (wave_of[i] - wmin), 1)] = base + i;
+}
+
+/// out[p] = first row whose axis-0 coordinate is >= lo0 + p (p = 0..nplanes): the rows are in
+/// lexicographic order, axis 0 most significant (common.hpp:41), so a plane range is a row range.
+__global__ void k_plane_starts(const int* __restrict__ coords, int n, int lo0, int nplanes, int* __restrict__ out) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p <= nplanes; p += gridDim.x * blockDim.x) {
+    int a = 0, b = n;
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (coords[3 * m] < lo0 + p) a = m + 1;
+      else b = m;
+    }
+    out[p] = a;
+  }
 }
 
 /// y_i (3) = sum_s H(i,s) x_col (objective.hpp:66-77), one warp per row.  All column ids and
@@ -467,7 +481,7 @@ __global__ void __launch_bounds__(kMgThreads) k_spmv(LevelView L, const double* 
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = gw; i < L.n; i += nw) {
+  for (int i = L.lo + gw; i < L.hi; i += nw) {
     double y0, y1, y2;
     row_product<R>(L, i, x, lane, y0, y1, y2, false);
     if (lane == 0) {
@@ -1184,40 +1198,53 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
   }
   static const int gx_blocks = coop_blocks((const void*)k_galerkin_x, kGalXWarps * 32, kGalXSmem);
   {
-    const int blocks = (int)std::min<long long>(gx_blocks, ((long long)fine.n + kGalXWarps - 1) / kGalXWarps);
+    const int blocks = (int)std::min<long long>(gx_blocks, ((long long)(fine.hi - fine.lo) + kGalXWarps - 1) / kGalXWarps);
     k_galerkin_x<<<std::max(1, blocks), kGalXWarps * 32, kGalXSmem, s>>>(fine, X);
     count_launches(1);
   }
-  { k_galerkin_c<<<mgrid((long long)coarse.n * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X); count_launches(1); }
+  if (coarse.hi > coarse.lo) {
+    k_galerkin_c<<<mgrid((long long)(coarse.hi - coarse.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X);
+    count_launches(1);
+  }
 }
 void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s) {
-  if (L.n) { k_level_dinv<<<mgrid(L.n, 256), 256, 0, s>>>(L, singular_flag); count_launches(1); }
+  if (L.hi > L.lo) { k_level_dinv<<<mgrid(L.hi - L.lo, 256), 256, 0, s>>>(L, singular_flag); count_launches(1); }
 }
 void launch_level_waves(LevelView L, int coarse, int modulus, const int* off, int* wave_of, cudaStream_t s) {
   if (L.n) { k_level_waves<<<mgrid(L.n, 256), 256, 0, s>>>(L, coarse, modulus, off[0], off[1], off[2], wave_of); count_launches(1); }
 }
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
-                        int nwaves, int* scan_tmp, cudaStream_t s) {
+                        int nwaves, int* scan_tmp, cudaStream_t s, int row_base) {
+  wave_of += row_base;
   cudaMemsetAsync(counts, 0, sizeof(int) * (nwaves + 1), s);
   if (n) { k_wave_count<<<mgrid(n, 256), 256, 0, s>>>(wave_of, n, wmin, counts); count_launches(1); }
   launch_exclusive_scan(counts, start, nwaves + 1, scan_tmp, nullptr, s);
   cudaMemcpyAsync(cursor, start, sizeof(int) * nwaves, cudaMemcpyDeviceToDevice, s);
-  if (n) { k_wave_scatter<<<mgrid(n, 256), 256, 0, s>>>(wave_of, n, wmin, cursor, rows); count_launches(1); }
+  if (n) { k_wave_scatter<<<mgrid(n, 256), 256, 0, s>>>(wave_of, n, wmin, cursor, rows, row_base); count_launches(1); }
+}
+void launch_plane_starts(const int* coords, int n, int lo0, int nplanes, int* out, cudaStream_t s) {
+  k_plane_starts<<<mgrid(nplanes + 1, 128), 128, 0, s>>>(coords, n, lo0, nplanes, out);
+  count_launches(1);
+}
+void launch_sgs_wave1(LevelView L, const int* rows, int cnt, double* u, const double* b, cudaStream_t s) {
+  if (cnt <= 0) return;
+  k_sgs_wave<<<(cnt + kWaveThreads / 32 - 1) / (kWaveThreads / 32), kWaveThreads, 0, s>>>(L, rows, cnt, u, b, 0);
+  count_launches(1);
 }
 void launch_spmv(LevelView L, const double* x, double* y, cudaStream_t s) {
-  if (!L.n) return;
+  if (L.hi <= L.lo) return;
   if (L.radius == 2)
-    k_spmv<2><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr);
+    k_spmv<2><<<mgrid((long long)(L.hi - L.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr);
   else
-    k_spmv<3><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr);
+    k_spmv<3><<<mgrid((long long)(L.hi - L.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(L, x, y, nullptr);
   count_launches(1);
 }
 void launch_residual(LevelView L, const double* b, const double* u, double* r, cudaStream_t s) {
-  if (!L.n) return;
+  if (L.hi <= L.lo) return;
   if (L.radius == 2)
-    k_spmv<2><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b);
+    k_spmv<2><<<mgrid((long long)(L.hi - L.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b);
   else
-    k_spmv<3><<<mgrid((long long)L.n * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b);
+    k_spmv<3><<<mgrid((long long)(L.hi - L.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(L, u, r, b);
   count_launches(1);
 }
 void launch_restrict(LevelView fine, LevelView coarse, const double* rf, double* bc, cudaStream_t s) {

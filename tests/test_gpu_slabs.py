@@ -1,0 +1,91 @@
+"""Slab-sharded step on the GPU: `size` ranks, each a process with
+its own context, joined by the host-staged transport over gloo.  The ranks share the one GPU
+of the test box; no kernel waits on another rank (every exchange is a host-side collective
+between launches), so the ranks need not be co-scheduled.
+
+The bar is stronger than the oracle's 1e-6: every row is computed with the single-GPU
+arithmetic in the single-GPU order and the replicated scalars are reduced identically, so the
+sharded step must equal the single-GPU step BITWISE, and therefore the oracle as closely as the
+single-GPU step does (tests/test_gpu_parity.py)."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "slab_worker.py")
+SCENES = os.path.join(ROOT, "scenes")
+
+pytestmark = pytest.mark.gpu
+
+# The slabs smooth level 0 with one launch per colour wave (k_sgs_wave).  On small grids the
+# single-GPU default is the dataflow kernel, whose per-row reduction tree differs (rounding
+# only); HOT_SGS_STREAM_MIN=0 selects the streaming wave kernel there, as on every grid with
+# >= 8K rows per wave (cfg2 and up), and that kernel is bitwise equal to k_sgs_wave
+# (test_vcycle_streaming_wave_schedule).  Same setting for every run, single or sharded.
+ENV = dict(os.environ, HOT_SGS_STREAM_MIN="0")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run_ranks(tmp_path, scene, size, steps, levels=None, tag="r"):
+    port = _free_port()
+    procs, outs = [], []
+    for r in range(size):
+        out = str(tmp_path / f"{tag}{size}_{r}.npz")
+        args = [sys.executable, WORKER, str(r), str(size), str(port), os.path.join(SCENES, scene), str(steps), out,
+                "host"] + ([str(levels)] if levels is not None else [])
+        procs.append(subprocess.Popen(args, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, env=ENV))
+        outs.append(out)
+    logs = []
+    for p in procs:
+        try:
+            o, _ = p.communicate(timeout=600)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+        logs.append(o)
+    for p, o in zip(procs, logs):
+        assert p.returncode == 0, o[-4000:]
+    return [dict(np.load(o)) for o in outs]
+
+
+@pytest.mark.parametrize("scene,steps", [("cfg1_stretched.json", 3), ("cfg1_drop.json", 3)])
+@pytest.mark.parametrize("size", [2, 3])
+def test_sharded_steps_equal_single_gpu_bitwise(tmp_path, scene, steps, size):
+    ref = run_ranks(tmp_path, scene, 1, steps, tag="single")[0]
+    ranks = run_ranks(tmp_path, scene, size, steps)
+    iters = ref["stats"][:, 1]
+    assert iters.sum() > 0, "the scene must exercise the solve"
+    for r, res in enumerate(ranks):
+        solved = iters > 0
+        assert (res["sharded"][solved] == 1).all(), (r, res["sharded"])
+        assert res["halos"] > 0 and res["gathers"] > 0
+        np.testing.assert_array_equal(res["stats"], ref["stats"])
+        for k in ("x", "v", "F", "C", "energy", "residual"):
+            np.testing.assert_array_equal(res[k], ref[k], err_msg=f"rank {r} {k}")
+    # the slabs tile the rows: contiguous, disjoint, covering [0, n)
+    last = ranks[0]["rows"][-1]
+    for r in range(1, size):
+        cur = ranks[r]["rows"][-1]
+        assert cur[0] == last[1] and cur[2] == last[3] and cur[4] == last[5]
+        last = cur
+    assert ranks[0]["rows"][-1][0] == 0 and ranks[-1]["rows"][-1][1] == ref["stats"][-1][3]
+
+
+def test_sharded_two_level_hierarchy(tmp_path):
+    """levels = 2: the coarse level that is replicated is also the coarsest (PCG) level."""
+    ref = run_ranks(tmp_path, "cfg1_stretched.json", 1, 2, levels=2, tag="single")[0]
+    ranks = run_ranks(tmp_path, "cfg1_stretched.json", 2, 2, levels=2)
+    for res in ranks:
+        assert res["sharded"].any()
+        for k in ("x", "v", "F", "C"):
+            np.testing.assert_array_equal(res[k], ref[k])
