@@ -213,6 +213,8 @@ struct Context {
     int a_lo = 0;                  // assembled level-0 rows [a_lo, r_hi): owned + 7 planes to the left
     int x_lo = 0;                  // Galerkin stage-1 fine rows [x_lo, r_hi): owned + 5 planes
     long long p_lo = 0, p_hi = 0;  // particles of the bins the assembled rows read (planes [P-8, Q+1))
+    long long pe_lo = 0;           // particles of the bins the gradient's node pass reads: [pe_lo, p_hi)
+    int b_lo = 0, b_hi = 0;        // those bins (rows of planes [P-1, Q+1))
     int c_lo = 0, c_hi = 0;        // owned level-1 rows (coarse planes [P/2, Q/2))
     int gc_lo = 0;                 // Galerkin stage-2 coarse rows [gc_lo, c_hi): owned + 2 coarse planes
     std::vector<int> bounds;       // size+1 plane cuts
@@ -227,6 +229,7 @@ struct Context {
     bool last = false;             // the last solve ran sharded
   } sh;
   DBuf plane_buf;
+  DBuf pe_buf, ne_buf, nt_buf;  // per-particle energy, per-node energy, per-node scaled-norm terms
 
   // profiling
   bool prof = false;
@@ -317,6 +320,9 @@ struct Context {
     if (ni) HOT_CUDA(cudaMemcpyAsync(host_int, iflags.p, sizeof(int) * ni, cudaMemcpyDeviceToHost, stream));
     sync();
     check_launch();
+    // slabs: the flags of split kernels differ per rank; every rank must take the same branch
+    // (the other ints are replicated, so their max is their value)
+    if (sh.on && ni) comm->allreduce_max(host_int, ni, stream);
   }
 
   void init(int dev) {
@@ -693,17 +699,20 @@ struct Context {
     // (particle tensors) from plane P-8 on.
     sh.a_lo = row_of(sh.P - 7);
     sh.x_lo = row_of(sh.P - 5);
-    const int prow[2] = {row_of(sh.P - 8), row_of(sh.Q + 1)};
-    int pb[2] = {0, 0};
-    for (int k = 0; k < 2; ++k)
+    sh.b_lo = row_of(sh.P - 1);
+    sh.b_hi = row_of(sh.Q + 1);
+    const int prow[3] = {row_of(sh.P - 8), sh.b_hi, sh.b_lo};
+    int pb[3] = {0, 0, 0};
+    for (int k = 0; k < 3; ++k)
       HOT_CUDA(cudaMemcpyAsync(&pb[k], bin_start.as<int>() + prow[k], sizeof(int), cudaMemcpyDeviceToHost, stream));
     sync();
     sh.p_lo = pb[0];
     sh.p_hi = pb[1];
+    sh.pe_lo = pb[2];
     sh.row_off.assign(R + 1, 0);
     for (int r = 0; r <= R; ++r) sh.row_off[r] = row_of(sh.bounds[r]);
-    // halo after a wave of colour c: only the rows of the edge plane with axis-0 residue c / 9
-    // changed; each side sends that one plane (or nothing)
+    // halo after the waves of residue group m (colours 9m .. 9m+8, sgs0_sharded): only the edge
+    // plane with axis-0 residue m changed; each side sends that one plane (or nothing)
     auto md3 = [](int v) { return ((v % 3) + 3) % 3; };
     for (int m = 0; m < 3; ++m) {
       std::vector<long long>& e = sh.halo_edges[m];
@@ -737,33 +746,54 @@ struct Context {
     sh.gc_lo = me == 0 ? 0 : crow(sh.bounds[me] / 2 - 2);
   }
 
-  /// Rows [row_off[r], row_off[r+1]) of a level-0 node vector from their owners to every rank.
-  void gather_rows0(void* vec) {
+  /// Rows [row_off[r], row_off[r+1]) of a level-0 node array (`bytes` per row) from their
+  /// owners to every rank.
+  void gather_rows0(void* vec, int bytes = 24) {
     const int h = prof_begin(P_COMM);
     std::vector<long long> off(sh.row_off.size());
-    for (size_t r = 0; r < off.size(); ++r) off[r] = 24LL * sh.row_off[r];
+    for (size_t r = 0; r < off.size(); ++r) off[r] = (long long)bytes * sh.row_off[r];
     comm->allgather_ranges(vec, off, stream);
     prof_end(h, (double)off.back());
   }
 
   /// smooth_sgs on level 0 (multigrid.hpp:298-316) over this rank's rows: the 27 colour waves
-  /// forward then backward, exactly the single-GPU schedule; after each wave the changed edge
-  /// plane goes to the neighbour, so every row reads the values the serial sweep reads.
+  /// forward then backward, exactly the single-GPU schedule.  Colour c = 9 (x mod 3) + ... :
+  /// waves 9m .. 9m+8 update only the planes x = m (mod 3), and a row reads its own plane and
+  /// the planes within 2 of it, which have other residues and stay fixed during the group.
+  /// So a plane's values are final at the end of its residue group, and one halo per group
+  /// (the edge plane of that residue, to each neighbour) gives every row exactly the values the
+  /// serial sweep reads: 6 exchanges per smoother call instead of 54.
   void sgs0_sharded(double* u, const double* b) {
     const Level& l = L[0];
     const LevelView v = l.view();
     for (int pass = 0; pass < 2; ++pass)
-      for (int k = 0; k < 27; ++k) {
-        const int c = pass == 0 ? k : 26 - k;
-        if (sh.wave_counts_global[c] == 0) continue;  // replicated: every rank skips the same waves
+      for (int gi = 0; gi < 3; ++gi) {
+        const int grp = pass == 0 ? gi : 2 - gi;
         const int h = prof_begin(P_SGS0);
-        launch_sgs_wave1(v, sh.wave_rows.as<int>() + sh.wave_start[c], sh.wave_start[c + 1] - sh.wave_start[c], u, b,
-                         stream);
-        prof_end(h, (double)(sh.wave_start[c + 1] - sh.wave_start[c]) * (72.0 * 125 + 72 + 24 + 48));
-        const std::vector<long long>& e = sh.halo_edges[c / 9];
+        long long rows = 0;
+        int big = 0;
+        for (int c = 9 * grp; c < 9 * grp + 9; ++c) {
+          rows += sh.wave_start[c + 1] - sh.wave_start[c];
+          big = std::max(big, sh.wave_start[c + 1] - sh.wave_start[c]);
+        }
+        // the group's 9 waves in one persistent bulk-copy launch (grid barrier between waves,
+        // ~2 us) unless they are tiny (then one launch per wave)
+        if (big >= std::min(512, stream_min_rows())) {
+          const int q0 = pass == 0 ? 9 * grp : 45 - 9 * grp;
+          launch_sgs_stream(v, sh.wave_starts.as<int>(), sh.wave_rows.as<int>(), 27, u, b, grid_bar.as<unsigned int>(),
+                            stream, q0, q0 + 9);
+        } else {
+          for (int k = 0; k < 9; ++k) {
+            const int c = 9 * grp + (pass == 0 ? k : 8 - k);
+            const int cnt = sh.wave_start[c + 1] - sh.wave_start[c];
+            launch_sgs_wave1(v, sh.wave_rows.as<int>() + sh.wave_start[c], cnt, u, b, stream);
+          }
+        }
+        prof_end(h, (double)rows * (72.0 * 125 + 72 + 24 + 48));
+        const std::vector<long long>& e = sh.halo_edges[grp];
         bool any = false;
         for (long long x : e) any |= x != 0;
-        if (any) {
+        if (any) {  // replicated: every rank makes the same decision
           const int hc = prof_begin(P_COMM);
           comm->halo(u, e, stream);
           prof_end(hc);
@@ -774,29 +804,61 @@ struct Context {
   // ------------------------------------------------------------------ objective
   int* flag_bad() { return iflags.as<int>() + 0; }
 
-  /// E(dv + alpha p) with stress stored for the gradient; returns through scal[0].
+  /// E(dv + alpha p) with stress stored for the gradient; returns through scal[0].  Per-particle
+  /// energies, per-node totals (bin + node terms), then a fixed-tree sum over the nodes: the
+  /// value does not depend on the slab cut.  Slabs: the particles of bins [P-1, Q+1) (the
+  /// gradient's stress), or [P-8, Q+1) when the SVD cache feeds the assembly; the node totals of
+  /// the slab's rows, gathered.
   void energy_async(const double* dvp, const double* p, double alpha, bool want_stress, bool store_svd = false) {
     int h = prof_begin(P_ENERGY);
     double* part = partials.as<double>();
-    node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
+    const int n = L[0].n;
+    node_u.ensure(sizeof(double) * 3 * std::max(n, 1));
+    pe_buf.ensure(sizeof(double) * std::max<long long>(np, 1));
+    ne_buf.ensure(sizeof(double) * std::max(n, 1));
     launch_node_u(gview(), dvp, p, alpha, node_u.as<double>(), stream);
     if (store_svd) svd.ensure(sizeof(double) * 21 * std::max<long long>(np, 1));
+    long long plo = 0, phi = -1;
+    int lo = 0, hi = n;
+    if (sh.on) {
+      plo = store_svd ? sh.p_lo : sh.pe_lo;
+      phi = sh.p_hi;
+      lo = sh.r_lo;
+      hi = sh.r_hi;
+    }
     launch_particle_energy(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
-                           want_stress ? stress.as<double>() : nullptr, store_svd ? svd.as<double>() : nullptr, part,
-                           nred, flag_bad(), stream);
-    launch_node_energy(gview(), dt, grav, dvp, p, alpha, part + nred, nred, stream);
-    launch_sum_partials(part, 2 * nred, scal.as<double>() + 0, stream);
-    prof_end(h, (double)np * (24 + 72 + 8 + 4 + 27 * 28) + (want_stress ? 72.0 * np : 0.0));
+                           want_stress ? stress.as<double>() : nullptr, store_svd ? svd.as<double>() : nullptr,
+                           pe_buf.as<double>(), nred, flag_bad(), stream, plo, phi);
+    launch_node_energy(gview(), bview(), pe_buf.as<double>(), dt, grav, dvp, p, alpha, ne_buf.as<double>(), lo, hi,
+                       stream);
+    prof_end(h, (double)(phi < 0 ? np : phi - plo) * (24 + 72 + 8 + 4 + 27 * 28 + 16) +
+                    (want_stress ? 72.0 * (phi < 0 ? np : phi - plo) : 0.0));
+    if (sh.on) gather_rows0(ne_buf.p, 8);
+    launch_sum_array(ne_buf.as<double>(), n, part, nred, stream);
+    launch_sum_partials(part, nred, scal.as<double>() + 0, stream);
   }
 
-  /// g(dv) from the stored stress; scaled-norm^2 into scal[2].
+  /// g(dv) from the stored stress; scaled-norm^2 into scal[2].  Slabs: the bin pass over bins
+  /// [P-1, Q+1), the node pass over the slab's rows, then g and the norm terms gathered.
   void gradient_async(const double* dvp, double* gout) {
     const int h = prof_begin(P_GRADIENT);
     double* part = partials.as<double>() + 2 * nred;
-    launch_node_gradient(pview(), bview(), gview(), dx, dt, grav, stress.as<double>(), dvp, gout, bin_part.as<double>(),
-                         part, nred, flag_bad(), stream);
+    const int n = L[0].n;
+    nt_buf.ensure(sizeof(double) * std::max(n, 1));
+    if (sh.on)
+      launch_node_gradient(pview(), bview(), gview(), dx, dt, grav, stress.as<double>(), dvp, gout,
+                           bin_part.as<double>(), nt_buf.as<double>(), flag_bad(), stream, sh.b_lo, sh.b_hi, sh.r_lo,
+                           sh.r_hi);
+    else
+      launch_node_gradient(pview(), bview(), gview(), dx, dt, grav, stress.as<double>(), dvp, gout,
+                           bin_part.as<double>(), nt_buf.as<double>(), flag_bad(), stream);
+    prof_end(h, 96.0 * np + 64.0 * n);  // x, V P F^T | dv, mass, g
+    if (sh.on) {
+      gather_rows0(gout, 24);
+      gather_rows0(nt_buf.p, 8);
+    }
+    launch_sum_array(nt_buf.as<double>(), n, part, nred, stream);
     launch_sum_partials(part, nred, scal.as<double>() + 2, stream);
-    prof_end(h, 96.0 * np + 64.0 * L[0].n);  // x, V P F^T | dv, mass, g
   }
 
   void check_flags() {
@@ -1052,14 +1114,19 @@ struct Context {
     return std::max(1, std::min(std::min(max_blocks, 2 * num_sms()), want));
   }
 
+  /// Rows per wave from which the level-0 smoother streams (k_sgs_stream); below it the
+  /// dataflow kernel (single GPU) or per-wave launches (slabs) run.
+  static int stream_min_rows() {
+    const char* env = std::getenv("HOT_SGS_STREAM_MIN");  // test hook: force either schedule
+    return env ? std::atoi(env) : 8 * 1024;
+  }
+
   void sgs(int m, double* u, const double* b) {
     Level& l = L[m];
     const int h = prof_begin(m == 0 ? P_SGS0 : P_SGSC);
     // large waves stream best as plain launches; small waves (coarse levels) run in one
     // persistent cooperative kernel with a grid barrier between waves
-    static const char* env = nullptr;
-    env = std::getenv("HOT_SGS_STREAM_MIN");  // test hook: force either schedule
-    const int stream_min = env ? std::atoi(env) : 8 * 1024;
+    const int stream_min = stream_min_rows();
     const char* sched = std::getenv("HOT_SGS_LEVEL0");  // "waves" | "stream" (default)
     const bool per_wave = sched && std::strcmp(sched, "waves") == 0;
     const char* coarse_sched = std::getenv("HOT_SGS_COARSE");  // "flow" (default) | "barrier"
@@ -1246,6 +1313,11 @@ struct Context {
     sh.last = false;
     if (cfg.window > kMaxWindow) throw std::invalid_argument("L-BFGS window too large");
     const double target = cfg.epsilon * std::sqrt((double)n);
+    struct ShardOff {  // the cut is per solve; taps and the other solvers run unsharded
+      Shard& s;
+      ~ShardOff() { s.on = false; }
+    } shard_off{sh};
+    sh.on = want_shard(levels) && plan_shard();
     HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
     HOT_CUDA(cudaMemsetAsync(iflags.p, 0, sizeof(int) * 8, stream));
     energy_async(dv.as<double>(), nullptr, 0.0, true, /*store_svd=*/true);
@@ -1258,11 +1330,6 @@ struct Context {
       out.converged = true;
       return out;
     }
-    struct ShardOff {  // the cut is per solve; taps and the other solvers run unsharded
-      Shard& s;
-      ~ShardOff() { s.on = false; }
-    } shard_off{sh};
-    sh.on = want_shard(levels) && plan_shard();
     sh.last = sh.on;
     if (sh.on) ++sh.solves;
     assemble_and_build_hierarchy(dv.as<double>(), levels, cfg.embedding, /*reuse_svd=*/true);

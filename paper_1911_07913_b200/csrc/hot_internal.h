@@ -111,16 +111,20 @@ void launch_mf_block_diag_inv(const ParticlesView& P, BinsView bins, GridView g,
 void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s);
 /// u = vel + (dv + alpha p) per node (p may be null): the nodal velocity the virtual F sees.
 void launch_node_u(GridView g, const double* dv, const double* p, double alpha, double* u, cudaStream_t s);
+/// Per-particle elastic energy pe[p] (+ stress, + SVD cache) for particles [plo, phi).
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                            const double* u, double* stress, double* svd_out, double* partials, int nblocks,
-                            int* bad_flag, cudaStream_t s);
-void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
-                        double* partials, int nblocks, cudaStream_t s);
-/// g_i = dt * sum_p (V P F^T) grad w + m_i (dv_i - dt*grav); 0 on Dirichlet; partial sums of
-/// |g_i|^2 / scale_i^2 into partials.
+                            const double* u, double* stress, double* svd_out, double* pe, int nblocks, int* bad_flag,
+                            cudaStream_t s, long long plo = 0, long long phi = -1);
+/// ne[i] = the bin's particle energies + the node's kinetic / gravity terms, rows [lo, hi).
+void launch_node_energy(GridView g, BinsView bins, const double* pe, double dt, const double* grav, const double* dv,
+                        const double* p, double alpha, double* ne, int lo, int hi, cudaStream_t s);
+/// g_i = dt * sum_p (V P F^T) grad w + m_i (dv_i - dt*grav); 0 on Dirichlet; nt[i] =
+/// |g_i|^2 / scale_i^2.  Bin pass over bins [jlo, jhi), node pass over rows [lo, hi) (-1: n).
 void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
-                          const double* stress, const double* dv, double* gout, double* bin_part, double* partials,
-                          int nblocks, int* bad_flag, cudaStream_t s);
+                          const double* stress, const double* dv, double* gout, double* bin_part, double* nt,
+                          int* bad_flag, cudaStream_t s, int jlo = 0, int jhi = -1, int lo = 0, int hi = -1);
+/// Fixed-tree block partials of sum(a[0, n)) (then launch_sum_partials).
+void launch_sum_array(const double* a, long long n, double* partials, int nblocks, cudaStream_t s);
 void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s);
 
 // vector helpers (deterministic block partials + fixed-order final sums)
@@ -184,8 +188,9 @@ void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, d
 void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* u, const double* b, int* flag,
                      int epoch, cudaStream_t s);
 /// Level-0 smoother: both passes, all waves, one persistent kernel with bulk-copy row streaming.
+/// [q_lo, q_hi): the part of the flat (forward waves, then backward waves) sequence to run.
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                       const double* b, unsigned int* bar, cudaStream_t s);
+                       const double* b, unsigned int* bar, cudaStream_t s, int q_lo = 0, int q_hi = -1);
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s);
 int sgs_max_blocks();

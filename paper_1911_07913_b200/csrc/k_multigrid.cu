@@ -869,7 +869,7 @@ struct StreamCursor {  // position in a warp's flat (wave, row) sequence
 
 __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     k_sgs_stream(LevelView L, const int* __restrict__ wave_start, const int* __restrict__ wave_rows, int nwaves,
-                 double* u, const double* __restrict__ b, unsigned int* bar) {
+                 double* u, const double* __restrict__ b, unsigned int* bar, int q_lo, int q_hi) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = blockIdx.x * kStreamWarps + wib, nw = gridDim.x * kStreamWarps;
@@ -877,8 +877,9 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   unsigned long long* mb =
       reinterpret_cast<unsigned long long*>(sm_raw + (size_t)kStreamWarps * kStreamStages * kStreamRowBytes) +
       wib * kStreamStages;
-  const int nq = 2 * nwaves;
-  auto wave_of = [&](int q) { return q < nwaves ? q : nq - 1 - q; };
+  // the flat sequence q = 0 .. 2 nwaves - 1 (forward, then backward); this launch runs [q_lo, q_hi)
+  const int nq = q_hi;
+  auto wave_of = [&](int q) { return q < nwaves ? q : 2 * nwaves - 1 - q; };
   auto count_of = [&](int q) {
     const int w = wave_of(q);
     return __ldg(wave_start + w + 1) - __ldg(wave_start + w);
@@ -908,7 +909,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     return i;
   };
   // prologue: fill the ring
-  StreamCursor prod{0, 0};
+  StreamCursor prod{q_lo, 0};
   settle(prod);
   int rowid[kStreamStages];
   for (int s = 0; s < kStreamStages; ++s) {
@@ -923,8 +924,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   }
   int stage = 0;
   unsigned phase_bits = 0;  // bit s: parity to wait for on stage s
-  for (int q = 0; q < nq; ++q) {
-    if (q > 0) sgs_grid_barrier(bar, (unsigned int)q);
+  for (int q = q_lo; q < nq; ++q) {
+    if (q > q_lo) sgs_grid_barrier(bar, (unsigned int)(q - q_lo));
     const int cnt = count_of(q);
     for (int r = gw; r < cnt; r += nw) {
       const int i = rowid[stage];
@@ -1275,11 +1276,13 @@ int sgs_stream_blocks() {
 }
 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                       const double* b, unsigned int* bar, cudaStream_t s) {
+                       const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi) {
   if (L.n == 0 || nwaves == 0) return;
+  if (q_hi < 0) q_hi = 2 * nwaves;
+  if (q_hi <= q_lo) return;
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
   int grid = sgs_stream_blocks();
-  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar};
+  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar, &q_lo, &q_hi};
   { cudaLaunchCooperativeKernel((const void*)k_sgs_stream, grid, kStreamWarps * 32, args, kStreamSmem, s); count_launches(1); }
 }
 

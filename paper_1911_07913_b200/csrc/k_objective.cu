@@ -46,13 +46,15 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) k_particle_energy(Particles
                                                                  const double* __restrict__ u,
                                                                  double* __restrict__ stress,
                                                                  double* __restrict__ svd_out,
-                                                                 double* __restrict__ partials, int* bad) {
-  double acc = 0.0;
+                                                                 double* __restrict__ pe, int* bad, long long plo,
+                                                                 long long phi) {
   const long long n = P.n;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+  for (long long p = plo + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < phi;
+       p += (long long)gridDim.x * blockDim.x) {
     M3 F, Fn;
     if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
       atomicExch(bad, 1);
+      pe[p] = 0.0;
       continue;
     }
     const DevMaterial mt = mats[P.mat[p]];
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) k_particle_energy(Particles
       for (int k = 0; k < 3; ++k) svd_out[(9 + k) * n + p] = s[k];
     }
     const double vol = P.vol[p];
-    acc += vol * fcr_psi(s, mt.mu, mt.lambda);
+    pe[p] = vol * fcr_psi(s, mt.mu, mt.lambda);
     if (stress) {
       const M3 Pk = fcr_P(F, U, V, mt.mu, mt.lambda);
       const M3 PFt = m3_mul_bt(Pk, Fn);
@@ -77,16 +79,20 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) k_particle_energy(Particles
       for (int k = 0; k < 9; ++k) stress[k * n + p] = vol * PFt.m[k];
     }
   }
-  const double b = block_sum<kEnergyThreads>(acc);
-  if (threadIdx.x == 0) partials[blockIdx.x] = b;
 }
 
-__global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, double dt, double g0, double g1, double g2,
+/// Node energy terms (objective.hpp:247-255) plus the elastic energy of the node's bin (its
+/// particles in bin order): ne[i] per row i in [lo, hi).  The total is a fixed-tree sum over
+/// ne[0, n), which does not depend on how rows are split between GPUs.
+__global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, BinsView bins, const double* __restrict__ pe,
+                                                             double dt, double g0, double g1, double g2,
                                                              const double* __restrict__ dv,
                                                              const double* __restrict__ pd, double alpha,
-                                                             double* __restrict__ partials) {
-  double acc = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+                                                             double* __restrict__ ne, int lo, int hi) {
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    const int pb = __ldg(bins.start + i), pend = __ldg(bins.start + i + 1);
+    for (int q = pb; q < pend; ++q) acc += __ldg(pe + q);
     double d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -96,10 +102,8 @@ __global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, double 
     const double m = g.mass[i];
     const double sq = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
     const double gu = g0 * (g.vel[3 * i] + d[0]) + g1 * (g.vel[3 * i + 1] + d[1]) + g2 * (g.vel[3 * i + 2] + d[2]);
-    acc += 0.5 * m * sq - dt * m * gu;
+    ne[i] = acc + (0.5 * m * sq - dt * m * gu);
   }
-  const double b = block_sum<kRedThreads>(acc);
-  if (threadIdx.x == 0) partials[blockIdx.x] = b;
 }
 
 /// Gradient, particle half (objective.hpp:276-280): for bin j and stencil position k, the sum
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(kRedThreads) k_node_energy(GridView g, double 
 constexpr int kBinWarps = 8;
 __global__ void __launch_bounds__(kBinWarps * 32) k_bin_force(ParticlesView P, BinsView bins, GridView g, double dx,
                                                              const double* __restrict__ stress,
-                                                             double* __restrict__ S) {
+                                                             double* __restrict__ S, int jlo, int jhi) {
   // per warp: the current chunk of <= 32 bin particles, [field][slot] (x 3, V P F^T 9), loaded
   // coalesced (lanes over particles) and read back as broadcasts by the stencil lanes
   __shared__ double stage[kBinWarps][12][32];
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_force(ParticlesView P, B
   // theirs by shuffle
   const int wu = min(lane / 9, 2), la = (lane % 9) / 3, lk = lane % 3;
   const int s0 = lane / 9, s1 = 3 + (lane / 3) % 3, s2 = 6 + lane % 3;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < g.n; j += nw) {
+  for (int j = jlo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); j < jhi; j += nw) {
     const int pb = __ldg(bins.start + j), pe = __ldg(bins.start + j + 1);
     const double ca = (double)(g.coords[3 * j + la] + lk - 1);
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
@@ -170,13 +174,13 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_force(ParticlesView P, B
 
 /// Node gradient (objective.hpp:260-287): one thread per node sums its 27 bins' contributions
 /// in offset order (bin at offset o - 1, where the node is stencil position 26 - o), fused with
-/// the scaled-norm residual (objective.hpp:476-486).
+/// the node's scaled-norm term (objective.hpp:476-486) nt[i] = |g_i|^2 / scale_i^2, rows
+/// [lo, hi).  The norm is a fixed-tree sum over nt[0, n) (split-independent).
 __global__ void __launch_bounds__(kRedThreads) k_node_gradient(GridView g, double dt, double g0, double g1, double g2,
                                                                const double* __restrict__ S,
                                                                const double* __restrict__ dv, double* __restrict__ gout,
-                                                               double* __restrict__ partials, int* bad) {
-  double acc_norm = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+                                                               double* __restrict__ nt, int* bad, int lo, int hi) {
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
     double f0 = 0.0, f1 = 0.0, f2 = 0.0;
     const int* nbi = g.nb27 + 27LL * i;
 #pragma unroll 9
@@ -196,10 +200,17 @@ __global__ void __launch_bounds__(kRedThreads) k_node_gradient(GridView g, doubl
     for (int a = 0; a < 3; ++a) gout[3 * i + a] = gi[a];
     const double sc = g.cn_scale[i];
     if (!(sc > 0.0)) atomicExch(bad, 2);
-    acc_norm += (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
+    nt[i] = (gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2]) / (sc * sc);
   }
-  const double b = block_sum<kRedThreads>(acc_norm);
-  if (threadIdx.x == 0) partials[blockIdx.x] = b;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_sum_array(const double* __restrict__ a, long long n,
+                                                           double* __restrict__ partials) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc += a[i];
+  const double r = block_sum<kRedThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = r;
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_sum_partials(const double* __restrict__ partials, int n,
@@ -319,32 +330,45 @@ int vgrid(long long n) {
 }  // namespace
 
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                            const double* u, double* stress, double* svd_out, double* partials, int nblocks,
-                            int* bad_flag, cudaStream_t s) {
-  { k_particle_energy<<<nblocks, kEnergyThreads, 0, s>>>(P, g, dx, dt, mats, u, stress, svd_out, partials, bad_flag); count_launches(1); }
+                            const double* u, double* stress, double* svd_out, double* pe, int nblocks, int* bad_flag,
+                            cudaStream_t s, long long plo, long long phi) {
+  if (phi < 0) phi = P.n;
+  if (phi <= plo) return;
+  const long long want = (phi - plo + kEnergyThreads - 1) / kEnergyThreads;
+  k_particle_energy<<<(int)std::max<long long>(1, std::min<long long>(nblocks, want)), kEnergyThreads, 0, s>>>(
+      P, g, dx, dt, mats, u, stress, svd_out, pe, bad_flag, plo, phi);
+  count_launches(1);
 }
 
-void launch_node_energy(GridView g, double dt, const double* grav, const double* dv, const double* p, double alpha,
-                        double* partials, int nblocks, cudaStream_t s) {
-  { k_node_energy<<<nblocks, kRedThreads, 0, s>>>(g, dt, grav[0], grav[1], grav[2], dv, p, alpha, partials); count_launches(1); }
+void launch_node_energy(GridView g, BinsView bins, const double* pe, double dt, const double* grav, const double* dv,
+                        const double* p, double alpha, double* ne, int lo, int hi, cudaStream_t s) {
+  if (hi <= lo) return;
+  k_node_energy<<<std::max(1, std::min((hi - lo + kRedThreads - 1) / kRedThreads, 16 * num_sms())), kRedThreads, 0, s>>>(
+      g, bins, pe, dt, grav[0], grav[1], grav[2], dv, p, alpha, ne, lo, hi);
+  count_launches(1);
 }
 
 void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, double dx, double dt, const double* grav,
-                          const double* stress, const double* dv, double* gout, double* bin_part, double* partials,
-                          int nblocks, int* bad_flag, cudaStream_t s) {
-  if (g.n > 0) {
+                          const double* stress, const double* dv, double* gout, double* bin_part, double* nt,
+                          int* bad_flag, cudaStream_t s, int jlo, int jhi, int lo, int hi) {
+  if (jhi < 0) jhi = g.n;
+  if (hi < 0) hi = g.n;
+  if (jhi > jlo) {
     static const int bin_blocks = resident_blocks((const void*)k_bin_force, kBinWarps * 32, 0);
-    k_bin_force<<<std::min<long long>(bin_blocks, (g.n + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
-        P, bins, g, dx, stress, bin_part);
+    k_bin_force<<<std::min<long long>(bin_blocks, (jhi - jlo + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
+        P, bins, g, dx, stress, bin_part, jlo, jhi);
     count_launches(1);
   }
-  static const int resident = resident_blocks((const void*)k_node_gradient, kRedThreads, 0);
-  const int nb = std::max(1, std::min(nblocks, resident));
-  if (nb < nblocks) {
-    cudaMemsetAsync(partials + nb, 0, sizeof(double) * (nblocks - nb), s);
+  if (hi > lo) {
+    k_node_gradient<<<std::max(1, std::min((hi - lo + kRedThreads - 1) / kRedThreads, 16 * num_sms())), kRedThreads, 0,
+                      s>>>(g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
+    count_launches(1);
   }
-  { k_node_gradient<<<nb, kRedThreads, 0, s>>>(g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, partials,
-                                              bad_flag); count_launches(1); }
+}
+
+void launch_sum_array(const double* a, long long n, double* partials, int nblocks, cudaStream_t s) {
+  k_sum_array<<<nblocks, kRedThreads, 0, s>>>(a, n, partials);
+  count_launches(1);
 }
 
 void launch_sum_partials(const double* partials, int n, double* out, cudaStream_t s) {

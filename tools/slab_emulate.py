@@ -165,6 +165,7 @@ def run(sc, particles, R, steps, warmup):
             comm.segments.append(time.perf_counter() - comm.t0)
             comm.t0 = time.perf_counter()
             marks[r] = (len(comm.segments), len(comm.recv_bytes))
+        sim.profile(True)
         t = time.perf_counter()
         outer = []
         for k in range(warmup, warmup + steps):
@@ -172,14 +173,16 @@ def run(sc, particles, R, steps, warmup):
         wall = time.perf_counter() - t
         if comm:
             comm.stop()
-        results[r] = dict(outer=outer, wall=wall, info=slabs.shard_info(sim))
+        prof = sim.profile_read()
+        results[r] = dict(outer=outer, wall=wall, info=slabs.shard_info(sim),
+                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0})
 
     threads = [threading.Thread(target=body, args=(r,)) for r in range(R)]
     for t in threads:
         t.start()
     for t in threads:
         t.join()
-    out = dict(ranks=R, outer=results[0]["outer"])
+    out = dict(ranks=R, outer=results[0]["outer"], rank0_phase_ms_per_step=results[0]["phases"])
     if R == 1:
         out["compute_ms_per_step"] = 1000 * results[0]["wall"] / steps
         out["collectives_per_step"] = 0
