@@ -663,7 +663,12 @@ struct Context {
   // ------------------------------------------------------------------ slabs
   /// The slab-sharded solve: HOT / LBFGS-H solves with a coarse level under the linear
   /// embedding, when a transport with more than one rank is attached.
-  bool want_shard(int levels) const { return comm && comm->size > 1 && cfg.embedding == 1 && levels >= 2; }
+  bool want_shard(int levels) const {
+    // HOT_SHARD_FORCE=1 (test hook): take the sharded path with one rank too, so the transport's
+    // calls run on a one-GPU box (one slab; halos have no peer, gathers broadcast to self)
+    static const bool force = std::getenv("HOT_SHARD_FORCE") != nullptr;
+    return comm && (comm->size > 1 || force) && cfg.embedding == 1 && levels >= 2;
+  }
   /// First level-0 row at or after absolute lattice plane `plane` (axis 0).
   int row_of(int plane) const {
     const int k = std::min(std::max(plane - L[0].lo[0], 0), L[0].ext[0]);

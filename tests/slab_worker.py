@@ -29,7 +29,7 @@ def main():
     if levels is not None:
         sim.set_solver(levels=levels)
     sim.set_particles(**sample_scene_particles(sc))
-    if size > 1:
+    if size > 1 or transport == "nccl":
         import torch.distributed as dist
 
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=size)
@@ -51,7 +51,7 @@ def main():
              halos=np.array(infos[-1]["halo_exchanges"] if infos else 0),
              gathers=np.array(infos[-1]["gathers"] if infos else 0),
              energy=diag["energy"], residual=diag["scaled_residual"])
-    if size > 1:
+    if size > 1 or transport == "nccl":
         import torch.distributed as dist
 
         dist.barrier()

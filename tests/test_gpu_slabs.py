@@ -89,3 +89,35 @@ def test_sharded_two_level_hierarchy(tmp_path):
         assert res["sharded"].any()
         for k in ("x", "v", "F", "C"):
             np.testing.assert_array_equal(res[k], ref[k])
+
+
+def test_sharded_benchmark_scene_two_steps(tmp_path):
+    """The benchmark workload (cfg2, 1.19M particles): 2 ranks equal 1 GPU bitwise.  Its waves
+    are > 8K rows, so the streaming smoother is the single-GPU default here anyway."""
+    scene = "cfg2_twisting_bars.json"
+    ref = run_ranks(tmp_path, scene, 1, 2, tag="single")[0]
+    ranks = run_ranks(tmp_path, scene, 2, 2)
+    assert ref["stats"][:, 1].sum() > 0
+    for res in ranks:
+        assert res["sharded"].any()
+        np.testing.assert_array_equal(res["stats"], ref["stats"])
+        for k in ("x", "v", "F", "C"):
+            np.testing.assert_array_equal(res[k], ref[k])
+
+
+def test_nccl_transport_single_rank(tmp_path):
+    """The NCCL transport's own calls on the one GPU of the test box: libnccl.so.2 loaded at run
+    time, communicator init, the row gathers (in-place broadcasts) and the flag allreduce, with
+    the sharded path forced at one rank (HOT_SHARD_FORCE).  NCCL refuses two ranks on one GPU,
+    so the send/recv halo pair cannot run here."""
+    ref = run_ranks(tmp_path, "cfg1_stretched.json", 1, 2, tag="single")[0]
+    port = _free_port()
+    out = str(tmp_path / "nccl1.npz")
+    env = dict(ENV, HOT_SHARD_FORCE="1")
+    p = subprocess.run([sys.executable, WORKER, "0", "1", str(port), os.path.join(SCENES, "cfg1_stretched.json"), "2",
+                        out, "nccl"], capture_output=True, text=True, env=env, timeout=600)
+    assert p.returncode == 0, (p.stdout + p.stderr)[-4000:]
+    res = dict(np.load(out))
+    assert res["sharded"].any() and res["gathers"] > 0
+    for k in ("x", "v", "F", "C"):
+        np.testing.assert_array_equal(res[k], ref[k])

@@ -175,7 +175,8 @@ def run(sc, particles, R, steps, warmup):
             comm.stop()
         prof = sim.profile_read()
         results[r] = dict(outer=outer, wall=wall, info=slabs.shard_info(sim),
-                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0})
+                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0},
+                          state=sim.particles())
 
     threads = [threading.Thread(target=body, args=(r,)) for r in range(R)]
     for t in threads:
@@ -193,11 +194,20 @@ def run(sc, particles, R, steps, warmup):
         recv = np.array([c.recv_bytes[b0:] for c in comms])
         out["compute_ms_per_step"] = 1000 * segs.max(axis=0).sum() / steps
         out["rank_busy_ms_per_step"] = [round(1000 * x / steps, 3) for x in segs.sum(axis=1)]
+        slow = int(np.argmax(segs.sum(axis=1)))
+        out["slowest_rank"] = slow
+        out["slowest_rank_phase_ms_per_step"] = results[slow]["phases"]
+        big = np.argsort(-segs[slow])[:5]
+        out["slowest_rank_top_segments_ms"] = [[int(k), round(1000 * segs[slow][k], 3)] for k in big]
         out["collectives_per_step"] = recv.shape[1] / steps
         out["recv_mb_per_step"] = float(recv.max(axis=0).sum()) / 1e6 / steps
         out["rows"] = [[res["info"]["row_lo"], res["info"]["row_hi"]] for res in results]
         for r in range(1, R):
             assert results[r]["outer"] == results[0]["outer"]
+    out["_state"] = results[0]["state"]
+    out["ranks_bitwise_equal"] = all(
+        all(np.array_equal(results[r]["state"][k], results[0]["state"][k]) for k in ("x", "v", "F", "C"))
+        for r in range(R))
     for s in sims:
         s.close()
     return out
@@ -215,8 +225,15 @@ def main():
     sc = load_scene_file(args.scene)
     particles = sample_scene_particles(sc)
     base = None
+    ref_state = None
     for R in [int(x) for x in args.ranks.split(",")]:
         o = run(sc, particles, R, args.steps, args.warmup)
+        state = o.pop("_state")
+        if R == 1:
+            ref_state = state
+        elif ref_state is not None:  # every rank's particles vs the single-GPU run, bit for bit
+            o["bitwise_equal_to_1_gpu"] = bool(o["ranks_bitwise_equal"]) and all(
+                np.array_equal(state[k], ref_state[k]) for k in ("x", "v", "F", "C"))
         comm_ms = o["collectives_per_step"] * args.lat_us / 1000 + o["recv_mb_per_step"] / args.bw_gbs
         o["comm_model_ms_per_step"] = comm_ms
         o["projected_ms_per_step"] = o["compute_ms_per_step"] + comm_ms
