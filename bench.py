@@ -175,11 +175,15 @@ def main():
 
     import torch
 
-    if world > 1:
+    force_slabs = bool(os.environ.get("HOT_SHARD_FORCE")) and args.mode == "slabs"
+    if world > 1 or force_slabs:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        if "MASTER_ADDR" in os.environ:
+            dist.init_process_group("nccl")
+        else:  # HOT_SHARD_FORCE without a launcher: a one-rank group
+            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0, world_size=1)
     device = local_rank
     torch.cuda.set_device(device)
     from paper_1911_07913_b200 import Simulation
@@ -187,7 +191,8 @@ def main():
     sim = Simulation(sc, device=device)
     sim.set_particles(**particles)
     stream = torch.cuda.ExternalStream(sim.stream(), device=device)
-    slabbed = world > 1 and args.mode == "slabs"
+    # HOT_SHARD_FORCE=1 (test hook): the slab path at one rank too (transport calls on one GPU)
+    slabbed = (world > 1 or force_slabs) and args.mode == "slabs"
     slab_error = None
     if slabbed:
         from paper_1911_07913_b200 import slabs
@@ -334,7 +339,7 @@ def main():
                 "clocks": clocks.summary()}
         print(json.dumps(line))
     sim.close()
-    if world > 1:
+    if world > 1 or force_slabs:
         torch.distributed.destroy_process_group()
 
 
