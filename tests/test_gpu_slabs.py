@@ -7,6 +7,7 @@ The bar is stronger than the oracle's 1e-6: every row is computed with the singl
 arithmetic in the single-GPU order and the replicated scalars are reduced identically, so the
 sharded step must equal the single-GPU step BITWISE, and therefore the oracle as closely as the
 single-GPU step does (tests/test_gpu_parity.py)."""
+import json
 import os
 import socket
 import subprocess
@@ -121,3 +122,47 @@ def test_nccl_transport_single_rank(tmp_path):
     assert res["sharded"].any() and res["gathers"] > 0
     for k in ("x", "v", "F", "C"):
         np.testing.assert_array_equal(res[k], ref[k])
+
+
+def _scene_file(tmp_path, name, objects):
+    d = {"dim": 3, "dx": 1.0 / 64, "gravity": [0.0, -9.8, 0.0], "fps": 500, "frames": 4, "epsilon": 1e-05, "seed": 7,
+         "ppc": 8, "domain": {"min": [0.0, 0.0, 0.0], "max": [1.0, 1.0, 1.0]},
+         "materials": [{"density": 1000.0, "youngs": 1e5, "poisson": 0.3}],
+         "objects": objects,
+         "colliders": [{"shape": {"kind": "half_space", "point": [0.0, 0.05, 0.0], "normal": [0.0, 1.0, 0.0]},
+                        "motion": {"kind": "static"}}]}
+    path = tmp_path / f"{name}.json"
+    path.write_text(json.dumps(d))
+    return str(path)
+
+
+def _stretched_box(lo, hi):
+    return {"shape": {"kind": "box", "min": lo, "max": hi}, "material": 0,
+            "initial_deformation": {"kind": "random_diagonal", "lo": 0.7, "hi": 1.3}}
+
+
+def test_sharded_gap_between_objects(tmp_path):
+    """Two boxes with empty lattice planes between them along axis 0: slabs whose rows are
+    unevenly spread, planes without rows inside a slab."""
+    scene = _scene_file(tmp_path, "gap", [_stretched_box([0.20, 0.3, 0.3], [0.30, 0.4, 0.4]),
+                                          _stretched_box([0.55, 0.3, 0.3], [0.70, 0.45, 0.45])])
+    ref = run_ranks(tmp_path, scene, 1, 2, tag="single")[0]
+    for size in (2, 3):
+        ranks = run_ranks(tmp_path, scene, size, 2, tag=f"gap{size}_")
+        for res in ranks:
+            assert res["sharded"].any()
+            for k in ("x", "v", "F", "C"):
+                np.testing.assert_array_equal(res[k], ref[k])
+
+
+def test_too_few_planes_runs_replicated(tmp_path):
+    """A sliver one cell thick along axis 0 has too few planes for 3 slabs of >= 2 planes at
+    even cuts: the planner declines, every rank runs the whole solve, results unchanged."""
+    scene = _scene_file(tmp_path, "sliver", [_stretched_box([0.40, 0.3, 0.3], [0.42, 0.5, 0.5])])
+    ref = run_ranks(tmp_path, scene, 1, 2, tag="single")[0]
+    assert ref["stats"][:, 1].sum() > 0
+    ranks = run_ranks(tmp_path, scene, 3, 2, tag="sliver")
+    for res in ranks:
+        assert not res["sharded"].any()
+        for k in ("x", "v", "F", "C"):
+            np.testing.assert_array_equal(res[k], ref[k])
