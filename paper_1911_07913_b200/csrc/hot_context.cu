@@ -227,6 +227,7 @@ struct Context {
     DBuf wave_rows, wave_counts, wave_starts, wave_cursor;
     long long solves = 0;          // sharded solves so far
     bool last = false;             // the last solve ran sharded
+    bool planned = false;          // this step's grid has a cut (set by prepare)
   } sh;
   DBuf plane_buf;
   DBuf pe_buf, ne_buf, nt_buf;  // per-particle energy, per-node energy, per-node scaled-norm terms
@@ -515,6 +516,7 @@ struct Context {
     }
     prof_end(h, (double)n * (3 + 3 + 9 + 9 + 2) * 8 + 4.0 * n);
     have_state = false;
+    sh.planned = false;
     if (mat && n) {
       int bad = 0;
       HOT_CUDA(cudaMemcpyAsync(&bad, iflags.as<int>() + 7, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -631,6 +633,22 @@ struct Context {
 
   void p2g_bc(double time_now) {
     const int h = prof_begin(P_P2G);
+    if (sh.planned) {  // slabs: bins [P-1, Q+1), the slab's rows, then every rank's rows to all
+      const int n = L[0].n;
+      HOT_CUDA(cudaMemsetAsync(L[0].dir.p, 0, std::max(n, 1), stream));
+      HOT_CUDA(cudaMemsetAsync(gbc.p, 0, sizeof(double) * 3 * std::max(n, 1), stream));
+      launch_p2g(pview(), bview(), gview(), dx, mats_d.as<DevMaterial>(), cn_factor * dx * dx, dt,
+                 bin_part.as<double>(), stream, sh.b_lo, sh.b_hi, sh.r_lo, sh.r_hi);
+      prof_end(h, (double)(sh.p_hi - sh.pe_lo) * 136 + (double)(sh.r_hi - sh.r_lo) * 88);
+      gather_rows0(gmass.p, 8);
+      gather_rows0(gmom.p, 24);
+      gather_rows0(gvel.p, 24);
+      gather_rows0(gcn.p, 8);
+      const int h2 = prof_begin(P_P2G);
+      launch_apply_bc(gview(), dx, cols_d.as<DevCollider>(), (int)cols_h.size(), stream);
+      prof_end(h2);
+      return;
+    }
     launch_p2g(pview(), bview(), gview(), dx, mats_d.as<DevMaterial>(), cn_factor * dx * dx, dt, bin_part.as<double>(),
                stream);
     launch_apply_bc(gview(), dx, cols_d.as<DevCollider>(), (int)cols_h.size(), stream);
@@ -654,6 +672,9 @@ struct Context {
   void prepare(double dt_in, double time_now) {
     dt = dt_in;
     activate();
+    // the slab cut of this step's grid (replicated inputs: every rank computes the same cut)
+    const int levels = cfg.kind == 0 ? cfg.levels : 0;  // HOT is the solver that splits
+    sh.planned = want_shard(levels) && plan_shard();
     p2g_bc(time_now);
     ensure_solver_buffers();
     have_state = true;
@@ -1322,7 +1343,7 @@ struct Context {
       Shard& s;
       ~ShardOff() { s.on = false; }
     } shard_off{sh};
-    sh.on = want_shard(levels) && plan_shard();
+    sh.on = want_shard(levels) && sh.planned;
     HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
     HOT_CUDA(cudaMemsetAsync(iflags.p, 0, sizeof(int) * 8, stream));
     energy_async(dv.as<double>(), nullptr, 0.0, true, /*store_svd=*/true);

@@ -85,7 +85,8 @@ void launch_flags_to_index(const uint8_t* flags, long long len, const int* ext, 
 void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n_nodes, int* bin_of, int* counts,
                           int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s);
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
-                double dt, double* bin_part, cudaStream_t s);
+                double dt, double* bin_part, cudaStream_t s, int jlo = 0, int jhi = -1, int lo = 0,
+                int hi = -1);  // bins [jlo, jhi), rows [lo, hi)
 /// Also writes dst.bin[t] = bin_of[pid[t]].
 void launch_reorder_particles(const ParticlesView& src, const ParticlesView& dst, const int* pid, const int* bin_of,
                               const int* orig_src,

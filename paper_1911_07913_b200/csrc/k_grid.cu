@@ -260,7 +260,7 @@ __global__ void k_bin_sort(const int* __restrict__ start, int n_nodes, int* pid)
 constexpr int kBinWarps = 8;
 __global__ void __launch_bounds__(kBinWarps * 32) k_bin_p2g(ParticlesView P, BinsView bins, GridView g, double dx,
                                                            const DevMaterial* __restrict__ mats,
-                                                           double* __restrict__ B) {
+                                                           double* __restrict__ B, int jlo, int jhi) {
   // per warp: the current chunk of <= 32 bin particles, [field][slot] (x 3, v 3, C 9, m, m xi),
   // loaded coalesced (lanes over particles) and read back as broadcasts by the stencil lanes
   __shared__ double stage[kBinWarps][17][32];
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_p2g(ParticlesView P, Bin
   const int wu = min(lane / 9, 2), la = (lane % 9) / 3, lk = lane % 3;
   const int s0 = lane / 9, s1 = 3 + (lane / 3) % 3, s2 = 6 + lane % 3;
   const int k0 = lane / 9 - 1, k1 = (lane / 3) % 3 - 1, k2 = lane % 3 - 1;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < g.n; j += nw) {
+  for (int j = jlo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); j < jhi; j += nw) {
     const int pb = __ldg(bins.start + j), pe = __ldg(bins.start + j + 1);
     const int ci0 = g.coords[3 * j] + k0, ci1 = g.coords[3 * j + 1] + k1, ci2 = g.coords[3 * j + 2] + k2;
     const double xi0 = (double)ci0 * dx, xi1 = (double)ci1 * dx, xi2 = (double)ci2 * dx;
@@ -334,8 +334,9 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_p2g(ParticlesView P, Bin
 /// P2G, node half: one thread per node sums its 27 bins' contributions in offset order (bin at
 /// offset o - 1, where the node is stencil position 26 - o), then v = mom / m and the characteristic-norm scale
 /// (objective.hpp:445-463); resets the boundary fields.
-__global__ void __launch_bounds__(256) k_p2g(GridView g, const double* __restrict__ B, double ell, double dt) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) k_p2g(GridView g, const double* __restrict__ B, double ell, double dt, int lo,
+                                             int hi) {
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
     double m = 0.0, mom0 = 0.0, mom1 = 0.0, mom2 = 0.0, num = 0.0;
     const int* nbi = g.nb27 + 27LL * i;
 #pragma unroll 9
@@ -548,15 +549,21 @@ void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n
 }
 
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
-                double dt, double* bin_part, cudaStream_t s) {
+                double dt, double* bin_part, cudaStream_t s, int jlo, int jhi, int lo, int hi) {
   if (g.n == 0) return;
+  if (jhi < 0) jhi = g.n;
+  if (hi < 0) hi = g.n;
   static const int blocks = resident_blocks((const void*)k_p2g, 256, 0);
-  const long long need = (32LL * g.n + 255) / 256;
   static const int bin_blocks = resident_blocks((const void*)k_bin_p2g, kBinWarps * 32, 0);
-  k_bin_p2g<<<std::min<long long>(bin_blocks, (g.n + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
-      P, bins, g, dx, mats, bin_part);
-  k_p2g<<<std::min<long long>(blocks, (g.n + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt);
-  count_launches(2);
+  if (jhi > jlo) {
+    k_bin_p2g<<<std::min<long long>(bin_blocks, (jhi - jlo + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
+        P, bins, g, dx, mats, bin_part, jlo, jhi);
+    count_launches(1);
+  }
+  if (hi > lo) {
+    k_p2g<<<std::min<long long>(blocks, (hi - lo + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt, lo, hi);
+    count_launches(1);
+  }
 }
 
 void launch_fill_nb27(GridView g, int* nb27, cudaStream_t s) {
