@@ -14,6 +14,7 @@
 #include <cooperative_groups.h>
 #include <climits>
 #include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "hot_async.cuh"
@@ -858,25 +859,26 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
 /// blocks and columns do not depend on u, so HBM streaming never drains at the grid barrier
 /// between waves; only the u gathers (ld.cg, L2) wait for it.  Row arithmetic is identical to
 /// k_sgs_wave (same summation order).
-constexpr int kStreamWarps = 8;
-constexpr int kStreamStages = 2;
 constexpr int kStreamRowBytes = 9 * kSlotPitch * 8 + kSlotPitch * 4;  // 9728
-constexpr int kStreamSmem = kStreamWarps * kStreamStages * kStreamRowBytes + kStreamWarps * kStreamStages * 8;
+/// W warps per CTA, S ring stages per warp (HOT_SGS_STREAM_CFG = "WxS"; default 8x2)
+template <int W, int S>
+constexpr int stream_smem() { return W * S * kStreamRowBytes + W * S * 8; }
 
 struct StreamCursor {  // position in a warp's flat (wave, row) sequence
   int q, m;           // q: 0..2*nwaves-1 (forward then backward), m: this warp's m-th row of wave w(q)
 };
 
-__global__ void __launch_bounds__(kStreamWarps * 32, 1)
+template <int W, int S>
+__global__ void __launch_bounds__(W * 32, 1)
     k_sgs_stream(LevelView L, const int* __restrict__ wave_start, const int* __restrict__ wave_rows, int nwaves,
                  double* u, const double* __restrict__ b, unsigned int* bar, int q_lo, int q_hi) {
   extern __shared__ __align__(128) unsigned char sm_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kStreamWarps + wib, nw = gridDim.x * kStreamWarps;
-  unsigned char* ring = sm_raw + (size_t)wib * kStreamStages * kStreamRowBytes;
+  const int gw = blockIdx.x * W + wib, nw = gridDim.x * W;
+  unsigned char* ring = sm_raw + (size_t)wib * S * kStreamRowBytes;
   unsigned long long* mb =
-      reinterpret_cast<unsigned long long*>(sm_raw + (size_t)kStreamWarps * kStreamStages * kStreamRowBytes) +
-      wib * kStreamStages;
+      reinterpret_cast<unsigned long long*>(sm_raw + (size_t)W * S * kStreamRowBytes) +
+      wib * S;
   // the flat sequence q = 0 .. 2 nwaves - 1 (forward, then backward); this launch runs [q_lo, q_hi)
   const int nq = q_hi;
   auto wave_of = [&](int q) { return q < nwaves ? q : 2 * nwaves - 1 - q; };
@@ -894,7 +896,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   unsigned long long policy = 0;
   if (lane == 0) {
     policy = l2_evict_first_policy();
-    for (int s = 0; s < kStreamStages; ++s) mbar_init(mb + s, 1);
+    for (int s = 0; s < S; ++s) mbar_init(mb + s, 1);
     mbar_fence_init();
   }
   __syncwarp();
@@ -911,8 +913,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   // prologue: fill the ring
   StreamCursor prod{q_lo, 0};
   settle(prod);
-  int rowid[kStreamStages];
-  for (int s = 0; s < kStreamStages; ++s) {
+  int rowid[S];
+  for (int s = 0; s < S; ++s) {
     rowid[s] = -1;
     if (prod.q < nq) {
       int i = 0;
@@ -979,7 +981,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
         u[3 * i + 1] = ub[1] + (D[3] * r0 + D[4] * r1 + D[5] * r2);
         u[3 * i + 2] = ub[2] + (D[6] * r0 + D[7] * r1 + D[8] * r2);
       }
-      stage = stage + 1 == kStreamStages ? 0 : stage + 1;
+      stage = stage + 1 == S ? 0 : stage + 1;
     }
   }
 }
@@ -1264,16 +1266,38 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
   { cudaLaunchCooperativeKernel((const void*)k_sgs, grid_blocks, kSgsThreads, args, kSgsSmem, s); count_launches(1); }
 }
 
-int sgs_stream_blocks() {
+template <int W, int S>
+int sgs_stream_blocks_t() {
   static int blocks = 0;
   if (!blocks) {
-    cudaFuncSetAttribute((const void*)k_sgs_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kStreamSmem);
+    cudaFuncSetAttribute((const void*)k_sgs_stream<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem<W, S>());
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_sgs_stream, kStreamWarps * 32, kStreamSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_sgs_stream<W, S>, W * 32, stream_smem<W, S>());
     blocks = std::max(1, per_sm) * num_sms();
   }
   return blocks;
 }
+
+template <int W, int S>
+void launch_sgs_stream_t(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
+                         const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi) {
+  int grid = sgs_stream_blocks_t<W, S>();
+  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar, &q_lo, &q_hi};
+  cudaLaunchCooperativeKernel((const void*)k_sgs_stream<W, S>, grid, W * 32, args, stream_smem<W, S>(), s);
+  count_launches(1);
+}
+
+int sgs_stream_cfg() {
+  static const int cfg = [] {
+    const char* e = std::getenv("HOT_SGS_STREAM_CFG");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "6x3" ? 1 : v == "4x4" ? 2 : v == "4x5" ? 3 : v == "16x1" ? 4 : 0;
+  }();
+  return cfg;
+}
+
+int sgs_stream_blocks() { return sgs_stream_blocks_t<8, 2>(); }
 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
                        const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi) {
@@ -1281,9 +1305,13 @@ void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows,
   if (q_hi < 0) q_hi = 2 * nwaves;
   if (q_hi <= q_lo) return;
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
-  int grid = sgs_stream_blocks();
-  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar, &q_lo, &q_hi};
-  { cudaLaunchCooperativeKernel((const void*)k_sgs_stream, grid, kStreamWarps * 32, args, kStreamSmem, s); count_launches(1); }
+  switch (sgs_stream_cfg()) {
+    case 1: launch_sgs_stream_t<6, 3>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
+    case 2: launch_sgs_stream_t<4, 4>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
+    case 3: launch_sgs_stream_t<4, 5>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
+    case 4: launch_sgs_stream_t<16, 1>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
+    default: launch_sgs_stream_t<8, 2>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
+  }
 }
 
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
