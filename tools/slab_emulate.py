@@ -219,13 +219,21 @@ def main():
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sweep", type=int, default=0, help="BASELINE config 5 particle set on an N^3 grid "
+                    "(tools/kernel_sweep.py) instead of --scene")
     ap.add_argument("--repeat", type=int, default=2, help="runs per rank count; the fastest critical path is kept "
                     "(host-side hiccups of the in-process emulation only ever add time)")
     ap.add_argument("--lat-us", type=float, default=15.0, help="model: seconds per collective (NCCL, NVLink)")
     ap.add_argument("--bw-gbs", type=float, default=350.0, help="model: received GB/s per rank (NCCL, NVLink 5)")
     args = ap.parse_args()
-    sc = load_scene_file(args.scene)
-    particles = sample_scene_particles(sc)
+    if args.sweep:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from kernel_sweep import particles_for, scene_for
+
+        sc, particles = scene_for(args.sweep), particles_for(args.sweep)
+    else:
+        sc = load_scene_file(args.scene)
+        particles = sample_scene_particles(sc)
     base = None
     ref_state = None
     for R in [int(x) for x in args.ranks.split(",")]:
