@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __r
   // One CTA (128 threads = one per diagonal-storage slot) per row; after the barrier only the
   // gather of the neighbours' u (one L2 round trip), the FMA and the CTA reduction remain.
   extern __shared__ __align__(16) char sgs_smem[];
-  __shared__ double red[kSgsThreads / 32][3];
+  __shared__ double red[kSgsThreads][3];
   cg::grid_group grid = cg::this_grid();
   const bool tr = trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
@@ -653,26 +653,26 @@ __global__ void __launch_bounds__(kSgsThreads) k_sgs(LevelView L, const int* __r
           x1 = __ldcg(xp + 1);
           x2 = __ldcg(xp + 2);
         }
-        double a0 = R.h[0] * x0 + R.h[1] * x1 + R.h[2] * x2;
-        double a1 = R.h[3] * x0 + R.h[4] * x1 + R.h[5] * x2;
-        double a2 = R.h[6] * x0 + R.h[7] * x1 + R.h[8] * x2;
-        a0 = wsum(a0);
-        a1 = wsum(a1);
-        a2 = wsum(a2);
-        if (lane == 0) {
-          red[wid][0] = a0;
-          red[wid][1] = a1;
-          red[wid][2] = a2;
-        }
+        // row sum in the streaming kernels' order (k_sgs_flow<2>): lane l adds slots l, l+32,
+        // l+64, l+96, then the warp sum
+        red[s][0] = R.h[0] * x0 + R.h[1] * x1 + R.h[2] * x2;
+        red[s][1] = R.h[3] * x0 + R.h[4] * x1 + R.h[5] * x2;
+        red[s][2] = R.h[6] * x0 + R.h[7] * x1 + R.h[8] * x2;
         __syncthreads();
-        if (s == 0) {
-          double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+        double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+        if (wid == 0) {
+          double b0 = 0.0, b1 = 0.0, b2 = 0.0;
 #pragma unroll
-          for (int q = 0; q < kSgsThreads / 32; ++q) {
-            y0 += red[q][0];
-            y1 += red[q][1];
-            y2 += red[q][2];
+          for (int k2 = 0; k2 < kSgsThreads / 32; ++k2) {
+            b0 += red[lane + 32 * k2][0];
+            b1 += red[lane + 32 * k2][1];
+            b2 += red[lane + 32 * k2][2];
           }
+          y0 = wsum(b0);
+          y1 = wsum(b1);
+          y2 = wsum(b2);
+        }
+        if (s == 0) {
           const double r0 = R.b[0] - y0, r1 = R.b[1] - y1, r2 = R.b[2] - y2;
           const int i = R.i;
           u[3 * i] = R.uo[0] + (R.D[0] * r0 + R.D[1] * r1 + R.D[2] * r2);
@@ -771,6 +771,10 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
   constexpr int T = level_pitch(R), S = level_slots(R);  // one thread per diagonal-storage slot
   __shared__ double red[T / 32][3];
   __shared__ double uold[3];  // u_i, from the diagonal slot's gather (no second L2 round trip)
+  // radius 2: the row sum in the streaming / per-wave kernels' order (lane l accumulates slots
+  // l, l+32, l+64, l+96, then the warp sum), so the level-0 update is bitwise the same whichever
+  // schedule runs it (one GPU small or large, or a slab)
+  __shared__ double term[R == 2 ? T : 1][3];
   const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
   for (int pass = 0; pass < 2; ++pass) {
     const int e = epoch + pass;
@@ -821,23 +825,44 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
       double a0 = h[0] * x0 + h[1] * x1 + h[2] * x2;
       double a1 = h[3] * x0 + h[4] * x1 + h[5] * x2;
       double a2 = h[6] * x0 + h[7] * x1 + h[8] * x2;
-      a0 = wsum(a0);
-      a1 = wsum(a1);
-      a2 = wsum(a2);
-      if (lane == 0) {
-        red[wid][0] = a0;
-        red[wid][1] = a1;
-        red[wid][2] = a2;
-      }
-      __syncthreads();
-      if (s == 0) {
-        double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+      if constexpr (R == 2) {
+        term[s][0] = a0;
+        term[s][1] = a1;
+        term[s][2] = a2;
+        __syncthreads();
+        if (wid == 0) {
+          double b0 = 0.0, b1 = 0.0, b2 = 0.0;
 #pragma unroll
-        for (int q = 0; q < T / 32; ++q) {
-          y0 += red[q][0];
-          y1 += red[q][1];
-          y2 += red[q][2];
+          for (int k = 0; k < T / 32; ++k) {
+            b0 += term[lane + 32 * k][0];
+            b1 += term[lane + 32 * k][1];
+            b2 += term[lane + 32 * k][2];
+          }
+          y0 = wsum(b0);
+          y1 = wsum(b1);
+          y2 = wsum(b2);
         }
+      } else {
+        a0 = wsum(a0);
+        a1 = wsum(a1);
+        a2 = wsum(a2);
+        if (lane == 0) {
+          red[wid][0] = a0;
+          red[wid][1] = a1;
+          red[wid][2] = a2;
+        }
+        __syncthreads();
+        if (s == 0) {
+#pragma unroll
+          for (int q = 0; q < T / 32; ++q) {
+            y0 += red[q][0];
+            y1 += red[q][1];
+            y2 += red[q][2];
+          }
+        }
+      }
+      if (s == 0) {
         const double uo0 = uold[0], uo1 = uold[1], uo2 = uold[2];
         const double r0 = rb[0] - y0, r1 = rb[1] - y1, r2 = rb[2] - y2;
         u[3 * i] = uo0 + (D[0] * r0 + D[1] * r1 + D[2] * r2);

@@ -22,12 +22,10 @@ SCENES = os.path.join(ROOT, "scenes")
 
 pytestmark = pytest.mark.gpu
 
-# The slabs smooth level 0 with one launch per colour wave (k_sgs_wave).  On small grids the
-# single-GPU default is the dataflow kernel, whose per-row reduction tree differs (rounding
-# only); HOT_SGS_STREAM_MIN=0 selects the streaming wave kernel there, as on every grid with
-# >= 8K rows per wave (cfg2 and up), and that kernel is bitwise equal to k_sgs_wave
-# (test_vcycle_streaming_wave_schedule).  Same setting for every run, single or sharded.
-ENV = dict(os.environ, HOT_SGS_STREAM_MIN="0")
+# Every level-0 smoother schedule (dataflow on small grids, streaming on large ones, per-wave
+# launches or streamed residue groups in a slab) sums a row in the same order, so sharded and
+# single-GPU steps agree bit for bit under the default settings.
+ENV = dict(os.environ)
 
 
 def _free_port():
@@ -93,8 +91,7 @@ def test_sharded_two_level_hierarchy(tmp_path):
 
 
 def test_sharded_benchmark_scene_two_steps(tmp_path):
-    """The benchmark workload (cfg2, 1.19M particles): 2 ranks equal 1 GPU bitwise.  Its waves
-    are > 8K rows, so the streaming smoother is the single-GPU default here anyway."""
+    """The benchmark workload (cfg2, 1.19M particles): 2 ranks equal 1 GPU bitwise."""
     scene = "cfg2_twisting_bars.json"
     ref = run_ranks(tmp_path, scene, 1, 2, tag="single")[0]
     ranks = run_ranks(tmp_path, scene, 2, 2)

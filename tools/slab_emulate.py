@@ -173,16 +173,19 @@ def run(sc, particles, R, steps, warmup):
         wall = time.perf_counter() - t
         if comm:
             comm.stop()
-        prof = sim.profile_read()
-        results[r] = dict(outer=outer, wall=wall, info=slabs.shard_info(sim),
-                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0},
-                          state=sim.particles())
+        results[r] = dict(outer=outer, wall=wall)
 
     threads = [threading.Thread(target=body, args=(r,)) for r in range(R)]
     for t in threads:
         t.start()
     for t in threads:
         t.join()
+    # read-backs after every rank is done (a rank that has left the baton protocol must not run
+    # GPU work or PCIe copies next to another rank's timed segment)
+    for r in range(R):
+        prof = sims[r].profile_read()
+        results[r].update(info=slabs.shard_info(sims[r]), state=sims[r].particles(),
+                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0})
     out = dict(ranks=R, outer=results[0]["outer"], rank0_phase_ms_per_step=results[0]["phases"])
     if R == 1:
         out["compute_ms_per_step"] = 1000 * results[0]["wall"] / steps
