@@ -200,7 +200,8 @@ long long hot_kernel_launches(hot_ctx* ctx);
  * Galerkin product and the level-0 smoother / residual between them.  All other state stays
  * replicated and every rank's result is bitwise identical to the single-GPU step.
  * Only the HOT solver (kind 0) with the linear embedding and >= 2 levels shards; other solver
- * configurations run replicated on every rank. */
+ * configurations run replicated on every rank.  Each rank stores only its rows of the level-0
+ * matrix, so after a sharded solve the matrix taps (hot_stage_level_*) report no level. */
 
 /* Caller-owned collectives (tests, or any transport the caller owns: gloo, MPI ...).  Every
  * callback is collective (all ranks call it in the same order) and returns 0 on success.

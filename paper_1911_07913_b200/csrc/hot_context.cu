@@ -97,6 +97,7 @@ struct Level {
   std::vector<int> wave_start_h;
   long long active_slots = 0;
   int radius = 2;  // diagonal-storage radius (3 on quadratic-embedding coarse levels)
+  int h_row0 = 0;  // H holds rows [h_row0, h_row0 + allocated rows) (slabs: only the rank's rows)
   DBuf b, u, r;    // V-cycle vectors
   DenseMap dmap() const {
     DenseMap m;
@@ -113,7 +114,8 @@ struct Level {
     v.coords = coords.as<int>();
     v.map = dmap();
     v.cols = cols.as<int>();
-    v.H = H.as<double>();
+    // rows outside the allocation are never touched (slabs)
+    v.H = H.as<double>() - (long long)h_row0 * 9 * pitch();
     v.dinv = dinv.as<double>();
     v.dir = dir.as<uint8_t>();
     v.radius = radius;
@@ -214,6 +216,7 @@ struct Context {
     int x_lo = 0;                  // Galerkin stage-1 fine rows [x_lo, r_hi): owned + 5 planes
     long long p_lo = 0, p_hi = 0;  // particles of the bins the assembled rows read (planes [P-8, Q+1))
     long long pe_lo = 0;           // particles of the bins the gradient's node pass reads: [pe_lo, p_hi)
+    int h_hi = 0;                  // level-0 matrix rows this rank stores: [a_lo, h_hi) (transposes reach Q+2)
     int b_lo = 0, b_hi = 0;        // those bins (rows of planes [P-1, Q+1))
     int c_lo = 0, c_hi = 0;        // owned level-1 rows (coarse planes [P/2, Q/2))
     int gc_lo = 0;                 // Galerkin stage-2 coarse rows [gc_lo, c_hi): owned + 2 coarse planes
@@ -231,6 +234,9 @@ struct Context {
   } sh;
   DBuf plane_buf;
   DBuf pe_buf, ne_buf, nt_buf;  // per-particle energy, per-node energy, per-node scaled-norm terms
+  long long tu_lo = 0;           // Tu holds the records of particles [tu_lo, ...)
+  /// Record base indexed by particle id (slabs: only [p_lo, p_hi) is allocated and touched).
+  double* tu_base() { return Tu.as<double>() - tu_lo * 126; }
 
   // profiling
   bool prof = false;
@@ -725,6 +731,7 @@ struct Context {
     // (particle tensors) from plane P-8 on.
     sh.a_lo = row_of(sh.P - 7);
     sh.x_lo = row_of(sh.P - 5);
+    sh.h_hi = row_of(sh.Q + 2);
     sh.b_lo = row_of(sh.P - 1);
     sh.b_hi = row_of(sh.Q + 1);
     const int prow[3] = {row_of(sh.P - 8), sh.b_hi, sh.b_lo};
@@ -807,7 +814,7 @@ struct Context {
         if (big >= std::min(512, stream_min_rows())) {
           const int q0 = pass == 0 ? 9 * grp : 45 - 9 * grp;
           launch_sgs_stream(v, sh.wave_starts.as<int>(), sh.wave_rows.as<int>(), 27, u, b, grid_bar.as<unsigned int>(),
-                            stream, q0, q0 + 9);
+                            stream, q0, q0 + 9, big);
         } else {
           for (int k = 0; k < 9; ++k) {
             const int c = 9 * grp + (pass == 0 ? k : 8 - k);
@@ -895,10 +902,12 @@ struct Context {
   }
 
   // ------------------------------------------------------------------ matrix + hierarchy
-  void alloc_level(Level& l) {
+  /// H rows [row0, row0 + rows) (default: all rows); every other array covers all rows.
+  void alloc_level(Level& l, int row0 = 0, int rows = -1) {
     const long long n = std::max(l.n, 1);
     l.cols.ensure(sizeof(int) * n * l.pitch());
-    l.H.ensure(sizeof(double) * n * 9 * l.pitch());
+    l.h_row0 = row0;
+    l.H.ensure(sizeof(double) * std::max<long long>(rows < 0 ? n : rows, 1) * 9 * l.pitch());
     l.dinv.ensure(sizeof(double) * 9 * n);
     l.b.ensure(sizeof(double) * 3 * n);
     l.u.ensure(sizeof(double) * 3 * n);
@@ -910,7 +919,10 @@ struct Context {
   /// reuse_svd: the last energy evaluation stored the SVD at exactly this dv (solve_qn start).
   void assemble(const double* dvp, bool project, bool reuse_svd = false) {
     Level& l0 = L[0];
-    alloc_level(l0);
+    if (sh.on)  // the rows this rank assembles, plus the 2 planes its transposes reach
+      alloc_level(l0, sh.a_lo, sh.h_hi - sh.a_lo);
+    else
+      alloc_level(l0);
     particle_tensors(dvp, project, reuse_svd);
     const int h = prof_begin(P_ASSEMBLE);
     launch_fill_cols(l0.view(), stream);
@@ -919,7 +931,7 @@ struct Context {
       v0.lo = sh.a_lo;
       v0.hi = sh.r_hi;
     }
-    launch_assemble_rows(pview(), bview(), gview(), v0, dx, Tu.as<double>(), grid_bar.as<unsigned int>() + 8, stream);
+    launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), grid_bar.as<unsigned int>() + 8, stream);
     // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
     prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
     have_H = true;
@@ -930,13 +942,15 @@ struct Context {
   /// particle half, objective.hpp:322-340).
   void particle_tensors(const double* dvp, bool project, bool reuse_svd) {
     int h = prof_begin(P_TENSORS);
-    Tu.ensure(sizeof(double) * 126 * std::max<long long>(np, 1));
+    // slabs: records of this rank's particle range only
+    tu_lo = sh.on ? sh.p_lo : 0;
+    Tu.ensure(sizeof(double) * 126 * std::max<long long>(sh.on ? sh.p_hi - sh.p_lo : np, 1));
     if (!reuse_svd) {
       node_u.ensure(sizeof(double) * 3 * std::max(L[0].n, 1));
       launch_node_u(gview(), dvp, nullptr, 0.0, node_u.as<double>(), stream);
     }
     launch_particle_tensors(pview(), gview(), dx, dt, mats_d.as<DevMaterial>(), node_u.as<double>(),
-                            reuse_svd ? svd.as<double>() : nullptr, project ? 1 : 0, Tu.as<double>(), flag_bad(), stream,
+                            reuse_svd ? svd.as<double>() : nullptr, project ? 1 : 0, tu_base(), flag_bad(), stream,
                             sh.on ? sh.p_lo : 0, sh.on ? sh.p_hi : -1);
     prof_end(h, (double)np * (24 + 72 + 8 + 4 + 126 * 8));  // x F vol mat in, kappa*T (packed) + W out
   }
@@ -1067,7 +1081,8 @@ struct Context {
       Level& f = L[m - 1];
       Level& c = L[m];
       const int span = f.radius + 3;  // quadratic X targets per axis
-      gal_x.ensure(sizeof(double) * 9 * (c.radius == 3 ? span * span * span : 64) * std::max(f.n, 1));
+      gal_x.ensure(sizeof(double) * 9 * (c.radius == 3 ? span * span * span : 64) *
+                   std::max(m == 1 && sh.on ? sh.r_hi - sh.x_lo : f.n, 1));
       if (m == 1 && sh.on) {
         // this slab's level-1 rows (and the 2 coarse planes whose transposes complete them), then
         // every rank's rows to every rank: levels >= 1 are replicated
@@ -1077,7 +1092,8 @@ struct Context {
         fv.hi = sh.r_hi;
         cv.lo = sh.gc_lo;
         cv.hi = sh.c_hi;
-        launch_galerkin(fv, cv, gal_x.as<double>(), stream);
+        // X of the fine rows [x_lo, r_hi) only, indexed by fine row
+        launch_galerkin(fv, cv, gal_x.as<double>() - (long long)sh.x_lo * 9 * 64, stream);
         const int hc = prof_begin(P_COMM);
         std::vector<long long> off(sh.crow_off.size());
         for (size_t r = 0; r < off.size(); ++r) off[r] = sh.crow_off[r] * 9LL * c.pitch() * (long long)sizeof(double);
@@ -1340,9 +1356,15 @@ struct Context {
     if (cfg.window > kMaxWindow) throw std::invalid_argument("L-BFGS window too large");
     const double target = cfg.epsilon * std::sqrt((double)n);
     struct ShardOff {  // the cut is per solve; taps and the other solvers run unsharded
-      Shard& s;
-      ~ShardOff() { s.on = false; }
-    } shard_off{sh};
+      Context& c;
+      ~ShardOff() {
+        if (c.sh.on) {  // level 0 holds only this rank's rows: no tap may read it
+          c.have_H = false;
+          c.nlevels = 0;
+        }
+        c.sh.on = false;
+      }
+    } shard_off{*this};
     sh.on = want_shard(levels) && sh.planned;
     HOT_CUDA(cudaMemsetAsync(dv.p, 0, sizeof(double) * std::max<long long>(n3, 1), stream));
     HOT_CUDA(cudaMemsetAsync(iflags.p, 0, sizeof(int) * 8, stream));
@@ -1520,7 +1542,7 @@ struct Context {
       if (variant == 1) {
         particle_tensors(dv.as<double>(), true, false);
         pn_dinv.ensure(sizeof(double) * 9 * std::max(n, 1));
-        launch_mf_block_diag_inv(pview(), bview(), gview(), Tu.as<double>(), pn_dinv.as<double>(), stream);
+        launch_mf_block_diag_inv(pview(), bview(), gview(), tu_base(), pn_dinv.as<double>(), stream);
         Dinv = pn_dinv.as<double>();
       } else {
         assemble(dv.as<double>(), true);
@@ -1552,7 +1574,7 @@ struct Context {
         pn_dP.ensure(sizeof(double) * 9 * std::max<long long>(np, 1));
         inner_this = pcg_level0(
             [&](const double* in, double* o) {
-              launch_mf_multiply(pview(), bview(), gview(), Tu.as<double>(), in, pn_dP.as<double>(), o, stream);
+              launch_mf_multiply(pview(), bview(), gview(), tu_base(), in, pn_dP.as<double>(), o, stream);
             },
             [&](const double* in, double* o) { launch_block_apply(Dinv, in, o, n, stream); }, pn_b.as<double>(),
             pn_x.as<double>(), k, cfg.cg_cap);

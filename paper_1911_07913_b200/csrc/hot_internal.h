@@ -191,7 +191,8 @@ void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* 
 /// Level-0 smoother: both passes, all waves, one persistent kernel with bulk-copy row streaming.
 /// [q_lo, q_hi): the part of the flat (forward waves, then backward waves) sequence to run.
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                       const double* b, unsigned int* bar, cudaStream_t s, int q_lo = 0, int q_hi = -1);
+                       const double* b, unsigned int* bar, cudaStream_t s, int q_lo = 0, int q_hi = -1,
+                       int max_rows = 0);  // max_rows > 0: size the grid for waves of at most that many rows
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s);
 int sgs_max_blocks();

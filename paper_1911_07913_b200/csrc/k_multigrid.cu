@@ -1305,8 +1305,10 @@ int sgs_stream_blocks_t() {
 
 template <int W, int S>
 void launch_sgs_stream_t(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                         const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi) {
+                         const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi, int max_rows) {
+  // fewer CTAs when no wave has rows for all warps: the grid barrier costs grow with the CTA count
   int grid = sgs_stream_blocks_t<W, S>();
+  if (max_rows > 0) grid = std::max(1, std::min(grid, (max_rows + W - 1) / W));
   void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &bar, &q_lo, &q_hi};
   cudaLaunchCooperativeKernel((const void*)k_sgs_stream<W, S>, grid, W * 32, args, stream_smem<W, S>(), s);
   count_launches(1);
@@ -1325,17 +1327,17 @@ int sgs_stream_cfg() {
 int sgs_stream_blocks() { return sgs_stream_blocks_t<8, 2>(); }
 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                       const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi) {
+                       const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi, int max_rows) {
   if (L.n == 0 || nwaves == 0) return;
   if (q_hi < 0) q_hi = 2 * nwaves;
   if (q_hi <= q_lo) return;
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
   switch (sgs_stream_cfg()) {
-    case 1: launch_sgs_stream_t<6, 3>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
-    case 2: launch_sgs_stream_t<4, 4>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
-    case 3: launch_sgs_stream_t<4, 5>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
-    case 4: launch_sgs_stream_t<16, 1>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
-    default: launch_sgs_stream_t<8, 2>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi); break;
+    case 1: launch_sgs_stream_t<6, 3>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
+    case 2: launch_sgs_stream_t<4, 4>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
+    case 3: launch_sgs_stream_t<4, 5>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
+    case 4: launch_sgs_stream_t<16, 1>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
+    default: launch_sgs_stream_t<8, 2>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
   }
 }
 

@@ -44,13 +44,21 @@ def main():
         infos.append(slabs.shard_info(sim))
     p = sim.particles()
     diag = sim.diagnostics()
+    # after a sharded solve level 0 holds only this rank's rows: the matrix taps must refuse
+    from paper_1911_07913_b200 import LogicError
+
+    try:
+        sim.level_shape(0)
+        tap_blocked = 0
+    except LogicError:
+        tap_blocked = 1
     np.savez(out, x=p["x"], v=p["v"], F=p["F"], C=p["C"], stats=np.array(stats),
              sharded=np.array([i["sharded"] for i in infos]),
              rows=np.array([[i["row_lo"], i["row_hi"], i["crow_lo"], i["crow_hi"], i["plane_lo"], i["plane_hi"]]
                             for i in infos]),
              halos=np.array(infos[-1]["halo_exchanges"] if infos else 0),
              gathers=np.array(infos[-1]["gathers"] if infos else 0),
-             energy=diag["energy"], residual=diag["scaled_residual"])
+             energy=diag["energy"], residual=diag["scaled_residual"], tap_blocked=np.array(tap_blocked))
     if size > 1 or transport == "nccl":
         import torch.distributed as dist
 

@@ -68,6 +68,8 @@ def test_sharded_steps_equal_single_gpu_bitwise(tmp_path, scene, steps, size):
         solved = iters > 0
         assert (res["sharded"][solved] == 1).all(), (r, res["sharded"])
         assert res["halos"] > 0 and res["gathers"] > 0
+        if res["sharded"][-1]:
+            assert res["tap_blocked"] == 1  # level 0 is split: no tap reads it
         np.testing.assert_array_equal(res["stats"], ref["stats"])
         for k in ("x", "v", "F", "C", "energy", "residual"):
             np.testing.assert_array_equal(res[k], ref[k], err_msg=f"rank {r} {k}")
