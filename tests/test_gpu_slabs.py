@@ -123,10 +123,10 @@ def test_nccl_transport_single_rank(tmp_path):
         np.testing.assert_array_equal(res[k], ref[k])
 
 
-def _scene_file(tmp_path, name, objects):
+def _scene_file(tmp_path, name, objects, materials=None):
     d = {"dim": 3, "dx": 1.0 / 64, "gravity": [0.0, -9.8, 0.0], "fps": 500, "frames": 4, "epsilon": 1e-05, "seed": 7,
          "ppc": 8, "domain": {"min": [0.0, 0.0, 0.0], "max": [1.0, 1.0, 1.0]},
-         "materials": [{"density": 1000.0, "youngs": 1e5, "poisson": 0.3}],
+         "materials": materials or [{"density": 1000.0, "youngs": 1e5, "poisson": 0.3}],
          "objects": objects,
          "colliders": [{"shape": {"kind": "half_space", "point": [0.0, 0.05, 0.0], "normal": [0.0, 1.0, 0.0]},
                         "motion": {"kind": "static"}}]}
@@ -163,5 +163,23 @@ def test_too_few_planes_runs_replicated(tmp_path):
     ranks = run_ranks(tmp_path, scene, 3, 2, tag="sliver")
     for res in ranks:
         assert not res["sharded"].any()
+        for k in ("x", "v", "F", "C"):
+            np.testing.assert_array_equal(res[k], ref[k])
+
+
+@pytest.mark.parametrize("plasticity", [{"kind": "von_mises", "yield_stress": 3e3},
+                                        {"kind": "snow_clamp", "lo": 0.975, "hi": 1.0075}])
+def test_sharded_plastic_materials(tmp_path, plasticity):
+    """Plastic materials (von Mises, the snow clamp) on stretched boxes that yield at once: the
+    return maps run in the replicated G2P; energy, gradient and assembly are split.  2 ranks
+    equal 1 GPU bitwise over 3 steps."""
+    mat = [{"density": 1000.0, "youngs": 1e5, "poisson": 0.3, "plasticity": plasticity}]
+    scene = _scene_file(tmp_path, "plastic", [_stretched_box([0.35, 0.35, 0.35], [0.6, 0.6, 0.6])], mat)
+    ref = run_ranks(tmp_path, scene, 1, 3, tag="single")[0]
+    assert ref["stats"][:, 1].sum() > 0
+    ranks = run_ranks(tmp_path, scene, 2, 3)
+    for res in ranks:
+        assert res["sharded"].any()
+        np.testing.assert_array_equal(res["stats"], ref["stats"])
         for k in ("x", "v", "F", "C"):
             np.testing.assert_array_equal(res[k], ref[k])
