@@ -801,7 +801,10 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
         const int wi = __ldg(wave_of + i), wc = __ldg(wave_of + c);
         int need = INT_MIN;
         if (pass == 0 ? wc < wi : wc > wi) need = e;
-        if (pass == 1 && c == i) need = e - 1;  // own forward update
+        // backward: every other column's forward update (the row's own included) must be in
+        // before this thread gathers it; with no CTA barrier after the waits, each thread
+        // waits for its own column (forward-earlier rows are usually long done: one poll)
+        else if (pass == 1) need = e - 1;
         if (need != INT_MIN) {
           int v;
           do {
@@ -809,7 +812,9 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
           } while (v < need);
         }
       }
-      __syncthreads();
+      // each thread gathers only the column it waited for (acquire, then load: ordered), so no
+      // CTA barrier between the waits and the gathers: threads whose column is ready gather
+      // while others still wait
       double x0 = 0.0, x1 = 0.0, x2 = 0.0;
       if (s < S) {
         const double* xp = u + 3 * (c >= 0 ? c : 0);  // inactive slots: zero block
