@@ -796,43 +796,54 @@ struct Context {
   /// So a plane's values are final at the end of its residue group, and one halo per group
   /// (the edge plane of that residue, to each neighbour) gives every row exactly the values the
   /// serial sweep reads: 6 exchanges per smoother call instead of 54.
-  void sgs0_sharded(double* u, const double* b) {
+  void sgs0_sharded(double* u, const double* b, bool gathered_after) {
     const Level& l = L[0];
     const LevelView v = l.view();
-    for (int pass = 0; pass < 2; ++pass)
-      for (int gi = 0; gi < 3; ++gi) {
-        const int grp = pass == 0 ? gi : 2 - gi;
-        const int h = prof_begin(P_SGS0);
-        long long rows = 0;
-        int big = 0;
-        for (int c = 9 * grp; c < 9 * grp + 9; ++c) {
-          rows += sh.wave_start[c + 1] - sh.wave_start[c];
-          big = std::max(big, sh.wave_start[c + 1] - sh.wave_start[c]);
-        }
-        // the group's 9 waves in one persistent bulk-copy launch (grid barrier between waves,
-        // ~2 us) unless they are tiny (then one launch per wave)
-        if (big >= std::min(512, stream_min_rows())) {
-          const int q0 = pass == 0 ? 9 * grp : 45 - 9 * grp;
-          launch_sgs_stream(v, sh.wave_starts.as<int>(), sh.wave_rows.as<int>(), 27, u, b, grid_bar.as<unsigned int>(),
-                            stream, q0, q0 + 9, big);
-        } else {
-          for (int k = 0; k < 9; ++k) {
-            const int c = 9 * grp + (pass == 0 ? k : 8 - k);
-            const int cnt = sh.wave_start[c + 1] - sh.wave_start[c];
-            launch_sgs_wave1(v, sh.wave_rows.as<int>() + sh.wave_start[c], cnt, u, b, stream);
-          }
-        }
-        prof_end(h, (double)rows * (72.0 * 125 + 72 + 24 + 48));
-        const std::vector<long long>& e = sh.halo_edges[grp];
-        bool any = false;
-        for (long long x : e) any |= x != 0;
-        if (any) {  // replicated: every rank makes the same decision
-          const int hc = prof_begin(P_COMM);
-          comm->halo(u, e, stream);
-          prof_end(hc);
+    // the sweep as 5 segments of the flat (forward waves 0..26, backward 26..0) sequence:
+    // forward groups 0 and 1, forward + backward group 2 together, backward groups 1 and 0.
+    // A residue-m plane is read by the neighbour only in groups != m, so the values between
+    // the forward and backward group 2 are never read across the cut: no halo there.  The
+    // last halo is skipped when the caller gathers every row right after (post-smoothing).
+    struct Seg {
+      int q0, q1, grp;
+    };
+    const Seg segs[5] = {{0, 9, 0}, {9, 18, 1}, {18, 36, 2}, {36, 45, 1}, {45, 54, 0}};
+    auto wave_of_q = [](int q) { return q < 27 ? q : 53 - q; };
+    for (int si = 0; si < 5; ++si) {
+      const Seg& sg = segs[si];
+      const int h = prof_begin(P_SGS0);
+      long long rows = 0;
+      int big = 0;
+      for (int q = sg.q0; q < sg.q1; ++q) {
+        const int c = wave_of_q(q);
+        rows += sh.wave_start[c + 1] - sh.wave_start[c];
+        big = std::max(big, sh.wave_start[c + 1] - sh.wave_start[c]);
+      }
+      // the segment's waves in one persistent bulk-copy launch (grid barrier between waves,
+      // ~2 us) unless they are tiny (then one launch per wave)
+      if (big >= std::min(512, stream_min_rows())) {
+        launch_sgs_stream(v, sh.wave_starts.as<int>(), sh.wave_rows.as<int>(), 27, u, b, grid_bar.as<unsigned int>(),
+                          stream, sg.q0, sg.q1, big);
+      } else {
+        for (int q = sg.q0; q < sg.q1; ++q) {
+          const int c = wave_of_q(q);
+          const int cnt = sh.wave_start[c + 1] - sh.wave_start[c];
+          launch_sgs_wave1(v, sh.wave_rows.as<int>() + sh.wave_start[c], cnt, u, b, stream);
         }
       }
+      prof_end(h, (double)rows * (72.0 * 125 + 72 + 24 + 48));
+      if (si == 4 && gathered_after) break;
+      const std::vector<long long>& e = sh.halo_edges[sg.grp];
+      bool any = false;
+      for (long long x : e) any |= x != 0;
+      if (any) {  // replicated: every rank makes the same decision
+        const int hc = prof_begin(P_COMM);
+        comm->halo(u, e, stream);
+        prof_end(hc);
+      }
+    }
   }
+
 
   // ------------------------------------------------------------------ objective
   int* flag_bad() { return iflags.as<int>() + 0; }
@@ -1222,7 +1233,7 @@ struct Context {
       HOT_CUDA(cudaMemsetAsync(l.u.p, 0, sizeof(double) * 3 * l.n, stream));
       const bool slab = m == 0 && sh.on;
       if (slab)
-        sgs0_sharded(l.u.as<double>(), l.b.as<double>());
+        sgs0_sharded(l.u.as<double>(), l.b.as<double>(), /*gathered_after=*/false);  // the residual reads halos
       else
         sgs(m, l.u.as<double>(), l.b.as<double>());
       // residual r = b - H u: the level's block-sparse SpMV (H, column ids, u b r)
@@ -1258,7 +1269,7 @@ struct Context {
       launch_prolong_add(l.view(), L[m + 1].view(), L[m + 1].u.as<double>(), l.u.as<double>(), stream);
       prof_end(h, 24.0 * L[m + 1].n + 48.0 * l.n);
       if (m == 0 && sh.on)
-        sgs0_sharded(l.u.as<double>(), l.b.as<double>());
+        sgs0_sharded(l.u.as<double>(), l.b.as<double>(), /*gathered_after=*/true);  // then gather_rows0(u)
       else
         sgs(m, l.u.as<double>(), l.b.as<double>());
     }
