@@ -108,28 +108,30 @@ __global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, int quad, uint8_t
 /// (exact symmetry); Dirichlet projection (multigrid.hpp:287) fused.  Linear embedding: child
 /// 2B+d of B has weight prod_a (d_a ? 1/2 : 1).
 constexpr int kGalX = 64 * 9;  // doubles of X per fine row
-constexpr int kGalXWarps = 4;
+// warps per CTA x ring stages per warp: HOT_GALX_CFG = "WxS" (default 8x1, launch_galerkin)
 
-constexpr int kGalXStages = 2;
+
 constexpr int kGalXRowBytes = 9 * kSlotPitch * 8;  // 9216: one fine row's blocks, contiguous
-constexpr int kGalXSmem = kGalXWarps * (kGalXStages * kGalXRowBytes + kGalXStages * 8);
+template <int W, int S>
+constexpr int galx_smem() { return W * (S * kGalXRowBytes + S * 8); }
 
 /// Stage 1 of the Galerkin product, HBM-streaming: each warp keeps kGalXStages fine rows in
 /// flight through the bulk-copy engine (one 9 KB cp.async.bulk per row, mbarrier completion)
 /// while it contracts the previous row into its 64 coarse targets.
-__global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, double* __restrict__ X) {
+template <int W, int S>
+__global__ void __launch_bounds__(W * 32) k_galerkin_x(LevelView f, double* __restrict__ X) {
   extern __shared__ __align__(128) unsigned char gx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  unsigned char* ring = gx_smem + (size_t)wib * kGalXStages * kGalXRowBytes;
+  unsigned char* ring = gx_smem + (size_t)wib * S * kGalXRowBytes;
   unsigned long long* mb =
-      reinterpret_cast<unsigned long long*>(gx_smem + (size_t)kGalXWarps * kGalXStages * kGalXRowBytes) +
-      wib * kGalXStages;
+      reinterpret_cast<unsigned long long*>(gx_smem + (size_t)W * S * kGalXRowBytes) +
+      wib * S;
   unsigned long long policy = 0;
   if (lane == 0) {
     policy = l2_evict_first_policy();
-    for (int s = 0; s < kGalXStages; ++s) mbar_init(mb + s, 1);
+    for (int s = 0; s < S; ++s) mbar_init(mb + s, 1);
     mbar_fence_init();
   }
   __syncwarp();
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, dou
     bulk_g2s_hint(ring + (size_t)s * kGalXRowBytes, f.H + (long long)row * 9 * kSlotPitch, kGalXRowBytes, bar, policy);
   };
   if (lane == 0)
-    for (int s = 0; s < kGalXStages; ++s)
+    for (int s = 0; s < S; ++s)
       if (f.lo + gw + s * nw < f.hi) issue(f.lo + gw + s * nw, s);
   unsigned phase_bits = 0;
   int s = 0;
@@ -182,8 +184,8 @@ __global__ void __launch_bounds__(kGalXWarps * 32) k_galerkin_x(LevelView f, dou
       for (int k = 0; k < 9; ++k) dst[k] = acc[k];
     }
     __syncwarp();  // the stage is refilled below
-    if (lane == 0 && i + kGalXStages * nw < f.hi) issue(i + kGalXStages * nw, s);
-    s = s + 1 == kGalXStages ? 0 : s + 1;
+    if (lane == 0 && i + S * nw < f.hi) issue(i + S * nw, s);
+    s = s + 1 == S ? 0 : s + 1;
   }
 }
 
@@ -1202,6 +1204,17 @@ void launch_mark_parents(LevelView fine, DenseMap cmap, int quad, uint8_t* flags
 void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, int quad, uint8_t* cdir, cudaStream_t s) {
   if (fine.n) { k_coarse_dirichlet<<<mgrid(fine.n, 256), 256, 0, s>>>(fine, cmap, quad, cdir); count_launches(1); }
 }
+template <int W, int S>
+void launch_galerkin_x_t(LevelView fine, double* X, cudaStream_t s) {
+  static const int gx_blocks = [] {
+    cudaFuncSetAttribute((const void*)k_galerkin_x<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, galx_smem<W, S>());
+    return coop_blocks((const void*)k_galerkin_x<W, S>, W * 32, galx_smem<W, S>());
+  }();
+  const int blocks = (int)std::min<long long>(gx_blocks, ((long long)(fine.hi - fine.lo) + W - 1) / W);
+  k_galerkin_x<W, S><<<std::max(1, blocks), W * 32, galx_smem<W, S>(), s>>>(fine, X);
+  count_launches(1);
+}
+
 void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s) {
   if (coarse.n == 0) return;
   if (coarse.radius == 3) {  // quadratic embedding
@@ -1229,11 +1242,19 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
     count_launches(2);
     return;
   }
-  static const int gx_blocks = coop_blocks((const void*)k_galerkin_x, kGalXWarps * 32, kGalXSmem);
-  {
-    const int blocks = (int)std::min<long long>(gx_blocks, ((long long)(fine.hi - fine.lo) + kGalXWarps - 1) / kGalXWarps);
-    k_galerkin_x<<<std::max(1, blocks), kGalXWarps * 32, kGalXSmem, s>>>(fine, X);
-    count_launches(1);
+  static const int cfg = [] {
+    const char* e = std::getenv("HOT_GALX_CFG");
+    const std::string v = e ? e : "";
+    return v == "4x2" ? 1 : v == "4x3" ? 2 : v == "16x1" ? 4 : v == "4x1" ? 5 : 0;
+  }();
+  // cfg2 hierarchy phase per step: 8x1 0.973 ms (default), 4x1 / 6x1 0.982, 4x2 1.044, 16x1
+  // 1.048, 4x3 1.188, 8x2 1.208: more warps in flight beat a deeper ring
+  switch (cfg) {
+    case 1: launch_galerkin_x_t<4, 2>(fine, X, s); break;
+    case 2: launch_galerkin_x_t<4, 3>(fine, X, s); break;
+    case 4: launch_galerkin_x_t<16, 1>(fine, X, s); break;
+    case 5: launch_galerkin_x_t<4, 1>(fine, X, s); break;
+    default: launch_galerkin_x_t<8, 1>(fine, X, s); break;
   }
   if (coarse.hi > coarse.lo) {
     k_galerkin_c<<<mgrid((long long)(coarse.hi - coarse.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X);
