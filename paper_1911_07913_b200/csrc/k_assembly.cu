@@ -173,12 +173,16 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
 /// template constants, so the per-particle loop has no tile branches.  Each (pair, lane) block
 /// accumulates in registers and is folded into the row's shared accumulator once per pair (bin
 /// o's lanes, then the mirror's: fixed order, no atomics).
-constexpr int kAsmChunk = 2;                                  // particles per bin per stage
-constexpr int kAsmStage = 2 * kAsmChunk * kTensorStride;       // doubles: [bin of pair][particle][...]
-constexpr int kAsmWarpDoubles = 2 * kAsmStage + kUpper * 9 + 1 + 2 + 28;  // + pad + 2 mbarriers + pair table; even
-constexpr int kAsmSmem = kAsmWarps * kAsmWarpDoubles * 8;
+// CH particles per bin per stage; AW warps per CTA (HOT_ASM_CFG = "AWxCH", default 4x2)
+template <int CH>
+constexpr int asm_stage() { return 2 * CH * kTensorStride; }  // doubles: [bin of pair][particle][...]
+template <int CH>
+constexpr int asm_warp_doubles() { return 2 * asm_stage<CH>() + kUpper * 9 + 1 + 2 + 28; }  // + pad + 2 mbarriers + pair table
+template <int AW, int CH>
+constexpr int asm_smem() { return AW * asm_warp_doubles<CH>() * 8; }
 constexpr unsigned kParticleBytes = kTensorStride * 8;  // 1008 = 63 x 16
-static_assert(kAsmWarpDoubles % 2 == 0, "16-byte aligned per-warp smem");
+static_assert(asm_warp_doubles<1>() % 2 == 0 && asm_warp_doubles<2>() % 2 == 0 && asm_warp_doubles<3>() % 2 == 0,
+              "16-byte aligned per-warp smem");
 
 /// S(o) = 25 o0 + 5 o1 + o2 of a stencil position, and kmin(o): the first stencil position k of
 /// the bin at offset o whose slot S(k) + S(o) is in the row's upper triangle (>= 62).
@@ -255,18 +259,19 @@ __device__ __forceinline__ void asm_fold(double* acc, int kmin, int So, int qm, 
   }
 }
 
-__global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
+template <int AW, int CH>
+__global__ void __launch_bounds__(AW * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
                                                                    const double* __restrict__ Tu,
                                                                    unsigned int* __restrict__ row_counter) {
   extern __shared__ __align__(16) double asm_smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // per warp: staging [2 buffers][kAsmStage] | acc [kUpper*9] | pad | mbarriers [2] | pair table
-  double* base = asm_smem + (size_t)wid * kAsmWarpDoubles;
+  // per warp: staging [2 buffers][asm_stage<CH>()] | acc [kUpper*9] | pad | mbarriers [2] | pair table
+  double* base = asm_smem + (size_t)wid * asm_warp_doubles<CH>();
   double* Sbuf = base;
-  double* acc = base + 2 * kAsmStage;
+  double* acc = base + 2 * asm_stage<CH>();
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(acc + kUpper * 9 + 1);
   int* PT = reinterpret_cast<int*>(acc + kUpper * 9 + 1 + 2);  // [14][pb1, n1, pb2, n2]
-  for (int q = lane; q < 2 * kAsmStage; q += 32) Sbuf[q] = 0.0;  // stale slots must hold finite data
+  for (int q = lane; q < 2 * asm_stage<CH>(); q += 32) Sbuf[q] = 0.0;  // stale slots must hold finite data
   __syncwarp();
   if (lane == 0) {
     mbar_init(mbar, 1);
@@ -291,11 +296,11 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
   }
   const bool lane_g = qk < 3;
   const int src8 = 4 * min(qk, 2) + 3;  // the pad lane holding M[8][g]
-  const int nwarps = gridDim.x * kAsmWarps;
+  const int nwarps = gridDim.x * AW;
   // rows are handed out in index order (a work counter, or a static stride without one), so the
   // rows in flight stay a narrow band and their particle bins stay in L2
   auto next_row = [&](int cur) {
-    if (!row_counter) return cur < 0 ? (int)(L.lo + blockIdx.x * kAsmWarps + wid) : cur + nwarps;
+    if (!row_counter) return cur < 0 ? (int)(L.lo + blockIdx.x * AW + wid) : cur + nwarps;
     int r = 0;
     if (lane == 0) r = (int)atomicAdd(row_counter, 1u);
     return L.lo + __shfl_sync(0xffffffffu, r, 0);
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
     // lane 0 runs the bulk-copy producer one chunk ahead along (pair, c0)
     int pq_n = 0, c0_n = 0;  // next chunk to issue (lane 0)
     auto advance = [&]() {   // lane 0: move (pq_n, c0_n) to the next non-empty chunk
-      c0_n += kAsmChunk;
+      c0_n += CH;
       while (pq_n < 14 && c0_n >= max(PT[4 * pq_n + 1], PT[4 * pq_n + 3])) {
         ++pq_n;
         c0_n = 0;
@@ -348,17 +353,17 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
     };
     auto issue = [&](int buf) {  // lane 0: one bulk copy per bin and chunk
       const int pb1 = PT[4 * pq_n], n1 = PT[4 * pq_n + 1], pb2 = PT[4 * pq_n + 2], n2 = PT[4 * pq_n + 3];
-      const int k1 = max(0, min(kAsmChunk, n1 - c0_n)), k2 = max(0, min(kAsmChunk, n2 - c0_n));
+      const int k1 = max(0, min(CH, n1 - c0_n)), k2 = max(0, min(CH, n2 - c0_n));
       const unsigned mb = smem_u32(mbar + buf);
-      double* dst = Sbuf + buf * kAsmStage;
+      double* dst = Sbuf + buf * asm_stage<CH>();
       mbar_expect_tx(mb, (k1 + k2) * kParticleBytes);
       if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0_n) * kRecStride, k1 * kParticleBytes, mb);
       if (k2)
-        bulk_g2s(dst + kAsmChunk * kRecStride, Tu + (long long)(pb2 + c0_n) * kRecStride, k2 * kParticleBytes, mb);
+        bulk_g2s(dst + CH * kRecStride, Tu + (long long)(pb2 + c0_n) * kRecStride, k2 * kParticleBytes, mb);
     };
     if (lane == 0) {
       pq_n = 0;
-      c0_n = -kAsmChunk;
+      c0_n = -CH;
       advance();
       if (pq_n < 14) issue(0);
       advance();
@@ -384,19 +389,19 @@ __global__ void __launch_bounds__(kAsmWarps * 32) k_assemble_rows(BinsView bins,
           oA0[mt] = kRecW + 3 * min(kmin0 + 8 * mt + qm, 26) + min(qk, 2);
           oA1[mt] = kRecW + 3 * min(kmin1 + 8 * mt + qm, 26) + min(qk, 2);
         }
-        for (int c0 = 0; c0 < nmax; c0 += kAsmChunk) {
+        for (int c0 = 0; c0 < nmax; c0 += CH) {
           if (lane == 0) {
             if (pq_n < 14) issue(buf ^ 1);
             advance();
           }
           mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
           phase ^= 1u << buf;
-          const double* S = Sbuf + buf * kAsmStage;
+          const double* S = Sbuf + buf * asm_stage<CH>();
 #pragma unroll 1
-          for (int t = 0; t < kAsmChunk; ++t) {
+          for (int t = 0; t < CH; ++t) {
             asm_particle<NT0>(S + t * kTensorStride, wa0, tb, src8, lane_g && c0 + t < n1, oA0, C0, E0);
             if (NT1 > 0)
-              asm_particle<NT1>(S + (kAsmChunk + t) * kTensorStride, wa1, tb, src8, lane_g && c0 + t < n2, oA1,
+              asm_particle<NT1>(S + (CH + t) * kTensorStride, wa1, tb, src8, lane_g && c0 + t < n2, oA1,
                                 C1, E1);
           }
           __syncwarp();  // buffer buf is refilled by the next iteration's issue
@@ -494,11 +499,10 @@ void launch_fill_cols(LevelView L, cudaStream_t s) {
   { k_fill_cols<<<agrid((long long)L.n * level_pitch(L.radius), 256), 256, 0, s>>>(L, const_cast<int*>(L.cols)); count_launches(1); }
 }
 
-void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
-                          const double* Tu, unsigned int* row_counter, cudaStream_t s) {
-  if (L.hi <= L.lo) return;
-  (void)dx;
-  static const int resident = resident_blocks((const void*)k_assemble_rows, kAsmWarps * 32, kAsmSmem);
+template <int AW, int CH>
+void launch_assemble_rows_t(BinsView bins, GridView g, LevelView L, const double* Tu, unsigned int* row_counter,
+                            cudaStream_t s) {
+  static const int resident = resident_blocks((const void*)k_assemble_rows<AW, CH>, AW * 32, asm_smem<AW, CH>());
   static const bool dynamic = [] {
     const char* e = std::getenv("HOT_ASM_ROWS");
     return !(e && std::string(e) == "static");
@@ -511,9 +515,29 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
     row_counter = nullptr;
     blocks = (long long)num_sms() * 16;
   }
-  blocks = std::min<long long>(blocks, ((long long)(L.hi - L.lo) + kAsmWarps - 1) / kAsmWarps);
-  k_assemble_rows<<<(int)blocks, kAsmWarps * 32, kAsmSmem, s>>>(bins, g, L, Tu, row_counter);
+  blocks = std::min<long long>(blocks, ((long long)(L.hi - L.lo) + AW - 1) / AW);
+  k_assemble_rows<AW, CH><<<(int)blocks, AW * 32, asm_smem<AW, CH>(), s>>>(bins, g, L, Tu, row_counter);
   count_launches(1);
+}
+
+void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
+                          const double* Tu, unsigned int* row_counter, cudaStream_t s) {
+  if (L.hi <= L.lo) return;
+  (void)dx;
+  (void)P;
+  static const int cfg = [] {
+    const char* e = std::getenv("HOT_ASM_CFG");
+    const std::string v = e ? e : "";
+    return v == "4x1" ? 1 : v == "8x1" ? 2 : v == "2x2" ? 3 : v == "4x3" ? 4 : v == "6x1" ? 5 : 0;
+  }();
+  switch (cfg) {
+    case 1: launch_assemble_rows_t<4, 1>(bins, g, L, Tu, row_counter, s); break;
+    case 2: launch_assemble_rows_t<8, 1>(bins, g, L, Tu, row_counter, s); break;
+    case 3: launch_assemble_rows_t<2, 2>(bins, g, L, Tu, row_counter, s); break;
+    case 4: launch_assemble_rows_t<4, 3>(bins, g, L, Tu, row_counter, s); break;
+    case 5: launch_assemble_rows_t<6, 1>(bins, g, L, Tu, row_counter, s); break;
+    default: launch_assemble_rows_t<4, 2>(bins, g, L, Tu, row_counter, s); break;
+  }
 }
 
 }  // namespace hotb200
