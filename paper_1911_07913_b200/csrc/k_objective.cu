@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "hot_internal.h"
 #include "hot_particle.cuh"
@@ -41,7 +43,8 @@ __device__ __forceinline__ double block_sum(double v) {
 
 constexpr int kEnergyThreads = 128;  // ~146 registers: 3 blocks (12 warps) per SM
 
-__global__ void __launch_bounds__(kEnergyThreads, 4) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
+template <int NT, int MINB, bool CONTIG = false>
+__global__ void __launch_bounds__(NT, MINB) k_particle_energy(ParticlesView P, GridView g, double dx, double dt,
                                                                  const DevMaterial* __restrict__ mats,
                                                                  const double* __restrict__ u,
                                                                  double* __restrict__ stress,
@@ -49,8 +52,13 @@ __global__ void __launch_bounds__(kEnergyThreads, 4) k_particle_energy(Particles
                                                                  double* __restrict__ pe, int* bad, long long plo,
                                                                  long long phi) {
   const long long n = P.n;
-  for (long long p = plo + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < phi;
-       p += (long long)gridDim.x * blockDim.x) {
+  // CONTIG: each block walks one contiguous chunk of the (bin-ordered) particles, so the
+  // stencil nodes its particles share stay in its SM's L1; otherwise a grid stride
+  const long long chunk = CONTIG ? (phi - plo + gridDim.x - 1) / gridDim.x : 0;
+  const long long p0 = CONTIG ? plo + blockIdx.x * chunk : plo + blockIdx.x * (long long)blockDim.x;
+  const long long p1 = CONTIG ? min(phi, p0 + chunk) : phi;
+  const long long stride = CONTIG ? (long long)blockDim.x : (long long)gridDim.x * blockDim.x;
+  for (long long p = p0 + threadIdx.x; p < p1; p += stride) {
     M3 F, Fn;
     if (!virtual_F(P, p, g, dx, dt, u, F, Fn)) {
       atomicExch(bad, 1);
@@ -329,15 +337,47 @@ int vgrid(long long n) {
 
 }  // namespace
 
+template <int NT, int MINB, bool CONTIG = false>
+void launch_particle_energy_t(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
+                              const double* u, double* stress, double* svd_out, double* pe, int nblocks, int* bad_flag,
+                              cudaStream_t s, long long plo, long long phi, int grid_scale = 1) {
+  // grid_scale x the thread count of nblocks x 128 threads over the particles (grid-stride)
+  const long long want = (phi - plo + NT - 1) / NT;
+  const long long cap = (long long)nblocks * kEnergyThreads * grid_scale / NT;
+  k_particle_energy<NT, MINB, CONTIG><<<(int)std::max<long long>(1, std::min<long long>(cap, want)), NT, 0, s>>>(
+      P, g, dx, dt, mats, u, stress, svd_out, pe, bad_flag, plo, phi);
+  count_launches(1);
+}
+
 void launch_particle_energy(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
                             const double* u, double* stress, double* svd_out, double* pe, int nblocks, int* bad_flag,
                             cudaStream_t s, long long plo, long long phi) {
   if (phi < 0) phi = P.n;
   if (phi <= plo) return;
-  const long long want = (phi - plo + kEnergyThreads - 1) / kEnergyThreads;
-  k_particle_energy<<<(int)std::max<long long>(1, std::min<long long>(nblocks, want)), kEnergyThreads, 0, s>>>(
-      P, g, dx, dt, mats, u, stress, svd_out, pe, bad_flag, plo, phi);
-  count_launches(1);
+  static const int cfg = [] {  // HOT_ENERGY_CFG = "threads x min blocks per SM" (default 512x1)
+    const char* e = std::getenv("HOT_ENERGY_CFG");
+    const std::string v = e ? e : "";
+    return v == "128x3" ? 1 : v == "64x8" ? 2 : v == "256x2" ? 3 : v == "128x2" ? 4 : v == "512x1" ? 5 :
+           v == "256x2b" ? 6 : v == "256x2h" ? 7 : v == "128x4c" ? 8 : v == "256x2c" ? 9 : v == "512x1c" ? 10 : v == "128x4" ? 11 : 0;
+  }();
+  switch (cfg) {
+    case 1: launch_particle_energy_t<128, 3>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 2: launch_particle_energy_t<64, 8>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 3: launch_particle_energy_t<256, 2>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 4: launch_particle_energy_t<128, 2>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 5: launch_particle_energy_t<512, 1>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 6: launch_particle_energy_t<256, 2>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi, 2); break;
+    case 7: launch_particle_energy_t<128, 4>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks / 2, bad_flag, s, plo, phi); break;
+    case 8: launch_particle_energy_t<128, 4, true>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 9: launch_particle_energy_t<256, 2, true>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 10: launch_particle_energy_t<512, 1, true>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    case 11: launch_particle_energy_t<128, 4>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
+    // cfg2 particle energy per step: 512x1 one resident wave 0.672 ms (default), 512x1 two waves
+    // 0.676, 256x2 0.755, 128x4 0.80, 512x1 / 256x2 / 128x4 with contiguous per-block chunks
+    // 0.73 / 0.82 / 0.86, 128x3 / 128x2 0.99: wide blocks keep a bin-ordered run of particles,
+    // whose stencils overlap, on one SM
+    default: launch_particle_energy_t<512, 1>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks / 2, bad_flag, s, plo, phi); break;
+  }
 }
 
 void launch_node_energy(GridView g, BinsView bins, const double* pe, double dt, const double* grav, const double* dv,
