@@ -37,7 +37,8 @@ constexpr int kTensorStride = kRecStride;
 /// particle's values, then the warp writes the 32 records part by part, consecutive lanes on
 /// consecutive addresses (a thread-per-particle store pattern puts every lane on its own line).
 constexpr int kTWarps = 4;
-__global__ void __launch_bounds__(kTWarps * 32) k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
+template <int MINB>
+__global__ void __launch_bounds__(kTWarps * 32, MINB) k_particle_tensors(ParticlesView P, GridView g, double dx, double dt,
                                                                    const DevMaterial* __restrict__ mats,
                                                                    const double* __restrict__ u,
                                                                    const double* __restrict__ svd_in, int project,
@@ -487,8 +488,19 @@ void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, doub
   if (phi < 0) phi = P.n;
   if (phi <= plo) return;
   const long long chunks = (phi - plo + 31) / 32;
-  k_particle_tensors<<<(int)std::min<long long>((chunks + kTWarps - 1) / kTWarps, 16LL * num_sms()), kTWarps * 32, 0,
-                       s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi);
+  // HOT_TENSORS_MINB: min CTAs per SM (register cap).  cfg2 tensors phase per step: 1 (253
+  // registers, default) 0.419 ms, 3 (168, small spills) 0.434, 4 (128) 0.495, 6 (80) 0.672
+  static const int minb = [] {
+    const char* e = std::getenv("HOT_TENSORS_MINB");
+    return e ? std::atoi(e) : 1;
+  }();
+  const int tgrid_ = (int)std::min<long long>((chunks + kTWarps - 1) / kTWarps, 16LL * num_sms());
+  switch (minb) {
+    case 3: k_particle_tensors<3><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
+    case 4: k_particle_tensors<4><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
+    case 6: k_particle_tensors<6><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
+    default: k_particle_tensors<1><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
+  }
   k_particle_W<<<(int)std::min<long long>((chunks + kWWarps - 1) / kWWarps, 32LL * num_sms()), kWWarps * 32, 0, s>>>(
       P, dx, Tu, plo, phi);
   count_launches(2);
