@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "hot_internal.h"
 #include "hot_particle.cuh"
@@ -334,8 +335,9 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_p2g(ParticlesView P, Bin
 /// P2G, node half: one thread per node sums its 27 bins' contributions in offset order (bin at
 /// offset o - 1, where the node is stencil position 26 - o), then v = mom / m and the characteristic-norm scale
 /// (objective.hpp:445-463); resets the boundary fields.
-__global__ void __launch_bounds__(256) k_p2g(GridView g, const double* __restrict__ B, double ell, double dt, int lo,
-                                             int hi) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_p2g(GridView g, const double* __restrict__ B, double ell, double dt, int lo,
+                                            int hi) {
   for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
     double m = 0.0, mom0 = 0.0, mom1 = 0.0, mom2 = 0.0, num = 0.0;
     const int* nbi = g.nb27 + 27LL * i;
@@ -553,7 +555,7 @@ void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, co
   if (g.n == 0) return;
   if (jhi < 0) jhi = g.n;
   if (hi < 0) hi = g.n;
-  static const int blocks = resident_blocks((const void*)k_p2g, 256, 0);
+  static const int blocks = resident_blocks((const void*)k_p2g<256>, 256, 0);
   static const int bin_blocks = resident_blocks((const void*)k_bin_p2g, kBinWarps * 32, 0);
   if (jhi > jlo) {
     k_bin_p2g<<<std::min<long long>(bin_blocks, (jhi - jlo + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
@@ -561,7 +563,16 @@ void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, co
     count_launches(1);
   }
   if (hi > lo) {
-    k_p2g<<<std::min<long long>(blocks, (hi - lo + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt, lo, hi);
+    static const int nt_ = [] {  // HOT_NODE_THREADS: threads per block of the node passes (default 256)
+      const char* e = std::getenv("HOT_NODE_THREADS");
+      return e ? std::atoi(e) : 256;
+    }();
+    if (nt_ == 1024)
+      k_p2g<1024><<<std::min<long long>(blocks / 4 + 1, (hi - lo + 1023) / 1024), 1024, 0, s>>>(g, bin_part, ell, dt, lo, hi);
+    else if (nt_ == 512)
+      k_p2g<512><<<std::min<long long>(blocks / 2 + 1, (hi - lo + 511) / 512), 512, 0, s>>>(g, bin_part, ell, dt, lo, hi);
+    else
+      k_p2g<256><<<std::min<long long>(blocks, (hi - lo + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt, lo, hi);
     count_launches(1);
   }
 }

@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_bin_force(ParticlesView P, B
 /// in offset order (bin at offset o - 1, where the node is stencil position 26 - o), fused with
 /// the node's scaled-norm term (objective.hpp:476-486) nt[i] = |g_i|^2 / scale_i^2, rows
 /// [lo, hi).  The norm is a fixed-tree sum over nt[0, n) (split-independent).
-__global__ void __launch_bounds__(kRedThreads) k_node_gradient(GridView g, double dt, double g0, double g1, double g2,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_node_gradient(GridView g, double dt, double g0, double g1, double g2,
                                                                const double* __restrict__ S,
                                                                const double* __restrict__ dv, double* __restrict__ gout,
                                                                double* __restrict__ nt, int* bad, int lo, int hi) {
@@ -400,8 +401,19 @@ void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, dou
     count_launches(1);
   }
   if (hi > lo) {
-    k_node_gradient<<<std::max(1, std::min((hi - lo + kRedThreads - 1) / kRedThreads, 16 * num_sms())), kRedThreads, 0,
-                      s>>>(g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
+    static const int nt_ = [] {  // HOT_NODE_THREADS: threads per block of the node passes (default 256)
+      const char* e = std::getenv("HOT_NODE_THREADS");
+      return e ? std::atoi(e) : 256;
+    }();
+    if (nt_ == 1024)
+      k_node_gradient<1024><<<std::max(1, std::min((hi - lo + 1023) / 1024, 4 * num_sms())), 1024, 0, s>>>(
+          g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
+    else if (nt_ == 512)
+      k_node_gradient<512><<<std::max(1, std::min((hi - lo + 511) / 512, 8 * num_sms())), 512, 0, s>>>(
+          g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
+    else
+      k_node_gradient<256><<<std::max(1, std::min((hi - lo + 255) / 256, 16 * num_sms())), 256, 0, s>>>(
+          g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
     count_launches(1);
   }
 }
