@@ -1160,11 +1160,26 @@ struct Context {
     build_values(built);
   }
 
+  /// Coarse-PCG rows per warp when sizing its cooperative grid (HOT_PCG_RPW; default 2).  cfg2
+  /// coarse PCG per step: 2 rows per warp 0.309 ms, 4 0.351, 8 0.576, 16 1.046 (more CTAs, each
+  /// with fewer rows, beat cheaper grid barriers here; 1 row per warp hits the CTA cap)
+  static int pcg_rows_per_warp() {
+    static const int v = [] {
+      const char* e = std::getenv("HOT_PCG_RPW");
+      return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    return v;
+  }
+
   /// Few, fat CTAs for the cooperative kernels: the grid barrier costs grow with the number of
   /// participating CTAs, while one wave / one PCG row-sweep only has tens to thousands of rows.
   static int coop_grid(int max_blocks, int rows, int warps_per_block, int rows_per_warp) {
     const int want = (rows + warps_per_block * rows_per_warp - 1) / (warps_per_block * rows_per_warp);
-    return std::max(1, std::min(std::min(max_blocks, 2 * num_sms()), want));
+    static const int per_sm = [] {  // HOT_PCG_CAP: CTAs per SM at most (default 2)
+      const char* e = std::getenv("HOT_PCG_CAP");
+      return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    return std::max(1, std::min(std::min(max_blocks, per_sm * num_sms()), want));
   }
 
   /// Rows per wave from which the level-0 smoother streams (k_sgs_stream); below it the
@@ -1258,7 +1273,8 @@ struct Context {
       const int cap = pinned ? pinned_cap : 10000;
       launch_pcg(bot.view(), bot.b.as<double>(), bot.u.as<double>(), pcg_r.as<double>(), pcg_z.as<double>(),
                  pcg_p.as<double>(), pcg_Ap.as<double>(), rel, cap, partials.as<double>() + 6 * nred,
-                 iflags.as<int>() + 4, iflags.as<int>() + 2, coop_grid(pcg_max_blocks(), bot.n, 8, 4), stream);
+                 iflags.as<int>() + 4, iflags.as<int>() + 2, coop_grid(pcg_max_blocks(), bot.n, 8, pcg_rows_per_warp()),
+                 stream);
       prof_end(h);
       // status word -> iflags[1] (max over the solve)
       copy_status();
