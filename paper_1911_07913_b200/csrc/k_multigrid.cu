@@ -1168,7 +1168,11 @@ int coop_blocks(const void* fn, int threads, int smem = 0) {
 template <int R>
 int sgs_flow_blocks() {
   static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
+  if (!v) {
+    v = coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
+    const char* e = std::getenv("HOT_FLOW_CTAS_PER_SM");  // experiment knob: fewer co-resident CTAs
+    if (e && std::atoi(e) > 0) v = std::min(v, std::atoi(e) * num_sms());
+  }
   return v;
 }
 
