@@ -6,7 +6,7 @@
 //   allgather_ranges  rank r's [off[r], off[r+1]) to every rank (level-1 matrix rows after the
 //                     Galerkin split, the level-0 residual and smoother output rows);
 //   halo              rank r's first / last lattice planes to its two neighbours (level-0 u after
-//                     every smoother wave: the 27 waves of a sweep are the only serial chain);
+//                     each residue group of smoother waves, hot_context.cu sgs0_sharded);
 //   allreduce_max     a few host ints (failure flags of sharded kernels, so every rank takes the
 //                     same branch and no rank is left waiting in a collective).
 #pragma once
