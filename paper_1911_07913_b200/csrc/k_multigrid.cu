@@ -1170,8 +1170,12 @@ int sgs_flow_blocks() {
   static int v = 0;
   if (!v) {
     v = coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
-    const char* e = std::getenv("HOT_FLOW_CTAS_PER_SM");  // experiment knob: fewer co-resident CTAs
-    if (e && std::atoi(e) > 0) v = std::min(v, std::atoi(e) * num_sms());
+    // at most 4 CTAs per SM (HOT_FLOW_CTAS_PER_SM; 0 = every co-resident CTA): cfg2 level-1
+    // smoother 0.998 vs 1.029 ms per step, the config-5 96^3 set 2.03 vs 2.04; the grid size
+    // does not change any value (the dataflow enforces the serial order)
+    const char* e = std::getenv("HOT_FLOW_CTAS_PER_SM");
+    const int cap = e ? std::atoi(e) : 4;
+    if (cap > 0) v = std::min(v, cap * num_sms());
   }
   return v;
 }
