@@ -1170,11 +1170,12 @@ int sgs_flow_blocks() {
   static int v = 0;
   if (!v) {
     v = coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
-    // at most 4 CTAs per SM (HOT_FLOW_CTAS_PER_SM; 0 = every co-resident CTA): cfg2 level-1
-    // smoother 0.998 vs 1.029 ms per step, the config-5 96^3 set 2.03 vs 2.04; the grid size
-    // does not change any value (the dataflow enforces the serial order)
+    // HOT_FLOW_CTAS_PER_SM caps the co-resident CTAs (0 / unset = all).  At 4 per SM the cfg2
+    // level-1 smoother drops 1.03 -> 1.00 ms per step but the level-0 streaming smoother that
+    // follows it rises 1.70 -> 1.91 (measured, bench.py), so the default keeps every CTA.  The
+    // grid size changes no value (the dataflow enforces the serial order).
     const char* e = std::getenv("HOT_FLOW_CTAS_PER_SM");
-    const int cap = e ? std::atoi(e) : 4;
+    const int cap = e ? std::atoi(e) : 0;
     if (cap > 0) v = std::min(v, cap * num_sms());
   }
   return v;
