@@ -1,20 +1,26 @@
 #!/usr/bin/env python
 """Benchmark of the B200 HOT implicit-MPM step (BASELINE.json metric: implicit MPM
-particle-steps/s, fp64, fixed tolerance; plus the dominant kernel's HBM roofline).
+particle-steps/s, fp64, fixed tolerance; plus the dominant kernel's roofline).
 
-Workload: BASELINE config 2, stiffness-contrast twisting bars (scenes/cfg2_twisting_bars.json:
-four 0.6 x 0.08 x 0.08 bars, dx = 0.6/128, 8 ppc jittered, 1,193,126 particles, soft/stiff
-segments E = 1e5 / 1e9, ends driven by rotating kinematic colliders at +-1 rad/s, fixed-
-corotated (the reference's only model), eps = 1e-5).  One step = one advance_step
-(simulation.hpp:286-323): activation + binning + P2G, the HOT solve, G2P + strain + advect.
+Headline workload: BASELINE configs[1], stiffness-contrast twisting bars
+(scenes/cfg2_twisting_bars.json: four 0.6 x 0.08 x 0.08 bars, dx = 0.6/128, 8 ppc jittered,
+1,193,126 particles, soft/stiff segments E = 1e5 / 1e9, ends driven by rotating kinematic
+colliders at +-1 rad/s, fixed-corotated (the reference's only model), eps = 1e-5, dt = CFL 0.6
+under a 1/24 s frame cap).  One step = one advance_step (simulation.hpp:286-323): activation +
+binning + P2G, the HOT solve, G2P + strain + advect.  The other single-GPU BASELINE configs
+(cfg4 colliding snow, 4.0M particles; cfg3 metal impact) are timed in the same run and reported
+under "other_configs".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
---impl reference times the reference CPU path (the oracle port, all host threads) on a
-bounded slab of the same workload.  Under torchrun (N > 1) the ranks share ONE copy of the
-workload and the solve is cut into slabs of lattice planes along axis 0 (NCCL inside the
-library): scaling "strong", value = the scene's particle-steps / the max over
-ranks of the device time.  --mode replicas runs N independent copies instead ("weak").
+--impl reference times the reference CPU path on the box's host cores: the oracle port of
+hotmpm::advance_step (oracle/, a line-by-line restatement; the reference itself needs Eigen,
+which no box has), all host threads, on the SAME full scene, sampled by the oracle's own
+restatement of sample_scene_particles, for the same warm-up and timed steps.  That arm never
+loads the product library.  Under torchrun (N > 1) the ranks share ONE copy of the workload and
+the solve is cut into slabs of lattice planes along axis 0 (NCCL inside the library;
+DESIGN.md §6): scaling "strong", value = the scene's particle-steps / the max over ranks of the
+device time.  --mode replicas runs N independent copies instead ("weak").
 """
 import argparse
 import json
@@ -97,38 +103,109 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def cpu_slab(particles, n_keep):
-    """Bounded CPU sample: the n_keep particles nearest the left end (x < x_cut across all four
-    bars): the driven end (rotating collider) plus free soft/stiff material beyond it, so the
-    sampled steps need the same solves as the full scene."""
-    order = np.argsort(particles["x"][:, 0], kind="stable")[: max(1, min(n_keep, particles["x"].shape[0]))]
-    keep = np.sort(order)
-    return {k: v[keep] for k, v in particles.items()}
+WORKLOADS = {
+    "cfg2_twisting_bars.json": "cfg2 twisting bars (BASELINE configs[1]), FCR, dt = CFL 0.6 (1/24 s frame cap), eps=1e-5",
+    "cfg4_snow.json": "cfg4 colliding snow boxes (BASELINE configs[3]), snow clamp, dt = CFL 0.6, eps=1e-5",
+    "cfg3_metal_impact.json": "cfg3 von Mises metal sphere on plate (BASELINE configs[2]), dt = CFL 0.6, eps=1e-5",
+}
+OTHER_SCENES = ["cfg4_snow.json", "cfg3_metal_impact.json"]
 
 
-def run_cpu_reference(sc, particles, steps, warmup, threads, n_keep):
-    """The reference CPU path (oracle port of hotmpm::advance_step) on the bounded slab."""
+def workload_config(scene, scene_path, n_particles):
+    """The workload description, identical in both arms (built from the scene JSON alone)."""
+    name = os.path.basename(scene_path)
+    return {"workload": WORKLOADS.get(name, name), "scene": name, "particles": int(n_particles),
+            "dx": scene["dx"], "ppc": scene.get("ppc", 0), "fps_cap": scene.get("fps", 24),
+            "levels": scene.get("levels", 3), "window": scene.get("window", 8), "epsilon": scene.get("epsilon", 1e-7),
+            "l2": "inputs larger than L2 (level-0 matrix > 126 MB)"}
+
+
+def frame_end(scene, k):
+    """frame_end of the k-th step (0-based) in both arms: step k may advance at most to (k+1)/fps."""
+    return (k + 1) / scene.get("fps", 24)
+
+
+def oracle_run(scene, steps, warmup, threads, keep=None):
+    """The reference CPU path: the oracle port of hotmpm::advance_step on the oracle's own sampled
+    particles (sample_scene_particles restated, simulation.hpp:221-254).  keep(x) -> bool mask
+    selects a bounded sample (cpu_baseline); None = the full scene.  Imports only oracle/."""
     from oracle import oracle as O
 
     O.set_threads(threads)
-    slab = cpu_slab(particles, n_keep)
-    orc = O.Oracle(3)
-    orc.set_scene(sc.source)
-    orc.set_particles(slab["x"], slab["v"], slab["mass"], slab["volume"], slab["F"].reshape(-1),
-                      slab["C"].reshape(-1), slab["material"])
-    t_all, n_steps = 0.0, 0
-    outer = []
+    orc = O.Oracle(int(scene.get("dim", 3)))
+    orc.set_scene(scene)
+    orc.sample_scene()
+    if keep is not None:
+        p = orc.get_particles()
+        m = keep(p["x"])
+        orc.set_particles(p["x"][m], p["v"][m], p["mass"][m], p["volume"][m], p["F"][m].reshape(-1),
+                          p["C"][m].reshape(-1), p["material"][m])
+    n = orc.particle_count()
+    t_all, outer = 0.0, []
     for k in range(warmup + steps):
         t0 = time.perf_counter()
-        st = orc.advance_step((k + 1) / sc.fps)
+        st = orc.advance_step(frame_end(scene, k))
         dt = time.perf_counter() - t0
         if k >= warmup:
             t_all += dt
-            n_steps += 1
             outer.append(st["outer_iterations"])
-    n = slab["x"].shape[0]
-    return dict(value=n * n_steps / t_all, particles=n, steps=n_steps, seconds=t_all, outer=outer,
-                ms_per_step=1000 * t_all / max(n_steps, 1), x_cut=float(slab["x"][:, 0].max()))
+    return dict(value=n * steps / t_all, particles=n, steps=steps, seconds=t_all, outer=outer,
+                ms_per_step=1000 * t_all / max(steps, 1))
+
+
+def reference_arm(args):
+    """--impl reference: rank 0 alone, all host threads, the full scene, the same W + K steps."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    with open(args.scene) as f:
+        scene = json.load(f)
+    threads = os.cpu_count() or 1
+    r = oracle_run(scene, max(args.steps, 1), args.warmup, threads)
+    config = workload_config(scene, args.scene, r["particles"])
+    sample = (f"the full scene ({r['particles']} particles), {args.warmup} warm-up + {r['steps']} timed steps from "
+              f"t=0 (the GPU arm's step sequence), oracle port of hotmpm::advance_step, {threads} threads; "
+              f"outer iterations {r['outer']}")
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling)",
+            "config": config, "outer_iterations": r["outer"],
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def gpu_other_config(name, device, steps=5, warmup=2):
+    """Device-resident particle-steps/s of another BASELINE scene on this GPU (no reference arm)."""
+    import torch
+
+    from paper_1911_07913_b200 import Simulation, load_scene_file, sample_scene_particles
+
+    path = os.path.join(ROOT, "scenes", name)
+    sc = load_scene_file(path)
+    p = sample_scene_particles(sc)
+    sim = Simulation(sc, device=device)
+    sim.set_particles(**p)
+    stream = torch.cuda.ExternalStream(sim.stream(), device=device)
+    for k in range(warmup):
+        sim.advance_step(frame_end(sc.source, k))
+    torch.cuda.synchronize(device)
+    sim.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    outer = []
+    e0.record(stream)
+    for k in range(warmup, warmup + steps):
+        outer.append(sim.advance_step(frame_end(sc.source, k))["outer_iterations"])
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    ms = e0.elapsed_time(e1)
+    prof = sim.profile_read()
+    sim.close()
+    n = p["x"].shape[0]
+    return {"config": workload_config(sc.source, path, n), "value": n * steps / (ms / 1000.0), "unit": UNIT,
+            "ms_per_step": ms / steps, "steps": steps, "warmup": warmup, "outer_iterations": outer,
+            "phase_ms_per_step": {k: round(v["ms"] / steps, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
+                                  if v["ms"] > 0}}
 
 
 def main():
@@ -139,8 +216,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scene", default=SCENE)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--mode", default="slabs", choices=["slabs", "replicas"], help="N > 1: slab-sharded or replicas")
     args = ap.parse_args()
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
 
     rank, world, local_rank = dist_env()
     from paper_1911_07913_b200 import load_scene_file, sample_scene_particles
@@ -148,30 +230,7 @@ def main():
     sc = load_scene_file(args.scene)
     particles = sample_scene_particles(sc)
     n_particles = particles["x"].shape[0]
-    config = {"workload": "cfg2 twisting bars (BASELINE configs[1]), FCR, eps=1e-5", "scene": os.path.basename(args.scene),
-              "particles": n_particles, "dx": sc.dx, "ppc": 8, "levels": sc.levels, "window": sc.window,
-              "epsilon": sc.epsilon, "l2": "inputs larger than L2 (level-0 matrix > 126 MB)"}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        threads = os.cpu_count() or 1
-        # slab sized so the whole run stays within ~2.5 min of CPU time: ~2.5K particle-steps/s
-        # per thread on this workload (1 outer iteration per step)
-        n_keep = int(2500 * threads * 150 / (max(args.steps, 1) + args.warmup))
-        r = run_cpu_reference(sc, particles, max(args.steps, 1), args.warmup, threads, n_keep)
-        sample = (f"{r['particles']} particles (x < {r['x_cut']:.3f} m slab of all four bars: driven end + free "
-                  f"material), {args.warmup} warm-up + {r['steps']} timed steps from t=0 (the GPU arm's step "
-                  f"sequence), {threads} threads; outer iterations {r['outer']}")
-        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling)",
-                "config": config,
-                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
-                                 "sample": sample},
-                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return
+    config = workload_config(sc.source, args.scene, n_particles)
 
     import torch
 
@@ -210,16 +269,14 @@ def main():
         torch.cuda.synchronize(device)
 
     step_no = 0
-
-    def frame_end():
-        return (step_no + 1) / sc.fps
-
     for _ in range(args.warmup):
-        sim.advance_step(frame_end())
+        sim.advance_step(frame_end(sc.source, step_no))
         step_no += 1
     sim.clear_diagnostics()
 
-    # ---- device-resident timed region
+    # ---- device-resident timed region.  The per-phase profile stays on: it records CUDA-event
+    # pairs on the context stream and nothing else (no extra kernel, no host synchronisation;
+    # the active-slot counts behind the algorithmic bytes are snapshotted on the device).
     barrier()
     sim.profile(True)
     launches0 = sim.kernel_launches()
@@ -228,7 +285,7 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         for _ in range(args.steps):
-            st = sim.advance_step(frame_end())
+            st = sim.advance_step(frame_end(sc.source, step_no))
             step_no += 1
             outer.append(st["outer_iterations"])
         ev1.record(stream)
@@ -271,7 +328,7 @@ def main():
     for _ in range(e2e_steps):
         sim.set_particles(pinned["x"], pinned["v"], static["mass"], static["volume"], pinned["F"], pinned["C"],
                           static["material"])
-        e2e_outer.append(sim.advance_step(frame_end())["outer_iterations"])
+        e2e_outer.append(sim.advance_step(frame_end(sc.source, step_no))["outer_iterations"])
         step_no += 1
         sim.particles(out=pinned)
     e1.record(stream)
@@ -292,7 +349,7 @@ def main():
     if "assemble_rows" in prof and prof["assemble_rows"]["ms"] > 0:
         ph = prof["assemble_rows"]
         ach = ph["flops"] / (ph["ms"] / 1000.0) / 1e12
-        roofline = {"bound": "fp64", "kernel": "k_assemble_rows", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+        roofline = {"bound": "tensor", "pipe": "fp64 DMMA m8n8k4", "kernel": "k_assemble_rows", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": TRAFFIC.get("assemble_rows"),
                     "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
                     "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
@@ -316,11 +373,24 @@ def main():
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = run_cpu_reference(sc, particles, 1, 0, 1, 100000)
+        # 1 thread (the reference default, cli.cpp:26) on a bounded sample: the first 0.05 m of
+        # all four bars (driven end + free material), the oracle's own sampling, 1 step from t=0
+        x_cut = 0.05
+        r = oracle_run(sc.source, 1, 0, 1, keep=lambda x: x[:, 0] < x_cut)
         cpu_baseline = {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "port",
-                        "sample": f"{r['particles']} particles (x < {r['x_cut']:.3f} m slab of all four bars), 1 step from t=0, "
+                        "sample": f"{r['particles']} particles (x < {x_cut} m slab of all four bars), 1 step from t=0, "
                                   f"oracle port of hotmpm::advance_step, 1 thread (reference default), "
                                   f"{r['seconds']:.1f} s, outer iterations {r['outer']}"}
+
+    other = None
+    if rank == 0 and world == 1 and not args.no_other_configs:
+        sim.close()
+        other = {}
+        for name in OTHER_SCENES:
+            try:
+                other[name] = gpu_other_config(name, device)
+            except Exception as e:  # reported, never fatal to the headline
+                other[name] = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         phases = {k: round(v["ms"] / args.steps, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
@@ -329,14 +399,15 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if slabbed else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded scene sampling, reference schema)",
-                "config": dict(config, parallelism=(f"slabs x{world} (axis-0 lattice planes, NCCL)" if slabbed else
-                                                    f"replicas x{world}" + (f" (slab transport failed: {slab_error})" if slab_error else "")
-                                                    if world > 1 else "single GPU"),
-                               outer_iterations=outer, phase_ms_per_step=phases, rank0_shard=shard),
+                "config": config,
+                "parallelism": (f"slabs x{world} (axis-0 lattice planes, NCCL)" if slabbed else
+                                f"replicas x{world}" + (f" (slab transport failed: {slab_error})" if slab_error else "")
+                                if world > 1 else "single GPU"),
+                "outer_iterations": outer, "phase_ms_per_step": phases, "rank0_shard": shard,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps, "outer_iterations": e2e_outer},
                 "gpu_launches": int(launches), "roofline": roofline, "roofline_hbm": roofline_hbm, "hbm_phases": hbm_all,
-                "cpu_baseline": cpu_baseline,
+                "cpu_baseline": cpu_baseline, "other_configs": other,
                 "clocks": clocks.summary()}
         print(json.dumps(line))
     sim.close()

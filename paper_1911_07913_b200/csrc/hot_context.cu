@@ -83,6 +83,29 @@ struct DBuf {
   }
 };
 
+/// Test and diagnostic hooks, read from the environment once per context (hot_create).  None of
+/// them changes a value: the schedules they select are bitwise identical.
+struct Options {
+  bool shard_force = false;        // HOT_SHARD_FORCE: the slab path at one rank (transport test)
+  bool sgs_level0_waves = false;   // HOT_SGS_LEVEL0=waves: one launch per level-0 wave
+  bool sgs_coarse_barrier = false; // HOT_SGS_COARSE=barrier: grid-barrier coarse smoother
+  bool sgs_trace = false;          // HOT_SGS_TRACE: per-wave timing of the barrier smoother
+  bool verbose = false;            // HOT_VERBOSE: per-solve diagnostics on stderr
+  int stream_min_rows = 8 * 1024;  // HOT_SGS_STREAM_MIN: rows per wave from which level 0 streams
+  void read_env() {
+    auto eq = [](const char* k, const char* v) {
+      const char* e = std::getenv(k);
+      return e && std::strcmp(e, v) == 0;
+    };
+    shard_force = std::getenv("HOT_SHARD_FORCE") != nullptr;
+    sgs_level0_waves = eq("HOT_SGS_LEVEL0", "waves");
+    sgs_coarse_barrier = eq("HOT_SGS_COARSE", "barrier");
+    sgs_trace = std::getenv("HOT_SGS_TRACE") != nullptr;
+    verbose = std::getenv("HOT_VERBOSE") != nullptr;
+    if (const char* e = std::getenv("HOT_SGS_STREAM_MIN")) stream_min_rows = std::atoi(e);
+  }
+};
+
 constexpr int kMaxLevels = 8;
 constexpr int kMaxWindow = 64;
 
@@ -161,6 +184,16 @@ enum Phase {
 
 struct Context {
   int device = 0;
+  Options opt;
+  DBuf active_dev;  // ull[kMaxLevels]: active slots per level of the current hierarchy (k_fill_cols)
+  static constexpr int kProfSolves = 8192;
+  DBuf prof_slots;  // ull[kProfSolves][kMaxLevels]: active_dev snapshot per profiled solve
+  int prof_solve = -1;
+  struct SlotTerm {
+    int phase, solve, level;
+    double coef;
+  };
+  std::vector<SlotTerm> slot_terms;
   cudaStream_t stream = nullptr;
   std::string err;
 
@@ -317,6 +350,20 @@ struct Context {
     phase_bytes[events[h].phase] += bytes;
     phase_flops[events[h].phase] += flops;
   }
+  /// Algorithmic bytes proportional to a level's active-slot count: coef x (active slots of level
+  /// m in the current profiled solve).  The counts stay on the device (k_fill_cols counts them;
+  /// one device-to-device snapshot per solve) and are only read by hot_profile_read, so profiling
+  /// adds no kernel and no host synchronisation to the step.
+  void prof_slot_bytes(int h, int m, double coef) {
+    if (h < 0 || prof_solve < 0) return;
+    slot_terms.push_back(SlotTerm{events[h].phase, prof_solve, m, coef});
+  }
+  void prof_snapshot_slots() {
+    if (!prof || prof_solve + 1 >= kProfSolves) return;
+    ++prof_solve;
+    HOT_CUDA(cudaMemcpyAsync(prof_slots.as<unsigned long long>() + (size_t)prof_solve * kMaxLevels, active_dev.p,
+                             sizeof(unsigned long long) * kMaxLevels, cudaMemcpyDeviceToDevice, stream));
+  }
   void sync() { HOT_CUDA(cudaStreamSynchronize(stream)); }
   void check_launch() {
     cudaError_t e = cudaGetLastError();
@@ -334,12 +381,15 @@ struct Context {
 
   void init(int dev) {
     device = dev;
+    opt.read_env();
     HOT_CUDA(cudaSetDevice(dev));
     HOT_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     HOT_CUDA(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
     HOT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     HOT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     struct_flags.ensure(sizeof(int) * 16);
+    active_dev.ensure(sizeof(unsigned long long) * kMaxLevels);
+    HOT_CUDA(cudaMemset(active_dev.p, 0, sizeof(unsigned long long) * kMaxLevels));
     grid_bar.ensure(sizeof(unsigned int) * 16);
     HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
     HOT_CUDA(cudaMallocHost(&host_int, sizeof(int) * 64));
@@ -693,8 +743,7 @@ struct Context {
   bool want_shard(int levels) const {
     // HOT_SHARD_FORCE=1 (test hook): take the sharded path with one rank too, so the transport's
     // calls run on a one-GPU box (one slab; halos have no peer, gathers broadcast to self)
-    static const bool force = std::getenv("HOT_SHARD_FORCE") != nullptr;
-    return comm && (comm->size > 1 || force) && cfg.embedding == 1 && levels >= 2;
+    return comm && (comm->size > 1 || opt.shard_force) && cfg.embedding == 1 && levels >= 2;
   }
   /// First level-0 row at or after absolute lattice plane `plane` (axis 0).
   int row_of(int plane) const {
@@ -821,7 +870,7 @@ struct Context {
       }
       // the segment's waves in one persistent bulk-copy launch (grid barrier between waves,
       // ~2 us) unless they are tiny (then one launch per wave)
-      if (big >= std::min(512, stream_min_rows())) {
+      if (big >= std::min(512, opt.stream_min_rows)) {
         launch_sgs_stream(v, sh.wave_starts.as<int>(), sh.wave_rows.as<int>(), 27, u, b, grid_bar.as<unsigned int>(),
                           stream, sg.q0, sg.q1, big);
       } else {
@@ -936,7 +985,7 @@ struct Context {
       alloc_level(l0);
     particle_tensors(dvp, project, reuse_svd);
     const int h = prof_begin(P_ASSEMBLE);
-    launch_fill_cols(l0.view(), stream);
+    launch_fill_cols(l0.view(), active_dev.as<unsigned long long>(), stream);
     LevelView v0 = l0.view();
     if (sh.on) {  // this slab's rows and the rows whose transposes complete them
       v0.lo = sh.a_lo;
@@ -1068,7 +1117,7 @@ struct Context {
       c.dir.ensure(std::max(nc, 1));
       HOT_CUDA(cudaMemsetAsync(c.dir.p, 0, nc, st));
       launch_coarse_dirichlet(f.view(), c.dmap(), quad, c.dir.as<uint8_t>(), st);
-      launch_fill_cols(c.view(), st);
+      launch_fill_cols(c.view(), active_dev.as<unsigned long long>() + m, st);
       level_waves(m, st, tmp);
       built = m + 1;
     }
@@ -1160,33 +1209,17 @@ struct Context {
     build_values(built);
   }
 
-  /// Coarse-PCG rows per warp when sizing its cooperative grid (HOT_PCG_RPW; default 2).  cfg2
-  /// coarse PCG per step: 2 rows per warp 0.309 ms, 4 0.351, 8 0.576, 16 1.046 (more CTAs, each
-  /// with fewer rows, beat cheaper grid barriers here; 1 row per warp hits the CTA cap)
-  static int pcg_rows_per_warp() {
-    static const int v = [] {
-      const char* e = std::getenv("HOT_PCG_RPW");
-      return e ? std::max(1, std::atoi(e)) : 2;
-    }();
-    return v;
-  }
+  /// Coarse-PCG rows per warp when sizing its cooperative grid.  cfg2 coarse PCG per step: 2
+  /// rows per warp 0.309 ms, 4 0.351, 8 0.576, 16 1.046 (more CTAs, each with fewer rows, beat
+  /// cheaper grid barriers here; 1 row per warp hits the CTA cap)
+  static int pcg_rows_per_warp() { return 2; }
 
   /// Few, fat CTAs for the cooperative kernels: the grid barrier costs grow with the number of
   /// participating CTAs, while one wave / one PCG row-sweep only has tens to thousands of rows.
+  /// At most 2 CTAs per SM.
   static int coop_grid(int max_blocks, int rows, int warps_per_block, int rows_per_warp) {
     const int want = (rows + warps_per_block * rows_per_warp - 1) / (warps_per_block * rows_per_warp);
-    static const int per_sm = [] {  // HOT_PCG_CAP: CTAs per SM at most (default 2)
-      const char* e = std::getenv("HOT_PCG_CAP");
-      return e ? std::max(1, std::atoi(e)) : 2;
-    }();
-    return std::max(1, std::min(std::min(max_blocks, per_sm * num_sms()), want));
-  }
-
-  /// Rows per wave from which the level-0 smoother streams (k_sgs_stream); below it the
-  /// dataflow kernel (single GPU) or per-wave launches (slabs) run.
-  static int stream_min_rows() {
-    const char* env = std::getenv("HOT_SGS_STREAM_MIN");  // test hook: force either schedule
-    return env ? std::atoi(env) : 8 * 1024;
+    return std::max(1, std::min(std::min(max_blocks, 2 * num_sms()), want));
   }
 
   void sgs(int m, double* u, const double* b) {
@@ -1194,11 +1227,9 @@ struct Context {
     const int h = prof_begin(m == 0 ? P_SGS0 : P_SGSC);
     // large waves stream best as plain launches; small waves (coarse levels) run in one
     // persistent cooperative kernel with a grid barrier between waves
-    const int stream_min = stream_min_rows();
-    const char* sched = std::getenv("HOT_SGS_LEVEL0");  // "waves" | "stream" (default)
-    const bool per_wave = sched && std::strcmp(sched, "waves") == 0;
-    const char* coarse_sched = std::getenv("HOT_SGS_COARSE");  // "flow" (default) | "barrier"
-    const bool flow = !(coarse_sched && std::strcmp(coarse_sched, "barrier") == 0);
+    const int stream_min = opt.stream_min_rows;
+    const bool per_wave = opt.sgs_level0_waves;
+    const bool flow = !opt.sgs_coarse_barrier;
     if (l.radius != 2 || (l.max_wave < stream_min && flow)) {  // radius-3 levels: dataflow kernel only
       launch_sgs_flow(l.view(), l.wave_rows.as<int>(), l.wave_of.as<int>(), u, b, l.sgs_flag.as<int>(), l.sgs_epoch,
                       stream);
@@ -1211,7 +1242,7 @@ struct Context {
     else
     {
       long long* trace = nullptr;
-      if (std::getenv("HOT_SGS_TRACE")) {
+      if (opt.sgs_trace) {
         sgs_trace.ensure(sizeof(long long) * 4 * 1025);
         HOT_CUDA(cudaMemsetAsync(sgs_trace.p, 0, sizeof(long long) * 4 * 1025, stream));
         trace = sgs_trace.as<long long>();
@@ -1235,7 +1266,8 @@ struct Context {
                      tail / nw, bar / nw, mhz);
       }
     }
-    prof_end(h, 2.0 * (72.0 * l.active_slots + 72.0 * l.n + 24.0 * l.n + 48.0 * l.n));
+    prof_end(h, 2.0 * (72.0 * l.n + 24.0 * l.n + 48.0 * l.n));
+    prof_slot_bytes(h, m, 2.0 * 72.0);
   }
 
   /// vcycle (multigrid.hpp:363-392), adaptive coarse mode; coarse iterations accumulate into
@@ -1260,7 +1292,8 @@ struct Context {
       }
       launch_residual(lv, l.b.as<double>(), l.u.as<double>(), l.r.as<double>(), stream);
       const double frac = slab && l.n ? (double)(sh.r_hi - sh.r_lo) / l.n : 1.0;
-      prof_end(hs, frac * (72.0 * l.active_slots + 4.0 * l.pitch() * l.n + 72.0 * l.n));
+      prof_end(hs, frac * (4.0 * l.pitch() * l.n + 72.0 * l.n));
+      prof_slot_bytes(hs, m, frac * 72.0);
       if (slab) gather_rows0(l.r.p);  // restriction (replicated) reads every fine row
       const int h = prof_begin(P_RESID);
       launch_restrict(l.view(), L[m + 1].view(), l.r.as<double>(), L[m + 1].b.as<double>(), stream);
@@ -1408,8 +1441,9 @@ struct Context {
     sh.last = sh.on;
     if (sh.on) ++sh.solves;
     assemble_and_build_hierarchy(dv.as<double>(), levels, cfg.embedding, /*reuse_svd=*/true);
-    static const bool verbose = std::getenv("HOT_VERBOSE") != nullptr;
-    if (prof || verbose)  // active-slot counts only feed the profile's algorithmic bytes
+    const bool verbose = opt.verbose;
+    prof_snapshot_slots();  // active-slot counts of this solve's levels (profile bytes)
+    if (verbose)
       for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
     if (verbose)
       for (int m = 0; m < nlevels; ++m)
@@ -1574,8 +1608,7 @@ struct Context {
       } else {
         assemble(dv.as<double>(), true);
         build_hierarchy(variant == 2 ? cfg.levels : 1, cfg.embedding);
-        if (prof)
-          for (int m = 0; m < nlevels; ++m) L[m].active_slots = count_active_slots(m);
+        prof_snapshot_slots();
         Dinv = L[0].dinv.as<double>();
       }
       // gpg = g^T D^-1 g (solvers.hpp:263-268); k = adaptive_cg_tolerance
@@ -1757,9 +1790,20 @@ struct hot_ctx {
 
 namespace {
 
+/// Makes the context's device current for the call and restores the caller's device after it
+/// (a host thread may drive contexts on several GPUs, or switch devices between calls).
+struct DeviceScope {
+  int saved = -1;
+  explicit DeviceScope(const hot_ctx* ctx);
+  ~DeviceScope() {
+    if (saved >= 0) cudaSetDevice(saved);
+  }
+};
+
 template <typename F>
 int guard(hot_ctx* ctx, F&& f) {
   try {
+    DeviceScope scope(ctx);
     f();
     return HOT_OK;
   } catch (const hotb200::SolverFailure& e) {
@@ -1786,6 +1830,16 @@ int guard(hot_ctx* ctx, F&& f) {
   }
 }
 
+DeviceScope::DeviceScope(const hot_ctx* ctx) {
+  if (!ctx) return;
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  if (cur != ctx->c.device) {
+    HOT_CUDA(cudaSetDevice(ctx->c.device));
+    saved = cur;
+  }
+}
+
 thread_local std::string g_create_error;
 
 void need_state(Context& c) {
@@ -1808,6 +1862,7 @@ int hot_create(hot_ctx** out, const hot_scene* scene, int device) {
   if (!out || !scene) return HOT_E_INVALID_ARGUMENT;
   *out = nullptr;
   auto* h = new hot_ctx;
+  h->c.device = device;  // guard() makes it current and restores the caller's device afterwards
   const int rc = guard(h, [&] {
     h->c.init(device);
     h->c.set_scene(*scene);
@@ -1821,7 +1876,15 @@ int hot_create(hot_ctx** out, const hot_scene* scene, int device) {
   return HOT_OK;
 }
 
-void hot_destroy(hot_ctx* ctx) { delete ctx; }
+void hot_destroy(hot_ctx* ctx) {
+  if (!ctx) return;
+  try {
+    DeviceScope scope(ctx);
+    delete ctx;
+  } catch (...) {
+    delete ctx;
+  }
+}
 
 const char* hot_last_error(const hot_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_create_error.c_str(); }
 
@@ -2086,6 +2149,10 @@ int hot_profile_enable(hot_ctx* ctx, int enable) {
     }
     c.events.clear();
     for (double& b : c.phase_bytes) b = 0;
+    for (double& f : c.phase_flops) f = 0;
+    c.slot_terms.clear();
+    c.prof_solve = -1;
+    if (enable) c.prof_slots.ensure(sizeof(unsigned long long) * Context::kProfSolves * hotb200::kMaxLevels);
     c.prof = enable != 0;
   });
 }
@@ -2102,12 +2169,20 @@ int hot_profile_read(hot_ctx* ctx, char* names, double* total_ms, long long* lau
       ms[e.phase] += t;
       cnt[e.phase] += 1;
     }
+    std::vector<double> slot_bytes(hotb200::kPhases, 0.0);
+    if (c.prof_solve >= 0) {
+      std::vector<unsigned long long> act((size_t)(c.prof_solve + 1) * hotb200::kMaxLevels);
+      HOT_CUDA(cudaMemcpy(act.data(), c.prof_slots.p, sizeof(unsigned long long) * act.size(), cudaMemcpyDeviceToHost));
+      for (const auto& t : c.slot_terms)
+        slot_bytes[t.phase] += t.coef * (double)act[(size_t)t.solve * hotb200::kMaxLevels + t.level];
+    }
     const int k = std::min(cap, hotb200::kPhases);
     for (int i = 0; i < k; ++i) {
       std::snprintf(names + 32 * i, 32, "%s", hotb200::kPhaseNames[i]);
       total_ms[i] = ms[i];
       launches[i] = cnt[i];
-      bytes[i] = c.phase_bytes[i] > 0 ? c.phase_bytes[i] : -c.phase_flops[i];  // < 0: fp64 flops
+      const double b = c.phase_bytes[i] + slot_bytes[i];
+      bytes[i] = b > 0 ? b : -c.phase_flops[i];  // < 0: fp64 flops
     }
     *n = k;
   });
@@ -2137,7 +2212,6 @@ int hot_nccl_unique_id(unsigned char id[128]) {
 int hot_set_comm_nccl(hot_ctx* ctx, const unsigned char id[128], int rank, int size) {
   if (!ctx || !id) return HOT_E_INVALID_ARGUMENT;
   return guard(ctx, [&] {
-    HOT_CUDA(cudaSetDevice(ctx->c.device));
     ctx->c.comm.reset(hotb200::make_nccl_comm(id, rank, size));
   });
 }

@@ -151,7 +151,8 @@ void launch_final_velocity(GridView g, const double* dv, double* out, cudaStream
 void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
                              const double* u, const double* svd_in, int project, double* Tu, int* bad_flag,
                              cudaStream_t s, long long plo = 0, long long phi = -1);  // particles [plo, phi)
-void launch_fill_cols(LevelView L, cudaStream_t s);
+/// Column ids of every slot (-1 inactive); *active = the level's active-slot count.
+void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s);
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, unsigned int* row_counter, cudaStream_t s);
 
@@ -212,10 +213,16 @@ void launch_soa_to_aos(const double* in, double* out, long long n, int comps, cu
 void launch_soa_to_aos_perm(const double* in, double* out, long long n, int comps, const int* perm, cudaStream_t s);
 void launch_iota(int* out, long long n, cudaStream_t s);
 
+constexpr int kMaxDevices = 64;
+/// SM count of the current device (cached per device).
 int num_sms();
+/// cudaFuncAttributeMaxDynamicSharedMemorySize = smem for fn on the current device (once per
+/// device; a no-op at <= 48 KB).
+void set_max_dynamic_smem(const void* fn, int smem);
 /// Co-resident CTAs of a kernel (occupancy x SMs).  Grid-stride kernels whose neighbouring
 /// items share data launch exactly this many CTAs, so at any time the active items form one
 /// contiguous window (L2 reuse) instead of being strided across the whole domain.
+/// Memoized per (device, fn, threads, smem); sets the dynamic shared-memory attribute first.
 int resident_blocks(const void* fn, int threads, int smem);
 
 /// Kernel launches issued by this process (all contexts); every launch_* wrapper counts.

@@ -145,8 +145,9 @@ __global__ void __launch_bounds__(kWWarps * 32) k_particle_W(ParticlesView P, do
   }
 }
 
-__global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
+__global__ void k_fill_cols(LevelView L, int* __restrict__ cols, unsigned long long* __restrict__ active) {
   const int R = L.radius, P = level_pitch(R), S = level_slots(R), W = 2 * R + 1;
+  unsigned long long cnt = 0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)L.n * P;
        t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t / P), s = (int)(t % P);
@@ -155,7 +156,11 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
       c = dense_lookup(L.map, L.coords[3 * i] + s / (W * W) - R, L.coords[3 * i + 1] + (s / W) % W - R,
                        L.coords[3 * i + 2] + s % W - R);
     cols[t] = c;
+    cnt += c >= 0 ? 1 : 0;
   }
+  // active-slot count of the level (algorithmic bytes of the profile), one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(active, cnt);
 }
 
 /// Row gather (objective.hpp:331-357), one warp per row i.  A particle p of a bin whose stencil
@@ -174,7 +179,7 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols) {
 /// template constants, so the per-particle loop has no tile branches.  Each (pair, lane) block
 /// accumulates in registers and is folded into the row's shared accumulator once per pair (bin
 /// o's lanes, then the mirror's: fixed order, no atomics).
-// CH particles per bin per stage; AW warps per CTA (HOT_ASM_CFG = "AWxCH", default 4x2)
+// CH particles per bin per stage; AW warps per CTA (4 x 2, launch_assemble_rows)
 template <int CH>
 constexpr int asm_stage() { return 2 * CH * kTensorStride; }  // doubles: [bin of pair][particle][...]
 template <int CH>
@@ -297,16 +302,14 @@ __global__ void __launch_bounds__(AW * 32) k_assemble_rows(BinsView bins, GridVi
   }
   const bool lane_g = qk < 3;
   const int src8 = 4 * min(qk, 2) + 3;  // the pad lane holding M[8][g]
-  const int nwarps = gridDim.x * AW;
-  // rows are handed out in index order (a work counter, or a static stride without one), so the
+  // rows are handed out in index order (a work counter), so the
   // rows in flight stay a narrow band and their particle bins stay in L2
-  auto next_row = [&](int cur) {
-    if (!row_counter) return cur < 0 ? (int)(L.lo + blockIdx.x * AW + wid) : cur + nwarps;
+  auto next_row = [&]() {
     int r = 0;
     if (lane == 0) r = (int)atomicAdd(row_counter, 1u);
     return L.lo + __shfl_sync(0xffffffffu, r, 0);
   };
-  for (int i = next_row(-1); i < L.hi; i = next_row(i)) {
+  for (int i = next_row(); i < L.hi; i = next_row()) {
     for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
     // the write-out's column ids and Dirichlet flags, loaded now so their latency hides under
     // the gather: slot s = lane + 32 j (zero fill), upper slot 62 + lane + 32 j
@@ -488,47 +491,19 @@ void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, doub
   if (phi < 0) phi = P.n;
   if (phi <= plo) return;
   const long long chunks = (phi - plo + 31) / 32;
-  // HOT_TENSORS_MINB: min CTAs per SM (register cap).  cfg2 tensors phase per step: 1 (253
-  // registers, default) 0.419 ms, 3 (168, small spills) 0.434, 4 (128) 0.495, 6 (80) 0.672
-  static const int minb = [] {
-    const char* e = std::getenv("HOT_TENSORS_MINB");
-    return e ? std::atoi(e) : 1;
-  }();
+  // min CTAs per SM 1 (253 registers): cfg2 tensors phase 0.419 ms per step against 0.434 /
+  // 0.495 / 0.672 ms at 3 / 4 / 6 (register caps that spill)
   const int tgrid_ = (int)std::min<long long>((chunks + kTWarps - 1) / kTWarps, 16LL * num_sms());
-  switch (minb) {
-    case 3: k_particle_tensors<3><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
-    case 4: k_particle_tensors<4><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
-    case 6: k_particle_tensors<6><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
-    default: k_particle_tensors<1><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi); break;
-  }
+  k_particle_tensors<1><<<tgrid_, kTWarps * 32, 0, s>>>(P, g, dx, dt, mats, u, svd_in, project, Tu, bad_flag, plo, phi);
   k_particle_W<<<(int)std::min<long long>((chunks + kWWarps - 1) / kWWarps, 32LL * num_sms()), kWWarps * 32, 0, s>>>(
       P, dx, Tu, plo, phi);
   count_launches(2);
 }
 
-void launch_fill_cols(LevelView L, cudaStream_t s) {
+void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s) {
+  cudaMemsetAsync(active, 0, sizeof(unsigned long long), s);
   if (L.n == 0) return;
-  { k_fill_cols<<<agrid((long long)L.n * level_pitch(L.radius), 256), 256, 0, s>>>(L, const_cast<int*>(L.cols)); count_launches(1); }
-}
-
-template <int AW, int CH>
-void launch_assemble_rows_t(BinsView bins, GridView g, LevelView L, const double* Tu, unsigned int* row_counter,
-                            cudaStream_t s) {
-  static const int resident = resident_blocks((const void*)k_assemble_rows<AW, CH>, AW * 32, asm_smem<AW, CH>());
-  static const bool dynamic = [] {
-    const char* e = std::getenv("HOT_ASM_ROWS");
-    return !(e && std::string(e) == "static");
-  }();
-  long long blocks;
-  if (dynamic) {  // resident grid, rows from the work counter
-    cudaMemsetAsync(row_counter, 0, sizeof(unsigned int), s);
-    blocks = resident;
-  } else {  // oversubscribed grid (16 CTAs per SM), static row stride
-    row_counter = nullptr;
-    blocks = (long long)num_sms() * 16;
-  }
-  blocks = std::min<long long>(blocks, ((long long)(L.hi - L.lo) + AW - 1) / AW);
-  k_assemble_rows<AW, CH><<<(int)blocks, AW * 32, asm_smem<AW, CH>(), s>>>(bins, g, L, Tu, row_counter);
+  k_fill_cols<<<agrid((long long)L.n * level_pitch(L.radius), 256), 256, 0, s>>>(L, const_cast<int*>(L.cols), active);
   count_launches(1);
 }
 
@@ -537,19 +512,14 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
   if (L.hi <= L.lo) return;
   (void)dx;
   (void)P;
-  static const int cfg = [] {
-    const char* e = std::getenv("HOT_ASM_CFG");
-    const std::string v = e ? e : "";
-    return v == "4x1" ? 1 : v == "8x1" ? 2 : v == "2x2" ? 3 : v == "4x3" ? 4 : v == "6x1" ? 5 : 0;
-  }();
-  switch (cfg) {
-    case 1: launch_assemble_rows_t<4, 1>(bins, g, L, Tu, row_counter, s); break;
-    case 2: launch_assemble_rows_t<8, 1>(bins, g, L, Tu, row_counter, s); break;
-    case 3: launch_assemble_rows_t<2, 2>(bins, g, L, Tu, row_counter, s); break;
-    case 4: launch_assemble_rows_t<4, 3>(bins, g, L, Tu, row_counter, s); break;
-    case 5: launch_assemble_rows_t<6, 1>(bins, g, L, Tu, row_counter, s); break;
-    default: launch_assemble_rows_t<4, 2>(bins, g, L, Tu, row_counter, s); break;
-  }
+  // 4 warps x 2 particles per bin chunk (cfg2 assembly per step: 4x2 3.56 ms, 2x2 3.54, 4x1
+  // 3.55, 6x1 3.73, 8x1 3.93, 4x3 3.92); a resident grid taking rows from the work counter
+  constexpr int AW = 4, CH = 2;
+  const int resident = resident_blocks((const void*)k_assemble_rows<AW, CH>, AW * 32, asm_smem<AW, CH>());
+  cudaMemsetAsync(row_counter, 0, sizeof(unsigned int), s);
+  const long long blocks = std::min<long long>(resident, ((long long)(L.hi - L.lo) + AW - 1) / AW);
+  k_assemble_rows<AW, CH><<<(int)blocks, AW * 32, asm_smem<AW, CH>(), s>>>(bins, g, L, Tu, row_counter);
+  count_launches(1);
 }
 
 }  // namespace hotb200

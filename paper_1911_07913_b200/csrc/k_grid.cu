@@ -13,6 +13,10 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "hot_internal.h"
 #include "hot_particle.cuh"
@@ -488,23 +492,54 @@ int grid_for(long long n, int threads) {
 
 }  // namespace
 
+namespace {
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+std::mutex g_dev_mutex;
+}  // namespace
+
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  // per device: a process may drive contexts on several GPUs
+  static int n[kMaxDevices] = {};
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  if (n[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
+}
+
+void set_max_dynamic_smem(const void* fn, int smem) {
+  if (smem <= 48 * 1024) return;
+  static std::set<std::tuple<int, const void*, int>> done;
+  const auto key = std::make_tuple(current_device(), fn, smem);
+  std::lock_guard<std::mutex> lk(g_dev_mutex);
+  if (done.count(key)) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done.insert(key);
 }
 
 int resident_blocks(const void* fn, int threads, int smem) {
+  static std::map<std::tuple<int, const void*, int, int>, int> memo;
+  const auto key = std::make_tuple(current_device(), fn, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mutex);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  set_max_dynamic_smem(fn, smem);
   int per_sm = 0;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   if (per_sm < 1) per_sm = 1;
-  return per_sm * num_sms();
+  const int v = per_sm * num_sms();
+  std::lock_guard<std::mutex> lk(g_dev_mutex);
+  memo[key] = v;
+  return v;
 }
 
 void launch_particle_bounds(const ParticlesView& P, double dx, int* bounds6, int* bad_flag, cudaStream_t s) {
@@ -555,24 +590,15 @@ void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, co
   if (g.n == 0) return;
   if (jhi < 0) jhi = g.n;
   if (hi < 0) hi = g.n;
-  static const int blocks = resident_blocks((const void*)k_p2g<256>, 256, 0);
-  static const int bin_blocks = resident_blocks((const void*)k_bin_p2g, kBinWarps * 32, 0);
+  const int blocks = resident_blocks((const void*)k_p2g<256>, 256, 0);
+  const int bin_blocks = resident_blocks((const void*)k_bin_p2g, kBinWarps * 32, 0);
   if (jhi > jlo) {
     k_bin_p2g<<<std::min<long long>(bin_blocks, (jhi - jlo + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
         P, bins, g, dx, mats, bin_part, jlo, jhi);
     count_launches(1);
   }
   if (hi > lo) {
-    static const int nt_ = [] {  // HOT_NODE_THREADS: threads per block of the node passes (default 256)
-      const char* e = std::getenv("HOT_NODE_THREADS");
-      return e ? std::atoi(e) : 256;
-    }();
-    if (nt_ == 1024)
-      k_p2g<1024><<<std::min<long long>(blocks / 4 + 1, (hi - lo + 1023) / 1024), 1024, 0, s>>>(g, bin_part, ell, dt, lo, hi);
-    else if (nt_ == 512)
-      k_p2g<512><<<std::min<long long>(blocks / 2 + 1, (hi - lo + 511) / 512), 512, 0, s>>>(g, bin_part, ell, dt, lo, hi);
-    else
-      k_p2g<256><<<std::min<long long>(blocks, (hi - lo + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt, lo, hi);
+    k_p2g<256><<<std::min<long long>(blocks, (hi - lo + 255) / 256), 256, 0, s>>>(g, bin_part, ell, dt, lo, hi);
     count_launches(1);
   }
 }

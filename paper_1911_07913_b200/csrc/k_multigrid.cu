@@ -108,7 +108,7 @@ __global__ void k_coarse_dirichlet(LevelView f, DenseMap cmap, int quad, uint8_t
 /// (exact symmetry); Dirichlet projection (multigrid.hpp:287) fused.  Linear embedding: child
 /// 2B+d of B has weight prod_a (d_a ? 1/2 : 1).
 constexpr int kGalX = 64 * 9;  // doubles of X per fine row
-// warps per CTA x ring stages per warp: HOT_GALX_CFG = "WxS" (default 8x1, launch_galerkin)
+// warps per CTA x ring stages per warp (8 x 1, launch_galerkin)
 
 
 constexpr int kGalXRowBytes = 9 * kSlotPitch * 8;  // 9216: one fine row's blocks, contiguous
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
 /// between waves; only the u gathers (ld.cg, L2) wait for it.  Row arithmetic is identical to
 /// k_sgs_wave (same summation order).
 constexpr int kStreamRowBytes = 9 * kSlotPitch * 8 + kSlotPitch * 4;  // 9728
-/// W warps per CTA, S ring stages per warp (HOT_SGS_STREAM_CFG = "WxS"; default 8x2)
+/// W warps per CTA, S ring stages per warp (8 x 2, launch_sgs_stream)
 template <int W, int S>
 constexpr int stream_smem() { return W * S * kStreamRowBytes + W * S * 8; }
 
@@ -1155,30 +1155,16 @@ int mgrid(long long n, int threads) {
   return b < 1 ? 1 : (int)b;
 }
 
-int coop_blocks(const void* fn, int threads, int smem = 0) {
-  int per_sm = 0;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
-  if (per_sm < 1) per_sm = 1;
-  return per_sm * num_sms();
-}
+int coop_blocks(const void* fn, int threads, int smem = 0) { return resident_blocks(fn, threads, smem); }
 
 }  // namespace
 
 template <int R>
 int sgs_flow_blocks() {
-  static int v = 0;
-  if (!v) {
-    v = coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
-    // HOT_FLOW_CTAS_PER_SM caps the co-resident CTAs (0 / unset = all).  At 4 per SM the cfg2
-    // level-1 smoother drops 1.03 -> 1.00 ms per step but the level-0 streaming smoother that
-    // follows it rises 1.70 -> 1.91 (measured, bench.py), so the default keeps every CTA.  The
-    // grid size changes no value (the dataflow enforces the serial order).
-    const char* e = std::getenv("HOT_FLOW_CTAS_PER_SM");
-    const int cap = e ? std::atoi(e) : 0;
-    if (cap > 0) v = std::min(v, cap * num_sms());
-  }
-  return v;
+  // every co-resident CTA: capped at 4 per SM the cfg2 level-1 smoother drops 1.03 -> 1.00 ms per
+  // step but the level-0 streaming smoother that follows it rises 1.70 -> 1.91 (bench.py).  The
+  // grid size changes no value (the dataflow enforces the serial order).
+  return coop_blocks((const void*)k_sgs_flow<R>, level_pitch(R), 0);
 }
 
 void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* u, const double* b, int* flag,
@@ -1196,15 +1182,9 @@ void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* 
   count_launches(1);
 }
 
-int sgs_max_blocks() {
-  static int v = 0;
-  if (!v) v = coop_blocks((const void*)k_sgs, kSgsThreads, kSgsSmem);
-  return v;
-}
+int sgs_max_blocks() { return coop_blocks((const void*)k_sgs, kSgsThreads, kSgsSmem); }
 int pcg_max_blocks() {
-  static int v = 0;
-  if (!v) v = std::min(coop_blocks((const void*)k_pcg<2>, kMgThreads), coop_blocks((const void*)k_pcg<3>, kMgThreads));
-  return v;
+  return std::min(coop_blocks((const void*)k_pcg<2>, kMgThreads), coop_blocks((const void*)k_pcg<3>, kMgThreads));
 }
 
 void launch_mark_parents(LevelView fine, DenseMap cmap, int quad, uint8_t* flags, cudaStream_t s) {
@@ -1215,10 +1195,7 @@ void launch_coarse_dirichlet(LevelView fine, DenseMap cmap, int quad, uint8_t* c
 }
 template <int W, int S>
 void launch_galerkin_x_t(LevelView fine, double* X, cudaStream_t s) {
-  static const int gx_blocks = [] {
-    cudaFuncSetAttribute((const void*)k_galerkin_x<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, galx_smem<W, S>());
-    return coop_blocks((const void*)k_galerkin_x<W, S>, W * 32, galx_smem<W, S>());
-  }();
+  const int gx_blocks = coop_blocks((const void*)k_galerkin_x<W, S>, W * 32, galx_smem<W, S>());
   const int blocks = (int)std::min<long long>(gx_blocks, ((long long)(fine.hi - fine.lo) + W - 1) / W);
   k_galerkin_x<W, S><<<std::max(1, blocks), W * 32, galx_smem<W, S>(), s>>>(fine, X);
   count_launches(1);
@@ -1230,15 +1207,7 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
     const int fr = fine.radius;
     const int smem = kGqWarps * 9 * level_pitch(fr) * 8;
     const void* fx = fr == 2 ? (const void*)k_galerkin_qx<2> : (const void*)k_galerkin_qx<3>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute((const void*)k_galerkin_qx<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kGqWarps * 9 * level_pitch(2) * 8);
-      cudaFuncSetAttribute((const void*)k_galerkin_qx<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kGqWarps * 9 * level_pitch(3) * 8);
-      attr = true;
-    }
-    (void)fx;
+    set_max_dynamic_smem(fx, smem);
     const int bx = mgrid((long long)fine.n * 32, kGqWarps * 32);
     const int bc = mgrid((long long)coarse.n * 32, kMgThreads);
     if (fr == 2) {
@@ -1251,20 +1220,9 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
     count_launches(2);
     return;
   }
-  static const int cfg = [] {
-    const char* e = std::getenv("HOT_GALX_CFG");
-    const std::string v = e ? e : "";
-    return v == "4x2" ? 1 : v == "4x3" ? 2 : v == "16x1" ? 4 : v == "4x1" ? 5 : 0;
-  }();
-  // cfg2 hierarchy phase per step: 8x1 0.973 ms (default), 4x1 / 6x1 0.982, 4x2 1.044, 16x1
-  // 1.048, 4x3 1.188, 8x2 1.208: more warps in flight beat a deeper ring
-  switch (cfg) {
-    case 1: launch_galerkin_x_t<4, 2>(fine, X, s); break;
-    case 2: launch_galerkin_x_t<4, 3>(fine, X, s); break;
-    case 4: launch_galerkin_x_t<16, 1>(fine, X, s); break;
-    case 5: launch_galerkin_x_t<4, 1>(fine, X, s); break;
-    default: launch_galerkin_x_t<8, 1>(fine, X, s); break;
-  }
+  // 8 warps x 1 row buffer.  cfg2 hierarchy phase per step: 8x1 0.973 ms, 4x1 / 6x1 0.982, 4x2
+  // 1.044, 16x1 1.048, 4x3 1.188, 8x2 1.208: more warps in flight beat a deeper ring
+  launch_galerkin_x_t<8, 1>(fine, X, s);
   if (coarse.hi > coarse.lo) {
     k_galerkin_c<<<mgrid((long long)(coarse.hi - coarse.lo) * 32, kMgThreads), kMgThreads, 0, s>>>(fine, coarse, X);
     count_launches(1);
@@ -1328,14 +1286,7 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
 
 template <int W, int S>
 int sgs_stream_blocks_t() {
-  static int blocks = 0;
-  if (!blocks) {
-    cudaFuncSetAttribute((const void*)k_sgs_stream<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem<W, S>());
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_sgs_stream<W, S>, W * 32, stream_smem<W, S>());
-    blocks = std::max(1, per_sm) * num_sms();
-  }
-  return blocks;
+  return coop_blocks((const void*)k_sgs_stream<W, S>, W * 32, stream_smem<W, S>());
 }
 
 template <int W, int S>
@@ -1349,16 +1300,6 @@ void launch_sgs_stream_t(LevelView L, const int* wave_start, const int* wave_row
   count_launches(1);
 }
 
-int sgs_stream_cfg() {
-  static const int cfg = [] {
-    const char* e = std::getenv("HOT_SGS_STREAM_CFG");
-    if (!e) return 0;
-    const std::string v(e);
-    return v == "6x3" ? 1 : v == "4x4" ? 2 : v == "4x5" ? 3 : v == "16x1" ? 4 : 0;
-  }();
-  return cfg;
-}
-
 int sgs_stream_blocks() { return sgs_stream_blocks_t<8, 2>(); }
 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
@@ -1367,18 +1308,14 @@ void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows,
   if (q_hi < 0) q_hi = 2 * nwaves;
   if (q_hi <= q_lo) return;
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned int), s);
-  switch (sgs_stream_cfg()) {
-    case 1: launch_sgs_stream_t<6, 3>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
-    case 2: launch_sgs_stream_t<4, 4>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
-    case 3: launch_sgs_stream_t<4, 5>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
-    case 4: launch_sgs_stream_t<16, 1>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
-    default: launch_sgs_stream_t<8, 2>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows); break;
-  }
+  // 8 warps x 2 ring stages per CTA.  cfg2 level-0 smoother per step: 8x2 1.52 ms, 16x1 1.52,
+  // 6x3 1.57, 4x4 1.78, 4x5 1.85: the limit is rows in flight, not bytes in flight
+  launch_sgs_stream_t<8, 2>(L, wave_start, wave_rows, nwaves, u, b, bar, s, q_lo, q_hi, max_rows);
 }
 
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s) {
-  static const int pdl = std::getenv("HOT_SGS_NOPDL") ? 0 : 1;
+  constexpr int pdl = 1;  // programmatic dependent launch between consecutive waves
   for (int pass = 0; pass < 2; ++pass)
     for (int k = 0; k < nwaves; ++k) {
       const int w = pass == 0 ? k : nwaves - 1 - k;

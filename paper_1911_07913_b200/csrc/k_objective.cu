@@ -355,30 +355,11 @@ void launch_particle_energy(const ParticlesView& P, GridView g, double dx, doubl
                             cudaStream_t s, long long plo, long long phi) {
   if (phi < 0) phi = P.n;
   if (phi <= plo) return;
-  static const int cfg = [] {  // HOT_ENERGY_CFG = "threads x min blocks per SM" (default 512x1)
-    const char* e = std::getenv("HOT_ENERGY_CFG");
-    const std::string v = e ? e : "";
-    return v == "128x3" ? 1 : v == "64x8" ? 2 : v == "256x2" ? 3 : v == "128x2" ? 4 : v == "512x1" ? 5 :
-           v == "256x2b" ? 6 : v == "256x2h" ? 7 : v == "128x4c" ? 8 : v == "256x2c" ? 9 : v == "512x1c" ? 10 : v == "128x4" ? 11 : 0;
-  }();
-  switch (cfg) {
-    case 1: launch_particle_energy_t<128, 3>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 2: launch_particle_energy_t<64, 8>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 3: launch_particle_energy_t<256, 2>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 4: launch_particle_energy_t<128, 2>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 5: launch_particle_energy_t<512, 1>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 6: launch_particle_energy_t<256, 2>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi, 2); break;
-    case 7: launch_particle_energy_t<128, 4>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks / 2, bad_flag, s, plo, phi); break;
-    case 8: launch_particle_energy_t<128, 4, true>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 9: launch_particle_energy_t<256, 2, true>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 10: launch_particle_energy_t<512, 1, true>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    case 11: launch_particle_energy_t<128, 4>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks, bad_flag, s, plo, phi); break;
-    // cfg2 particle energy per step: 512x1 one resident wave 0.672 ms (default), 512x1 two waves
-    // 0.676, 256x2 0.755, 128x4 0.80, 512x1 / 256x2 / 128x4 with contiguous per-block chunks
-    // 0.73 / 0.82 / 0.86, 128x3 / 128x2 0.99: wide blocks keep a bin-ordered run of particles,
-    // whose stencils overlap, on one SM
-    default: launch_particle_energy_t<512, 1>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks / 2, bad_flag, s, plo, phi); break;
-  }
+  // 512 threads x 1 CTA per SM, one resident wave.  cfg2 particle energy per step: 0.672 ms,
+  // against 0.676 (two waves), 0.755 (256 x 2), 0.80 (128 x 4), 0.73 / 0.82 / 0.86 (512 / 256 /
+  // 128 with contiguous per-block chunks) and 0.99 (128 x 3, 128 x 2): wide blocks keep a
+  // bin-ordered run of particles, whose stencils overlap, on one SM
+  launch_particle_energy_t<512, 1>(P, g, dx, dt, mats, u, stress, svd_out, pe, nblocks / 2, bad_flag, s, plo, phi);
 }
 
 void launch_node_energy(GridView g, BinsView bins, const double* pe, double dt, const double* grav, const double* dv,
@@ -395,25 +376,14 @@ void launch_node_gradient(const ParticlesView& P, BinsView bins, GridView g, dou
   if (jhi < 0) jhi = g.n;
   if (hi < 0) hi = g.n;
   if (jhi > jlo) {
-    static const int bin_blocks = resident_blocks((const void*)k_bin_force, kBinWarps * 32, 0);
+    const int bin_blocks = resident_blocks((const void*)k_bin_force, kBinWarps * 32, 0);
     k_bin_force<<<std::min<long long>(bin_blocks, (jhi - jlo + kBinWarps - 1) / kBinWarps), kBinWarps * 32, 0, s>>>(
         P, bins, g, dx, stress, bin_part, jlo, jhi);
     count_launches(1);
   }
   if (hi > lo) {
-    static const int nt_ = [] {  // HOT_NODE_THREADS: threads per block of the node passes (default 256)
-      const char* e = std::getenv("HOT_NODE_THREADS");
-      return e ? std::atoi(e) : 256;
-    }();
-    if (nt_ == 1024)
-      k_node_gradient<1024><<<std::max(1, std::min((hi - lo + 1023) / 1024, 4 * num_sms())), 1024, 0, s>>>(
-          g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
-    else if (nt_ == 512)
-      k_node_gradient<512><<<std::max(1, std::min((hi - lo + 511) / 512, 8 * num_sms())), 512, 0, s>>>(
-          g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
-    else
-      k_node_gradient<256><<<std::max(1, std::min((hi - lo + 255) / 256, 16 * num_sms())), 256, 0, s>>>(
-          g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
+    k_node_gradient<256><<<std::max(1, std::min((hi - lo + 255) / 256, 16 * num_sms())), 256, 0, s>>>(
+        g, dt, grav[0], grav[1], grav[2], bin_part, dv, gout, nt, bad_flag, lo, hi);
     count_launches(1);
   }
 }

@@ -189,7 +189,7 @@ void launch_mf_multiply(const ParticlesView& P, BinsView bins, GridView g, const
                         double* dP, double* y, cudaStream_t s) {
   if (P.n) { k_mf_particle<<<pgrid(P.n, 128), 128, 0, s>>>(P, g, Tu, u, dP); count_launches(1); }
   if (g.n) {
-    static const int blocks = resident_blocks((const void*)k_mf_node, 256, 0);
+    const int blocks = resident_blocks((const void*)k_mf_node, 256, 0);
     k_mf_node<<<std::min<long long>(blocks, (32LL * g.n + 255) / 256), 256, 0, s>>>(P, bins, g, Tu, dP, u, y);
     count_launches(1);
   }
@@ -197,7 +197,7 @@ void launch_mf_multiply(const ParticlesView& P, BinsView bins, GridView g, const
 void launch_mf_block_diag_inv(const ParticlesView& P, BinsView bins, GridView g, const double* Tu, double* dinv,
                               cudaStream_t s) {
   if (g.n) {
-    static const int blocks = resident_blocks((const void*)k_mf_diag, 256, 0);
+    const int blocks = resident_blocks((const void*)k_mf_diag, 256, 0);
     k_mf_diag<<<std::min<long long>(blocks, (32LL * g.n + 255) / 256), 256, 0, s>>>(P, bins, g, Tu, dinv);
     count_launches(1);
   }

@@ -126,19 +126,10 @@ int tgrid(long long n, int threads) {
 void launch_g2p_strain_advect(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
                               int* inverted, cudaStream_t s) {
   if (P.n == 0) return;
-  // HOT_G2P_CFG = threads per block.  cfg2 per step: 512 0.265 ms (default), 384 0.323, 256
-  // 0.454, 128 0.453: wide blocks keep a bin-ordered run of particles, whose stencils overlap,
-  // on one SM (L1 hits on the node velocities), which outweighs the register cap's spills
-  static const int cfg = [] {
-    const char* e = std::getenv("HOT_G2P_CFG");
-    return e ? std::atoi(e) : 512;
-  }();
-  switch (cfg) {
-    case 128: k_g2p_strain_advect<128><<<tgrid(P.n, 128), 128, 0, s>>>(P, g, dx, dt, mats, inverted); break;
-    case 256: k_g2p_strain_advect<256><<<tgrid(P.n, 256), 256, 0, s>>>(P, g, dx, dt, mats, inverted); break;
-    case 384: k_g2p_strain_advect<384><<<tgrid(P.n, 384), 384, 0, s>>>(P, g, dx, dt, mats, inverted); break;
-    default: k_g2p_strain_advect<512><<<tgrid(P.n, 512), 512, 0, s>>>(P, g, dx, dt, mats, inverted); break;
-  }
+  // 512 threads per block.  cfg2 per step: 512 0.265 ms, 384 0.323, 256 0.454, 128 0.453: wide
+  // blocks keep a bin-ordered run of particles, whose stencils overlap, on one SM (L1 hits on
+  // the node velocities), which outweighs the register cap's spills
+  k_g2p_strain_advect<512><<<tgrid(P.n, 512), 512, 0, s>>>(P, g, dx, dt, mats, inverted);
   count_launches(1);
 }
 

@@ -164,10 +164,15 @@ def attach_nccl(sim, group=None) -> None:
             pass
     rank, size = dist.get_rank(group), dist.get_world_size(group)
     uid = (C.c_ubyte * 128)()
-    if rank == 0:
-        capi.raise_for(capi.lib().hot_nccl_unique_id(uid), "hot_nccl_unique_id failed (libnccl.so.2)")
-    box = [bytes(uid)]
+    err = None
+    if rank == 0:  # never raise before the broadcast: the other ranks would wait in it forever
+        rc = capi.lib().hot_nccl_unique_id(uid)
+        if rc != 0:
+            err = f"hot_nccl_unique_id failed (libnccl.so.2), status {rc}"
+    box = [bytes(uid), err]
     dist.broadcast_object_list(box, src=0, group=group)
+    if box[1] is not None:  # every rank raises together
+        raise RuntimeError(box[1])
     uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
     sim._check(sim._lib.hot_set_comm_nccl(sim.handle, uid, rank, size))
 

@@ -100,16 +100,35 @@ def test_kernel_sweep_particle_sets():
     assert np.allclose(np.einsum("nij,nkj->nik", R, R), np.eye(3)) and np.allclose(np.linalg.det(R), 1.0)
 
 
-def test_bench_cpu_slab_keeps_the_left_end():
-    import importlib.util
+def test_bench_reference_arm_is_oracle_only_and_same_config():
+    """bench.py --impl reference: the oracle on the full scene, sampled by the oracle itself; the
+    product package is never imported; its config equals the GPU arm's (same workload dict)."""
+    import json
     import os
+    import subprocess
+    import sys
 
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py")
-    spec = importlib.util.spec_from_file_location("bench_mod", path)
-    bm = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(bm)
-    rng = np.random.default_rng(1)
-    parts = dict(x=rng.uniform(0, 1, (100, 3)), v=np.zeros((100, 3)), mass=np.ones(100))
-    s = bm.cpu_slab(parts, 10)
-    assert s["x"].shape[0] == 10
-    assert s["x"][:, 0].max() <= np.sort(parts["x"][:, 0])[9] + 1e-15
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    scene = os.path.join(root, "scenes", "cfg1_cube.json")
+    code = f"""
+import sys, json, types
+sys.argv = ["bench.py", "--impl", "reference", "--scene", {scene!r}, "--steps", "1", "--warmup", "0"]
+sys.path.insert(0, {root!r})
+import bench
+bench.main()
+print(json.dumps({{"product_loaded": any(m.startswith("paper_1911_07913_b200") for m in sys.modules)}}))
+"""
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    ref, flag = lines[0], lines[1]
+    assert flag["product_loaded"] is False
+    assert ref["impl"] == "reference" and ref["steps"] == 1 and ref["cpu_baseline"]["kind"] == "port"
+    from paper_1911_07913_b200 import load_scene_file, sample_scene_particles
+
+    sys.path.insert(0, root)
+    import bench
+
+    sc = load_scene_file(scene)
+    n = sample_scene_particles(sc)["x"].shape[0]
+    assert ref["config"] == json.loads(json.dumps(bench.workload_config(sc.source, scene, n)))
