@@ -3,6 +3,9 @@
 // /root/reference/proj/include/hotmpm.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "hot_oracle.hpp"
 
 namespace hot_oracle {
@@ -943,6 +946,19 @@ VecX lbfgs_direction(const VecX& g, const LBFGSHistory& h, Init&& initializer) {
   return r;
 }
 
+/// Phase timing of the oracle (diagnostics only; HOT_ORACLE_TIMING=1 prints per-phase wall time
+/// of every advance_step to stderr).  No effect on any value.
+struct OracleTimer {
+  bool on = std::getenv("HOT_ORACLE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[oracle] %-16s %9.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 inline double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -1009,8 +1025,11 @@ SolveResult solve_quasi_newton(const ObjectiveState<d>& st, const SolverConfig& 
     out.converged = true;
     return out;
   }
+  OracleTimer tm;
   const BlockSparseMatrix<d> H = assemble_hessian<d>(st, loop.dv, true);
+  tm.lap("  assemble");
   const MultigridHierarchy<d> hier = build_hierarchy<d>(H, *st.grid, levels, cfg.embedding);
+  tm.lap("  hierarchy");
   out.hierarchy_rebuilds = 1;
   LBFGSHistory history(cfg.window);
   for (int outer = 1; outer <= cfg.outer_cap; ++outer) {
@@ -1021,7 +1040,9 @@ SolveResult solve_quasi_newton(const ObjectiveState<d>& st, const SolverConfig& 
       return v.u;
     };
     const VecX p = lbfgs_direction(loop.g, history, initializer);
+    tm.lap("  direction");
     auto [s, y] = loop.accept(p, outer, inner_this);
+    tm.lap("  accept");
     history.push(std::move(s), std::move(y));
     out.outer_iterations = outer;
     out.inner_total += inner_this;
@@ -1465,6 +1486,7 @@ struct StepStats {  // simulation.hpp:275-281
 template <int d>
 StepStats advance_step(SimulationState<d>& sim, const SceneConfig& scene, const SolverConfig& cfg, double frame_end) {
   const double dx = scene.dx;
+  OracleTimer tm;
   double v_max = 0.0;
   for (const auto& p : sim.particles) v_max = std::max(v_max, norm(p.v));
   double dt = cfl_dt(v_max, dx, scene.fps);
@@ -1472,23 +1494,30 @@ StepStats advance_step(SimulationState<d>& sim, const SceneConfig& scene, const 
   if (!(dt > 0.0)) throw SolverFailure("advance_step: non-positive time step");
   std::vector<Vec<d>> positions(sim.particles.size());
   for (std::size_t i = 0; i < sim.particles.size(); ++i) positions[i] = sim.particles[i].x;
+  tm.lap("cfl");
   SparseGrid<d> grid = activate_grid<d>(positions, dx, KernelKind::QuadraticBSpline);
+  tm.lap("activate");
   p2g<d>(sim.particles, grid);
+  tm.lap("p2g");
   apply_boundary_scripts<d>(grid, scene, sim.time);
+  tm.lap("boundary");
   const auto materials = materials_from_scene(scene);
   const Vec<d> gravity = take<d>(scene.gravity);
   const ObjectiveState<d> st =
       make_objective_state<d>(sim.particles, grid, materials, dt, gravity, scene.cn_length_factor);
+  tm.lap("objective_state");
   GridStepResult<d> step;
   try {
     step = step_grid<d>(st, cfg, &sim.diagnostics, sim.frame, sim.step_index);
   } catch (const SolverFailure& e) {
     throw SolverFailure("step " + std::to_string(sim.step_index) + ": " + e.what());
   }
+  tm.lap("step_grid");
   grid.velocity = step.velocity;
   g2p<d>(grid, sim.particles);
   sim.inversion_warnings += update_strain<d>(sim.particles, grid, dt, materials);
   advect<d>(sim.particles, dt);
+  tm.lap("g2p_strain_adv");
   sim.time += dt;
   ++sim.step_index;
   return {dt, step.solve.outer_iterations, step.solve.inner_total, grid.node_count(), step.solve.converged};

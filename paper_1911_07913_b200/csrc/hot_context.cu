@@ -2075,13 +2075,16 @@ int hot_stage_level_matrix(hot_ctx* ctx, int level, double* blocks, int* cols, i
     const hotb200::Level& l = c.L[level];
     const long long n = l.n;
     const int pitch = l.pitch(), ns = l.slots();
-    std::vector<int> cl(n * pitch);
-    std::vector<double> H(n * 9 * pitch);
-    HOT_CUDA(cudaMemcpyAsync(cl.data(), l.cols.p, sizeof(int) * cl.size(), cudaMemcpyDeviceToHost, c.stream));
-    HOT_CUDA(cudaMemcpyAsync(H.data(), l.H.p, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, c.stream));
+    std::vector<int> cl((cols || blocks) ? n * pitch : 0);
+    std::vector<double> H(blocks ? n * 9 * pitch : 0);  // only when the blocks are asked for (GB at level 0)
+    if (!cl.empty())
+      HOT_CUDA(cudaMemcpyAsync(cl.data(), l.cols.p, sizeof(int) * cl.size(), cudaMemcpyDeviceToHost, c.stream));
+    if (!H.empty())
+      HOT_CUDA(cudaMemcpyAsync(H.data(), l.H.p, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, c.stream));
     if (coords) HOT_CUDA(cudaMemcpyAsync(coords, l.coords.p, sizeof(int) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
     if (dirichlet) HOT_CUDA(cudaMemcpyAsync(dirichlet, l.dir.p, n, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    if (cl.empty()) return;
     for (long long i = 0; i < n; ++i)
       for (int s = 0; s < ns; ++s) {
         const int col = cl[i * pitch + s];

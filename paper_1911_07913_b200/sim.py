@@ -190,6 +190,14 @@ class Simulation:
         self._check(self._lib.hot_stage_level_shape(self._h, level, C.byref(r), C.byref(s)))
         return r.value, s.value
 
+    def level_coords(self, level=0):
+        """coords and Dirichlet flags of a level (no matrix copy)."""
+        rows, _ = self.level_shape(level)
+        coords = np.zeros((rows, self.dim), np.int32)
+        dirm = np.zeros(rows, np.uint8)
+        self._check(self._lib.hot_stage_level_matrix(self._h, level, None, None, iptr(coords), u8ptr(dirm)))
+        return dict(coords=coords, dirichlet=dirm)
+
     def level_matrix(self, level=0):
         rows, slots = self.level_shape(level)
         d = self.dim
