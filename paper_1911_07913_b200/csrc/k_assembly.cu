@@ -163,59 +163,63 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols, unsigned long l
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(active, cnt);
 }
 
-/// Row gather (objective.hpp:331-357), one warp per row i.  A particle p of a bin whose stencil
-/// holds i at position a contributes to the row's upper-triangle block at stencil position k
-///   C_k[c][e] += sum_g W_k[g] M[c][e][g],   M[c][e][g] = sum_f W_a[f] T[(3c+f),(3e+g)].
-/// Per particle that is a rank-3 update of the (upper positions) x (ce) block, which runs on the
-/// fp64 tensor cores (DMMA m8n8k4): M-dim = upper positions (tiles of 8), N-dim = ce 0..7, K = g
-/// (3, padded to 4 with a zero row of B).  The ninth column ce = 8 would waste a whole second
-/// N tile, so it goes to the FMA pipe instead: each lane accumulates A[k][g] * M[8][g] and the
-/// four g lanes are summed once per bin pair.  Every lane computes its own B-fragment entry
-/// M[ce][g] (3 FMA from the staged T and W_a), so M never goes through shared memory.
+/// Level-0 assembly (objective.hpp:318-363), row tiles fed by a producer warp.
 ///
-/// Bin offset o and its mirror 26-o are walked together (their upper position counts add up to
-/// 28), both bins' particles staged by the bulk-copy engine (one cp.async.bulk per bin chunk,
-/// mbarrier completion, double buffered one chunk ahead).  The tile counts of a pair are
-/// template constants, so the per-particle loop has no tile branches.  Each (pair, lane) block
-/// accumulates in registers and is folded into the row's shared accumulator once per pair (bin
-/// o's lanes, then the mirror's: fixed order, no atomics).
-// CH particles per bin per stage; AW warps per CTA (4 x 2, launch_assemble_rows)
-template <int CH>
-constexpr int asm_stage() { return 2 * CH * kTensorStride; }  // doubles: [bin of pair][particle][...]
-template <int CH>
-constexpr int asm_warp_doubles() { return 2 * asm_stage<CH>() + kUpper * 9 + 1 + 2 + 28; }  // + pad + 2 mbarriers + pair table
-template <int AW, int CH>
-constexpr int asm_smem() { return AW * asm_warp_doubles<CH>() * 8; }
-constexpr unsigned kParticleBytes = kTensorStride * 8;  // 1008 = 63 x 16
-static_assert(asm_warp_doubles<1>() % 2 == 0 && asm_warp_doubles<2>() % 2 == 0 && asm_warp_doubles<3>() % 2 == 0,
-              "16-byte aligned per-warp smem");
-
-/// S(o) = 25 o0 + 5 o1 + o2 of a stencil position, and kmin(o): the first stencil position k of
-/// the bin at offset o whose slot S(k) + S(o) is in the row's upper triangle (>= 62).
-struct Kmin27 {
-  int S[27], kmin[27];
-  constexpr Kmin27() : S(), kmin() {
-    for (int o = 0; o < 27; ++o) S[o] = 25 * (o / 9) + 5 * ((o / 3) % 3) + o % 3;
-    for (int o = 0; o < 27; ++o) {
-      int k = 0;
-      while (k < 27 && S[k] + S[o] < kDiagSlot) ++k;
-      kmin[o] = k;
-    }
-  }
+/// A tile is T consecutive level-0 rows (T consumer warps, one row each).  Rows are sorted
+/// lexicographically, so a tile's rows usually share (x, y) and run along z; every particle bin
+/// their stencils reach is bulk-copied into shared memory ONCE per tile and consumed by every
+/// tile row whose 27-stencil it touches (up to 3 of them), instead of once per row.
+///
+/// Groups.  Consecutive tile rows with the same (x, y) and z steps of at most 3 form a group; the
+/// producer stages, per group, the 9 bin columns (x + dx, y + dy) over z in [zfirst-1, zlast+1]
+/// (each column is a contiguous particle range: bins are node-ordered), and only that group's
+/// rows consume them.  So every row sees each of its 27 bins exactly once, in a fixed order
+/// (column-major, z ascending, particles in storage order): the row sums are deterministic and
+/// independent of the tiling (the slab-sharded assembly stays bitwise equal to one GPU).
+///
+/// Per (row i, particle p of a bin whose stencil holds i at position a) the row's upper blocks
+/// k >= a (slot S(k) - S(a) above the diagonal, S(v) = 25 v0 + 5 v1 + v2) get the rank-3 update
+///   C_k[c][e] += sum_g W_k[g] M[c][e][g],   M[c][e][g] = sum_f W_a[f] T[(3c+f),(3e+g)],
+/// on the fp64 tensor cores (DMMA m8n8k4: M-dim = upper positions k in tiles of 8, N-dim =
+/// ce 0..7, K = g padded to 4); the ninth column ce = 8 goes to the FMA pipe.  Each lane forms its
+/// own B-fragment entry M[ce][g] from three staged T entries and W_a.
+///
+/// Pipeline: a ring of S slots of CP particle records (CP x 1008 B each).  The producer warp's
+/// lane 0 fills a slot with one bulk copy of a bin chunk (plus a bulk copy from a zero buffer
+/// padding the chunk to CP records, so the consumers' unrolled particle loop needs no predicates:
+/// a zero record contributes exactly zero), the slot's metadata and an mbarrier
+/// arrive.expect_tx; the T consumer warps wait on the slot's full barrier and release it on its
+/// empty barrier.  The register accumulators of a (bin, row) are folded into the row's shared
+/// accumulator once per bin, in a fixed order (no atomics).
+constexpr int kAsmT = 4;                  // rows (consumer warps) per tile
+constexpr int kAsmCP = 4;                 // particle records per ring slot
+constexpr int kAsmS = 10;                 // ring slots
+constexpr int kAsmSpan = 3 * kAsmT + 2;   // z extent of a group's bin columns, at most
+constexpr unsigned kRecBytes = kTensorStride * 8;  // 1008 = 63 x 16
+enum : int { kSlotData = 0, kSlotTileEnd = 1, kSlotStop = 2 };
+struct AsmMeta {
+  int kind, tile, group, col, bz, last, pad0, pad1;
 };
-constexpr Kmin27 kKmin27{};
-__constant__ int c_S27[27] = {
-#define HOT_S(o) (25 * ((o) / 9) + 5 * (((o) / 3) % 3) + (o) % 3)
-    HOT_S(0),  HOT_S(1),  HOT_S(2),  HOT_S(3),  HOT_S(4),  HOT_S(5),  HOT_S(6),  HOT_S(7),  HOT_S(8),
-    HOT_S(9),  HOT_S(10), HOT_S(11), HOT_S(12), HOT_S(13), HOT_S(14), HOT_S(15), HOT_S(16), HOT_S(17),
-    HOT_S(18), HOT_S(19), HOT_S(20), HOT_S(21), HOT_S(22), HOT_S(23), HOT_S(24), HOT_S(25), HOT_S(26)};
-#undef HOT_S
-__constant__ int c_kmin27[27] = {
-    kKmin27.kmin[0],  kKmin27.kmin[1],  kKmin27.kmin[2],  kKmin27.kmin[3],  kKmin27.kmin[4],  kKmin27.kmin[5],
-    kKmin27.kmin[6],  kKmin27.kmin[7],  kKmin27.kmin[8],  kKmin27.kmin[9],  kKmin27.kmin[10], kKmin27.kmin[11],
-    kKmin27.kmin[12], kKmin27.kmin[13], kKmin27.kmin[14], kKmin27.kmin[15], kKmin27.kmin[16], kKmin27.kmin[17],
-    kKmin27.kmin[18], kKmin27.kmin[19], kKmin27.kmin[20], kKmin27.kmin[21], kKmin27.kmin[22], kKmin27.kmin[23],
-    kKmin27.kmin[24], kKmin27.kmin[25], kKmin27.kmin[26]};
+constexpr size_t kAsmRingBytes = (size_t)kAsmS * kAsmCP * kRecBytes;
+constexpr size_t kAsmAccBytes = (size_t)kAsmT * kUpper * 9 * 8;
+constexpr size_t kAsmBarBytes = (size_t)2 * kAsmS * 8;
+constexpr size_t kAsmMetaBytes = (size_t)kAsmS * sizeof(AsmMeta);
+constexpr size_t kAsmTableBytes = (size_t)9 * kAsmSpan * 2 * 4;
+constexpr size_t kAsmSmem = kAsmRingBytes + kAsmAccBytes + kAsmBarBytes + kAsmMetaBytes + kAsmTableBytes;
+static_assert(kAsmRingBytes % 16 == 0 && kAsmAccBytes % 16 == 0, "16-byte aligned regions");
+
+/// Group start (index within the tile) of tile row w: rows w' < w with the same (x, y) and z
+/// steps of at most 3 belong to the same group.  Both sides of the pipeline call this.
+__device__ __forceinline__ int asm_group_of(const LevelView& L, int r0, int w) {
+  int g = w;
+  while (g > 0) {
+    const int* c1 = L.coords + 3 * (r0 + g);
+    const int* c0 = c1 - 3;
+    if (c0[0] != c1[0] || c0[1] != c1[1] || c1[2] - c0[2] > 3) break;
+    --g;
+  }
+  return g;
+}
 
 /// D = A B + D on the fp64 tensor cores: m8n8k4, A row-major (lane: row lane/4, col lane%4),
 /// B column-major (lane: row lane%4, col lane/4), C/D (lane: row lane/4, cols 2(lane%4)+{0,1}).
@@ -225,31 +229,41 @@ __device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-/// One bin of a pair, one particle: B-fragment entries from the staged T and W_a, then the
-/// DMMA tiles (ce 0..7) and the FMA column (ce 8).  Lanes g < 3 form M[ce = qm][g]; the g = 3
-/// pad lanes qm < 3 form M[8][qm] in the same loads, and a shuffle hands M[8][g] to the lanes of
-/// column g.  `valid` = the slot holds a particle of this bin (stale slots hold finite data of an
-/// earlier particle and get B = 0).
+/// One ring slot (CP records) for a row at stencil position a = kmin: B-fragment entries from the
+/// staged T and W_a, then NT DMMA tiles (ce 0..7) and the FMA column (ce 8).  Lanes g < 3 form
+/// M[ce = qm][g]; the g = 3 pad lanes qm < 3 form M[8][qm] in the same loads, and a shuffle hands
+/// M[8][g] to the lanes of column g.  gmask zeroes the pad lanes' B row and FMA term.
 template <int NT>
-__device__ __forceinline__ void asm_particle(const double* __restrict__ P, int wa, const int (&tb)[3], int src8,
-                                             bool valid, const int (&oA)[4], double (&C)[4][2], double (&E)[4]) {
-  const double w0 = P[wa], w1 = P[wa + 1], w2 = P[wa + 2];
-  const double raw = w0 * P[tb[0]] + w1 * P[tb[1]] + w2 * P[tb[2]];
-  const double m8raw = __shfl_sync(0xffffffffu, raw, src8);
-  const double b = valid ? raw : 0.0;
-  const double m8 = valid ? m8raw : 0.0;
+__device__ __forceinline__ void asm_chunk(const double* __restrict__ S, int kmin, const int (&tb)[3], int src8,
+                                          double gmask, int qm, int qk, double (&C)[4][2], double (&E)[4]) {
+  const double* pw = S + kRecW + 3 * kmin;
+  const double* pt0 = S + tb[0];
+  const double* pt1 = S + tb[1];
+  const double* pt2 = S + tb[2];
+  const double* pa[4];
 #pragma unroll
-  for (int mt = 0; mt < NT; ++mt) {
-    const double a = P[oA[mt]];
-    dmma_f64(C[mt], a, b);
-    E[mt] = fma(a, m8, E[mt]);
+  for (int mt = 0; mt < NT; ++mt) pa[mt] = S + kRecW + 3 * min(kmin + 8 * mt + qm, 26) + min(qk, 2);
+#pragma unroll
+  for (int t = 0; t < kAsmCP; ++t) {
+    const int o = t * kTensorStride;
+    const double w0 = pw[o], w1 = pw[o + 1], w2 = pw[o + 2];
+    const double raw = w0 * pt0[o] + w1 * pt1[o] + w2 * pt2[o];
+    const double m8 = __shfl_sync(0xffffffffu, raw, src8) * gmask;
+    const double b = raw * gmask;
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt) {
+      const double av = pa[mt][o];
+      dmma_f64(C[mt], av, b);
+      E[mt] = fma(av, m8, E[mt]);
+    }
   }
 }
 
-/// Fold one bin's register blocks into the row accumulator (upper slots su = S(k) + S(o) - 62).
+/// Fold a (bin, row)'s register blocks into the row accumulator (upper slot su = S(k) - S(a)),
+/// then clear them.
 template <int NT>
-__device__ __forceinline__ void asm_fold(double* acc, int kmin, int So, int qm, int qk, double (&C)[4][2],
-                                         double (&E)[4]) {
+__device__ __forceinline__ void asm_fold(double* acc, int kmin, int qm, int qk, double (&C)[4][2], double (&E)[4]) {
+  const int Sa = 25 * (kmin / 9) + 5 * ((kmin / 3) % 3) + kmin % 3;
 #pragma unroll
   for (int mt = 0; mt < NT; ++mt) {
     double e = E[mt];
@@ -257,36 +271,162 @@ __device__ __forceinline__ void asm_fold(double* acc, int kmin, int So, int qm, 
     e += __shfl_xor_sync(0xffffffffu, e, 2);
     const int k = kmin + 8 * mt + qm;
     if (k <= 26) {
-      const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 + So - kDiagSlot;
+      const int su = 25 * (k / 9) + 5 * ((k / 3) % 3) + k % 3 - Sa;
       acc[su * 9 + 2 * qk] += C[mt][0];
       acc[su * 9 + 2 * qk + 1] += C[mt][1];
       if (qk == 0) acc[su * 9 + 8] += e;
     }
+    C[mt][0] = C[mt][1] = E[mt] = 0.0;
   }
 }
 
-template <int AW, int CH>
-__global__ void __launch_bounds__(AW * 32) k_assemble_rows(BinsView bins, GridView g, LevelView L,
-                                                                   const double* __restrict__ Tu,
-                                                                   unsigned int* __restrict__ row_counter) {
-  extern __shared__ __align__(16) double asm_smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // per warp: staging [2 buffers][asm_stage<CH>()] | acc [kUpper*9] | pad | mbarriers [2] | pair table
-  double* base = asm_smem + (size_t)wid * asm_warp_doubles<CH>();
-  double* Sbuf = base;
-  double* acc = base + 2 * asm_stage<CH>();
-  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(acc + kUpper * 9 + 1);
-  int* PT = reinterpret_cast<int*>(acc + kUpper * 9 + 1 + 2);  // [14][pb1, n1, pb2, n2]
-  for (int q = lane; q < 2 * asm_stage<CH>(); q += 32) Sbuf[q] = 0.0;  // stale slots must hold finite data
-  __syncwarp();
-  if (lane == 0) {
-    mbar_init(mbar, 1);
-    mbar_init(mbar + 1, 1);
-    mbar_fence_init();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before the bulk copies
+/// The row's write-out: upper slots + transposed mirror, mass diagonal, symmetrised diagonal
+/// block (objective.hpp:349-351), Dirichlet projection (objective.hpp:133-144); inactive and pad
+/// slots hold zeros.  zc / uc / ud / di / mi were loaded when the row's tile started.
+__device__ __forceinline__ void asm_write_row(const LevelView& L, int i, int lane, const double* acc,
+                                              const int (&zc)[kSlotPitch / 32], const int (&uc)[2],
+                                              const bool (&ud)[2], bool di, double mi) {
+#pragma unroll
+  for (int j = 0; j < kSlotPitch / 32; ++j) {
+    if (zc[j] < 0)
+#pragma unroll
+      for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + lane + 32 * j, 0.0);
   }
-  __syncwarp();
-  unsigned phase = 0;  // bit b: parity of the next completion of buffer b
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int u = lane + 32 * j, sl = kDiagSlot + u;
+    const int col = uc[j];
+    if (col < 0) continue;
+    double Cb[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Cb[k] = acc[u * 9 + k];
+    const bool zero = di || ud[j];
+    if (sl == kDiagSlot) {
+      if (di) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Cb[k] = (k % 4 == 0) ? 1.0 : 0.0;
+      } else {
+        const double t01 = 0.5 * (Cb[1] + Cb[3]), t02 = 0.5 * (Cb[2] + Cb[6]), t12 = 0.5 * (Cb[5] + Cb[7]);
+        Cb[1] = Cb[3] = t01;
+        Cb[2] = Cb[6] = t02;
+        Cb[5] = Cb[7] = t12;
+        Cb[0] += mi;
+        Cb[4] += mi;
+        Cb[8] += mi;
+      }
+    } else if (zero) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) Cb[k] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + sl, Cb[k]);
+    if (sl != kDiagSlot) {
+      const int sm = kSlots - 1 - sl;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) __stcs(L.H + ((long long)col * 9 + 3 * r + c) * kSlotPitch + sm, Cb[3 * c + r]);
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__((kAsmT + 1) * 32) k_assemble_tiles(BinsView bins, GridView g, LevelView L,
+                                                                      const double* __restrict__ Tu,
+                                                                      const double* __restrict__ zeros,
+                                                                      unsigned int* __restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char asm_sm[];
+  double* ring = reinterpret_cast<double*>(asm_sm);
+  double* accs = reinterpret_cast<double*>(asm_sm + kAsmRingBytes);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(asm_sm + kAsmRingBytes + kAsmAccBytes);
+  unsigned long long* empty = full + kAsmS;
+  AsmMeta* meta = reinterpret_cast<AsmMeta*>(asm_sm + kAsmRingBytes + kAsmAccBytes + kAsmBarBytes);
+  int* table = reinterpret_cast<int*>(asm_sm + kAsmRingBytes + kAsmAccBytes + kAsmBarBytes + kAsmMetaBytes);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kAsmS; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, kAsmT);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int ntiles = (L.hi - L.lo + kAsmT - 1) / kAsmT;
+
+  if (wid == kAsmT) {  // ------------------------------------------------ producer warp
+    int it = 0;        // slots issued (lane 0 counts; broadcast after each group)
+    auto acquire = [&]() {  // lane 0: wait until slot it % S is free again
+      const int slot = it % kAsmS;
+      mbar_wait(smem_u32(empty + slot), ((it / kAsmS) & 1) ^ 1);
+      return slot;
+    };
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = (int)atomicAdd(tile_counter, 1u);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= ntiles) break;
+      const int r0 = L.lo + t * kAsmT;
+      const int nr = min(kAsmT, L.hi - r0);
+      for (int w = 0; w < nr; ++w) {
+        if (asm_group_of(L, r0, w) != w) continue;  // w starts a group
+        int wl = w;
+        while (wl + 1 < nr && asm_group_of(L, r0, wl + 1) == w) ++wl;
+        const int x = L.coords[3 * (r0 + w)], y = L.coords[3 * (r0 + w) + 1];
+        const int zlo = L.coords[3 * (r0 + w) + 2] - 1;
+        const int span = L.coords[3 * (r0 + wl) + 2] + 1 - zlo + 1;
+        // bin table of the group: (first particle, count) per (column, z), warp-parallel lookups
+        for (int e = lane; e < 9 * span; e += 32) {
+          const int col = e / span, z = zlo + e % span;
+          const int j = dense_lookup(L.map, x + col / 3 - 1, y + col % 3 - 1, z);
+          int st = 0, cnt = 0;
+          if (j >= 0) {
+            st = __ldg(bins.start + j);
+            cnt = __ldg(bins.start + j + 1) - st;
+          }
+          table[2 * e] = st;
+          table[2 * e + 1] = cnt;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          for (int e = 0; e < 9 * span; ++e) {
+            const int st = table[2 * e], cnt = table[2 * e + 1];
+            for (int c0 = 0; c0 < cnt; c0 += kAsmCP) {
+              const int slot = acquire();
+              const int k = min(kAsmCP, cnt - c0);
+              meta[slot] = AsmMeta{kSlotData, t, w, e / span, zlo + e % span, c0 + kAsmCP >= cnt ? 1 : 0, 0, 0};
+              const unsigned mb = smem_u32(full + slot);
+              double* dst = ring + (size_t)slot * kAsmCP * kTensorStride;
+              mbar_expect_tx(mb, kAsmCP * kRecBytes);
+              bulk_g2s(dst, Tu + (long long)(st + c0) * kTensorStride, k * kRecBytes, mb);
+              if (k < kAsmCP) bulk_g2s(dst + k * kTensorStride, zeros, (kAsmCP - k) * kRecBytes, mb);
+              ++it;
+            }
+          }
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+        __syncwarp();  // the table is rewritten by the next group
+      }
+      if (lane == 0) {  // the tile's rows are complete: write-out marker
+        const int slot = acquire();
+        meta[slot] = AsmMeta{kSlotTileEnd, t, 0, 0, 0, 0, 0, 0};
+        mbar_arrive(smem_u32(full + slot));
+        ++it;
+      }
+      it = __shfl_sync(0xffffffffu, it, 0);
+    }
+    if (lane == 0) {
+      const int slot = acquire();
+      meta[slot] = AsmMeta{kSlotStop, 0, 0, 0, 0, 0, 0, 0};
+      mbar_arrive(smem_u32(full + slot));
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------- consumer warp wid
+  double* acc = accs + (size_t)wid * kUpper * 9;
   const int qk = lane & 3, qm = lane >> 2;
   // lane's load f: M[ce = qm][g = qk] needs T[(3c+f),(3e+g)]; the g = 3 pad lanes qm < 3 load
   // T[(6+f),(6+qm)] (the ce = 8 column), the other pad lanes repeat a neighbour's address
@@ -300,179 +440,68 @@ __global__ void __launch_bounds__(AW * 32) k_assemble_rows(BinsView bins, GridVi
       else tb[f] = kRecT + tslot(3 * c + f, 3 * e + 2);
     }
   }
-  const bool lane_g = qk < 3;
+  const double gmask = qk < 3 ? 1.0 : 0.0;
   const int src8 = 4 * min(qk, 2) + 3;  // the pad lane holding M[8][g]
-  // rows are handed out in index order (a work counter), so the
-  // rows in flight stay a narrow band and their particle bins stay in L2
-  auto next_row = [&]() {
-    int r = 0;
-    if (lane == 0) r = (int)atomicAdd(row_counter, 1u);
-    return L.lo + __shfl_sync(0xffffffffu, r, 0);
-  };
-  for (int i = next_row(); i < L.hi; i = next_row()) {
-    for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
-    // the write-out's column ids and Dirichlet flags, loaded now so their latency hides under
-    // the gather: slot s = lane + 32 j (zero fill), upper slot 62 + lane + 32 j
-    const int* crow = L.cols + (long long)i * kSlotPitch;
-    int zc[kSlotPitch / 32], uc[2];
-    bool ud[2];
+  double C[4][2], E[4];
 #pragma unroll
-    for (int j = 0; j < kSlotPitch / 32; ++j) zc[j] = lane + 32 * j < kSlots ? __ldg(crow + lane + 32 * j) : -1;
+  for (int mt = 0; mt < 4; ++mt) C[mt][0] = C[mt][1] = E[mt] = 0.0;
+  int cur = -1, row = -1, grp = 0, zr = 0;
+  // write-out inputs of the current row (loaded when its tile starts, so their latency hides)
+  int zc[kSlotPitch / 32], uc[2];
+  bool ud[2], di = false;
+  double mi = 0.0;
+  for (int it = 0;; ++it) {
+    const int slot = it % kAsmS;
+    mbar_wait(smem_u32(full + slot), (it / kAsmS) & 1);
+    const AsmMeta m = meta[slot];
+    if (m.kind == kSlotStop) break;
+    if (m.tile != cur) {  // a new tile: this warp's row, its group, accumulator, write-out inputs
+      cur = m.tile;
+      const int r0 = L.lo + cur * kAsmT;
+      row = r0 + wid < L.hi ? r0 + wid : -1;
+      if (row >= 0) {
+        grp = asm_group_of(L, r0, wid);
+        zr = L.coords[3 * row + 2];
+        for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
+        const int* crow = L.cols + (long long)row * kSlotPitch;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) uc[j] = lane + 32 * j < kUpper ? __ldg(crow + kDiagSlot + lane + 32 * j) : -1;
+        for (int j = 0; j < kSlotPitch / 32; ++j) zc[j] = lane + 32 * j < kSlots ? __ldg(crow + lane + 32 * j) : -1;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) ud[j] = uc[j] >= 0 && g.dir[uc[j]] != 0;
-    const bool di = g.dir[i] != 0;
-    const double mi = g.mass[i];
-    const int ci0 = L.coords[3 * i], ci1 = L.coords[3 * i + 1], ci2 = L.coords[3 * i + 2];
-    // lane o < 27 resolves bin offset o (bin node = i + o - 1): first particle and count
-    int my_pb = 0, my_np = 0;
-    if (lane < 27) {
-      const int j = dense_lookup(L.map, ci0 + lane / 9 - 1, ci1 + (lane / 3) % 3 - 1, ci2 + lane % 3 - 1);
-      if (j >= 0) {
-        my_pb = __ldg(bins.start + j);
-        my_np = __ldg(bins.start + j + 1) - my_pb;
-      }
-    }
-    // pair q < 14: bins q and 26-q (q = 13: the centre bin alone); its table row in shared memory
-    {
-      const int pb2 = __shfl_sync(0xffffffffu, my_pb, 26 - min(lane, 26));
-      const int n2 = __shfl_sync(0xffffffffu, my_np, 26 - min(lane, 26));
-      if (lane < 14) {
-        PT[4 * lane] = my_pb;
-        PT[4 * lane + 1] = my_np;
-        PT[4 * lane + 2] = pb2;
-        PT[4 * lane + 3] = lane < 13 ? n2 : 0;
+        for (int j = 0; j < 2; ++j) uc[j] = lane + 32 * j < kUpper ? __ldg(crow + kDiagSlot + lane + 32 * j) : -1;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) ud[j] = uc[j] >= 0 && g.dir[uc[j]] != 0;
+        di = g.dir[row] != 0;
+        mi = g.mass[row];
       }
       __syncwarp();
     }
-    // lane 0 runs the bulk-copy producer one chunk ahead along (pair, c0)
-    int pq_n = 0, c0_n = 0;  // next chunk to issue (lane 0)
-    auto advance = [&]() {   // lane 0: move (pq_n, c0_n) to the next non-empty chunk
-      c0_n += CH;
-      while (pq_n < 14 && c0_n >= max(PT[4 * pq_n + 1], PT[4 * pq_n + 3])) {
-        ++pq_n;
-        c0_n = 0;
-      }
-    };
-    auto issue = [&](int buf) {  // lane 0: one bulk copy per bin and chunk
-      const int pb1 = PT[4 * pq_n], n1 = PT[4 * pq_n + 1], pb2 = PT[4 * pq_n + 2], n2 = PT[4 * pq_n + 3];
-      const int k1 = max(0, min(CH, n1 - c0_n)), k2 = max(0, min(CH, n2 - c0_n));
-      const unsigned mb = smem_u32(mbar + buf);
-      double* dst = Sbuf + buf * asm_stage<CH>();
-      mbar_expect_tx(mb, (k1 + k2) * kParticleBytes);
-      if (k1) bulk_g2s(dst, Tu + (long long)(pb1 + c0_n) * kRecStride, k1 * kParticleBytes, mb);
-      if (k2)
-        bulk_g2s(dst + CH * kRecStride, Tu + (long long)(pb2 + c0_n) * kRecStride, k2 * kParticleBytes, mb);
-    };
-    if (lane == 0) {
-      pq_n = 0;
-      c0_n = -CH;
-      advance();
-      if (pq_n < 14) issue(0);
-      advance();
-    }
-    int buf = 0;
-    for (int pq = 0; pq < 14; ++pq) {
-      const int n1 = PT[4 * pq + 1], n2 = PT[4 * pq + 3];
-      const int nmax = max(n1, n2);
-      if (nmax == 0) continue;
-      // bin b's upper stencil positions: the suffix k >= kmin_b (slot S(k) + S(o_b) >= 62,
-      // S(v) = 25 v0 + 5 v1 + v2); o_0 = pq, o_1 = 26 - pq (S(o_1) = 62 - S(o_0)); the row sits
-      // at stencil position 26 - o_b of the bin's particles
-      const int So0 = c_S27[pq], So1 = 62 - So0;
-      const int kmin0 = c_kmin27[pq], kmin1 = pq == 13 ? 27 : c_kmin27[26 - pq];  // the centre bin has no mirror
-      const int wa0 = kRecW + 3 * (26 - pq), wa1 = kRecW + 3 * pq;
-      auto run = [&](auto nt0c, auto nt1c) {
-        constexpr int NT0 = decltype(nt0c)::value, NT1 = decltype(nt1c)::value;
-        double C0[4][2], C1[4][2], E0[4], E1[4];
-        int oA0[4], oA1[4];  // A fragment W_k[g]: k clamped to 26 (rows past 26 are never folded)
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          C0[mt][0] = C0[mt][1] = C1[mt][0] = C1[mt][1] = E0[mt] = E1[mt] = 0.0;
-          oA0[mt] = kRecW + 3 * min(kmin0 + 8 * mt + qm, 26) + min(qk, 2);
-          oA1[mt] = kRecW + 3 * min(kmin1 + 8 * mt + qm, 26) + min(qk, 2);
+    if (m.kind == kSlotData) {
+      const int a2 = zr - m.bz + 1;
+      if (row >= 0 && m.group == grp && a2 >= 0 && a2 <= 2) {
+        // the row sits at stencil position a = (1 - dx, 1 - dy, a2) of the bin's particles
+        const int kmin = 9 * (2 - m.col / 3) + 3 * (2 - m.col % 3) + a2;
+        const double* S = ring + (size_t)slot * kAsmCP * kTensorStride;
+        // DMMA tiles over the upper positions: ceil((27 - kmin) / 8)
+        if (kmin >= 19) {
+          asm_chunk<1>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          if (m.last) asm_fold<1>(acc, kmin, qm, qk, C, E);
+        } else if (kmin >= 11) {
+          asm_chunk<2>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          if (m.last) asm_fold<2>(acc, kmin, qm, qk, C, E);
+        } else if (kmin >= 3) {
+          asm_chunk<3>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          if (m.last) asm_fold<3>(acc, kmin, qm, qk, C, E);
+        } else {
+          asm_chunk<4>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          if (m.last) asm_fold<4>(acc, kmin, qm, qk, C, E);
         }
-        for (int c0 = 0; c0 < nmax; c0 += CH) {
-          if (lane == 0) {
-            if (pq_n < 14) issue(buf ^ 1);
-            advance();
-          }
-          mbar_wait(smem_u32(mbar + buf), (phase >> buf) & 1u);
-          phase ^= 1u << buf;
-          const double* S = Sbuf + buf * asm_stage<CH>();
-#pragma unroll 1
-          for (int t = 0; t < CH; ++t) {
-            asm_particle<NT0>(S + t * kTensorStride, wa0, tb, src8, lane_g && c0 + t < n1, oA0, C0, E0);
-            if (NT1 > 0)
-              asm_particle<NT1>(S + (CH + t) * kTensorStride, wa1, tb, src8, lane_g && c0 + t < n2, oA1,
-                                C1, E1);
-          }
-          __syncwarp();  // buffer buf is refilled by the next iteration's issue
-          buf ^= 1;
-        }
-        // fold the pair's accumulators into the row: bin 0, then the mirror bin
-        asm_fold<NT0>(acc, kmin0, So0, qm, qk, C0, E0);
-        __syncwarp();
-        if (NT1 > 0) asm_fold<NT1>(acc, kmin1, So1, qm, qk, C1, E1);
-        __syncwarp();
-      };
-      using I0 = std::integral_constant<int, 0>;
-      using I1 = std::integral_constant<int, 1>;
-      using I2 = std::integral_constant<int, 2>;
-      using I3 = std::integral_constant<int, 3>;
-      using I4 = std::integral_constant<int, 4>;
-      // tile counts ceil((27 - kmin) / 8) per bin: (1,4) pq 0-2, (1,3) 3-7, (2,3) 8-10, (2,2) 11-12, (2,0) 13
-      if (pq < 3) run(I1{}, I4{});
-      else if (pq < 8) run(I1{}, I3{});
-      else if (pq < 11) run(I2{}, I3{});
-      else if (pq < 13) run(I2{}, I2{});
-      else run(I2{}, I0{});
-    }
-    // write-out: upper slots + transposed mirror, mass diagonal, Dirichlet projection
-#pragma unroll
-    for (int j = 0; j < kSlotPitch / 32; ++j) {  // inactive / pad slots hold zeros
-      if (zc[j] < 0)
-#pragma unroll
-        for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + lane + 32 * j, 0.0);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int u = lane + 32 * j, s = kDiagSlot + u;
-      const int col = uc[j];
-      if (col < 0) continue;
-      double C[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) C[k] = acc[u * 9 + k];
-      const bool zero = di || ud[j];
-      if (s == kDiagSlot) {
-        if (di) {
-#pragma unroll
-          for (int k = 0; k < 9; ++k) C[k] = (k % 4 == 0) ? 1.0 : 0.0;
-        } else {  // symmetrise (objective.hpp:349-351), then the mass diagonal
-          const double t01 = 0.5 * (C[1] + C[3]), t02 = 0.5 * (C[2] + C[6]), t12 = 0.5 * (C[5] + C[7]);
-          C[1] = C[3] = t01;
-          C[2] = C[6] = t02;
-          C[5] = C[7] = t12;
-          C[0] += mi;
-          C[4] += mi;
-          C[8] += mi;
-        }
-      } else if (zero) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) C[k] = 0.0;
       }
-#pragma unroll
-      for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + s, C[k]);
-      if (s != kDiagSlot) {
-        const int sm = kSlots - 1 - s;
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) __stcs(L.H + ((long long)col * 9 + 3 * r + c) * kSlotPitch + sm, C[3 * c + r]);
-      }
+    } else if (m.kind == kSlotTileEnd && row >= 0) {
+      __syncwarp();
+      asm_write_row(L, row, lane, acc, zc, uc, ud, di, mi);
     }
     __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(empty + slot));
   }
 }
 
@@ -508,18 +537,20 @@ void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s) {
 }
 
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
-                          const double* Tu, unsigned int* row_counter, cudaStream_t s) {
+                          const double* Tu, const double* zeros, unsigned int* tile_counter, cudaStream_t s) {
   if (L.hi <= L.lo) return;
   (void)dx;
   (void)P;
-  // 4 warps x 2 particles per bin chunk (cfg2 assembly per step: 4x2 3.56 ms, 2x2 3.54, 4x1
-  // 3.55, 6x1 3.73, 8x1 3.93, 4x3 3.92); a resident grid taking rows from the work counter
-  constexpr int AW = 4, CH = 2;
-  const int resident = resident_blocks((const void*)k_assemble_rows<AW, CH>, AW * 32, asm_smem<AW, CH>());
-  cudaMemsetAsync(row_counter, 0, sizeof(unsigned int), s);
-  const long long blocks = std::min<long long>(resident, ((long long)(L.hi - L.lo) + AW - 1) / AW);
-  k_assemble_rows<AW, CH><<<(int)blocks, AW * 32, asm_smem<AW, CH>(), s>>>(bins, g, L, Tu, row_counter);
+  // a resident grid of (T consumer + 1 producer)-warp CTAs taking row tiles from a counter in
+  // index order, so the tiles in flight stay a narrow band and their particle bins stay in L2
+  const int resident = resident_blocks((const void*)k_assemble_tiles, (kAsmT + 1) * 32, (int)kAsmSmem);
+  cudaMemsetAsync(tile_counter, 0, sizeof(unsigned int), s);
+  const long long tiles = ((long long)(L.hi - L.lo) + kAsmT - 1) / kAsmT;
+  const long long blocks = std::min<long long>(resident, tiles);
+  k_assemble_tiles<<<(int)blocks, (kAsmT + 1) * 32, kAsmSmem, s>>>(bins, g, L, Tu, zeros, tile_counter);
   count_launches(1);
 }
+
+size_t assemble_zero_bytes() { return (size_t)kAsmCP * kRecBytes; }
 
 }  // namespace hotb200

@@ -142,21 +142,50 @@ def test_cfg4_snow_full_scene_step():
     _baseline_steps("cfg4_snow", 1)
 
 
-@pytest.mark.parametrize("plasticity", [None, {"kind": "von_mises", "yield_stress": 2.0e3}])
-def test_inverted_particles(plasticity):
-    """det F < 0 particles: svd_rv's sign convention on sigma_3 (constitutive.hpp:66-82) in the
-    energy, gradient and projected Hessian, and the von Mises map's skip of inverted particles
-    (transfer.hpp:107-110); x, v, F per element against the oracle over 3 steps."""
-    d = block_scene_dict(youngs=2e5, extra={"fps": 48})
+def _inverted_block(rng, frac, fps, plasticity=None):
+    d = block_scene_dict(youngs=2e5, extra={"fps": fps})
     if plasticity:
         d["materials"][0]["plasticity"] = dict(plasticity)
     sc = scene_from_dict(d)
-    rng = np.random.default_rng(33)
     p = random_block_particles(rng, 0.02, 6, f_spread=0.1, v_spread=0.3)
-    flip = rng.random(p["F"].shape[0]) < 0.2  # a fifth of the particles inverted: one column negated
+    flip = rng.random(p["F"].shape[0]) < frac  # inverted particles: one column of F negated
     p["F"][flip, :, 2] *= -1.0
-    assert (np.linalg.det(p["F"]) < 0).sum() == flip.sum()
-    pr = Pair(sc, p)
+    assert (np.linalg.det(p["F"]) < 0).sum() == flip.sum() > 0
+    return Pair(sc, p)
+
+
+def test_inverted_particles_stages():
+    """det F < 0 on a fifth of the particles: svd_rv's sign convention on sigma_3
+    (constitutive.hpp:66-82) and the |sigma_i + sigma_j| >= 1e-6 clamp of the rotation blocks
+    (constitutive.hpp:178-185) in the energy, the gradient and the projected and unprojected
+    Hessians, against the oracle at dv = 0 and at a random dv."""
+    from tests.gpu_common import rel_err
+    from tests.test_gpu_parity import _sym_err
+
+    pr = _inverted_block(np.random.default_rng(33), 0.2, 48)
+    n = pr.prepare(1.0 / 48)
+    rng = np.random.default_rng(5)
+    for dv in (np.zeros(3 * n), rng.uniform(-0.05, 0.05, 3 * n)):
+        assert pr.gpu.energy(dv) == pytest.approx(pr.orc.energy(dv), rel=1e-11)
+        g, _ = pr.gpu.gradient(dv)
+        assert rel_err(g, pr.orc.gradient(dv)) < 1e-10
+        for project in (True, False):
+            pr.gpu.assemble(dv, project=project)
+            pr.orc.assemble(dv, project=project)
+            G = pr.gpu.level_matrix(0)
+            bo, co = pr.orc.level_matrix(0)
+            assert np.array_equal(G["cols"], co)
+            assert rel_err(G["blocks"], bo) < 1e-10, project
+            assert _sym_err(G) == 0.0
+
+
+@pytest.mark.parametrize("plasticity", [None, {"kind": "von_mises", "yield_stress": 2.0e3}])
+def test_inverted_particles_steps(plasticity):
+    """Steps with 3% of the particles inverted (short steps, so the solve stays well
+    conditioned): x, v, F per element against the oracle over 3 steps, and the von Mises map's
+    skip of inverted particles (transfer.hpp:107-110) with the same inversion counts."""
+    pr = _inverted_block(np.random.default_rng(34), 0.03, 5000, plasticity)
+    sc = pr.sc
     for k in range(3):
         frame_end = (k + 1) / sc.fps
         s = pr.gpu.advance_step(frame_end)
