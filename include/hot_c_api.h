@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define HOT_API_VERSION 1
+#define HOT_API_VERSION 2
 
 enum hot_status {
   HOT_OK = 0,
@@ -40,11 +40,17 @@ enum hot_status {
 
 typedef struct hot_ctx hot_ctx;
 
-/* scene.hpp:13-23 MaterialSpec; plasticity 0 none, 1 von_mises, 2 snow_clamp */
+/* scene.hpp:13-23 MaterialSpec; plasticity 0 none, 1 von_mises, 2 snow_clamp, 3 drucker_prager.
+ * The last three fields are extensions the reference does not have:
+ * elasticity 0 fixed-corotated (the reference's only model), 1 Neo-Hookean; hardening = the
+ * Stomakhin snow hardening coefficient xi (0 = the reference's plain clamp); friction_angle =
+ * the Drucker-Prager friction angle in degrees. */
 typedef struct {
   double density, youngs, poisson;
   int plasticity;
   double yield_stress, clamp_lo, clamp_hi;
+  int elasticity;
+  double hardening, friction_angle;
 } hot_material;
 
 /* scene.hpp:25-32 ShapeSpec; kind 0 box, 1 sphere, 2 half_space, 3 cylinder */
@@ -142,6 +148,12 @@ int hot_sample_scene_particles(const hot_scene* scene, long long* n, double* x, 
 
 int hot_upload_particles(hot_ctx* ctx, long long n, const double* x, const double* v, const double* mass,
                          const double* volume, const double* F, const double* C, const int* material);
+/* Plastic volume ratio J_p per particle, caller order (extension: Stomakhin snow hardening; the
+ * reference's Particle has no plastic state, transfer.hpp:12-21).  Defaults to 1 at upload; only
+ * scenes with a snow material store it (hot_set_plastic_state returns HOT_E_INVALID_ARGUMENT
+ * otherwise; hot_get_plastic_state reports 1).  n = hot_particle_count. */
+int hot_set_plastic_state(hot_ctx* ctx, const double* Jp);
+int hot_get_plastic_state(hot_ctx* ctx, double* Jp);
 int hot_download_particles(hot_ctx* ctx, double* x, double* v, double* F, double* C);
 int hot_particle_count(hot_ctx* ctx, long long* n);
 int hot_set_time(hot_ctx* ctx, double time, int frame, long long step_index);

@@ -459,7 +459,11 @@ inline double cfl_dt(double v_max, double dx, double fps) {
 // constitutive.hpp
 // ---------------------------------------------------------------------------------------
 
-enum class PlasticityKind { None = 0, VonMises = 1, SnowClamp = 2 };
+enum class PlasticityKind { None = 0, VonMises = 1, SnowClamp = 2, DruckerPrager = 3 };
+/// Elastic energy of a material.  The reference has fixed-corotated only (objective.hpp:244,
+/// 268,297 call fcr_* unconditionally); Neo-Hookean is an extension BASELINE configs 2 and 5
+/// name, parity-unpinned against the reference and pinned here by FD tests.
+enum class ElasticityKind { FixedCorotated = 0, NeoHookean = 1 };
 
 /// constitutive.hpp:12-52
 struct Material {
@@ -467,6 +471,13 @@ struct Material {
   PlasticityKind plasticity = PlasticityKind::None;
   double yield_stress = 0;
   double clamp_lo = 1, clamp_hi = 1;
+  // extensions (not in the reference): elastic model, snow hardening
+  // coefficient xi (Stomakhin et al. 2013: mu, lambda scaled by exp(xi (1 - J_p))), and the
+  // Drucker-Prager friction coefficient alpha = sqrt(2/3) 2 sin(phi) / (3 - sin(phi)) (Klar et
+  // al. 2016) from the friction angle phi
+  ElasticityKind elasticity = ElasticityKind::FixedCorotated;
+  double hardening = 0;
+  double friction_angle = 0, dp_alpha = 0;
 
   static Material elastic(double density, double youngs, double poisson) {
     if (!(youngs > 0.0)) throw std::invalid_argument("material: Young's modulus must be positive");
@@ -494,6 +505,38 @@ struct Material {
     m.clamp_lo = lo;
     m.clamp_hi = hi;
     return m;
+  }
+  /// Drucker-Prager sand (extension): friction angle in degrees, in [0, 90).
+  static Material drucker_prager(double density, double youngs, double poisson, double friction_deg) {
+    Material m = elastic(density, youngs, poisson);
+    if (!(friction_deg >= 0.0 && friction_deg < 90.0))
+      throw std::invalid_argument("material: friction angle must lie in [0, 90) degrees");
+    m.plasticity = PlasticityKind::DruckerPrager;
+    m.friction_angle = friction_deg;
+    const double sp = std::sin(friction_deg * 3.14159265358979323846 / 180.0);
+    m.dp_alpha = std::sqrt(2.0 / 3.0) * 2.0 * sp / (3.0 - sp);
+    return m;
+  }
+  /// The extension fields on top of a reference material.
+  Material& with_elasticity(ElasticityKind e) {
+    elasticity = e;
+    return *this;
+  }
+  Material& with_hardening(double xi) {
+    if (!(xi >= 0.0)) throw std::invalid_argument("material: hardening must be non-negative");
+    hardening = xi;
+    return *this;
+  }
+  /// Lame parameters scaled by the snow hardening factor h (h == 1: this material, unchanged).
+  Material hardened(double h) const {
+    Material m = *this;
+    m.mu *= h;
+    m.lambda *= h;
+    return m;
+  }
+  /// exp(xi (1 - J_p)) for snow with hardening, else 1 (Stomakhin et al. 2013, eq. 9).
+  double hardening_factor(double Jp) const {
+    return (plasticity == PlasticityKind::SnowClamp && hardening > 0.0) ? std::exp(hardening * (1.0 - Jp)) : 1.0;
   }
 };
 
@@ -782,6 +825,108 @@ StressDerivative<d> fcr_stress_derivative(const Mat<d>& F, const Material& m) {
   return sym;
 }
 
+// ---------------------------------------------------------------------------------------
+// Neo-Hookean (extension; BASELINE configs 2 and 5).  psi = mu/2 (tr F^T F - d) - mu log J +
+// lambda/2 (log J)^2 (Bonet & Wood; the compressible form used by Stomakhin et al. and the HOT
+// paper's Neo-Hookean scenes).  Undefined for J <= 0: the energy is +inf there (the line search
+// backtracks), the stress and its derivative throw std::domain_error.
+// ---------------------------------------------------------------------------------------
+template <int d>
+double nh_energy_density(const Mat<d>& F, const Material& m) {
+  check_finite_f(F, "nh_energy_density");
+  const auto s = svd_rv(F).sigma;
+  double J = s[0], q = s[0] * s[0];
+  for (int k = 1; k < d; ++k) {
+    J *= s[k];
+    q += s[k] * s[k];
+  }
+  if (!(J > 0.0)) return std::numeric_limits<double>::infinity();
+  const double lj = std::log(J);
+  return 0.5 * m.mu * (q - d) - m.mu * lj + 0.5 * m.lambda * lj * lj;
+}
+
+/// P = mu F + (lambda log J - mu) F^{-T},  F^{-T} = cof(F) / J.
+template <int d>
+Mat<d> nh_stress(const Mat<d>& F, const Material& m) {
+  check_finite_f(F, "nh_stress");
+  const double J = determinant(F);
+  if (!(J > 0.0)) throw std::domain_error("nh_stress: Neo-Hookean requires det(F) > 0");
+  return m.mu * F + ((m.lambda * std::log(J) - m.mu) / J) * cofactor(F);
+}
+
+/// dP/dF in the fcr_stress_derivative layout (row-major (ij),(kl), symmetrised): the same
+/// diagonal-space construction with the Neo-Hookean derivatives of psi(sigma):
+///   psi_i = mu s_i + (lambda log J - mu) / s_i,
+///   psi_ii = mu + (mu - lambda (log J - 1)) / s_i^2,  psi_ij = lambda / (s_i s_j),
+///   (psi_i - psi_j) / (s_i - s_j) = mu + (mu - lambda log J) / (s_i s_j)   (no division by 0),
+///   (psi_i + psi_j) / (s_i + s_j) with the reference's |s_i + s_j| >= 1e-6 clamp.
+template <int d>
+StressDerivative<d> nh_stress_derivative(const Mat<d>& F, const Material& m) {
+  check_finite_f(F, "nh_stress_derivative");
+  constexpr int D = d * d;
+  const auto svd = svd_rv(F);
+  const Vec<d>& s = svd.sigma;
+  double J = s[0];
+  for (int k = 1; k < d; ++k) J *= s[k];
+  if (!(J > 0.0)) throw std::domain_error("nh_stress_derivative: Neo-Hookean requires det(F) > 0");
+  const double mu = m.mu, la = m.lambda, lj = std::log(J);
+  Vec<d> psi;
+  for (int i = 0; i < d; ++i) psi[i] = mu * s[i] + (la * lj - mu) / s[i];
+  std::array<double, D * D> Mhat{};
+  auto MH = [&](int r, int c) -> double& { return Mhat[r * D + c]; };
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      MH(i * d + i, j * d + j) = i == j ? mu + (mu - la * (lj - 1.0)) / (s[i] * s[i]) : la / (s[i] * s[j]);
+  for (int i = 0; i < d; ++i)
+    for (int j = i + 1; j < d; ++j) {
+      const double bd = mu + (mu - la * lj) / (s[i] * s[j]);
+      double sum = s[i] + s[j];
+      const double mag = std::max(std::abs(sum), 1e-6);
+      sum = sum >= 0.0 ? mag : -mag;
+      const double bs = (psi[i] + psi[j]) / sum;
+      const int a = i * d + j, b = j * d + i;
+      MH(a, a) = MH(b, b) = 0.5 * (bd + bs);
+      MH(a, b) = MH(b, a) = 0.5 * (bd - bs);
+    }
+  std::array<double, D * D> Q{};
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      for (int k = 0; k < d; ++k)
+        for (int l = 0; l < d; ++l) Q[(i * d + j) * D + k * d + l] = svd.U(i, k) * svd.V(j, l);
+  std::array<double, D * D> QM{};
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) {
+      double acc = 0.0;
+      for (int k = 0; k < D; ++k) acc += Q[r * D + k] * Mhat[k * D + c];
+      QM[r * D + c] = acc;
+    }
+  StressDerivative<d> out{};
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) {
+      double acc = 0.0;
+      for (int k = 0; k < D; ++k) acc += QM[r * D + k] * Q[c * D + k];
+      out[r * D + c] = acc;
+    }
+  StressDerivative<d> sym{};
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) sym[r * D + c] = 0.5 * (out[r * D + c] + out[c * D + r]);
+  return sym;
+}
+
+/// The material's elastic model (FCR: the reference's functions, unchanged).
+template <int d>
+double energy_density(const Mat<d>& F, const Material& m) {
+  return m.elasticity == ElasticityKind::NeoHookean ? nh_energy_density<d>(F, m) : fcr_energy_density<d>(F, m);
+}
+template <int d>
+Mat<d> stress(const Mat<d>& F, const Material& m) {
+  return m.elasticity == ElasticityKind::NeoHookean ? nh_stress<d>(F, m) : fcr_stress<d>(F, m);
+}
+template <int d>
+StressDerivative<d> stress_derivative(const Mat<d>& F, const Material& m) {
+  return m.elasticity == ElasticityKind::NeoHookean ? nh_stress_derivative<d>(F, m) : fcr_stress_derivative<d>(F, m);
+}
+
 namespace detail {
 /// Cyclic Jacobi eigen-decomposition of a symmetric n x n matrix (stands in for
 /// Eigen::SelfAdjointEigenSolver, constitutive.hpp:208).  On return A's diagonal holds
@@ -865,18 +1010,52 @@ std::array<double, n * n> project_spd(const std::array<double, n * n>& A) {
   return out;
 }
 
-/// constitutive.hpp:224-251
+/// constitutive.hpp:224-251.  Jp (may be null): the plastic volume ratio J_p, updated by the
+/// snow map as J_p <- J_p det(F_trial) / det(F_clamped) (the total J = J_e J_p is unchanged by
+/// the projection; Stomakhin et al. 2013) -- state the reference does not have (SURVEY.md
+/// §0.3), only used by the hardening extension.  Drucker-Prager is an extension (Klar et al.
+/// 2016, section 7.3): projection of the Hencky strain onto the friction cone, or its tip.
 template <int d>
-Mat<d> return_map(const Mat<d>& F_trial, const Material& m) {
+Mat<d> return_map(const Mat<d>& F_trial, const Material& m, double* Jp = nullptr) {
   check_finite_f(F_trial, "return_map");
   switch (m.plasticity) {
     case PlasticityKind::None:
       return F_trial;
     case PlasticityKind::SnowClamp: {
       auto svd = svd_rv(F_trial);
-      for (int i = 0; i < d; ++i) svd.sigma[i] = std::clamp(svd.sigma[i], m.clamp_lo, m.clamp_hi);
+      double Jt = 1.0, Jc = 1.0;
+      for (int i = 0; i < d; ++i) {
+        Jt *= svd.sigma[i];
+        svd.sigma[i] = std::clamp(svd.sigma[i], m.clamp_lo, m.clamp_hi);
+        Jc *= svd.sigma[i];
+      }
+      if (Jp) *Jp *= Jt / Jc;
       Mat<d> S = Mat<d>::zero();
       for (int i = 0; i < d; ++i) S(i, i) = svd.sigma[i];
+      return svd.U * S * transpose(svd.V);
+    }
+    case PlasticityKind::DruckerPrager: {
+      const auto svd = svd_rv(F_trial);
+      double mn = svd.sigma[0];
+      for (int i = 1; i < d; ++i) mn = std::min(mn, svd.sigma[i]);
+      if (!(mn > 0.0)) throw std::domain_error("return_map: Drucker-Prager requires det(F) > 0");
+      Vec<d> eps;
+      double tr = 0.0;
+      for (int i = 0; i < d; ++i) {
+        eps[i] = std::log(svd.sigma[i]);
+        tr += eps[i];
+      }
+      Mat<d> S = Mat<d>::zero();
+      if (tr >= 0.0) {  // expansion: project to the cone's tip, sigma = 1
+        for (int i = 0; i < d; ++i) S(i, i) = 1.0;
+        return svd.U * S * transpose(svd.V);
+      }
+      Vec<d> dev;
+      for (int i = 0; i < d; ++i) dev[i] = eps[i] - tr / d;
+      const double nd = norm(dev);
+      const double dgamma = nd + (d * m.lambda + 2.0 * m.mu) / (2.0 * m.mu) * tr * m.dp_alpha;
+      if (dgamma <= 0.0 || nd == 0.0) return F_trial;  // inside the cone
+      for (int i = 0; i < d; ++i) S(i, i) = std::exp(eps[i] - dgamma * dev[i] / nd);
       return svd.U * S * transpose(svd.V);
     }
     case PlasticityKind::VonMises: {
@@ -904,7 +1083,7 @@ Mat<d> return_map(const Mat<d>& F_trial, const Material& m) {
 /// constitutive.hpp:255-258
 template <int d>
 double stiffness_scale(const Material& m) {
-  const auto T = fcr_stress_derivative<d>(Mat<d>::identity(), m);
+  const auto T = stress_derivative<d>(Mat<d>::identity(), m);
   double s = 0.0;
   for (double v : T) s += v * v;
   return std::sqrt(s);
@@ -923,6 +1102,7 @@ struct Particle {
   Mat<d> F = Mat<d>::identity();
   Mat<d> C = Mat<d>::zero();
   int material = 0;
+  double Jp = 1.0;  // plastic volume ratio (snow hardening extension; the reference has none)
 };
 
 /// transfer.hpp:28-40
@@ -999,9 +1179,10 @@ long update_strain(std::span<Particle<d>> particles, const SparseGrid<d>& grid, 
     const auto& m = materials[p.material];
     if (determinant(p.F) <= 0.0) {
       inv[pi] = 1;
-      if (m.plasticity == PlasticityKind::VonMises) return;
+      // the Hencky-strain maps are undefined for inverted F (Drucker-Prager: extension)
+      if (m.plasticity == PlasticityKind::VonMises || m.plasticity == PlasticityKind::DruckerPrager) return;
     }
-    p.F = return_map(p.F, m);
+    p.F = return_map(p.F, m, &p.Jp);
   });
   long n = 0;
   for (char c : inv) n += c;

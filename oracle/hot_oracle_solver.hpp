@@ -143,6 +143,7 @@ struct ObjectiveState {
     double volume = 0;
     Mat<d> F;
     int material = 0;
+    double hard = 1.0;  // snow hardening factor exp(xi (1 - J_p)) (extension; 1 in the reference)
     std::array<int, stencil_size> node;
     std::array<double, stencil_size> w;
     std::array<Vec<d>, stencil_size> grad;
@@ -182,6 +183,7 @@ ObjectiveState<d> make_objective_state(std::span<const Particle<d>> particles, c
     ref.volume = p.volume;
     ref.F = p.F;
     ref.material = p.material;
+    ref.hard = st.materials[p.material].hardening_factor(p.Jp);
     ref.node.fill(-1);
     ref.w.fill(0.0);
     int k = 0;
@@ -208,6 +210,27 @@ Mat<d> virtual_f(const ObjectiveState<d>& st, const typename ObjectiveState<d>::
   return (Mat<d>::identity() + st.dt * G) * ref.F;
 }
 
+/// The particle's material model: fcr_* for the reference's materials (objective.hpp:244, 268,
+/// 297); Neo-Hookean and the hardened Lame parameters are the extensions.
+template <int d>
+double particle_energy_density(const ObjectiveState<d>& st, const typename ObjectiveState<d>::ParticleRef& ref,
+                               const Mat<d>& F) {
+  const Material& m = st.materials[ref.material];
+  return ref.hard == 1.0 ? energy_density<d>(F, m) : energy_density<d>(F, m.hardened(ref.hard));
+}
+template <int d>
+Mat<d> particle_stress(const ObjectiveState<d>& st, const typename ObjectiveState<d>::ParticleRef& ref,
+                       const Mat<d>& F) {
+  const Material& m = st.materials[ref.material];
+  return ref.hard == 1.0 ? stress<d>(F, m) : stress<d>(F, m.hardened(ref.hard));
+}
+template <int d>
+StressDerivative<d> particle_stress_derivative(const ObjectiveState<d>& st,
+                                               const typename ObjectiveState<d>::ParticleRef& ref, const Mat<d>& F) {
+  const Material& m = st.materials[ref.material];
+  return ref.hard == 1.0 ? stress_derivative<d>(F, m) : stress_derivative<d>(F, m.hardened(ref.hard));
+}
+
 /// objective.hpp:236-257
 template <int d>
 double energy(const ObjectiveState<d>& st, const VecX& dv) {
@@ -216,7 +239,7 @@ double energy(const ObjectiveState<d>& st, const VecX& dv) {
   std::vector<double> phi(np);
   parallel_for(np, [&](std::int64_t pi) {
     const auto& ref = st.particles[pi];
-    phi[pi] = ref.volume * fcr_energy_density<d>(virtual_f(st, ref, dv), st.materials[ref.material]);
+    phi[pi] = ref.volume * particle_energy_density<d>(st, ref, virtual_f(st, ref, dv));
   });
   double e = 0.0;
   for (std::int64_t pi = 0; pi < np; ++pi) e += phi[pi];
@@ -239,7 +262,7 @@ VecX gradient(const ObjectiveState<d>& st, const VecX& dv) {
   std::vector<std::array<Vec<d>, S>> contrib(np);
   parallel_for(np, [&](std::int64_t pi) {
     const auto& ref = st.particles[pi];
-    const Mat<d> P = fcr_stress<d>(virtual_f(st, ref, dv), st.materials[ref.material]);
+    const Mat<d> P = particle_stress<d>(st, ref, virtual_f(st, ref, dv));
     const Mat<d> PFt = P * transpose(ref.F);
     for (int k = 0; k < S; ++k)
       contrib[pi][k] = ref.node[k] < 0 ? Vec<d>{} : ref.volume * (PFt * ref.grad[k]);
@@ -263,7 +286,7 @@ VecX gradient(const ObjectiveState<d>& st, const VecX& dv) {
 template <int d>
 StressDerivative<d> particle_tensor(const ObjectiveState<d>& st, const typename ObjectiveState<d>::ParticleRef& ref,
                                     const VecX& dv, bool project) {
-  StressDerivative<d> Tn = fcr_stress_derivative<d>(virtual_f(st, ref, dv), st.materials[ref.material]);
+  StressDerivative<d> Tn = particle_stress_derivative<d>(st, ref, virtual_f(st, ref, dv));
   if (project) Tn = project_spd<d * d>(Tn);
   return Tn;
 }
@@ -1200,6 +1223,9 @@ struct MaterialSpec {  // scene.hpp:13-23
   double density = 0, youngs = 0, poisson = 0;
   PlasticityKind plasticity = PlasticityKind::None;
   double yield_stress = 0, clamp_lo = 0.99, clamp_hi = 1.001;
+  // extensions: elastic model, snow hardening, Drucker-Prager friction angle
+  ElasticityKind elasticity = ElasticityKind::FixedCorotated;
+  double hardening = 0, friction_angle = 0;
 };
 struct ObjectSpec {
   ShapeSpec shape;
@@ -1421,8 +1447,13 @@ inline std::vector<Material> materials_from_scene(const SceneConfig& scene) {  /
         break;
       case PlasticityKind::SnowClamp:
         mats.push_back(Material::snow(m.density, m.youngs, m.poisson, m.clamp_lo, m.clamp_hi));
+        mats.back().with_hardening(m.hardening);
+        break;
+      case PlasticityKind::DruckerPrager:
+        mats.push_back(Material::drucker_prager(m.density, m.youngs, m.poisson, m.friction_angle));
         break;
     }
+    mats.back().with_elasticity(m.elasticity);
   }
   return mats;
 }

@@ -29,7 +29,8 @@ class OracleError(RuntimeError):
 class Material(C.Structure):
     _fields_ = [("density", C.c_double), ("youngs", C.c_double), ("poisson", C.c_double),
                 ("plasticity", C.c_int), ("yield_stress", C.c_double), ("clamp_lo", C.c_double),
-                ("clamp_hi", C.c_double)]
+                ("clamp_hi", C.c_double), ("elasticity", C.c_int), ("hardening", C.c_double),
+                ("friction_angle", C.c_double)]
 
 
 class Shape(C.Structure):
@@ -75,7 +76,7 @@ ENERGY_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
 SOLVERS = {"hot": 0, "pn-pcg": 1, "pn-pcg-mf": 2, "pn-mgpcg": 3, "lbfgs-h": 4}
 SHAPES = {"box": 0, "sphere": 1, "half_space": 2, "cylinder": 3}
 MOTIONS = {"static": 0, "linear": 1, "rotation": 2}
-PLAST = {"none": 0, "von_mises": 1, "snow_clamp": 2}
+PLAST = {"none": 0, "von_mises": 1, "snow_clamp": 2, "drucker_prager": 3}
 QUADRATIC, LINEAR = 0, 1
 
 _lib = None
@@ -132,6 +133,13 @@ def lib():
         L.orc_lbfgs_size.argtypes = [vp]
         L.orc_lbfgs_direction.argtypes = [vp, C.c_int, dp, APPLY_FN, vp, dp]
         L.orc_set_gravity_dx.argtypes = [vp, dp, C.c_double, C.c_double]
+        L.orc_particle_jp.argtypes = [vp, dp, dp]
+        L.orc_model_energy.argtypes = [C.c_int, dp, vp, C.c_double, dp]
+        L.orc_model_stress.argtypes = [C.c_int, dp, vp, C.c_double, dp]
+        L.orc_model_dpdf.argtypes = [C.c_int, dp, vp, C.c_double, C.c_int, dp]
+        L.orc_return_map_jp.argtypes = [C.c_int, dp, vp, dp, dp]
+        L.orc_hardening_factor.restype = C.c_double
+        L.orc_hardening_factor.argtypes = [vp, C.c_double]
         _lib = L
     return _lib
 
@@ -181,10 +189,15 @@ def _shape(d, dim):
     return s
 
 
+ELASTICITY = {"fixed_corotated": 0, "neo_hookean": 1}
+
+
 def material_struct(m):
     pl = m.get("plasticity", {"kind": "none"})
     return Material(float(m["density"]), float(m["youngs"]), float(m["poisson"]), PLAST[pl["kind"]],
-                    float(pl.get("yield_stress", 0.0)), float(pl.get("lo", 0.99)), float(pl.get("hi", 1.001)))
+                    float(pl.get("yield_stress", 0.0)), float(pl.get("lo", 0.99)), float(pl.get("hi", 1.001)),
+                    ELASTICITY[m.get("elasticity", "fixed_corotated")], float(pl.get("hardening", 0.0)),
+                    float(pl.get("friction_angle", 0.0)))
 
 
 def scene_struct(sc):
@@ -344,6 +357,43 @@ def return_map(F, m):
     return out
 
 
+def energy_density(F, m, h=1.0):
+    """The material's own elastic model (fixed-corotated or the Neo-Hookean extension), Lame
+    parameters scaled by the hardening factor h."""
+    F = _f64(F)
+    out = C.c_double()
+    _check_point(lib().orc_model_energy(F.shape[0], _dp(F), C.byref(material_struct(m)), h, C.byref(out)))
+    return out.value
+
+
+def stress(F, m, h=1.0):
+    F = _f64(F)
+    out = np.zeros_like(F)
+    _check_point(lib().orc_model_stress(F.shape[0], _dp(F), C.byref(material_struct(m)), h, _dp(out)))
+    return out
+
+
+def stress_derivative(F, m, h=1.0, project=False):
+    F = _f64(F)
+    d = F.shape[0]
+    out = np.zeros((d * d, d * d))
+    _check_point(lib().orc_model_dpdf(d, _dp(F), C.byref(material_struct(m)), h, int(project), _dp(out)))
+    return out
+
+
+def return_map_jp(F, m, Jp=1.0):
+    """return_map with the plastic volume ratio: returns (F, J_p)."""
+    F = _f64(F)
+    out = np.zeros_like(F)
+    jp = C.c_double(Jp)
+    _check_point(lib().orc_return_map_jp(F.shape[0], _dp(F), C.byref(material_struct(m)), C.byref(jp), _dp(out)))
+    return out, jp.value
+
+
+def hardening_factor(m, Jp):
+    return lib().orc_hardening_factor(C.byref(material_struct(m)), Jp)
+
+
 def stiffness_scale(m, dim):
     out = C.c_double()
     _check_point(lib().orc_stiffness_scale(dim, C.byref(material_struct(m)), C.byref(out)))
@@ -471,6 +521,15 @@ class Oracle:
         self._check(lib().orc_get_particles(self.ctx, _dp(out["x"]), _dp(out["v"]), _dp(out["mass"]),
                                             _dp(out["volume"]), _dp(out["F"]), _dp(out["C"]), _ip(out["material"])))
         return out
+
+    def particle_jp(self):
+        out = np.zeros(self.particle_count())
+        self._check(lib().orc_particle_jp(self.ctx, _dp(out), None))
+        return out
+
+    def set_particle_jp(self, jp):
+        jp = _f64(jp, self.particle_count())
+        self._check(lib().orc_particle_jp(self.ctx, None, _dp(jp)))
 
     def sim_state(self):
         t, s, inv, fr = C.c_double(), C.c_longlong(), C.c_longlong(), C.c_int()

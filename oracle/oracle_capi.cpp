@@ -14,8 +14,10 @@ extern "C" {
 
 typedef struct {
   double density, youngs, poisson;
-  int plasticity;
+  int plasticity;  // 0 none, 1 von Mises, 2 snow clamp, 3 Drucker-Prager (extension)
   double yield_stress, clamp_lo, clamp_hi;
+  int elasticity;  // 0 fixed-corotated (the reference), 1 Neo-Hookean (extension)
+  double hardening, friction_angle;  // snow hardening xi; Drucker-Prager friction angle (degrees)
 } orc_material;
 typedef struct {
   int kind;
@@ -156,14 +158,23 @@ SolverConfig to_solver(const orc_solver& s) {
 }
 
 Material to_material(const orc_material& m) {
+  Material out;
   switch (m.plasticity) {
     case 1:
-      return Material::von_mises(m.density, m.youngs, m.poisson, m.yield_stress);
+      out = Material::von_mises(m.density, m.youngs, m.poisson, m.yield_stress);
+      break;
     case 2:
-      return Material::snow(m.density, m.youngs, m.poisson, m.clamp_lo, m.clamp_hi);
+      out = Material::snow(m.density, m.youngs, m.poisson, m.clamp_lo, m.clamp_hi);
+      out.with_hardening(m.hardening);
+      break;
+    case 3:
+      out = Material::drucker_prager(m.density, m.youngs, m.poisson, m.friction_angle);
+      break;
     default:
-      return Material::elastic(m.density, m.youngs, m.poisson);
+      out = Material::elastic(m.density, m.youngs, m.poisson);
   }
+  out.with_elasticity(static_cast<ElasticityKind>(m.elasticity));
+  return out;
 }
 
 template <int d>
@@ -240,6 +251,9 @@ int orc_set_scene(void* p, const orc_scene* s) {
       ms.yield_stress = m.yield_stress;
       ms.clamp_lo = m.clamp_lo;
       ms.clamp_hi = m.clamp_hi;
+      ms.elasticity = static_cast<ElasticityKind>(m.elasticity);
+      ms.hardening = m.hardening;
+      ms.friction_angle = m.friction_angle;
       sc.materials.push_back(ms);
     }
     for (int i = 0; i < s->n_objects; ++i) {
@@ -408,6 +422,24 @@ int orc_get_particles(void* p, double* x, double* v, double* mass, double* vol, 
       get_particles_impl<2>(c->s2, x, v, mass, vol, F, C, mat);
     else
       get_particles_impl<3>(c->s3, x, v, mass, vol, F, C, mat);
+  });
+}
+
+/// Plastic volume ratio J_p per particle (snow hardening extension); get/set.
+int orc_particle_jp(void* p, double* out, const double* in) {
+  auto* c = static_cast<Ctx*>(p);
+  return guard(c, [&] {
+    auto io = [&](auto& s) {
+      const long long n = static_cast<long long>(s.sim.particles.size());
+      for (long long i = 0; i < n; ++i) {
+        if (in) s.sim.particles[i].Jp = in[i];
+        if (out) out[i] = s.sim.particles[i].Jp;
+      }
+    };
+    if (c->dim == 2)
+      io(c->s2);
+    else
+      io(c->s3);
   });
 }
 
@@ -965,6 +997,52 @@ int orc_return_map(int dim, const double* F, const orc_material* m, double* out)
       store_mat<3>(return_map<3>(load_mat<3>(F), mm), out);
   });
 }
+
+// ---- the material's own model (extensions dispatch: Neo-Hookean, hardening factor h) ----------
+int orc_model_energy(int dim, const double* F, const orc_material* m, double h, double* out) {
+  return pguard([&] {
+    const Material mm = to_material(*m).hardened(h);
+    *out = dim == 2 ? energy_density<2>(load_mat<2>(F), mm) : energy_density<3>(load_mat<3>(F), mm);
+  });
+}
+
+int orc_model_stress(int dim, const double* F, const orc_material* m, double h, double* out) {
+  return pguard([&] {
+    const Material mm = to_material(*m).hardened(h);
+    if (dim == 2)
+      store_mat<2>(stress<2>(load_mat<2>(F), mm), out);
+    else
+      store_mat<3>(stress<3>(load_mat<3>(F), mm), out);
+  });
+}
+
+int orc_model_dpdf(int dim, const double* F, const orc_material* m, double h, int project, double* out) {
+  return pguard([&] {
+    const Material mm = to_material(*m).hardened(h);
+    if (dim == 2) {
+      auto T = stress_derivative<2>(load_mat<2>(F), mm);
+      if (project) T = project_spd<4>(T);
+      std::memcpy(out, T.data(), sizeof(T));
+    } else {
+      auto T = stress_derivative<3>(load_mat<3>(F), mm);
+      if (project) T = project_spd<9>(T);
+      std::memcpy(out, T.data(), sizeof(T));
+    }
+  });
+}
+
+/// return_map with the plastic volume ratio (in/out through *Jp).
+int orc_return_map_jp(int dim, const double* F, const orc_material* m, double* Jp, double* out) {
+  return pguard([&] {
+    Material mm = to_material(*m);
+    if (dim == 2)
+      store_mat<2>(return_map<2>(load_mat<2>(F), mm, Jp), out);
+    else
+      store_mat<3>(return_map<3>(load_mat<3>(F), mm, Jp), out);
+  });
+}
+
+double orc_hardening_factor(const orc_material* m, double Jp) { return to_material(*m).hardening_factor(Jp); }
 
 int orc_stiffness_scale(int dim, const orc_material* m, double* out) {
   return pguard([&] {

@@ -14,7 +14,10 @@ import numpy as np
 from .scene import SceneConfig
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhotb200.so")
+# HOT_LIB_VARIANT=<name> loads lib/libhotb200_<name>.so: a tuning build of the same sources
+# with other compile-time constants (tools/asm_variants.sh); unset in tests and the bench
+_VARIANT = os.environ.get("HOT_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, "lib", f"libhotb200_{_VARIANT}.so" if _VARIANT else "libhotb200.so")
 
 HOT_OK, HOT_E_INVALID_ARGUMENT, HOT_E_SOLVER_FAILURE, HOT_E_LOGIC, HOT_E_DOMAIN, HOT_E_CUDA, HOT_E_UNSUPPORTED = range(7)
 
@@ -57,7 +60,8 @@ _ERRORS = {HOT_E_INVALID_ARGUMENT: InvalidArgument, HOT_E_SOLVER_FAILURE: Solver
 
 class hot_material(C.Structure):
     _fields_ = [("density", C.c_double), ("youngs", C.c_double), ("poisson", C.c_double), ("plasticity", C.c_int),
-                ("yield_stress", C.c_double), ("clamp_lo", C.c_double), ("clamp_hi", C.c_double)]
+                ("yield_stress", C.c_double), ("clamp_lo", C.c_double), ("clamp_hi", C.c_double),
+                ("elasticity", C.c_int), ("hardening", C.c_double), ("friction_angle", C.c_double)]
 
 
 class hot_shape(C.Structure):
@@ -111,6 +115,7 @@ class hot_diag_row(C.Structure):
 EXPORTS = [
     "hot_version", "hot_device_count", "hot_create", "hot_destroy", "hot_last_error", "hot_set_solver",
     "hot_sample_scene_particles", "hot_upload_particles", "hot_download_particles", "hot_particle_count",
+    "hot_set_plastic_state", "hot_get_plastic_state",
     "hot_set_time", "hot_get_time", "hot_advance_step", "hot_diagnostics", "hot_clear_diagnostics",
     "hot_stage_prepare", "hot_stage_node_count", "hot_stage_grid", "hot_stage_set_grid", "hot_stage_energy",
     "hot_stage_gradient", "hot_stage_assemble", "hot_stage_build_hierarchy", "hot_stage_level_count",
@@ -159,6 +164,8 @@ def lib():
     L.hot_sample_scene_particles.argtypes = [C.POINTER(hot_scene), i64p, dp, dp, dp, dp, dp, dp, ip]
     L.hot_upload_particles.argtypes = [vp, C.c_longlong, dp, dp, dp, dp, dp, dp, ip]
     L.hot_download_particles.argtypes = [vp, dp, dp, dp, dp]
+    L.hot_set_plastic_state.argtypes = [vp, dp]
+    L.hot_get_plastic_state.argtypes = [vp, dp]
     L.hot_particle_count.argtypes = [vp, i64p]
     L.hot_set_time.argtypes = [vp, C.c_double, C.c_int, C.c_longlong]
     L.hot_get_time.argtypes = [vp, dp, ip, i64p, i64p]
@@ -216,7 +223,8 @@ def raise_for(code, msg):
 # -------------------------------------------------------------------------------------------
 _SHAPES = {"box": 0, "sphere": 1, "half_space": 2, "cylinder": 3}
 _MOTIONS = {"static": 0, "linear": 1, "rotation": 2}
-_PLAST = {"none": 0, "von_mises": 1, "snow_clamp": 2}
+_PLAST = {"none": 0, "von_mises": 1, "snow_clamp": 2, "drucker_prager": 3}
+_ELASTICITY = {"fixed_corotated": 0, "neo_hookean": 1}
 SOLVER_KINDS = {"hot": 0, "pn-pcg": 1, "pn-pcg-mf": 2, "pn-mgpcg": 3, "lbfgs-h": 4}
 
 
@@ -241,7 +249,8 @@ def scene_to_c(sc: SceneConfig):
     mats = (hot_material * len(sc.materials))()
     for i, m in enumerate(sc.materials):
         mats[i] = hot_material(m.density, m.youngs, m.poisson, _PLAST[m.plasticity.kind], m.plasticity.yield_stress,
-                               m.plasticity.clamp_lo, m.plasticity.clamp_hi)
+                               m.plasticity.clamp_lo, m.plasticity.clamp_hi, _ELASTICITY[m.elasticity],
+                               m.plasticity.hardening, m.plasticity.friction_angle)
     objs = (hot_object * len(sc.objects))()
     for i, o in enumerate(sc.objects):
         objs[i].shape = _shape(o.shape)

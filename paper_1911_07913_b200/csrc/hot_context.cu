@@ -208,6 +208,8 @@ struct Context {
   long long np = 0;
   DBuf px, pv, pF, pC, pmass, pvol, pmat, stage, porig;
   DBuf qx, qv, qF, qC, qmass, qvol, qmat, qorig;  // reorder targets (swapped each step)
+  DBuf pjp, qjp;         // plastic volume ratio per particle (snow materials; hardening extension)
+  bool track_jp = false; // some material is snow: J_p is stored, reordered and updated
   double time = 0;
   int frame = 0;
   long long step_index = 0, inversions = 0;
@@ -305,6 +307,7 @@ struct Context {
     P.vol = pvol.as<double>();
     P.mat = pmat.as<int>();
     P.bin = pbin.as<int>();
+    P.Jp = track_jp ? pjp.as<double>() : nullptr;
     P.n = np;
     return P;
   }
@@ -414,6 +417,8 @@ struct Context {
     for (int a = 0; a < 3; ++a) grav[a] = s.gravity[a];
     mats_h.clear();
     for (int i = 0; i < s.n_materials; ++i) mats_h.push_back(make_material(s.materials[i]));
+    track_jp = false;
+    for (const DevMaterial& m : mats_h) track_jp = track_jp || m.plasticity == 2;
     if ((int)mats_h.size() > kMaxMaterials) throw std::invalid_argument("too many materials");
     cols_h.clear();
     for (int i = 0; i < s.n_colliders; ++i) cols_h.push_back(make_collider(s.colliders[i]));
@@ -447,13 +452,24 @@ struct Context {
     d.mu = m.youngs / (2.0 * (1.0 + m.poisson));
     d.lambda = m.youngs * m.poisson / ((1.0 + m.poisson) * (1.0 - 2.0 * m.poisson));
     d.plasticity = m.plasticity;
+    if (m.elasticity != 0 && m.elasticity != 1) throw std::invalid_argument("material: unknown elasticity");
+    d.elasticity = m.elasticity;
     if (m.plasticity == 1) {
       if (!(m.yield_stress > 0.0)) throw std::invalid_argument("material: yield stress must be positive");
       d.yield_stress = m.yield_stress;
     } else if (m.plasticity == 2) {
       if (!(m.clamp_lo <= 1.0 && 1.0 <= m.clamp_hi)) throw std::invalid_argument("material: snow clamp must bracket 1");
+      if (!(m.hardening >= 0.0)) throw std::invalid_argument("material: hardening must be non-negative");
       d.clamp_lo = m.clamp_lo;
       d.clamp_hi = m.clamp_hi;
+      d.hardening = m.hardening;
+    } else if (m.plasticity == 3) {  // Drucker-Prager (extension; oracle Material::drucker_prager)
+      if (!(m.friction_angle >= 0.0 && m.friction_angle < 90.0))
+        throw std::invalid_argument("material: friction angle must lie in [0, 90) degrees");
+      const double sp = std::sin(m.friction_angle * 3.14159265358979323846 / 180.0);
+      d.dp_alpha = std::sqrt(2.0 / 3.0) * 2.0 * sp / (3.0 - sp);
+    } else if (m.plasticity != 0) {
+      throw std::invalid_argument("material: unknown plasticity");
     }
     // dP/dF at F = I in diagonal space: (mm) block 2mu I + la 11^T; 2x2 blocks with
     // bd = 2mu - la*0, bs = (psi_i+psi_j)/2 = 0 -> entries (mu, mu).  Frobenius norm is basis
@@ -525,6 +541,11 @@ struct Context {
     qvol.ensure(sizeof(double) * std::max<long long>(n, 1));
     qmat.ensure(sizeof(int) * std::max<long long>(n, 1));
     qorig.ensure(sizeof(int) * std::max<long long>(n, 1));
+    if (track_jp) {  // J_p = 1: no plastic volume change yet (hot_set_plastic_state overrides)
+      pjp.ensure(sizeof(double) * std::max<long long>(n, 1));
+      qjp.ensure(sizeof(double) * std::max<long long>(n, 1));
+      launch_fill(pjp.as<double>(), n, 1.0, stream);
+    }
     // one staging region per interleaved field, so the host->device copies run back to back
     // (no DMA gaps for the transposes) and the transposes follow
     stage.ensure(sizeof(double) * 24 * std::max<long long>(n, 1));
@@ -609,6 +630,27 @@ struct Context {
     sync();
   }
 
+  /// Plastic volume ratio J_p in the caller's particle order (snow materials; extension).
+  void set_plastic_state(const double* Jp) {
+    if (!track_jp) throw std::invalid_argument("no snow material: there is no plastic state");
+    if (np == 0) return;
+    stage.ensure(sizeof(double) * std::max<long long>(np, 1));
+    HOT_CUDA(cudaMemcpyAsync(stage.p, Jp, sizeof(double) * np, cudaMemcpyHostToDevice, stream));
+    launch_gather_perm(stage.as<double>(), pjp.as<double>(), np, porig.as<int>(), stream);
+    sync();
+  }
+  void get_plastic_state(double* Jp) {
+    if (np == 0) return;
+    if (!track_jp) {
+      std::fill(Jp, Jp + np, 1.0);
+      return;
+    }
+    stage.ensure(sizeof(double) * std::max<long long>(np, 1));
+    launch_soa_to_aos_perm(pjp.as<double>(), stage.as<double>(), np, 1, porig.as<int>(), stream);
+    HOT_CUDA(cudaMemcpyAsync(Jp, stage.p, sizeof(double) * np, cudaMemcpyDeviceToHost, stream));
+    sync();
+  }
+
   // ------------------------------------------------------------------ step stages
   /// activate_grid (grid.hpp:137-165) + particle binning by stencil centre.
   void activate() {
@@ -671,6 +713,7 @@ struct Context {
     Q.mass = qmass.as<double>();
     Q.vol = qvol.as<double>();
     Q.mat = qmat.as<int>();
+    Q.Jp = track_jp ? qjp.as<double>() : nullptr;
     pbin.ensure(sizeof(int) * std::max<long long>(np, 1));
     Q.bin = pbin.as<int>();
     launch_reorder_particles(P, Q, bin_pid.as<int>(), bin_of.as<int>(), porig.as<int>(), qorig.as<int>(), stream);
@@ -682,6 +725,7 @@ struct Context {
     pvol.swap(qvol);
     pmat.swap(qmat);
     porig.swap(qorig);
+    if (track_jp) pjp.swap(qjp);
     nb27.ensure(sizeof(int) * 27 * std::max(n, 1));
     bin_part.ensure(sizeof(double) * 135 * std::max(n, 1));  // per (bin, stencil position): P2G 5, gradient 3
     launch_fill_nb27(gview(), nb27.as<int>(), stream);
@@ -1925,6 +1969,16 @@ int hot_upload_particles(hot_ctx* ctx, long long n, const double* x, const doubl
 
 int hot_download_particles(hot_ctx* ctx, double* x, double* v, double* F, double* C) {
   return guard(ctx, [&] { ctx->c.download(x, v, F, C); });
+}
+
+int hot_set_plastic_state(hot_ctx* ctx, const double* Jp) {
+  if (!ctx || !Jp) return HOT_E_INVALID_ARGUMENT;
+  return guard(ctx, [&] { ctx->c.set_plastic_state(Jp); });
+}
+
+int hot_get_plastic_state(hot_ctx* ctx, double* Jp) {
+  if (!ctx || !Jp) return HOT_E_INVALID_ARGUMENT;
+  return guard(ctx, [&] { ctx->c.get_plastic_state(Jp); });
 }
 
 int hot_particle_count(hot_ctx* ctx, long long* n) {

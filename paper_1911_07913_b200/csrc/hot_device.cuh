@@ -8,9 +8,14 @@
 //   fcr_energy_density / fcr_stress / fcr_stress_derivative      constitutive.hpp:115-199
 //   project_spd (eigen-clamp at 0, identity when nothing clamps)  constitutive.hpp:203-219
 //   return_map (snow clamp, von Mises on Hencky strain)           constitutive.hpp:224-251
+// Extensions the reference does not have, restated from the oracle
+// (oracle/hot_oracle.hpp nh_*, return_map): Neo-Hookean psi / P / dP/dF, the snow map's plastic
+// volume ratio (hardening), the Drucker-Prager return map.
 #pragma once
 
 #include <cstdint>
+
+#include <math_constants.h>
 
 namespace hotb200 {
 
@@ -22,8 +27,10 @@ constexpr int kMaxMaterials = 16;
 struct DevMaterial {
   double mu, lambda, xi;  // Lame parameters, stiffness scale (constitutive.hpp:255-258)
   double yield_stress, clamp_lo, clamp_hi;
-  int plasticity;         // 0 none, 1 von Mises, 2 snow clamp
-  int pad;
+  double hardening;       // snow: Stomakhin hardening xi (extension; 0 = the reference's clamp)
+  double dp_alpha;        // Drucker-Prager friction coefficient (extension)
+  int plasticity;         // 0 none, 1 von Mises, 2 snow clamp, 3 Drucker-Prager (extension)
+  int elasticity;         // 0 fixed-corotated (the reference), 1 Neo-Hookean (extension)
 };
 
 struct DenseMap {
@@ -347,6 +354,54 @@ __device__ __forceinline__ M3 fcr_P(const M3& F, const M3& U, const M3& V, doubl
   return P;
 }
 
+/// Neo-Hookean psi = mu/2 (sum s^2 - 3) - mu log J + lambda/2 (log J)^2 (extension; +inf for
+/// J <= 0, where the model is undefined: the line search backtracks).
+__device__ __forceinline__ double nh_psi(const double s[3], double mu, double la) {
+  const double J = s[0] * s[1] * s[2];
+  if (!(J > 0.0)) return CUDART_INF;
+  const double q = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+  const double lj = log(J);
+  return 0.5 * mu * (q - 3.0) - mu * lj + 0.5 * la * lj * lj;
+}
+
+/// Neo-Hookean P = mu F + (lambda log J - mu) cof(F) / J (extension); NaN for J <= 0 (the
+/// oracle throws domain_error there; a NaN gradient is reported the same way by the solve).
+__device__ __forceinline__ M3 nh_P(const M3& F, double mu, double la) {
+  const double J = m3_det(F);
+  M3 P;
+  if (!(J > 0.0)) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) P.m[i] = CUDART_NAN;
+    return P;
+  }
+  const M3 cof = m3_cofactor(F);
+  const double c = (la * log(J) - mu) / J;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) P.m[i] = mu * F.m[i] + c * cof.m[i];
+  return P;
+}
+
+/// The material's elastic energy density / first Piola stress (FCR: the reference's).
+__device__ __forceinline__ double model_psi(const double s[3], double mu, double la, int elasticity) {
+  return elasticity == 1 ? nh_psi(s, mu, la) : fcr_psi(s, mu, la);
+}
+__device__ __forceinline__ M3 model_P(const M3& F, const M3& U, const M3& V, double mu, double la, int elasticity) {
+  return elasticity == 1 ? nh_P(F, mu, la) : fcr_P(F, U, V, mu, la);
+}
+
+/// Lame parameters of particle p's material with the snow hardening factor exp(xi (1 - J_p))
+/// (extension; 1 -- and the material's own values, bit for bit -- without hardening).
+__device__ __forceinline__ void particle_lame(const DevMaterial& m, const double* __restrict__ Jp, long long p,
+                                              double& mu, double& la) {
+  mu = m.mu;
+  la = m.lambda;
+  if (m.plasticity == 2 && m.hardening > 0.0) {
+    const double h = exp(m.hardening * (1.0 - Jp[p]));
+    mu *= h;
+    la *= h;
+  }
+}
+
 /// Symmetric 3x3 eigen-decomposition by cyclic Jacobi (for the diagonal-space block of
 /// dP/dF).  A is overwritten with a diagonal; Q columns are eigenvectors.
 __device__ __forceinline__ void sym3_eig(double A[3][3], double Q[3][3]) {
@@ -396,24 +451,38 @@ __device__ __forceinline__ void sym3_eig(double A[3][3], double Q[3][3]) {
 /// three 2x2 blocks on the (mn),(nm) pairs), so clamping Mhat's eigenvalues and conjugating
 /// back equals the reference's 9x9 eigen-clamp up to rounding.  When no eigenvalue is
 /// negative the unclamped Mhat is used (the reference returns its input unchanged).
-__device__ __forceinline__ void fcr_dpdf_projected(const M3& U, const double s[3], const M3& V, double mu, double la,
-                                                   double kappa, bool project, double Tu[45]) {
+///
+/// elasticity 1 (Neo-Hookean, extension) uses the same construction with its derivatives of
+/// psi(sigma) (oracle nh_stress_derivative): psi_i = mu s_i + (lambda log J - mu) / s_i,
+/// psi_ii = mu + (mu - lambda (log J - 1)) / s_i^2, psi_ij = lambda / (s_i s_j), and
+/// (psi_i - psi_j) / (s_i - s_j) = mu + (mu - lambda log J) / (s_i s_j).
+__device__ __forceinline__ void model_dpdf_projected(const M3& U, const double s[3], const M3& V, double mu,
+                                                     double la, int elasticity, double kappa, bool project,
+                                                     double Tu[45]) {
   const double J = s[0] * s[1] * s[2];
+  const bool nh = elasticity == 1;
+  const double lj = nh ? log(J) : 0.0;  // NaN for J <= 0: the record is poisoned like the oracle's throw
   const double Jp[3] = {s[1] * s[2], s[0] * s[2], s[0] * s[1]};
   double psi[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) psi[i] = 2.0 * mu * (s[i] - 1.0) + la * (J - 1.0) * Jp[i];
+  for (int i = 0; i < 3; ++i)
+    psi[i] = nh ? mu * s[i] + (la * lj - mu) / s[i] : 2.0 * mu * (s[i] - 1.0) + la * (J - 1.0) * Jp[i];
   // 3x3 block on the (mm) indices
   double A[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      double a = la * Jp[i] * Jp[j];
-      if (i == j)
-        a += 2.0 * mu;
-      else
-        a += la * (J - 1.0) * s[3 - i - j];
+      double a;
+      if (nh) {
+        a = i == j ? mu + (mu - la * (lj - 1.0)) / (s[i] * s[i]) : la / (s[i] * s[j]);
+      } else {
+        a = la * Jp[i] * Jp[j];
+        if (i == j)
+          a += 2.0 * mu;
+        else
+          a += la * (J - 1.0) * s[3 - i - j];
+      }
       A[i][j] = a;
     }
   // 2x2 blocks: pairs (0,1), (0,2), (1,2): diag value e1, off value e2
@@ -422,7 +491,7 @@ __device__ __forceinline__ void fcr_dpdf_projected(const M3& U, const double s[3
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int i = pi[k], j = pj[k];
-    const double bd = 2.0 * mu - la * (J - 1.0) * s[3 - i - j];
+    const double bd = nh ? mu + (mu - la * lj) / (s[i] * s[j]) : 2.0 * mu - la * (J - 1.0) * s[3 - i - j];
     double sum = s[i] + s[j];
     const double mag = fmax(fabs(sum), 1e-6);
     sum = sum >= 0.0 ? mag : -mag;
@@ -516,17 +585,39 @@ __device__ __forceinline__ void fcr_dpdf_projected(const M3& U, const double s[3
 /// Index of (r, c), r <= c, in the 45-entry row-major upper triangle of a 9x9.
 __host__ __device__ __forceinline__ int tri9(int r, int c) { return r * 9 - (r * (r - 1)) / 2 + (c - r); }
 
-/// Plastic return map (constitutive.hpp:224-251).  Returns false (and leaves F) for von
-/// Mises on a non-positive singular value, which the caller never reaches (update_strain
-/// skips inverted von Mises particles, transfer.hpp:107-110).
-__device__ __forceinline__ void return_map(M3& F, const DevMaterial& m) {
+/// Plastic return map (constitutive.hpp:224-251).  Leaves F for von Mises on a non-positive
+/// singular value, which the caller never reaches (update_strain skips inverted von Mises
+/// particles, transfer.hpp:107-110).  Extensions: the snow map multiplies the plastic volume
+/// ratio *Jp by det(F_trial) / det(F_clamped); Drucker-Prager (Klar et al. 2016) projects the
+/// Hencky strain onto the friction cone (expansion: onto its tip, sigma = 1).
+__device__ __forceinline__ void return_map(M3& F, const DevMaterial& m, double* Jp) {
   if (m.plasticity == 0) return;
   M3 U, V;
   double s[3];
   svd3(F, U, s, V);
   if (m.plasticity == 2) {
+    const double Jt = s[0] * s[1] * s[2];
 #pragma unroll
     for (int i = 0; i < 3; ++i) s[i] = fmin(fmax(s[i], m.clamp_lo), m.clamp_hi);
+    *Jp *= Jt / (s[0] * s[1] * s[2]);
+  } else if (m.plasticity == 3) {
+    if (!(fmin(s[0], fmin(s[1], s[2])) > 0.0)) return;
+    double eps[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) eps[i] = log(s[i]);
+    const double tr = eps[0] + eps[1] + eps[2];
+    if (tr >= 0.0) {
+      s[0] = s[1] = s[2] = 1.0;
+    } else {
+      double dev[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dev[i] = eps[i] - tr / 3.0;
+      const double nd = sqrt(dev[0] * dev[0] + dev[1] * dev[1] + dev[2] * dev[2]);
+      const double dgamma = nd + (3.0 * m.lambda + 2.0 * m.mu) / (2.0 * m.mu) * tr * m.dp_alpha;
+      if (dgamma <= 0.0 || nd == 0.0) return;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s[i] = exp(eps[i] - dgamma * dev[i] / nd);
+    }
   } else {
     if (!(fmin(s[0], fmin(s[1], s[2])) > 0.0)) return;
     double eps[3];

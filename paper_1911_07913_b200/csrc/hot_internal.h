@@ -20,6 +20,7 @@ struct ParticlesView {
   double* vol;
   int* mat;
   int* bin;  // stencil-centre node (bin) of each particle slot; valid after activation (bin order)
+  double* Jp;  // plastic volume ratio (snow materials only, else null; extension: hardening)
   long long n;
 };
 
@@ -214,6 +215,9 @@ void launch_soa_to_aos(const double* in, double* out, long long n, int comps, cu
 /// out[perm[t]*comps + k] = in[k*n + t]  (back to the caller's particle order)
 void launch_soa_to_aos_perm(const double* in, double* out, long long n, int comps, const int* perm, cudaStream_t s);
 void launch_iota(int* out, long long n, cudaStream_t s);
+/// out[t] = in[perm[t]]
+void launch_gather_perm(const double* in, double* out, long long n, const int* perm, cudaStream_t s);
+void launch_fill(double* out, long long n, double value, cudaStream_t s);
 
 constexpr int kMaxDevices = 64;
 /// SM count of the current device (cached per device).

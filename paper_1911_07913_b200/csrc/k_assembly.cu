@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(kTWarps * 32, MINB) k_particle_tensors(Particl
       }
       if (ok) {
         const DevMaterial mt = mats[mat];
+        double mu, la;
+        particle_lame(mt, P.Jp, p, mu, la);
         double T[45];
-        fcr_dpdf_projected(U, s, V, mt.mu, mt.lambda, dt * dt * vol, project != 0, T);
+        model_dpdf_projected(U, s, V, mu, la, mt.elasticity, dt * dt * vol, project != 0, T);
 #pragma unroll
         for (int q = 0; q < kTPacked; ++q) stage[wib][lane][tperm(q)] = T[q];  // T slot tslot(r, c)
       }
@@ -191,9 +193,18 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols, unsigned long l
 /// arrive.expect_tx; the T consumer warps wait on the slot's full barrier and release it on its
 /// empty barrier.  The register accumulators of a (bin, row) are folded into the row's shared
 /// accumulator once per bin, in a fixed order (no atomics).
-constexpr int kAsmT = 4;                  // rows (consumer warps) per tile
-constexpr int kAsmCP = 4;                 // particle records per ring slot
-constexpr int kAsmS = 10;                 // ring slots
+#ifndef HOT_ASM_T
+#define HOT_ASM_T 4
+#endif
+#ifndef HOT_ASM_CP
+#define HOT_ASM_CP 4
+#endif
+#ifndef HOT_ASM_S
+#define HOT_ASM_S 10
+#endif
+constexpr int kAsmT = HOT_ASM_T;          // rows (consumer warps) per tile
+constexpr int kAsmCP = HOT_ASM_CP;        // particle records per ring slot
+constexpr int kAsmS = HOT_ASM_S;          // ring slots
 constexpr int kAsmSpan = 3 * kAsmT + 2;   // z extent of a group's bin columns, at most
 constexpr unsigned kRecBytes = kTensorStride * 8;  // 1008 = 63 x 16
 enum : int { kSlotData = 0, kSlotTileEnd = 1, kSlotStop = 2 };
@@ -330,6 +341,20 @@ __device__ __forceinline__ void asm_write_row(const LevelView& L, int i, int lan
   }
 }
 
+/// mbarrier wait that suspends the warp in hardware between probes instead of spinning (the
+/// spin loop's YIELD / TRYWAIT / BRA otherwise steal issue slots from the compute warps).
+__device__ __forceinline__ void mbar_wait_sleep(unsigned bar, unsigned parity) {
+#ifndef HOT_ASM_SPIN
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          bar),
+      "r"(parity), "r"(100000)
+      : "memory");
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -360,7 +385,7 @@ __global__ void __launch_bounds__((kAsmT + 1) * 32) k_assemble_tiles(BinsView bi
     int it = 0;        // slots issued (lane 0 counts; broadcast after each group)
     auto acquire = [&]() {  // lane 0: wait until slot it % S is free again
       const int slot = it % kAsmS;
-      mbar_wait(smem_u32(empty + slot), ((it / kAsmS) & 1) ^ 1);
+      mbar_wait_sleep(smem_u32(empty + slot), ((it / kAsmS) & 1) ^ 1);
       return slot;
     };
     for (;;) {
@@ -452,7 +477,7 @@ __global__ void __launch_bounds__((kAsmT + 1) * 32) k_assemble_tiles(BinsView bi
   double mi = 0.0;
   for (int it = 0;; ++it) {
     const int slot = it % kAsmS;
-    mbar_wait(smem_u32(full + slot), (it / kAsmS) & 1);
+    mbar_wait_sleep(smem_u32(full + slot), (it / kAsmS) & 1);
     const AsmMeta m = meta[slot];
     if (m.kind == kSlotStop) break;
     if (m.tile != cur) {  // a new tile: this warp's row, its group, accumulator, write-out inputs

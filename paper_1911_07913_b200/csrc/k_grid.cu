@@ -456,6 +456,7 @@ __global__ void k_reorder(ParticlesView src, ParticlesView dst, const int* __res
     }
     dst.mass[t] = src.mass[p];
     dst.vol[t] = src.vol[p];
+    if (src.Jp) dst.Jp[t] = src.Jp[p];
     dst.mat[t] = src.mat[p];
     dst.bin[t] = bin_of[p];
     orig_dst[t] = orig_src[p];

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(NT, MINB) k_particle_energy(ParticlesView P, G
       continue;
     }
     const DevMaterial mt = mats[P.mat[p]];
+    double mu, la;
+    particle_lame(mt, P.Jp, p, mu, la);
     M3 U, V;
     double s[3];
     svd3(F, U, s, V);
@@ -79,9 +81,9 @@ __global__ void __launch_bounds__(NT, MINB) k_particle_energy(ParticlesView P, G
       for (int k = 0; k < 3; ++k) svd_out[(9 + k) * n + p] = s[k];
     }
     const double vol = P.vol[p];
-    pe[p] = vol * fcr_psi(s, mt.mu, mt.lambda);
+    pe[p] = vol * model_psi(s, mu, la, mt.elasticity);
     if (stress) {
-      const M3 Pk = fcr_P(F, U, V, mt.mu, mt.lambda);
+      const M3 Pk = model_P(F, U, V, mu, la, mt.elasticity);
       const M3 PFt = m3_mul_bt(Pk, Fn);
 #pragma unroll
       for (int k = 0; k < 9; ++k) stress[k * n + p] = vol * PFt.m[k];

@@ -75,9 +75,13 @@ __global__ void __launch_bounds__(NT) k_g2p_strain_advect(ParticlesView P, GridV
     bool skip_map = false;
     if (m3_det(F) <= 0.0) {
       atomicAdd(inverted, 1);
-      skip_map = mt.plasticity == 1;
+      skip_map = mt.plasticity == 1 || mt.plasticity == 3;  // Hencky-strain maps (Drucker-Prager: extension)
     }
-    if (!skip_map) return_map(F, mt);
+    if (!skip_map) {
+      double jp = P.Jp ? P.Jp[p] : 1.0;
+      return_map(F, mt, &jp);
+      if (P.Jp) P.Jp[p] = jp;
+    }
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
       P.F[k * n + p] = F.m[k];
@@ -180,6 +184,22 @@ __global__ void k_iota(int* out, long long n) {
 void launch_soa_to_aos_perm(const double* in, double* out, long long n, int comps, const int* perm, cudaStream_t s) {
   if (n) { k_soa_to_aos_perm<<<tgrid(n * comps, 256), 256, 0, s>>>(in, out, n, comps, perm); count_launches(1); }
 }
+__global__ void k_gather_perm(const double* __restrict__ in, double* __restrict__ out, long long n,
+                              const int* __restrict__ perm) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    out[t] = in[perm[t]];
+}
+__global__ void k_fill(double* __restrict__ out, long long n, double value) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    out[t] = value;
+}
+void launch_gather_perm(const double* in, double* out, long long n, const int* perm, cudaStream_t s) {
+  if (n) { k_gather_perm<<<tgrid(n, 256), 256, 0, s>>>(in, out, n, perm); count_launches(1); }
+}
+void launch_fill(double* out, long long n, double value, cudaStream_t s) {
+  if (n) { k_fill<<<tgrid(n, 256), 256, 0, s>>>(out, n, value); count_launches(1); }
+}
+
 void launch_iota(int* out, long long n, cudaStream_t s) {
   if (n) { k_iota<<<tgrid(n, 256), 256, 0, s>>>(out, n); count_launches(1); }
 }

@@ -105,6 +105,18 @@ class Simulation:
                                                      dptr(out["C"])))
         return out
 
+    def plastic_state(self):
+        """J_p per particle (snow hardening extension; 1 when no material is snow)."""
+        out = np.zeros(self.particle_count())
+        self._check(self._lib.hot_get_plastic_state(self._h, dptr(out)))
+        return out
+
+    def set_plastic_state(self, jp):
+        jp = np.ascontiguousarray(jp, dtype=np.float64)
+        if jp.shape != (self.particle_count(),):
+            raise ValueError("one J_p per particle")
+        self._check(self._lib.hot_set_plastic_state(self._h, dptr(jp)))
+
     def set_time(self, time=0.0, frame=0, step_index=0):
         self._lib.hot_set_time(self._h, time, frame, step_index)
 

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(capi.EXPORTS)
-    assert capi.lib().hot_version() == 1
+    assert capi.lib().hot_version() == 2
 
 
 def test_library_is_sm100a():
