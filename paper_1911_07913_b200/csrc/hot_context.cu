@@ -234,7 +234,6 @@ struct Context {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DBuf scan_tmp2, struct_flags;
   DBuf grid_bar;  // words 0-1: the persistent smoothers' grid barrier; word 8: the assembly's tile counter
-  DBuf asm_zeros; // zero particle records padding the assembly's staged bin chunks
   DBuf bin_part;  // per (bin, stencil position) particle sums feeding the node gathers (P2G, gradient)
   DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
@@ -393,8 +392,6 @@ struct Context {
     HOT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     struct_flags.ensure(sizeof(int) * 16);
     active_dev.ensure(sizeof(unsigned long long) * kMaxLevels);
-    asm_zeros.ensure(assemble_zero_bytes());
-    HOT_CUDA(cudaMemset(asm_zeros.p, 0, assemble_zero_bytes()));
     HOT_CUDA(cudaMemset(active_dev.p, 0, sizeof(unsigned long long) * kMaxLevels));
     grid_bar.ensure(sizeof(unsigned int) * 16);
     HOT_CUDA(cudaMallocHost(&host_scal, sizeof(double) * 64));
@@ -1038,8 +1035,7 @@ struct Context {
       v0.lo = sh.a_lo;
       v0.hi = sh.r_hi;
     }
-    launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), asm_zeros.as<double>(),
-                         grid_bar.as<unsigned int>() + 8, stream);
+    launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), grid_bar.as<unsigned int>() + 8, stream);
     // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
     prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
     have_H = true;

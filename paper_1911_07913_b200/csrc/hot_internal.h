@@ -154,10 +154,9 @@ void launch_particle_tensors(const ParticlesView& P, GridView g, double dx, doub
                              cudaStream_t s, long long plo = 0, long long phi = -1);  // particles [plo, phi)
 /// Column ids of every slot (-1 inactive); *active = the level's active-slot count.
 void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s);
-/// zeros: assemble_zero_bytes() of zeros (pads the staged bin chunks); tile_counter: 1 word.
+/// tile_counter: 1 device word (the row tiles' work counter).
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
-                          const double* Tu, const double* zeros, unsigned int* tile_counter, cudaStream_t s);
-size_t assemble_zero_bytes();
+                          const double* Tu, unsigned int* tile_counter, cudaStream_t s);
 
 // ---------------------------------------------------------------- multigrid (k_multigrid.cu)
 /// quad: quadratic node embedding (multigrid.hpp:72-90).

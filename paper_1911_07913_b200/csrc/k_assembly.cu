@@ -186,21 +186,26 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols, unsigned long l
 /// ce 0..7, K = g padded to 4); the ninth column ce = 8 goes to the FMA pipe.  Each lane forms its
 /// own B-fragment entry M[ce][g] from three staged T entries and W_a.
 ///
-/// Pipeline: a ring of S slots of CP particle records (CP x 1008 B each).  The producer warp's
-/// lane 0 fills a slot with one bulk copy of a bin chunk (plus a bulk copy from a zero buffer
-/// padding the chunk to CP records, so the consumers' unrolled particle loop needs no predicates:
-/// a zero record contributes exactly zero), the slot's metadata and an mbarrier
-/// arrive.expect_tx; the T consumer warps wait on the slot's full barrier and release it on its
-/// empty barrier.  The register accumulators of a (bin, row) are folded into the row's shared
-/// accumulator once per bin, in a fixed order (no atomics).
+/// Pipeline: a ring of S slots of up to CP particle records (CP x 1008 B each).  The producer
+/// warp's lane 0 fills a slot with one bulk copy of a bin chunk, the slot's metadata and an
+/// mbarrier arrive.expect_tx; the T consumer warps wait on the slot's full barrier (suspending
+/// in hardware, not spinning) and release it on its empty barrier.  The consumers' particle loop
+/// is unrolled over CP with a warp-uniform exit at the chunk's count, so every load uses an
+/// immediate offset from a per-chunk base.  The register accumulators of a (bin, row) are
+/// folded into the row's shared accumulator once per bin, in a fixed order (no atomics).
+///
+/// Tuning (cfg2, level-0 assembly per step, tools/asm_variants.sh; the old one-row-per-warp
+/// kernel took 5.73 ms): CP x S = 8 x 4 5.29 ms, 8 x 5 5.93, 8 x 6 5.88, 4 x 8 5.79, 16 x 2
+/// 6.97; T = 2 / 8 rows per tile 8.4 / 7.7 ms against 6.6 at T = 4 (CP 4); register caps for
+/// more CTAs per SM spill and lose (6.3-6.7 ms); two accumulator chains per chunk 6.0 vs 5.84.
 #ifndef HOT_ASM_T
 #define HOT_ASM_T 4
 #endif
 #ifndef HOT_ASM_CP
-#define HOT_ASM_CP 4
+#define HOT_ASM_CP 8
 #endif
 #ifndef HOT_ASM_S
-#define HOT_ASM_S 10
+#define HOT_ASM_S 4
 #endif
 constexpr int kAsmT = HOT_ASM_T;          // rows (consumer warps) per tile
 constexpr int kAsmCP = HOT_ASM_CP;        // particle records per ring slot
@@ -209,7 +214,7 @@ constexpr int kAsmSpan = 3 * kAsmT + 2;   // z extent of a group's bin columns, 
 constexpr unsigned kRecBytes = kTensorStride * 8;  // 1008 = 63 x 16
 enum : int { kSlotData = 0, kSlotTileEnd = 1, kSlotStop = 2 };
 struct AsmMeta {
-  int kind, tile, group, col, bz, last, pad0, pad1;
+  int kind, tile, group, col, bz, last, cnt, pad1;
 };
 constexpr size_t kAsmRingBytes = (size_t)kAsmS * kAsmCP * kRecBytes;
 constexpr size_t kAsmAccBytes = (size_t)kAsmT * kUpper * 9 * 8;
@@ -246,7 +251,7 @@ __device__ __forceinline__ void dmma_f64(double (&c)[2], double a, double b) {
 /// M[8][g] to the lanes of column g.  gmask zeroes the pad lanes' B row and FMA term.
 template <int NT>
 __device__ __forceinline__ void asm_chunk(const double* __restrict__ S, int kmin, const int (&tb)[3], int src8,
-                                          double gmask, int qm, int qk, double (&C)[4][2], double (&E)[4]) {
+                                          double gmask, int qm, int qk, double (&C)[4][2], double (&E)[4], int cnt) {
   const double* pw = S + kRecW + 3 * kmin;
   const double* pt0 = S + tb[0];
   const double* pt1 = S + tb[1];
@@ -256,6 +261,7 @@ __device__ __forceinline__ void asm_chunk(const double* __restrict__ S, int kmin
   for (int mt = 0; mt < NT; ++mt) pa[mt] = S + kRecW + 3 * min(kmin + 8 * mt + qm, 26) + min(qk, 2);
 #pragma unroll
   for (int t = 0; t < kAsmCP; ++t) {
+    if (t >= cnt) break;  // warp-uniform: the slot's record count
     const int o = t * kTensorStride;
     const double w0 = pw[o], w1 = pw[o + 1], w2 = pw[o + 2];
     const double raw = w0 * pt0[o] + w1 * pt1[o] + w2 * pt2[o];
@@ -344,24 +350,25 @@ __device__ __forceinline__ void asm_write_row(const LevelView& L, int i, int lan
 /// mbarrier wait that suspends the warp in hardware between probes instead of spinning (the
 /// spin loop's YIELD / TRYWAIT / BRA otherwise steal issue slots from the compute warps).
 __device__ __forceinline__ void mbar_wait_sleep(unsigned bar, unsigned parity) {
-#ifndef HOT_ASM_SPIN
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
           bar),
       "r"(parity), "r"(100000)
       : "memory");
-#else
-  mbar_wait(bar, parity);
-#endif
+
 }
 
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-__global__ void __launch_bounds__((kAsmT + 1) * 32) k_assemble_tiles(BinsView bins, GridView g, LevelView L,
+#ifdef HOT_ASM_MINB
+#define HOT_ASM_BOUNDS __launch_bounds__((kAsmT + 1) * 32, HOT_ASM_MINB)
+#else
+#define HOT_ASM_BOUNDS __launch_bounds__((kAsmT + 1) * 32)
+#endif
+__global__ void HOT_ASM_BOUNDS k_assemble_tiles(BinsView bins, GridView g, LevelView L,
                                                                       const double* __restrict__ Tu,
-                                                                      const double* __restrict__ zeros,
                                                                       unsigned int* __restrict__ tile_counter) {
   extern __shared__ __align__(16) unsigned char asm_sm[];
   double* ring = reinterpret_cast<double*>(asm_sm);
@@ -421,12 +428,11 @@ __global__ void __launch_bounds__((kAsmT + 1) * 32) k_assemble_tiles(BinsView bi
             for (int c0 = 0; c0 < cnt; c0 += kAsmCP) {
               const int slot = acquire();
               const int k = min(kAsmCP, cnt - c0);
-              meta[slot] = AsmMeta{kSlotData, t, w, e / span, zlo + e % span, c0 + kAsmCP >= cnt ? 1 : 0, 0, 0};
+              meta[slot] = AsmMeta{kSlotData, t, w, e / span, zlo + e % span, c0 + kAsmCP >= cnt ? 1 : 0, k, 0};
               const unsigned mb = smem_u32(full + slot);
               double* dst = ring + (size_t)slot * kAsmCP * kTensorStride;
-              mbar_expect_tx(mb, kAsmCP * kRecBytes);
+              mbar_expect_tx(mb, k * kRecBytes);
               bulk_g2s(dst, Tu + (long long)(st + c0) * kTensorStride, k * kRecBytes, mb);
-              if (k < kAsmCP) bulk_g2s(dst + k * kTensorStride, zeros, (kAsmCP - k) * kRecBytes, mb);
               ++it;
             }
           }
@@ -508,16 +514,16 @@ __global__ void __launch_bounds__((kAsmT + 1) * 32) k_assemble_tiles(BinsView bi
         const double* S = ring + (size_t)slot * kAsmCP * kTensorStride;
         // DMMA tiles over the upper positions: ceil((27 - kmin) / 8)
         if (kmin >= 19) {
-          asm_chunk<1>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          asm_chunk<1>(S, kmin, tb, src8, gmask, qm, qk, C, E, m.cnt);
           if (m.last) asm_fold<1>(acc, kmin, qm, qk, C, E);
         } else if (kmin >= 11) {
-          asm_chunk<2>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          asm_chunk<2>(S, kmin, tb, src8, gmask, qm, qk, C, E, m.cnt);
           if (m.last) asm_fold<2>(acc, kmin, qm, qk, C, E);
         } else if (kmin >= 3) {
-          asm_chunk<3>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          asm_chunk<3>(S, kmin, tb, src8, gmask, qm, qk, C, E, m.cnt);
           if (m.last) asm_fold<3>(acc, kmin, qm, qk, C, E);
         } else {
-          asm_chunk<4>(S, kmin, tb, src8, gmask, qm, qk, C, E);
+          asm_chunk<4>(S, kmin, tb, src8, gmask, qm, qk, C, E, m.cnt);
           if (m.last) asm_fold<4>(acc, kmin, qm, qk, C, E);
         }
       }
@@ -562,7 +568,7 @@ void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s) {
 }
 
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
-                          const double* Tu, const double* zeros, unsigned int* tile_counter, cudaStream_t s) {
+                          const double* Tu, unsigned int* tile_counter, cudaStream_t s) {
   if (L.hi <= L.lo) return;
   (void)dx;
   (void)P;
@@ -572,10 +578,8 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
   cudaMemsetAsync(tile_counter, 0, sizeof(unsigned int), s);
   const long long tiles = ((long long)(L.hi - L.lo) + kAsmT - 1) / kAsmT;
   const long long blocks = std::min<long long>(resident, tiles);
-  k_assemble_tiles<<<(int)blocks, (kAsmT + 1) * 32, kAsmSmem, s>>>(bins, g, L, Tu, zeros, tile_counter);
+  k_assemble_tiles<<<(int)blocks, (kAsmT + 1) * 32, kAsmSmem, s>>>(bins, g, L, Tu, tile_counter);
   count_launches(1);
 }
-
-size_t assemble_zero_bytes() { return (size_t)kAsmCP * kRecBytes; }
 
 }  // namespace hotb200

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Tuning builds of the product library with other compile-time constants of the level-0
 # assembly (k_assembly.cu: HOT_ASM_T rows per tile, HOT_ASM_CP records per ring slot, HOT_ASM_S
-# ring slots, HOT_ASM_SPIN = spinning mbarrier waits).  Each lands in lib/libhotb200_<name>.so and
+# ring slots, HOT_ASM_MINB = min CTAs per SM).  Each lands in lib/libhotb200_<name>.so and
 # is loaded with HOT_LIB_VARIANT=<name>; the default build is untouched.
 #   tools/asm_variants.sh build name "-DHOT_ASM_T=2 ..."      (on the CPU box)
 #   tools/asm_variants.sh time  name scene                    (on the GPU box)
