@@ -107,8 +107,14 @@ WORKLOADS = {
     "cfg2_twisting_bars.json": "cfg2 twisting bars (BASELINE configs[1]), FCR, dt = CFL 0.6 (1/24 s frame cap), eps=1e-5",
     "cfg4_snow.json": "cfg4 colliding snow boxes (BASELINE configs[3]), snow clamp, dt = CFL 0.6, eps=1e-5",
     "cfg3_metal_impact.json": "cfg3 von Mises metal sphere on plate (BASELINE configs[2]), dt = CFL 0.6, eps=1e-5",
+    "cfg2_twisting_bars_nh.json": "cfg2 twisting bars with Neo-Hookean (as BASELINE configs[1] specifies; extension)",
+    "cfg4_snow_hardening.json": "cfg4 colliding snow boxes with hardening 10 (as BASELINE configs[3] specifies; extension)",
+    "sand_column_dp.json": "sand column collapse, Drucker-Prager 30 deg (north star; extension)",
 }
-OTHER_SCENES = ["cfg4_snow.json", "cfg3_metal_impact.json"]
+# (scene, solver overrides): the other single-GPU BASELINE configs, the extension variants the
+# configs name, and the paper's default tolerance eps = 1e-7 (scene.hpp:68) on the headline scene
+OTHER_SCENES = [("cfg4_snow.json", {}), ("cfg3_metal_impact.json", {}), ("cfg2_twisting_bars.json", {"epsilon": 1e-7}),
+                ("cfg2_twisting_bars_nh.json", {}), ("cfg4_snow_hardening.json", {}), ("sand_column_dp.json", {})]
 
 
 def workload_config(scene, scene_path, n_particles):
@@ -175,7 +181,7 @@ def reference_arm(args):
     print(json.dumps(line))
 
 
-def gpu_other_config(name, device, steps=5, warmup=2):
+def gpu_other_config(name, device, overrides=None, steps=5, warmup=2):
     """Device-resident particle-steps/s of another BASELINE scene on this GPU (no reference arm)."""
     import torch
 
@@ -185,6 +191,8 @@ def gpu_other_config(name, device, steps=5, warmup=2):
     sc = load_scene_file(path)
     p = sample_scene_particles(sc)
     sim = Simulation(sc, device=device)
+    if overrides:
+        sim.set_solver(**overrides)
     sim.set_particles(**p)
     stream = torch.cuda.ExternalStream(sim.stream(), device=device)
     for k in range(warmup):
@@ -202,7 +210,9 @@ def gpu_other_config(name, device, steps=5, warmup=2):
     prof = sim.profile_read()
     sim.close()
     n = p["x"].shape[0]
-    return {"config": workload_config(sc.source, path, n), "value": n * steps / (ms / 1000.0), "unit": UNIT,
+    cfg = workload_config(sc.source, path, n)
+    cfg.update(overrides or {})
+    return {"config": cfg, "value": n * steps / (ms / 1000.0), "unit": UNIT,
             "ms_per_step": ms / steps, "steps": steps, "warmup": warmup, "outer_iterations": outer,
             "phase_ms_per_step": {k: round(v["ms"] / steps, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])
                                   if v["ms"] > 0}}
@@ -386,11 +396,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_other_configs:
         sim.close()
         other = {}
-        for name in OTHER_SCENES:
+        for name, ov in OTHER_SCENES:
+            key = name + "".join(f"@{k}={v}" for k, v in ov.items())
             try:
-                other[name] = gpu_other_config(name, device)
+                other[key] = gpu_other_config(name, device, ov)
             except Exception as e:  # reported, never fatal to the headline
-                other[name] = {"error": f"{type(e).__name__}: {e}"}
+                other[key] = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         phases = {k: round(v["ms"] / args.steps, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])

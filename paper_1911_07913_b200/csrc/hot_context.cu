@@ -88,6 +88,7 @@ struct DBuf {
 struct Options {
   bool shard_force = false;        // HOT_SHARD_FORCE: the slab path at one rank (transport test)
   bool sgs_level0_waves = false;   // HOT_SGS_LEVEL0=waves: one launch per level-0 wave
+  bool sgs_level0_stream = false;  // HOT_SGS_LEVEL0=stream: the grid-barrier streaming kernel
   bool sgs_coarse_barrier = false; // HOT_SGS_COARSE=barrier: grid-barrier coarse smoother
   bool sgs_trace = false;          // HOT_SGS_TRACE: per-wave timing of the barrier smoother
   bool verbose = false;            // HOT_VERBOSE: per-solve diagnostics on stderr
@@ -99,6 +100,7 @@ struct Options {
     };
     shard_force = std::getenv("HOT_SHARD_FORCE") != nullptr;
     sgs_level0_waves = eq("HOT_SGS_LEVEL0", "waves");
+    sgs_level0_stream = eq("HOT_SGS_LEVEL0", "stream");
     sgs_coarse_barrier = eq("HOT_SGS_COARSE", "barrier");
     sgs_trace = std::getenv("HOT_SGS_TRACE") != nullptr;
     verbose = std::getenv("HOT_VERBOSE") != nullptr;
@@ -114,8 +116,7 @@ struct Level {
   int lo[3] = {0, 0, 0}, ext[3] = {0, 0, 0};
   DBuf map, coords, cols, H, dinv, dir, flags;
   DBuf wave_of, wave_counts, wave_start, wave_cursor, wave_rows, wave_start_c;
-  DBuf sgs_flag;      // per-row epoch flags of the dataflow smoother
-  int sgs_epoch = 1;
+  DBuf sgs_uf, sgs_ub;  // the dataflow smoother's forward / backward results (also its flags)
   int nwaves = 0, max_wave = 0;
   std::vector<int> wave_start_h;
   long long active_slots = 0;
@@ -1115,9 +1116,8 @@ struct Context {
     starts.push_back(acc);
     l.nwaves = (int)starts.size() - 1;
     l.wave_start_h = starts;
-    l.sgs_flag.ensure(sizeof(int) * std::max(l.n, 1));
-    HOT_CUDA(cudaMemsetAsync(l.sgs_flag.p, 0, sizeof(int) * std::max(l.n, 1), st));
-    l.sgs_epoch = 1;
+    l.sgs_uf.ensure(sizeof(double) * 3 * std::max(l.n, 1));
+    l.sgs_ub.ensure(sizeof(double) * 3 * std::max(l.n, 1));
     l.wave_start_c.ensure(sizeof(int) * starts.size());
     HOT_CUDA(cudaMemcpyAsync(l.wave_start_c.p, starts.data(), sizeof(int) * starts.size(), cudaMemcpyHostToDevice,
                              st));
@@ -1275,10 +1275,12 @@ struct Context {
     const bool per_wave = opt.sgs_level0_waves;
     const bool flow = !opt.sgs_coarse_barrier;
     if (l.radius != 2 || (l.max_wave < stream_min && flow)) {  // radius-3 levels: dataflow kernel only
-      launch_sgs_flow(l.view(), l.wave_rows.as<int>(), l.wave_of.as<int>(), u, b, l.sgs_flag.as<int>(), l.sgs_epoch,
-                      stream);
-      l.sgs_epoch += 2;
-    } else if (l.max_wave >= stream_min && !per_wave)
+      launch_sgs_flow(l.view(), l.wave_rows.as<int>(), l.wave_of.as<int>(), u, b, l.sgs_uf.as<double>(),
+                      l.sgs_ub.as<double>(), stream);
+    } else if (l.max_wave >= stream_min && !per_wave && !opt.sgs_level0_stream)
+      launch_sgs_flow0(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
+                       l.sgs_uf.as<double>(), l.sgs_ub.as<double>(), stream);
+    else if (l.max_wave >= stream_min && !per_wave)
       launch_sgs_stream(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
                         grid_bar.as<unsigned int>(), stream);
     else if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)

@@ -187,15 +187,19 @@ void launch_sgs(LevelView L, const int* wave_start, const int* wave_rows, int nw
 void launch_pcg(LevelView L, const double* b, double* x, double* r, double* z, double* p, double* Ap, double rel,
                 int cap, double* partials, int* stat, int* iter_acc, int grid_blocks, cudaStream_t s);
 /// The same sweep as one streaming launch per wave (large levels; waves given on the host).
-/// Coarse smoother: both passes as a dataflow kernel with per-row epoch flags (flag must hold
-/// values < epoch; the kernel leaves epoch+1 in every row).
-void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* u, const double* b, int* flag,
-                     int epoch, cudaStream_t s);
+/// Coarse smoother: both passes as a dataflow kernel; uf / ub: 3n-double scratch (the forward
+/// and backward results, which double as the dependency flags).
+void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* u, const double* b, double* uf,
+                     double* ub, cudaStream_t s);
 /// Level-0 smoother: both passes, all waves, one persistent kernel with bulk-copy row streaming.
 /// [q_lo, q_hi): the part of the flat (forward waves, then backward waves) sequence to run.
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
                        const double* b, unsigned int* bar, cudaStream_t s, int q_lo = 0, int q_hi = -1,
                        int max_rows = 0);  // max_rows > 0: size the grid for waves of at most that many rows
+/// Level-0 smoother (single GPU): both passes as a streaming dataflow kernel, no grid barriers;
+/// uf / ub: 3n-double scratch (the passes' results, which double as the dependency flags).
+void launch_sgs_flow0(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
+                      const double* b, double* uf, double* ub, cudaStream_t s);
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s);
 int sgs_max_blocks();

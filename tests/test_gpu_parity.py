@@ -226,17 +226,27 @@ def test_vcycle_coarse_smoother_schedules(monkeypatch, coarse):
     uo, ito = pr.orc.vcycle(b)
     assert it == ito and rel_err(u, uo) < 1e-9
     monkeypatch.setenv("HOT_SGS_COARSE", "barrier" if coarse == "flow" else "flow")
-    u2, it2 = pr.gpu.vcycle(b)
+    from paper_1911_07913_b200 import Simulation
+
+    g2 = Simulation(pr.sc)  # the options are read when a context is created
+    g2.set_particles(**pr.p)
+    g2.stage_prepare(0.01)
+    g2.assemble()
+    g2.build_hierarchy(3)
+    u2, it2 = g2.vcycle(b)
     assert it2 == it and np.array_equal(u, u2)
 
 
-@pytest.mark.parametrize("schedule", ["stream", "waves"])
+@pytest.mark.parametrize("schedule", ["flow", "stream", "waves"])
 def test_vcycle_streaming_wave_schedule(monkeypatch, schedule):
     """Same V-cycle parity with every SGS level run on the large-wave schedules the benchmark's
-    level 0 uses: the persistent bulk-copy streaming kernel, or one launch per wave.  Both
-    compute every row with the same arithmetic, so they agree bit for bit."""
+    level 0 uses: the streaming dataflow kernel (default, no grid barriers), the persistent
+    bulk-copy streaming kernel with a grid barrier per wave, or one launch per wave.  All
+    compute every row with the same arithmetic in the same sequential order, so they agree bit
+    for bit."""
     monkeypatch.setenv("HOT_SGS_STREAM_MIN", "0")
-    monkeypatch.setenv("HOT_SGS_LEVEL0", schedule)
+    if schedule != "flow":
+        monkeypatch.setenv("HOT_SGS_LEVEL0", schedule)
     pr = _stretched_block_pair(seed=12, cells=6, youngs=1e6)
     n = pr.prepare(0.01)
     pr.gpu.assemble()
@@ -247,8 +257,18 @@ def test_vcycle_streaming_wave_schedule(monkeypatch, schedule):
     u, it = pr.gpu.vcycle(b)
     uo, ito = pr.orc.vcycle(b)
     assert it == ito and rel_err(u, uo) < 1e-9
-    monkeypatch.setenv("HOT_SGS_LEVEL0", "waves" if schedule == "stream" else "stream")
-    u2, it2 = pr.gpu.vcycle(b)
+    other = {"flow": "stream", "stream": "waves", "waves": "flow"}[schedule]
+    monkeypatch.delenv("HOT_SGS_LEVEL0", raising=False)
+    if other != "flow":
+        monkeypatch.setenv("HOT_SGS_LEVEL0", other)
+    from paper_1911_07913_b200 import Simulation
+
+    g2 = Simulation(pr.sc)  # the options are read when a context is created
+    g2.set_particles(**pr.p)
+    g2.stage_prepare(0.01)
+    g2.assemble()
+    g2.build_hierarchy(3)
+    u2, it2 = g2.vcycle(b)
     assert it2 == it and np.array_equal(u, u2)
 
 
