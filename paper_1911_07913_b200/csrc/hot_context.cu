@@ -88,7 +88,6 @@ struct DBuf {
 struct Options {
   bool shard_force = false;        // HOT_SHARD_FORCE: the slab path at one rank (transport test)
   bool sgs_level0_waves = false;   // HOT_SGS_LEVEL0=waves: one launch per level-0 wave
-  bool sgs_level0_stream = false;  // HOT_SGS_LEVEL0=stream: the grid-barrier streaming kernel
   bool sgs_coarse_barrier = false; // HOT_SGS_COARSE=barrier: grid-barrier coarse smoother
   bool sgs_trace = false;          // HOT_SGS_TRACE: per-wave timing of the barrier smoother
   bool verbose = false;            // HOT_VERBOSE: per-solve diagnostics on stderr
@@ -100,7 +99,6 @@ struct Options {
     };
     shard_force = std::getenv("HOT_SHARD_FORCE") != nullptr;
     sgs_level0_waves = eq("HOT_SGS_LEVEL0", "waves");
-    sgs_level0_stream = eq("HOT_SGS_LEVEL0", "stream");
     sgs_coarse_barrier = eq("HOT_SGS_COARSE", "barrier");
     sgs_trace = std::getenv("HOT_SGS_TRACE") != nullptr;
     verbose = std::getenv("HOT_VERBOSE") != nullptr;
@@ -1277,10 +1275,7 @@ struct Context {
     if (l.radius != 2 || (l.max_wave < stream_min && flow)) {  // radius-3 levels: dataflow kernel only
       launch_sgs_flow(l.view(), l.wave_rows.as<int>(), l.wave_of.as<int>(), u, b, l.sgs_uf.as<double>(),
                       l.sgs_ub.as<double>(), stream);
-    } else if (l.max_wave >= stream_min && !per_wave && !opt.sgs_level0_stream)
-      launch_sgs_flow0(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
-                       l.sgs_uf.as<double>(), l.sgs_ub.as<double>(), stream);
-    else if (l.max_wave >= stream_min && !per_wave)
+    } else if (l.max_wave >= stream_min && !per_wave)
       launch_sgs_stream(l.view(), l.wave_start_c.as<int>(), l.wave_rows.as<int>(), l.nwaves, u, b,
                         grid_bar.as<unsigned int>(), stream);
     else if (l.max_wave >= stream_min || l.nwaves > kSgsMaxWavesPersistent)

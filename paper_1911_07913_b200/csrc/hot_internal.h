@@ -196,10 +196,6 @@ void launch_sgs_flow(LevelView L, const int* order, const int* wave_of, double* 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
                        const double* b, unsigned int* bar, cudaStream_t s, int q_lo = 0, int q_hi = -1,
                        int max_rows = 0);  // max_rows > 0: size the grid for waves of at most that many rows
-/// Level-0 smoother (single GPU): both passes as a streaming dataflow kernel, no grid barriers;
-/// uf / ub: 3n-double scratch (the passes' results, which double as the dependency flags).
-void launch_sgs_flow0(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                      const double* b, double* uf, double* ub, cudaStream_t s);
 void launch_sgs_waves(LevelView L, const int* wave_start_host, const int* wave_rows, int nwaves, double* u,
                       const double* b, cudaStream_t s);
 int sgs_max_blocks();

@@ -1041,178 +1041,6 @@ __global__ void __launch_bounds__(W * 32, 1)
   }
 }
 
-/// Level-0 symmetric Gauss-Seidel as a streaming DATAFLOW kernel (single GPU): the rows of
-/// both passes in wave order, dealt to the warps exactly as in k_sgs_stream (same ring, same
-/// bulk-copy producer running ahead across waves), but with no grid barrier between waves.
-/// Like the coarse dataflow kernel (k_sgs_flow) the values are their own flags: the forward
-/// pass writes uf, the backward pass ub (and u), both NaN-sentinel filled before the sweep.
-/// A lane's gather of a column that precedes the row in the pass order (lower colour forward,
-/// higher colour backward; every forward value backward) polls that column's entry until it is
-/// written -- the poll IS the gather, so a row costs no extra round trip -- and the other columns
-/// read the pass input.  Colours come from the lattice (colour(x) = (x0 mod 3, x1 mod 3, x2 mod 3)
-/// lexicographic, k_level_waves), so no wave ids are loaded per column.  Row arithmetic is the
-/// other level-0 schedules' (same summation order): the result is bitwise the same.
-/// Progress: every warp walks its rows in the global pass order, all CTAs are co-resident
-/// (cooperative launch), so the globally first unfinished row always has its predecessors done.
-__device__ __forceinline__ int colour3(int x, int y, int z) {
-  auto md = [](int v) { return ((v % 3) + 3) % 3; };
-  return (md(x) * 3 + md(y)) * 3 + md(z);
-}
-
-template <int W, int S>
-__global__ void __launch_bounds__(W * 32, 1)
-    k_sgs_flow0(LevelView L, const int* __restrict__ wave_start, const int* __restrict__ wave_rows, int nwaves,
-                double* u, const double* __restrict__ b, double* uf, double* ub) {
-  extern __shared__ __align__(128) unsigned char sm_raw[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int gw = blockIdx.x * W + wib, nw = gridDim.x * W;
-  unsigned char* ring = sm_raw + (size_t)wib * S * kStreamRowBytes;
-  unsigned long long* mb =
-      reinterpret_cast<unsigned long long*>(sm_raw + (size_t)W * S * kStreamRowBytes) + wib * S;
-  const int nq = 2 * nwaves;
-  auto wave_of = [&](int q) { return q < nwaves ? q : 2 * nwaves - 1 - q; };
-  auto count_of = [&](int q) {
-    const int w = wave_of(q);
-    return __ldg(wave_start + w + 1) - __ldg(wave_start + w);
-  };
-  auto settle = [&](StreamCursor& c) {
-    while (c.q < nq && gw + c.m * nw >= count_of(c.q)) {
-      ++c.q;
-      c.m = 0;
-    }
-  };
-  unsigned long long policy = 0;
-  if (lane == 0) {
-    policy = l2_evict_first_policy();
-    for (int st = 0; st < S; ++st) mbar_init(mb + st, 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  auto issue = [&](const StreamCursor& c, int stage) {
-    const int w = wave_of(c.q);
-    const int i = __ldg(wave_rows + __ldg(wave_start + w) + gw + c.m * nw);
-    unsigned char* dst = ring + (size_t)stage * kStreamRowBytes;
-    const unsigned mbar = smem_u32(mb + stage);
-    mbar_expect_tx(mbar, kStreamRowBytes);
-    bulk_g2s_hint(dst, L.H + (long long)i * 9 * kSlotPitch, 9 * kSlotPitch * 8, mbar, policy);
-    bulk_g2s_hint(dst + 9 * kSlotPitch * 8, L.cols + (long long)i * kSlotPitch, kSlotPitch * 4, mbar, policy);
-    return i;
-  };
-  StreamCursor prod{0, 0};
-  settle(prod);
-  int rowid[S];
-  for (int st = 0; st < S; ++st) {
-    rowid[st] = -1;
-    if (prod.q < nq) {
-      int i = 0;
-      if (lane == 0) i = issue(prod, st);
-      rowid[st] = __shfl_sync(0xffffffffu, i, 0);
-      ++prod.m;
-      settle(prod);
-    }
-  }
-  // slot offsets of this lane's 4 slots (lane + 32 k): (s / 25 - 2, (s / 5) % 5 - 2, s % 5 - 2)
-  int od[4][3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int sl = lane + 32 * k;
-    od[k][0] = sl / 25 - 2;
-    od[k][1] = (sl / 5) % 5 - 2;
-    od[k][2] = sl % 5 - 2;
-  }
-  int stage = 0;
-  unsigned phase_bits = 0;
-  for (int q = 0; q < nq; ++q) {
-    const bool fwd = q < nwaves;
-    const int cnt = count_of(q);
-    for (int r = gw; r < cnt; r += nw) {
-      const int i = rowid[stage];
-      const int x0 = __ldg(L.coords + 3 * i), x1 = __ldg(L.coords + 3 * i + 1), x2 = __ldg(L.coords + 3 * i + 2);
-      const int ci = colour3(x0, x1, x2);
-      mbar_wait(smem_u32(mb + stage), (phase_bits >> stage) & 1u);
-      phase_bits ^= 1u << stage;
-      const double* H = reinterpret_cast<const double*>(ring + (size_t)stage * kStreamRowBytes);
-      const int* cols = reinterpret_cast<const int*>(ring + (size_t)stage * kStreamRowBytes + 9 * kSlotPitch * 8);
-      int c[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) c[k] = cols[lane + 32 * k];
-      double xv[4][3];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (c[k] < 0) {  // inactive slot: zero block (the input's row 0, as the other schedules)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) xv[k][a] = __ldcg(u + a);
-          continue;
-        }
-        const int cc = colour3(x0 + od[k][0], x1 + od[k][1], x2 + od[k][2]);
-        const double* src;
-        bool poll;
-        if (fwd) {
-          poll = cc < ci;
-          src = poll ? uf : u;
-        } else {
-          poll = true;
-          src = cc > ci ? ub : uf;
-        }
-        if (poll) sgs_poll3(src + 3 * c[k], xv[k][0], xv[k][1], xv[k][2]);
-        else {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) xv[k][a] = __ldcg(src + 3 * c[k] + a);
-        }
-      }
-      double D[9], rb[3], uo[3];
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) D[k] = __ldg(L.dinv + 9 * i + k);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) rb[a] = __ldg(b + 3 * i + a);
-        if (fwd) {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) uo[a] = __ldcg(u + 3 * i + a);
-        } else {
-          sgs_poll3(uf + 3 * i, uo[0], uo[1], uo[2]);
-        }
-      }
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int sl = lane + 32 * k;
-        double hv[9];
-#pragma unroll
-        for (int e = 0; e < 9; ++e) hv[e] = H[e * kSlotPitch + sl];
-        a0 += hv[0] * xv[k][0] + hv[1] * xv[k][1] + hv[2] * xv[k][2];
-        a1 += hv[3] * xv[k][0] + hv[4] * xv[k][1] + hv[5] * xv[k][2];
-        a2 += hv[6] * xv[k][0] + hv[7] * xv[k][1] + hv[8] * xv[k][2];
-      }
-      __syncwarp();  // all lanes are done with this stage's shared memory
-      if (prod.q < nq) {
-        int ni = 0;
-        if (lane == 0) ni = issue(prod, stage);
-        rowid[stage] = __shfl_sync(0xffffffffu, ni, 0);
-        ++prod.m;
-        settle(prod);
-      }
-      const double y0 = wsum(a0), y1 = wsum(a1), y2 = wsum(a2);
-      if (lane == 0) {
-        const double r0 = rb[0] - y0, r1 = rb[1] - y1, r2 = rb[2] - y2;
-        const double n0 = uo[0] + (D[0] * r0 + D[1] * r1 + D[2] * r2);
-        const double n1 = uo[1] + (D[3] * r0 + D[4] * r1 + D[5] * r2);
-        const double n2 = uo[2] + (D[6] * r0 + D[7] * r1 + D[8] * r2);
-        double* out = (fwd ? uf : ub) + 3 * i;
-        st_relaxed(out, n0);
-        st_relaxed(out + 1, n1);
-        st_relaxed(out + 2, n2);
-        if (!fwd) {
-          u[3 * i] = n0;
-          u[3 * i + 1] = n1;
-          u[3 * i + 2] = n2;
-        }
-      }
-      stage = stage + 1 == S ? 0 : stage + 1;
-    }
-  }
-}
-
 /// Deterministic grid reduction: every block sums all block partials in the same fixed tree.
 __device__ __forceinline__ double grid_total(const double* partials, int nparts) {
   __shared__ double ws[kMgWarps];
@@ -1500,17 +1328,6 @@ void launch_sgs_stream_t(LevelView L, const int* wave_start, const int* wave_row
 
 int sgs_stream_blocks() { return sgs_stream_blocks_t<8, 2>(); }
 
-void launch_sgs_flow0(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
-                      const double* b, double* uf, double* ub, cudaStream_t s) {
-  if (L.n == 0 || nwaves == 0) return;
-  constexpr int W = 8, S = 2;
-  cudaMemsetAsync(uf, 0xff, sizeof(double) * 3 * (size_t)L.n, s);
-  cudaMemsetAsync(ub, 0xff, sizeof(double) * 3 * (size_t)L.n, s);
-  const int grid = coop_blocks((const void*)k_sgs_flow0<W, S>, W * 32, stream_smem<W, S>());
-  void* args[] = {&L, (void*)&wave_start, (void*)&wave_rows, &nwaves, &u, (void*)&b, &uf, &ub};
-  cudaLaunchCooperativeKernel((const void*)k_sgs_flow0<W, S>, grid, W * 32, args, stream_smem<W, S>(), s);
-  count_launches(1);
-}
 
 void launch_sgs_stream(LevelView L, const int* wave_start, const int* wave_rows, int nwaves, double* u,
                        const double* b, unsigned int* bar, cudaStream_t s, int q_lo, int q_hi, int max_rows) {

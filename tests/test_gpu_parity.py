@@ -237,15 +237,14 @@ def test_vcycle_coarse_smoother_schedules(monkeypatch, coarse):
     assert it2 == it and np.array_equal(u, u2)
 
 
-@pytest.mark.parametrize("schedule", ["flow", "stream", "waves"])
+@pytest.mark.parametrize("schedule", ["stream", "waves"])
 def test_vcycle_streaming_wave_schedule(monkeypatch, schedule):
     """Same V-cycle parity with every SGS level run on the large-wave schedules the benchmark's
-    level 0 uses: the streaming dataflow kernel (default, no grid barriers), the persistent
-    bulk-copy streaming kernel with a grid barrier per wave, or one launch per wave.  All
-    compute every row with the same arithmetic in the same sequential order, so they agree bit
-    for bit."""
+    level 0 uses: the persistent bulk-copy streaming kernel (grid barrier per wave), or one
+    launch per wave.  Both compute every row with the same arithmetic in the same sequential
+    order, so they agree bit for bit."""
     monkeypatch.setenv("HOT_SGS_STREAM_MIN", "0")
-    if schedule != "flow":
+    if schedule != "stream":
         monkeypatch.setenv("HOT_SGS_LEVEL0", schedule)
     pr = _stretched_block_pair(seed=12, cells=6, youngs=1e6)
     n = pr.prepare(0.01)
@@ -257,9 +256,9 @@ def test_vcycle_streaming_wave_schedule(monkeypatch, schedule):
     u, it = pr.gpu.vcycle(b)
     uo, ito = pr.orc.vcycle(b)
     assert it == ito and rel_err(u, uo) < 1e-9
-    other = {"flow": "stream", "stream": "waves", "waves": "flow"}[schedule]
+    other = "waves" if schedule == "stream" else "stream"
     monkeypatch.delenv("HOT_SGS_LEVEL0", raising=False)
-    if other != "flow":
+    if other != "stream":
         monkeypatch.setenv("HOT_SGS_LEVEL0", other)
     from paper_1911_07913_b200 import Simulation
 
