@@ -248,6 +248,9 @@ typedef struct {
   int asm_lo, asm_hi;       /* level-0 rows this rank assembles (owned + the left extension) */
   long long halo_exchanges; /* level-0 halo exchanges issued since creation */
   long long gathers;        /* row-range allgathers issued since creation */
+  long long particles_local; /* particles this rank stores (owned + ghost copies when partitioned) */
+  long long particles_total; /* particles of the scene */
+  int partitioned;          /* 1: particles are partitioned along the slab cut */
 } hot_shard_info_t;
 int hot_shard_info(hot_ctx* ctx, hot_shard_info_t* out);
 

@@ -64,6 +64,8 @@ struct SceneC {
   std::vector<hot_collider> cols;
   hot_scene s{};
   explicit SceneC(const SceneConfig& sc) {
+    // the extension fields (elasticity, hardening, friction_angle) stay zero: the reference's
+    // own materials (fixed-corotated, plain snow clamp)
     for (const auto& m : sc.materials)
       mats.push_back({m.density, m.youngs, m.poisson, static_cast<int>(m.plasticity.kind), m.plasticity.yield_stress,
                       m.plasticity.clamp_lo, m.plasticity.clamp_hi});

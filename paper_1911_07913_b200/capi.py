@@ -139,7 +139,8 @@ class hot_shard_info_t(C.Structure):
     _fields_ = [("rank", C.c_int), ("size", C.c_int), ("sharded", C.c_int), ("plane_lo", C.c_int),
                 ("plane_hi", C.c_int), ("row_lo", C.c_int), ("row_hi", C.c_int), ("crow_lo", C.c_int),
                 ("crow_hi", C.c_int), ("asm_lo", C.c_int), ("asm_hi", C.c_int), ("halo_exchanges", C.c_longlong),
-                ("gathers", C.c_longlong)]
+                ("gathers", C.c_longlong), ("particles_local", C.c_longlong), ("particles_total", C.c_longlong),
+                ("partitioned", C.c_int)]
 
 
 _lib = None

@@ -87,6 +87,7 @@ struct DBuf {
 /// them changes a value: the schedules they select are bitwise identical.
 struct Options {
   bool shard_force = false;        // HOT_SHARD_FORCE: the slab path at one rank (transport test)
+  bool shard_replicate = false;    // HOT_SHARD_REPLICATE: sharded solves keep every particle on every rank
   bool sgs_level0_waves = false;   // HOT_SGS_LEVEL0=waves: one launch per level-0 wave
   bool sgs_coarse_barrier = false; // HOT_SGS_COARSE=barrier: grid-barrier coarse smoother
   bool sgs_trace = false;          // HOT_SGS_TRACE: per-wave timing of the barrier smoother
@@ -98,6 +99,7 @@ struct Options {
       return e && std::strcmp(e, v) == 0;
     };
     shard_force = std::getenv("HOT_SHARD_FORCE") != nullptr;
+    shard_replicate = std::getenv("HOT_SHARD_REPLICATE") != nullptr;
     sgs_level0_waves = eq("HOT_SGS_LEVEL0", "waves");
     sgs_coarse_barrier = eq("HOT_SGS_COARSE", "barrier");
     sgs_trace = std::getenv("HOT_SGS_TRACE") != nullptr;
@@ -208,6 +210,15 @@ struct Context {
   DBuf px, pv, pF, pC, pmass, pvol, pmat, stage, porig;
   DBuf qx, qv, qF, qC, qmass, qvol, qmat, qorig;  // reorder targets (swapped each step)
   DBuf pjp, qjp;         // plastic volume ratio per particle (snow materials; hardening extension)
+  // particle partition: once a sharded step has cut the slabs, every rank stores
+  // only the particles of its band [P - kPPLeft, Q + kPPRight) (owned: [P, Q); the rest ghost
+  // copies), exchanged after every advection.  np is then the local count.
+  static constexpr int kPPLeft = 8;   // bins the assembly reads from plane P - 8 (plan_shard)
+  static constexpr int kPPRight = 1;  // bins the P2G / energy / gradient node passes read up to plane Q
+  bool pp_on = false;
+  std::vector<int> pp_bounds;         // the frozen cut (size + 1 planes) the partition follows
+  long long np_global = 0;            // particles of the whole scene
+  DBuf pp_keep, pp_pack, pp_kpos, pp_ppos, pp_send, pp_rflag, pp_rpos, pp_small;
   bool track_jp = false; // some material is snow: J_p is stored, reordered and updated
   double time = 0;
   int frame = 0;
@@ -520,6 +531,8 @@ struct Context {
               const double* C, const int* mat) {
     const int h = prof_begin(P_IO);
     np = n;
+    np_global = n;
+    pp_on = false;
     const size_t n3 = sizeof(double) * 3 * std::max<long long>(n, 1), n9 = sizeof(double) * 9 * std::max<long long>(n, 1);
     px.ensure(n3);
     pv.ensure(n3);
@@ -605,6 +618,23 @@ struct Context {
 
   void download(double* x, double* v, double* F, double* C) {
     const int h = prof_begin(P_IO);
+    if (pp_on) {  // partitioned: every rank's owned particles, in the caller's order
+      const long long total = pp_gather_owned_records();
+      stage.ensure(sizeof(double) * 24 * std::max<long long>(total, 1));
+      double* sx = stage.as<double>();
+      double* sv = sx + 3 * total;
+      double* sF = sv + 3 * total;
+      double* sC = sF + 9 * total;
+      launch_pp_unpack_caller(pp_send.as<double>(), total, x ? sx : nullptr, v ? sv : nullptr, F ? sF : nullptr,
+                              C ? sC : nullptr, nullptr, stream);
+      if (x) HOT_CUDA(cudaMemcpyAsync(x, sx, sizeof(double) * 3 * total, cudaMemcpyDeviceToHost, stream));
+      if (v) HOT_CUDA(cudaMemcpyAsync(v, sv, sizeof(double) * 3 * total, cudaMemcpyDeviceToHost, stream));
+      if (F) HOT_CUDA(cudaMemcpyAsync(F, sF, sizeof(double) * 9 * total, cudaMemcpyDeviceToHost, stream));
+      if (C) HOT_CUDA(cudaMemcpyAsync(C, sC, sizeof(double) * 9 * total, cudaMemcpyDeviceToHost, stream));
+      prof_end(h, (double)total * 24 * 8);
+      sync();
+      return;
+    }
     stage.ensure(sizeof(double) * 24 * std::max<long long>(np, 1));
     struct Field {
       const DBuf* src;
@@ -630,15 +660,25 @@ struct Context {
   void set_plastic_state(const double* Jp) {
     if (!track_jp) throw std::invalid_argument("no snow material: there is no plastic state");
     if (np == 0) return;
-    stage.ensure(sizeof(double) * std::max<long long>(np, 1));
-    HOT_CUDA(cudaMemcpyAsync(stage.p, Jp, sizeof(double) * np, cudaMemcpyHostToDevice, stream));
+    // the caller's array has every particle; local slot t holds original id porig[t]
+    stage.ensure(sizeof(double) * std::max<long long>(np_global, 1));
+    HOT_CUDA(cudaMemcpyAsync(stage.p, Jp, sizeof(double) * np_global, cudaMemcpyHostToDevice, stream));
     launch_gather_perm(stage.as<double>(), pjp.as<double>(), np, porig.as<int>(), stream);
     sync();
   }
   void get_plastic_state(double* Jp) {
-    if (np == 0) return;
+    if (np_global == 0) return;
     if (!track_jp) {
-      std::fill(Jp, Jp + np, 1.0);
+      std::fill(Jp, Jp + np_global, 1.0);
+      return;
+    }
+    if (pp_on) {
+      const long long total = pp_gather_owned_records();
+      stage.ensure(sizeof(double) * std::max<long long>(total, 1));
+      launch_pp_unpack_caller(pp_send.as<double>(), total, nullptr, nullptr, nullptr, nullptr, stage.as<double>(),
+                              stream);
+      HOT_CUDA(cudaMemcpyAsync(Jp, stage.p, sizeof(double) * total, cudaMemcpyDeviceToHost, stream));
+      sync();
       return;
     }
     stage.ensure(sizeof(double) * std::max<long long>(np, 1));
@@ -658,9 +698,19 @@ struct Context {
     int hb[8];
     HOT_CUDA(cudaMemcpyAsync(hb, bounds.p, sizeof(hb), cudaMemcpyDeviceToHost, stream));
     sync();
+    if (pp_on) {  // partitioned particles: the bounding box (and the failure flag) of all ranks
+      const auto all = allgather_block(hb, sizeof(hb));
+      const int* v = reinterpret_cast<const int*>(all.data());
+      for (int r = 0; r < comm->size; ++r)
+        for (int a = 0; a < 3; ++a) {
+          hb[a] = std::min(hb[a], v[8 * r + a]);
+          hb[3 + a] = std::max(hb[3 + a], v[8 * r + 3 + a]);
+          hb[6] = std::max(hb[6], v[8 * r + 6]);
+        }
+    }
     if (hb[6]) throw std::invalid_argument("activate_grid: non-finite particle position");
     Level& l0 = L[0];
-    if (np == 0) {
+    if (np_global == 0) {
       l0.n = 0;
       for (int a = 0; a < 3; ++a) l0.lo[a] = 0, l0.ext[a] = 1;
     } else {
@@ -677,8 +727,19 @@ struct Context {
     HOT_CUDA(cudaMemsetAsync(l0.flags.p, 0, len + 16, stream));
     DenseMap dm = l0.dmap();
     launch_mark_active(P, dx, dm, l0.flags.as<uint8_t>(), stream);
+    if (pp_on) {  // each rank's flags are exact on its own planes: put the slabs together
+      const int R = comm->size;
+      const long long plane = (long long)l0.ext[1] * l0.ext[2];
+      std::vector<long long> off(R + 1);
+      for (int r = 0; r <= R; ++r) {
+        const int pl = r == R ? l0.lo[0] + l0.ext[0] : std::max(l0.lo[0], std::min(pp_owned_lo(r), l0.lo[0] + l0.ext[0]));
+        off[r] = (long long)(pl - l0.lo[0]) * plane;
+      }
+      off[0] = 0;
+      comm->allgather_ranges(l0.flags.p, off, stream);
+    }
     // coords sized for the worst case (every box node active) only when needed
-    l0.coords.ensure(sizeof(int) * 3 * std::min<long long>(len, 27LL * std::max<long long>(np, 1)));
+    l0.coords.ensure(sizeof(int) * 3 * std::min<long long>(len, 27LL * std::max<long long>(np_global, 1)));
     launch_flags_to_index(l0.flags.as<uint8_t>(), len, l0.ext, l0.lo, l0.map.as<int>(), l0.coords.as<int>(),
                           scan_tmp.as<int>(), iflags.as<int>() + 8, stream);
     int n_nodes = 0;
@@ -699,7 +760,7 @@ struct Context {
     bin_pid.ensure(sizeof(int) * std::max<long long>(np, 1));
     scan_tmp.ensure(sizeof(int) * ((long long)n / 4096 + 64 + len / 4096));
     launch_bin_particles(P, dx, l0.dmap(), n, bin_of.as<int>(), bin_counts.as<int>(), bin_start.as<int>(),
-                         bin_cursor.as<int>(), bin_pid.as<int>(), scan_tmp.as<int>(), stream);
+                         bin_cursor.as<int>(), bin_pid.as<int>(), scan_tmp.as<int>(), porig.as<int>(), stream);
     // store the particles in bin order (orig keeps the caller's order for download)
     ParticlesView Q = P;
     Q.x = qx.as<double>();
@@ -774,6 +835,11 @@ struct Context {
     // the slab cut of this step's grid (replicated inputs: every rank computes the same cut)
     const int levels = cfg.kind == 0 ? cfg.levels : 0;  // HOT is the solver that splits
     sh.planned = want_shard(levels) && plan_shard();
+    if (pp_on && !sh.planned) {  // the frozen cut no longer fits: every particle back everywhere
+      pp_gather_all();
+      activate();
+      sh.planned = want_shard(levels) && plan_shard();
+    }
     p2g_bc(time_now);
     ensure_solver_buffers();
     have_state = true;
@@ -809,9 +875,17 @@ struct Context {
     std::vector<long long> w(np0);
     for (int k = 0; k < np0; ++k) w[k] = sh.ps0[k + 1] - sh.ps0[k];  // rows per plane
     sh.bounds.assign(R + 1, 0);
-    // interior cuts at even planes (the level-1 cut is then exact: coarse plane = fine / 2) and
-    // at least 2 planes per slab (a row's coupling radius: halos come from one neighbour)
-    if (!plan_slabs(l0.lo[0], np0, w.data(), R, 2, 2, sh.bounds.data())) return false;
+    if (pp_on) {  // the partitioned particles follow the cut that partitioned them
+      sh.bounds = pp_bounds;
+      sh.bounds[0] = l0.lo[0];
+      sh.bounds[R] = l0.lo[0] + np0;
+      for (int r = 0; r < R; ++r)
+        if (sh.bounds[r + 1] - sh.bounds[r] < 2) return false;  // caller gathers and re-plans
+    } else {
+      // interior cuts at even planes (the level-1 cut is then exact: coarse plane = fine / 2) and
+      // at least 2 planes per slab (a row's coupling radius: halos come from one neighbour)
+      if (!plan_slabs(l0.lo[0], np0, w.data(), R, 2, 2, sh.bounds.data())) return false;
+    }
     sh.P = sh.bounds[me];
     sh.Q = sh.bounds[me + 1];
     sh.r_lo = row_of(sh.P);
@@ -850,6 +924,166 @@ struct Context {
       }
     }
     return true;
+  }
+
+  // ------------------------------------------------------------------ particle partition
+  bool pp_enabled() const { return comm != nullptr && !opt.shard_replicate; }
+  int pp_owned_lo(int r) const { return r == 0 ? -(1 << 29) : pp_bounds[r]; }
+  int pp_owned_hi(int r) const { return r == comm->size - 1 ? (1 << 29) : pp_bounds[r + 1]; }
+
+  /// Every rank's `bytes` bytes (one allgather over a small device buffer).
+  std::vector<unsigned char> allgather_block(const void* mine, size_t bytes) {
+    const int R = comm->size;
+    pp_small.ensure(bytes * R);
+    HOT_CUDA(cudaMemcpyAsync(pp_small.as<unsigned char>() + bytes * comm->rank, mine, bytes, cudaMemcpyHostToDevice,
+                             stream));
+    std::vector<long long> off(R + 1);
+    for (int r = 0; r <= R; ++r) off[r] = (long long)bytes * r;
+    sync();
+    comm->allgather_ranges(pp_small.p, off, stream);
+    std::vector<unsigned char> out(bytes * R);
+    HOT_CUDA(cudaMemcpyAsync(out.data(), pp_small.p, bytes * R, cudaMemcpyDeviceToHost, stream));
+    sync();
+    return out;
+  }
+  std::vector<long long> allgather_ll(long long mine) {
+    const auto b = allgather_block(&mine, 8);
+    std::vector<long long> v(comm->size);
+    std::memcpy(v.data(), b.data(), 8 * v.size());
+    return v;
+  }
+  /// Exclusive scan of n flags into pos; returns the total.
+  long long pp_scan(const int* flag, int* pos, long long n) {
+    if (n == 0) return 0;
+    if (n > (long long)INT_MAX - 4096) throw std::invalid_argument("particle partition: too many particles per rank");
+    scan_tmp.ensure(sizeof(int) * (n / 4096 + 64));
+    launch_exclusive_scan(flag, pos, (int)n, scan_tmp.as<int>(), iflags.as<int>() + 9, stream);
+    int t = 0;
+    HOT_CUDA(cudaMemcpyAsync(&t, iflags.as<int>() + 9, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    return t;
+  }
+  void pp_flags(long long n) {
+    const size_t b = sizeof(int) * (size_t)std::max<long long>(n + 1, 1);
+    pp_keep.ensure(b);
+    pp_pack.ensure(b);
+    pp_kpos.ensure(b);
+    pp_ppos.ensure(b);
+  }
+  /// The local particles become the kept ones, then the kept records (in that order).
+  void pp_rebuild(long long n_keep, const double* rec, long long mrec, long long n_recv) {
+    const long long nn = n_keep + n_recv;
+    const size_t n3 = sizeof(double) * 3 * std::max<long long>(nn, 1), n9 = sizeof(double) * 9 * std::max<long long>(nn, 1);
+    const size_t n1 = sizeof(double) * std::max<long long>(nn, 1), i1 = sizeof(int) * std::max<long long>(nn, 1);
+    qx.ensure(n3);
+    qv.ensure(n3);
+    qF.ensure(n9);
+    qC.ensure(n9);
+    qmass.ensure(n1);
+    qvol.ensure(n1);
+    qmat.ensure(i1);
+    qorig.ensure(i1);
+    if (track_jp) qjp.ensure(n1);
+    ParticlesView Q = pview();
+    Q.x = qx.as<double>();
+    Q.v = qv.as<double>();
+    Q.F = qF.as<double>();
+    Q.C = qC.as<double>();
+    Q.mass = qmass.as<double>();
+    Q.vol = qvol.as<double>();
+    Q.mat = qmat.as<int>();
+    Q.Jp = track_jp ? qjp.as<double>() : nullptr;
+    Q.n = nn;
+    launch_pp_rebuild(pview(), porig.as<int>(), pp_keep.as<int>(), pp_kpos.as<int>(), rec, mrec,
+                      pp_rflag.as<int>(), pp_rpos.as<int>(), n_keep, Q, qorig.as<int>(), stream);
+    px.swap(qx);
+    pv.swap(qv);
+    pF.swap(qF);
+    pC.swap(qC);
+    pmass.swap(qmass);
+    pvol.swap(qvol);
+    pmat.swap(qmat);
+    porig.swap(qorig);
+    if (track_jp) pjp.swap(qjp);
+    np = nn;
+    sync();
+    check_launch();
+  }
+  /// Records of this rank's particles flagged in pp_pack (positions pp_ppos, n_pack of them),
+  /// gathered from every rank into pp_send; returns the total record count.
+  long long pp_allgather_records(long long n_pack) {
+    const int R = comm->size, me = comm->rank;
+    const auto counts = allgather_ll(n_pack);
+    std::vector<long long> off(R + 1, 0);
+    for (int r = 0; r < R; ++r) off[r + 1] = off[r] + counts[r];
+    const long long total = off[R];
+    const int rec = pp_record_doubles();
+    pp_send.ensure(sizeof(double) * rec * std::max<long long>(total, 1));
+    launch_pp_pack(pview(), porig.as<int>(), pp_pack.as<int>(), pp_ppos.as<int>(), dx,
+                   pp_send.as<double>() + off[me] * rec, stream);
+    std::vector<long long> boff(R + 1);
+    for (int r = 0; r <= R; ++r) boff[r] = off[r] * rec * (long long)sizeof(double);
+    sync();
+    comm->allgather_ranges(pp_send.p, boff, stream);
+    return total;
+  }
+  /// After a sharded step: every rank keeps its owned particles that stay inside
+  /// its slab away from the copied bands, and sends the others (leaving the slab, or within
+  /// kPPLeft planes of Q / kPPRight planes of P, which other ranks copy) to all ranks; each rank
+  /// keeps the records inside its band.  The first call (every rank holds every particle) only
+  /// filters.  Owners are decided by the stencil-centre plane after advection.
+  void pp_exchange() {
+    const int me = comm->rank;
+    const long long n = np;
+    pp_flags(n);
+    const int olo = pp_owned_lo(me), ohi = pp_owned_hi(me);
+    if (!pp_on) {
+      launch_pp_classify(pview(), nullptr, olo - kPPLeft, ohi + kPPRight, INT_MIN, INT_MAX, 0, 0, dx, pp_keep.as<int>(),
+                         pp_pack.as<int>(), stream);
+      const long long n_keep = pp_scan(pp_keep.as<int>(), pp_kpos.as<int>(), n);
+      pp_rebuild(n_keep, nullptr, 0, 0);
+      pp_on = true;
+      return;
+    }
+    launch_pp_classify(pview(), L[0].coords.as<int>(), olo, ohi, olo, ohi, kPPLeft, kPPRight, dx, pp_keep.as<int>(),
+                       pp_pack.as<int>(), stream);
+    const long long n_keep = pp_scan(pp_keep.as<int>(), pp_kpos.as<int>(), n);
+    const long long n_pack = pp_scan(pp_pack.as<int>(), pp_ppos.as<int>(), n);
+    const long long total = pp_allgather_records(n_pack);
+    pp_rflag.ensure(sizeof(int) * std::max<long long>(total + 1, 1));
+    pp_rpos.ensure(sizeof(int) * std::max<long long>(total + 1, 1));
+    launch_pp_recv_flag(pp_send.as<double>(), total, olo - kPPLeft, ohi + kPPRight, pp_rflag.as<int>(), stream);
+    const long long n_recv = pp_scan(pp_rflag.as<int>(), pp_rpos.as<int>(), total);
+    pp_rebuild(n_keep, pp_send.as<double>(), total, n_recv);
+  }
+  /// Every owned particle (plane of its current position in the rank's slab) as records in
+  /// pp_send, from every rank (np_global of them).
+  long long pp_gather_owned_records() {
+    const int me = comm->rank;
+    const long long n = np;
+    pp_flags(n);
+    launch_pp_classify(pview(), nullptr, pp_owned_lo(me), pp_owned_hi(me), pp_owned_lo(me), pp_owned_hi(me), 0, 0, dx,
+                       pp_keep.as<int>(), pp_pack.as<int>(), stream);
+    // gL = gR = 0: keep = owned and staying; pack = leaving -- here every owned particle is sent
+    HOT_CUDA(cudaMemcpyAsync(pp_pack.p, pp_keep.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, stream));
+    const long long n_pack = pp_scan(pp_pack.as<int>(), pp_ppos.as<int>(), n);
+    const long long total = pp_allgather_records(n_pack);
+    if (total != np_global) throw std::logic_error("particle partition: owned particles do not add up");
+    return total;
+  }
+  /// Back to every particle on every rank (before a replicated solve or a stage tap).
+  void pp_gather_all() {
+    if (!pp_on) return;
+    const long long total = pp_gather_owned_records();
+    pp_rflag.ensure(sizeof(int) * std::max<long long>(total + 1, 1));
+    pp_rpos.ensure(sizeof(int) * std::max<long long>(total + 1, 1));
+    launch_pp_recv_flag(pp_send.as<double>(), total, INT_MIN, INT_MAX, pp_rflag.as<int>(), stream);
+    const long long n_recv = pp_scan(pp_rflag.as<int>(), pp_rpos.as<int>(), total);
+    pp_flags(np);
+    HOT_CUDA(cudaMemsetAsync(pp_keep.p, 0, sizeof(int) * std::max<long long>(np, 1), stream));
+    pp_rebuild(0, pp_send.as<double>(), total, n_recv);
+    pp_on = false;
+    have_state = false;
   }
 
   /// Level-1 cut: coarse planes [P/2, Q/2) (interior cuts are even).
@@ -1751,6 +1985,9 @@ struct Context {
       sync();
       v_max = host_scal[8];
     }
+    if (pp_on)  // the largest particle speed of every rank (ghosts are copies: max unchanged)
+      for (long long b : allgather_ll(*reinterpret_cast<const long long*>(&v_max)))
+        v_max = std::max(v_max, *reinterpret_cast<const double*>(&b));
     const double frame = 1.0 / fps;
     double dtn = v_max <= 0.0 ? frame : std::min(frame, 0.6 * dx / v_max);  // cfl_dt (grid.hpp:168-173)
     if (frame_end > 0.0) dtn = std::min(dtn, frame_end - time);
@@ -1767,13 +2004,28 @@ struct Context {
     gvel.swap(vout);
     const int h = prof_begin(P_G2P);
     HOT_CUDA(cudaMemsetAsync(iflags.as<int>() + 6, 0, sizeof(int), stream));
-    launch_g2p_strain_advect(pview(), gview(), dx, dtn, mats_d.as<DevMaterial>(), iflags.as<int>() + 6, stream);
+    if (pp_on)  // inversions counted by the owners
+      launch_g2p_strain_advect(pview(), gview(), dx, dtn, mats_d.as<DevMaterial>(), iflags.as<int>() + 6, stream,
+                               pp_owned_lo(comm->rank), pp_owned_hi(comm->rank));
+    else
+      launch_g2p_strain_advect(pview(), gview(), dx, dtn, mats_d.as<DevMaterial>(), iflags.as<int>() + 6, stream);
     prof_end(h, (double)np * (24 + 24 + 72 + 72 + 4 + 24 + 96) + 24.0 * L[0].n);
     int inv = 0;
     HOT_CUDA(cudaMemcpyAsync(&inv, iflags.as<int>() + 6, sizeof(int), cudaMemcpyDeviceToHost, stream));
     sync();
     check_launch();
+    if (pp_on) {
+      long long total = 0;
+      for (long long c : allgather_ll(inv)) total += c;
+      inv = (int)total;
+    }
     inversions += inv;
+    if (pp_enabled() && sh.planned) {  // partition the particles along this step's cut
+      if (!pp_on) pp_bounds = sh.bounds;
+      const int hp = prof_begin(P_COMM);
+      pp_exchange();
+      prof_end(hp);
+    }
     time += dtn;
     ++step_index;
     have_state = false;
@@ -1975,7 +2227,7 @@ int hot_get_plastic_state(hot_ctx* ctx, double* Jp) {
 }
 
 int hot_particle_count(hot_ctx* ctx, long long* n) {
-  *n = ctx->c.np;
+  *n = ctx->c.np_global;
   return HOT_OK;
 }
 
@@ -2012,7 +2264,8 @@ int hot_clear_diagnostics(hot_ctx* ctx) {
 }
 
 int hot_stage_prepare(hot_ctx* ctx, double dt, double time) {
-  return guard(ctx, [&] { ctx->c.prepare(dt, time); ctx->c.sync(); });
+  // the stage taps compare every particle: partitioned particles come back to every rank first
+  return guard(ctx, [&] { ctx->c.pp_gather_all(); ctx->c.prepare(dt, time); ctx->c.sync(); });
 }
 
 int hot_stage_node_count(hot_ctx* ctx, int* n) {
@@ -2287,6 +2540,9 @@ int hot_shard_info(hot_ctx* ctx, hot_shard_info_t* out) {
   out->asm_hi = c.sh.r_hi;
   out->halo_exchanges = c.comm ? c.comm->halos : 0;
   out->gathers = c.comm ? c.comm->gathers : 0;
+  out->particles_local = c.np;
+  out->particles_total = c.np_global;
+  out->partitioned = c.pp_on ? 1 : 0;
   return HOT_OK;
 }
 

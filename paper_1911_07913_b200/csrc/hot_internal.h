@@ -83,8 +83,9 @@ void launch_mark_active(const ParticlesView& P, double dx, DenseMap map, uint8_t
 /// the active count through *count_dev.  tile_sums must hold ceil(len/4096)+1 ints.
 void launch_flags_to_index(const uint8_t* flags, long long len, const int* ext, const int* lo, int* idx, int* coords,
                            int* tile_sums, int* count_dev, cudaStream_t s);
+/// orig: original ids of the particle slots (the within-bin order).
 void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n_nodes, int* bin_of, int* counts,
-                          int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s);
+                          int* start, int* cursor, int* pid, int* scan_tmp, const int* orig, cudaStream_t s);
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
                 double dt, double* bin_part, cudaStream_t s, int jlo = 0, int jhi = -1, int lo = 0,
                 int hi = -1);  // bins [jlo, jhi), rows [lo, hi)
@@ -203,8 +204,9 @@ constexpr int kSgsMaxWavesPersistent = 4096;
 int pcg_max_blocks();
 
 // ---------------------------------------------------------------- transfer (k_transfer.cu)
+/// Inversions are counted for particles whose bin plane (axis 0) is in [own_lo, own_hi).
 void launch_g2p_strain_advect(const ParticlesView& P, GridView g, double dx, double dt, const DevMaterial* mats,
-                              int* inverted, cudaStream_t s);
+                              int* inverted, cudaStream_t s, int own_lo = -(1 << 30), int own_hi = 1 << 30);
 void launch_vmax(const ParticlesView& P, unsigned long long* vmax_bits, cudaStream_t s);
 /// *bad = 1 if any id is outside [0, limit).
 void launch_check_ids(const int* ids, long long n, int limit, int* bad, cudaStream_t s);
@@ -220,6 +222,24 @@ void launch_fill(double* out, long long n, double value, cudaStream_t s);
 
 constexpr int kMaxDevices = 64;
 /// SM count of the current device (cached per device).
+// ---------------------------------------------------------------- particle partition (k_transfer.cu)
+/// keep / pack flags per local particle (see k_pp_classify).  coords: level-0 coords for the
+/// pre-step plane of P.bin (null: take it from x).  Planes are absolute; owned [owned_lo,
+/// owned_hi) after the step, pre-step owned [pre_lo, pre_hi).
+void launch_pp_classify(const ParticlesView& P, const int* coords, int owned_lo, int owned_hi, int pre_lo, int pre_hi,
+                        int gL, int gR, double dx, int* keep, int* pack, cudaStream_t s);
+void launch_pp_pack(const ParticlesView& P, const int* orig, const int* flag, const int* pos, double dx, double* out,
+                    cudaStream_t s);
+void launch_pp_recv_flag(const double* rec, long long m, int lo, int hi, int* flag, cudaStream_t s);
+/// Q (Q.n = n_keep + kept records): the kept particles of P in order, then the kept records.
+void launch_pp_rebuild(const ParticlesView& P, const int* orig, const int* keep, const int* keep_pos, const double* rec,
+                       long long mrec, const int* rflag, const int* rpos, long long n_keep, const ParticlesView& Q,
+                       int* qorig, cudaStream_t s);
+int pp_record_doubles();
+/// Records -> interleaved caller-order device arrays (by original id); null outputs skipped.
+void launch_pp_unpack_caller(const double* rec, long long m, double* x, double* v, double* F, double* C, double* Jp,
+                             cudaStream_t s);
+
 int num_sms();
 /// cudaFuncAttributeMaxDynamicSharedMemorySize = smem for fn on the current device (once per
 /// device; a no-op at <= 48 KB).

@@ -243,13 +243,17 @@ __global__ void k_bin_scatter(const int* __restrict__ bin_of, long long n, int* 
 
 /// Canonical (ascending particle id) order inside each bin, so every gather below is
 /// run-to-run deterministic.
-__global__ void k_bin_sort(const int* __restrict__ start, int n_nodes, int* pid) {
+/// Particles of a bin in ascending ORIGINAL id (the caller's upload order): the order every
+/// per-bin sum uses, the same whichever subset of the particles a rank stores (particle
+/// partition), so the sharded sums are bitwise the single-GPU ones.
+__global__ void k_bin_sort(const int* __restrict__ start, int n_nodes, int* pid, const int* __restrict__ orig) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_nodes; j += gridDim.x * blockDim.x) {
     const int b = start[j], e = start[j + 1];
     for (int i = b + 1; i < e; ++i) {
       const int v = pid[i];
+      const int ov = orig[v];
       int k = i - 1;
-      while (k >= b && pid[k] > v) {
+      while (k >= b && orig[pid[k]] > ov) {
         pid[k + 1] = pid[k];
         --k;
       }
@@ -577,13 +581,13 @@ void launch_exclusive_scan(const int* in, int* out, int n, int* tmp, int* total_
 }
 
 void launch_bin_particles(const ParticlesView& P, double dx, DenseMap map, int n_nodes, int* bin_of, int* counts,
-                          int* start, int* cursor, int* pid, int* scan_tmp, cudaStream_t s) {
+                          int* start, int* cursor, int* pid, int* scan_tmp, const int* orig, cudaStream_t s) {
   cudaMemsetAsync(counts, 0, sizeof(int) * (n_nodes + 1), s);
   if (P.n > 0) { k_bin_count<<<grid_for(P.n, 256), 256, 0, s>>>(P.x, P.n, dx, map, bin_of, counts); count_launches(1); }
   launch_exclusive_scan(counts, start, n_nodes + 1, scan_tmp, nullptr, s);
   cudaMemcpyAsync(cursor, start, sizeof(int) * n_nodes, cudaMemcpyDeviceToDevice, s);
   if (P.n > 0) { k_bin_scatter<<<grid_for(P.n, 256), 256, 0, s>>>(bin_of, P.n, cursor, pid); count_launches(1); }
-  if (n_nodes > 0) { k_bin_sort<<<grid_for(n_nodes, 128), 128, 0, s>>>(start, n_nodes, pid); count_launches(1); }
+  if (n_nodes > 0) { k_bin_sort<<<grid_for(n_nodes, 128), 128, 0, s>>>(start, n_nodes, pid, orig); count_launches(1); }
 }
 
 void launch_p2g(const ParticlesView& P, BinsView bins, GridView g, double dx, const DevMaterial* mats, double ell,
