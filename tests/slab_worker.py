@@ -57,6 +57,9 @@ def main():
              rows=np.array([[i["row_lo"], i["row_hi"], i["crow_lo"], i["crow_hi"], i["plane_lo"], i["plane_hi"]]
                             for i in infos]),
              halos=np.array(infos[-1]["halo_exchanges"] if infos else 0),
+             particles_local=np.array([i["particles_local"] for i in infos]),
+             particles_total=np.array([i["particles_total"] for i in infos]),
+             partitioned=np.array([i["partitioned"] for i in infos]),
              gathers=np.array(infos[-1]["gathers"] if infos else 0),
              energy=diag["energy"], residual=diag["scaled_residual"], tap_blocked=np.array(tap_blocked))
     if size > 1 or transport == "nccl":

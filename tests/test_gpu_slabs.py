@@ -70,6 +70,10 @@ def test_sharded_steps_equal_single_gpu_bitwise(tmp_path, scene, steps, size):
         assert res["halos"] > 0 and res["gathers"] > 0
         if res["sharded"][-1]:
             assert res["tap_blocked"] == 1  # level 0 is split: no tap reads it
+        # after the first sharded step the particles are partitioned: each rank stores its band
+        first = int(np.argmax(res["sharded"] == 1))
+        assert (res["partitioned"][first:] == 1).all(), res["partitioned"]
+        assert (res["particles_local"][first:] < res["particles_total"][first:]).all(), res["particles_local"]
         np.testing.assert_array_equal(res["stats"], ref["stats"])
         for k in ("x", "v", "F", "C", "energy", "residual"):
             np.testing.assert_array_equal(res[k], ref[k], err_msg=f"rank {r} {k}")
@@ -103,6 +107,25 @@ def test_sharded_benchmark_scene_two_steps(tmp_path):
         np.testing.assert_array_equal(res["stats"], ref["stats"])
         for k in ("x", "v", "F", "C"):
             np.testing.assert_array_equal(res[k], ref[k])
+        # partitioned after the first step: a rank stores its half plus 9 planes of ghosts
+        assert res["partitioned"][-1] == 1
+        assert res["particles_local"][-1] < 0.75 * res["particles_total"][-1], res["particles_local"]
+
+
+def test_sharded_four_ranks_partition_memory(tmp_path):
+    """4 ranks: bitwise equal to 1 GPU, and the particles each rank stores shrink with the rank
+    count (owned slab + the 8 + 1 ghost planes the assembly and the node passes read)."""
+    scene = "cfg1_stretched.json"
+    ref = run_ranks(tmp_path, scene, 1, 3, tag="single")[0]
+    two = run_ranks(tmp_path, scene, 2, 3, tag="two")
+    four = run_ranks(tmp_path, scene, 4, 3)
+    for res in two + four:
+        np.testing.assert_array_equal(res["stats"], ref["stats"])
+        for k in ("x", "v", "F", "C", "energy", "residual"):
+            np.testing.assert_array_equal(res[k], ref[k])
+    total = four[0]["particles_total"][-1]
+    assert sum(r["partitioned"][-1] for r in four) == 4
+    assert max(r["particles_local"][-1] for r in four) < max(r["particles_local"][-1] for r in two) < total
 
 
 def test_nccl_transport_single_rank(tmp_path):
