@@ -1985,9 +1985,19 @@ struct Context {
       sync();
       v_max = host_scal[8];
     }
-    if (pp_on)  // the largest particle speed of every rank (ghosts are copies: max unchanged)
-      for (long long b : allgather_ll(*reinterpret_cast<const long long*>(&v_max)))
-        v_max = std::max(v_max, *reinterpret_cast<const double*>(&b));
+    if (pp_on) {  // the largest particle speed of every rank (ghosts are copies: max unchanged)
+      const double mine = v_max;
+      long long bits = 0;
+      std::memcpy(&bits, &mine, sizeof(bits));
+      for (long long b : allgather_ll(bits)) {
+        double other = 0.0;
+        std::memcpy(&other, &b, sizeof(other));
+        v_max = std::max(v_max, other);
+      }
+      if (opt.verbose)
+        std::fprintf(stderr, "[hot] rank %d: %lld local particles of %lld, v_max local %.9g global %.9g\n", comm->rank,
+                     np, np_global, mine, v_max);
+    }
     const double frame = 1.0 / fps;
     double dtn = v_max <= 0.0 ? frame : std::min(frame, 0.6 * dx / v_max);  // cfl_dt (grid.hpp:168-173)
     if (frame_end > 0.0) dtn = std::min(dtn, frame_end - time);
