@@ -40,7 +40,7 @@ SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
 FP64_PEAK_TFLOPS = 37.06  # fp64 peak measured on this pool's B200: DMMA m8n8k4 37.06, DFMA 34.79 (profiles/r01_fp64_peak.json)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
-TRAFFIC = {"assemble_rows": 3.585794e9, "sgs_level0": 4.085396e9}  # per launch, from profiles/r01_ncu_full_summary.txt
+TRAFFIC = {"assemble_rows": 3.466343e9, "sgs_level0": 4.087008e9}  # per launch, from profiles/r02_ncu_full_summary.txt
 UNIT = "particle-steps/s"
 
 
@@ -359,7 +359,7 @@ def main():
     if "assemble_rows" in prof and prof["assemble_rows"]["ms"] > 0:
         ph = prof["assemble_rows"]
         ach = ph["flops"] / (ph["ms"] / 1000.0) / 1e12
-        roofline = {"bound": "tensor", "pipe": "fp64 DMMA m8n8k4", "kernel": "k_assemble_rows", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+        roofline = {"bound": "tensor", "pipe": "fp64 DMMA m8n8k4", "kernel": "k_assemble_tiles", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": TRAFFIC.get("assemble_rows"),
                     "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
                     "flops_per_launch": ph["flops"] / max(ph["launches"], 1),

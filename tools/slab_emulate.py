@@ -153,6 +153,7 @@ def run(sc, particles, R, steps, warmup):
             comms.append(comm)
     results = [None] * R
     marks = [None] * R
+    ends = [None] * R
 
     def body(r):
         sim = sims[r]
@@ -171,21 +172,24 @@ def run(sc, particles, R, steps, warmup):
         for k in range(warmup, warmup + steps):
             outer.append(sim.advance_step((k + 1) / sc.fps)["outer_iterations"])
         wall = time.perf_counter() - t
+        if comm:  # the timed segments end at the same logical point on every rank
+            comm.segments.append(time.perf_counter() - comm.t0)
+            comm.t0 = time.perf_counter()
+            ends[r] = (len(comm.segments), len(comm.recv_bytes))
+        prof = sim.profile_read()
+        # the download is a collective when the particles are partitioned
+        state = sim.particles()
+        info = slabs.shard_info(sim)
         if comm:
             comm.stop()
-        results[r] = dict(outer=outer, wall=wall)
+        results[r] = dict(outer=outer, wall=wall, state=state, info=info,
+                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0})
 
     threads = [threading.Thread(target=body, args=(r,)) for r in range(R)]
     for t in threads:
         t.start()
     for t in threads:
         t.join()
-    # read-backs after every rank is done (a rank that has left the baton protocol must not run
-    # GPU work or PCIe copies next to another rank's timed segment)
-    for r in range(R):
-        prof = sims[r].profile_read()
-        results[r].update(info=slabs.shard_info(sims[r]), state=sims[r].particles(),
-                          phases={k: round(v["ms"] / steps, 3) for k, v in prof.items() if v["ms"] > 0})
     out = dict(ranks=R, outer=results[0]["outer"], rank0_phase_ms_per_step=results[0]["phases"])
     if R == 1:
         out["compute_ms_per_step"] = 1000 * results[0]["wall"] / steps
@@ -193,8 +197,9 @@ def run(sc, particles, R, steps, warmup):
         out["recv_mb_per_step"] = 0.0
     else:
         s0, b0 = marks[0]
-        segs = np.array([c.segments[s0:] for c in comms])  # [R, nseg]
-        recv = np.array([c.recv_bytes[b0:] for c in comms])
+        s1, b1 = ends[0]
+        segs = np.array([c.segments[s0:s1] for c in comms])  # [R, nseg]
+        recv = np.array([c.recv_bytes[b0:b1] for c in comms])
         out["compute_ms_per_step"] = 1000 * segs.max(axis=0).sum() / steps
         out["rank_busy_ms_per_step"] = [round(1000 * x / steps, 3) for x in segs.sum(axis=1)]
         slow = int(np.argmax(segs.sum(axis=1)))
@@ -205,6 +210,8 @@ def run(sc, particles, R, steps, warmup):
         out["collectives_per_step"] = recv.shape[1] / steps
         out["recv_mb_per_step"] = float(recv.max(axis=0).sum()) / 1e6 / steps
         out["rows"] = [[res["info"]["row_lo"], res["info"]["row_hi"]] for res in results]
+        out["particles_local"] = [res["info"]["particles_local"] for res in results]
+        out["particles_total"] = results[0]["info"]["particles_total"]
         for r in range(1, R):
             assert results[r]["outer"] == results[0]["outer"]
     out["_state"] = results[0]["state"]
