@@ -9,10 +9,10 @@
  * plain structs, caller-owned host buffers, int status codes, no torch / CUDA types.
  *
  * Conventions (mirroring the reference):
- *   - fp64, dim = 3 on the device (dim = 2 returns HOT_E_UNSUPPORTED);
- *   - particle arrays are interleaved per particle: x[3*p+a], F[9*p + 3*row + col]
+ *   - fp64, dim = 3 or dim = 2 on the device (a dim = 2 scene gets the 2D path, k2d.cu);
+ *   - particle arrays are interleaved per particle: x[d*p+a], F[d*d*p + d*row + col]
  *     (row-major; the reference stores Eigen column-major, only the layout differs);
- *   - node vectors are interleaved [3*i+a] in lexicographic lattice order
+ *   - node vectors are interleaved [d*i+a] in lexicographic lattice order
  *     (grid.hpp:137-165, common.hpp:41);
  *   - errors map one-to-one onto the reference's exception types (section 5 of SURVEY.md);
  *     on HOT_E_SOLVER_FAILURE from hot_advance_step the particles are left unmodified
@@ -35,7 +35,7 @@ enum hot_status {
   HOT_E_LOGIC = 3,            /* std::logic_error */
   HOT_E_DOMAIN = 4,           /* std::domain_error */
   HOT_E_CUDA = 5,             /* CUDA runtime / device failure */
-  HOT_E_UNSUPPORTED = 6       /* feature not built for the device path (2D) */
+  HOT_E_UNSUPPORTED = 6       /* feature not built for the device path (2D multi-GPU slabs) */
 };
 
 typedef struct hot_ctx hot_ctx;

@@ -130,7 +130,7 @@ class Stepper {
   /// Same contract as hotmpm::advance_step (simulation.hpp:286-323).
   template <typename T, int d>
   StepStats<T> advance_step(SimulationState<T, d>& sim, const SolverConfig<T>& cfg, T frame_end) {
-    static_assert(d == 3 && sizeof(T) == 8, "the B200 path is fp64, 3D");
+    static_assert((d == 2 || d == 3) && sizeof(T) == 8, "the B200 path is fp64, 2D or 3D");
     hot_solver_config c{};
     c.epsilon = cfg.epsilon;
     c.tau = cfg.tau;
@@ -147,22 +147,22 @@ class Stepper {
     c.cn_length_factor = cfg.cn_length_factor;
     check(hot_set_solver(ctx_.get(), &c));
     const long long n = static_cast<long long>(sim.particles.size());
-    std::vector<double> x(3 * n), v(3 * n), m(n), vol(n), F(9 * n), C(9 * n);
+    std::vector<double> x(d * n), v(d * n), m(n), vol(n), F(d * d * n), C(d * d * n);
     std::vector<int> mat(n);
     if (!uploaded_) {
       for (long long p = 0; p < n; ++p) {
         const auto& q = sim.particles[p];
-        for (int a = 0; a < 3; ++a) {
-          x[3 * p + a] = q.x[a];
-          v[3 * p + a] = q.v[a];
+        for (int a = 0; a < d; ++a) {
+          x[d * p + a] = q.x[a];
+          v[d * p + a] = q.v[a];
         }
         m[p] = q.mass;
         vol[p] = q.volume;
         mat[p] = q.material;
-        for (int r = 0; r < 3; ++r)
-          for (int s = 0; s < 3; ++s) {
-            F[9 * p + 3 * r + s] = q.F(r, s);  // Eigen (r,s) accessor: layout independent
-            C[9 * p + 3 * r + s] = q.C(r, s);
+        for (int r = 0; r < d; ++r)
+          for (int s = 0; s < d; ++s) {
+            F[d * d * p + d * r + s] = q.F(r, s);  // Eigen (r,s) accessor: layout independent
+            C[d * d * p + d * r + s] = q.C(r, s);
           }
       }
       check(hot_upload_particles(ctx_.get(), n, x.data(), v.data(), m.data(), vol.data(), F.data(), C.data(),
@@ -175,14 +175,14 @@ class Stepper {
     check(hot_download_particles(ctx_.get(), x.data(), v.data(), F.data(), C.data()));
     for (long long p = 0; p < n; ++p) {
       auto& q = sim.particles[p];
-      for (int a = 0; a < 3; ++a) {
-        q.x[a] = x[3 * p + a];
-        q.v[a] = v[3 * p + a];
+      for (int a = 0; a < d; ++a) {
+        q.x[a] = x[d * p + a];
+        q.v[a] = v[d * p + a];
       }
-      for (int r = 0; r < 3; ++r)
-        for (int s = 0; s < 3; ++s) {
-          q.F(r, s) = F[9 * p + 3 * r + s];
-          q.C(r, s) = C[9 * p + 3 * r + s];
+      for (int r = 0; r < d; ++r)
+        for (int s = 0; s < d; ++s) {
+          q.F(r, s) = F[d * d * p + d * r + s];
+          q.C(r, s) = C[d * d * p + d * r + s];
         }
     }
     double t;

@@ -22,6 +22,7 @@
 
 #include "../../include/hot_c_api.h"
 #include "hot_comm.h"
+#include "hot2d.h"
 #include "hot_internal.h"
 
 namespace hotb200 {
@@ -30,21 +31,51 @@ long long sample_scene(const hot_scene& sc, std::vector<double>& x, std::vector<
                        std::vector<double>& vol, std::vector<double>& F, std::vector<double>& C,
                        std::vector<int>& mat);
 
+/// Material::elastic / von_mises / snow (constitutive.hpp:12-52) + stiffness_scale
+/// (constitutive.hpp:255-258) in dimension dim.
+DevMaterial make_dev_material(const hot_material& m, int dim) {
+  if (!(m.youngs > 0.0)) throw std::invalid_argument("material: Young's modulus must be positive");
+  if (!(m.poisson >= 0.0 && m.poisson < 0.5)) throw std::invalid_argument("material: Poisson ratio must lie in [0, 0.5)");
+  DevMaterial d{};
+  d.mu = m.youngs / (2.0 * (1.0 + m.poisson));
+  d.lambda = m.youngs * m.poisson / ((1.0 + m.poisson) * (1.0 - 2.0 * m.poisson));
+  d.plasticity = m.plasticity;
+  if (m.elasticity != 0 && m.elasticity != 1) throw std::invalid_argument("material: unknown elasticity");
+  d.elasticity = m.elasticity;
+  if (m.plasticity == 1) {
+    if (!(m.yield_stress > 0.0)) throw std::invalid_argument("material: yield stress must be positive");
+    d.yield_stress = m.yield_stress;
+  } else if (m.plasticity == 2) {
+    if (!(m.clamp_lo <= 1.0 && 1.0 <= m.clamp_hi)) throw std::invalid_argument("material: snow clamp must bracket 1");
+    if (!(m.hardening >= 0.0)) throw std::invalid_argument("material: hardening must be non-negative");
+    d.clamp_lo = m.clamp_lo;
+    d.clamp_hi = m.clamp_hi;
+    d.hardening = m.hardening;
+  } else if (m.plasticity == 3) {  // Drucker-Prager (extension; oracle Material::drucker_prager)
+    if (!(m.friction_angle >= 0.0 && m.friction_angle < 90.0))
+      throw std::invalid_argument("material: friction angle must lie in [0, 90) degrees");
+    const double sp = std::sin(m.friction_angle * 3.14159265358979323846 / 180.0);
+    d.dp_alpha = std::sqrt(2.0 / 3.0) * 2.0 * sp / (3.0 - sp);
+  } else if (m.plasticity != 0) {
+    throw std::invalid_argument("material: unknown plasticity");
+  }
+  // dP/dF at F = I in diagonal space: (mm) block 2mu I + la 11^T; 2x2 blocks with
+  // bd = 2mu - la*0, bs = (psi_i+psi_j)/2 = 0 -> entries (mu, mu).  Frobenius norm is basis
+  // invariant (Q orthogonal): sum of squares of Mhat.
+  const double a = 2.0 * d.mu + d.lambda, b = d.lambda;
+  const double mh = 0.5 * (2.0 * d.mu);
+  // d diagonal entries a, d(d-1) off-diagonal b, d(d-1)/2 2x2 blocks of four entries mh
+  const double fro2 = dim * a * a + dim * (dim - 1) * b * b + (dim * (dim - 1) / 2) * 4.0 * mh * mh;
+  d.xi = std::sqrt(fro2);
+  return d;
+}
+
 static std::atomic<long long> g_launches{0};
 long long kernel_launch_count() { return g_launches.load(); }
 void count_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 namespace {
 
-struct SolverFailure : std::runtime_error {
-  explicit SolverFailure(const std::string& m) : std::runtime_error(m) {}
-};
-struct CudaError : std::runtime_error {
-  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
-};
-struct Unsupported : std::runtime_error {
-  explicit Unsupported(const std::string& m) : std::runtime_error(m) {}
-};
 
 #define HOT_CUDA(x)                                                                                      \
   do {                                                                                                   \
@@ -416,7 +447,7 @@ struct Context {
   }
 
   void set_scene(const hot_scene& s) {
-    if (s.dim != 3) throw Unsupported("the B200 path is built for dim = 3 (2D: see DESIGN.md, next)");
+    if (s.dim != 3) throw std::invalid_argument("the 3D context takes dim = 3 scenes");
     if (!(s.dx > 0)) throw std::invalid_argument("activate_grid: dx must be positive");
     dx = s.dx;
     fps = s.fps;
@@ -450,43 +481,7 @@ struct Context {
     cfg.cn_length_factor = s.cn_length_factor;
   }
 
-  /// Material::elastic / von_mises / snow (constitutive.hpp:12-52) + stiffness_scale
-  /// (constitutive.hpp:255-258): ||dP/dF(I)||_F = sqrt(3 (2mu+la)^2 + 6 la^2 + 6 ((2mu+0)/... )).
-  static DevMaterial make_material(const hot_material& m) {
-    if (!(m.youngs > 0.0)) throw std::invalid_argument("material: Young's modulus must be positive");
-    if (!(m.poisson >= 0.0 && m.poisson < 0.5)) throw std::invalid_argument("material: Poisson ratio must lie in [0, 0.5)");
-    DevMaterial d{};
-    d.mu = m.youngs / (2.0 * (1.0 + m.poisson));
-    d.lambda = m.youngs * m.poisson / ((1.0 + m.poisson) * (1.0 - 2.0 * m.poisson));
-    d.plasticity = m.plasticity;
-    if (m.elasticity != 0 && m.elasticity != 1) throw std::invalid_argument("material: unknown elasticity");
-    d.elasticity = m.elasticity;
-    if (m.plasticity == 1) {
-      if (!(m.yield_stress > 0.0)) throw std::invalid_argument("material: yield stress must be positive");
-      d.yield_stress = m.yield_stress;
-    } else if (m.plasticity == 2) {
-      if (!(m.clamp_lo <= 1.0 && 1.0 <= m.clamp_hi)) throw std::invalid_argument("material: snow clamp must bracket 1");
-      if (!(m.hardening >= 0.0)) throw std::invalid_argument("material: hardening must be non-negative");
-      d.clamp_lo = m.clamp_lo;
-      d.clamp_hi = m.clamp_hi;
-      d.hardening = m.hardening;
-    } else if (m.plasticity == 3) {  // Drucker-Prager (extension; oracle Material::drucker_prager)
-      if (!(m.friction_angle >= 0.0 && m.friction_angle < 90.0))
-        throw std::invalid_argument("material: friction angle must lie in [0, 90) degrees");
-      const double sp = std::sin(m.friction_angle * 3.14159265358979323846 / 180.0);
-      d.dp_alpha = std::sqrt(2.0 / 3.0) * 2.0 * sp / (3.0 - sp);
-    } else if (m.plasticity != 0) {
-      throw std::invalid_argument("material: unknown plasticity");
-    }
-    // dP/dF at F = I in diagonal space: (mm) block 2mu I + la 11^T; 2x2 blocks with
-    // bd = 2mu - la*0, bs = (psi_i+psi_j)/2 = 0 -> entries (mu, mu).  Frobenius norm is basis
-    // invariant (Q orthogonal): sum of squares of Mhat.
-    const double a = 2.0 * d.mu + d.lambda, b = d.lambda;
-    const double mh = 0.5 * (2.0 * d.mu);
-    const double fro2 = 3.0 * a * a + 6.0 * b * b + 3.0 * 4.0 * mh * mh;
-    d.xi = std::sqrt(fro2);
-    return d;
-  }
+  static DevMaterial make_material(const hot_material& m) { return make_dev_material(m, 3); }
 
   static DevCollider make_collider(const hot_collider& c) {
     DevCollider d{};
@@ -2088,7 +2083,9 @@ using hotb200::Context;
 using hotb200::CudaError;
 
 struct hot_ctx {
-  Context c;
+  Context c;                       // the 3D context (errors of both paths land in c.err)
+  hotb200::Context2D* c2 = nullptr;  // dim = 2 scenes: the 2D device path (k2d.cu)
+  ~hot_ctx() { hotb200::ctx2d_delete(c2); }
 };
 
 namespace {
@@ -2167,6 +2164,11 @@ int hot_create(hot_ctx** out, const hot_scene* scene, int device) {
   auto* h = new hot_ctx;
   h->c.device = device;  // guard() makes it current and restores the caller's device afterwards
   const int rc = guard(h, [&] {
+    if (scene->dim == 2) {  // the 2D device path (k2d.cu)
+      h->c2 = hotb200::ctx2d_new(device, *scene);
+      return;
+    }
+    if (scene->dim != 3) throw std::invalid_argument("scene dim must be 2 or 3");
     h->c.init(device);
     h->c.set_scene(*scene);
   });
@@ -2192,6 +2194,8 @@ void hot_destroy(hot_ctx* ctx) {
 const char* hot_last_error(const hot_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_create_error.c_str(); }
 
 int hot_set_solver(hot_ctx* ctx, const hot_solver_config* cfg) {
+  if (ctx && ctx->c2 && cfg && cfg->levels >= 1 && cfg->window >= 1)
+    return guard(ctx, [&] { hotb200::ctx2d_set_solver(ctx->c2, *cfg); });
   return guard(ctx, [&] {
     if (cfg->levels < 1) throw std::invalid_argument("levels must be at least 1");
     if (cfg->window < 1) throw std::invalid_argument("window must be at least 1");
@@ -2219,29 +2223,41 @@ int hot_sample_scene_particles(const hot_scene* scene, long long* n, double* x, 
 
 int hot_upload_particles(hot_ctx* ctx, long long n, const double* x, const double* v, const double* mass,
                          const double* volume, const double* F, const double* C, const int* material) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_upload(ctx->c2, n, x, v, mass, volume, F, C, material); });
   return guard(ctx, [&] { ctx->c.upload(n, x, v, mass, volume, F, C, material); });
 }
 
 int hot_download_particles(hot_ctx* ctx, double* x, double* v, double* F, double* C) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_download(ctx->c2, x, v, F, C); });
   return guard(ctx, [&] { ctx->c.download(x, v, F, C); });
 }
 
 int hot_set_plastic_state(hot_ctx* ctx, const double* Jp) {
+  if (ctx && ctx->c2 && Jp) return guard(ctx, [&] { hotb200::ctx2d_set_plastic_state(ctx->c2, Jp); });
   if (!ctx || !Jp) return HOT_E_INVALID_ARGUMENT;
   return guard(ctx, [&] { ctx->c.set_plastic_state(Jp); });
 }
 
 int hot_get_plastic_state(hot_ctx* ctx, double* Jp) {
+  if (ctx && ctx->c2 && Jp) return guard(ctx, [&] { hotb200::ctx2d_get_plastic_state(ctx->c2, Jp); });
   if (!ctx || !Jp) return HOT_E_INVALID_ARGUMENT;
   return guard(ctx, [&] { ctx->c.get_plastic_state(Jp); });
 }
 
 int hot_particle_count(hot_ctx* ctx, long long* n) {
+  if (ctx->c2) {
+    *n = hotb200::ctx2d_particle_count(ctx->c2);
+    return HOT_OK;
+  }
   *n = ctx->c.np_global;
   return HOT_OK;
 }
 
 int hot_set_time(hot_ctx* ctx, double time, int frame, long long step_index) {
+  if (ctx->c2) {
+    hotb200::ctx2d_set_time(ctx->c2, time, frame, step_index);
+    return HOT_OK;
+  }
   ctx->c.time = time;
   ctx->c.frame = frame;
   ctx->c.step_index = step_index;
@@ -2249,6 +2265,10 @@ int hot_set_time(hot_ctx* ctx, double time, int frame, long long step_index) {
 }
 
 int hot_get_time(hot_ctx* ctx, double* time, int* frame, long long* step_index, long long* inversion_warnings) {
+  if (ctx->c2) {
+    hotb200::ctx2d_get_time(ctx->c2, time, frame, step_index, inversion_warnings);
+    return HOT_OK;
+  }
   if (time) *time = ctx->c.time;
   if (frame) *frame = ctx->c.frame;
   if (step_index) *step_index = ctx->c.step_index;
@@ -2257,10 +2277,15 @@ int hot_get_time(hot_ctx* ctx, double* time, int* frame, long long* step_index, 
 }
 
 int hot_advance_step(hot_ctx* ctx, double frame_end, hot_step_stats* out) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_advance(ctx->c2, frame_end, out); });
   return guard(ctx, [&] { ctx->c.advance(frame_end, out); });
 }
 
 int hot_diagnostics(hot_ctx* ctx, hot_diag_row* rows, int cap, int* n) {
+  if (ctx->c2) {
+    *n = hotb200::ctx2d_diagnostics(ctx->c2, rows, cap);
+    return HOT_OK;
+  }
   const int cnt = (int)ctx->c.diag.size();
   *n = cnt;
   if (rows)
@@ -2269,22 +2294,35 @@ int hot_diagnostics(hot_ctx* ctx, hot_diag_row* rows, int cap, int* n) {
 }
 
 int hot_clear_diagnostics(hot_ctx* ctx) {
+  if (ctx->c2) {
+    hotb200::ctx2d_clear_diagnostics(ctx->c2);
+    return HOT_OK;
+  }
   ctx->c.diag.clear();
   return HOT_OK;
 }
 
 int hot_stage_prepare(hot_ctx* ctx, double dt, double time) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_prepare(ctx->c2, dt, time); });
   // the stage taps compare every particle: partitioned particles come back to every rank first
   return guard(ctx, [&] { ctx->c.pp_gather_all(); ctx->c.prepare(dt, time); ctx->c.sync(); });
 }
 
 int hot_stage_node_count(hot_ctx* ctx, int* n) {
+  if (ctx->c2) {
+    *n = hotb200::ctx2d_node_count(ctx->c2);
+    return HOT_OK;
+  }
   *n = ctx->c.L[0].n;
   return HOT_OK;
 }
 
 int hot_stage_grid(hot_ctx* ctx, int* coords, double* mass, double* velocity, double* momentum, unsigned char* dirichlet,
                    double* bc_velocity, double* cn_scale) {
+  if (ctx && ctx->c2)
+    return guard(ctx, [&] {
+      hotb200::ctx2d_grid(ctx->c2, coords, mass, velocity, momentum, dirichlet, bc_velocity, cn_scale);
+    });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     need_state(c);
@@ -2304,6 +2342,7 @@ int hot_stage_grid(hot_ctx* ctx, int* coords, double* mass, double* velocity, do
 }
 
 int hot_stage_set_grid(hot_ctx* ctx, const double* velocity, const unsigned char* dirichlet, const double* bc_velocity) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_set_grid(ctx->c2, velocity, dirichlet, bc_velocity); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     need_state(c);
@@ -2317,6 +2356,7 @@ int hot_stage_set_grid(hot_ctx* ctx, const double* velocity, const unsigned char
 }
 
 int hot_stage_energy(hot_ctx* ctx, const double* dv, double* energy) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_energy(ctx->c2, dv, energy); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     need_state(c);
@@ -2331,6 +2371,7 @@ int hot_stage_energy(hot_ctx* ctx, const double* dv, double* energy) {
 }
 
 int hot_stage_gradient(hot_ctx* ctx, const double* dv, double* gout, double* scaled_norm) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_gradient(ctx->c2, dv, gout, scaled_norm); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     need_state(c);
@@ -2347,6 +2388,7 @@ int hot_stage_gradient(hot_ctx* ctx, const double* dv, double* gout, double* sca
 }
 
 int hot_stage_assemble(hot_ctx* ctx, const double* dv, int project) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_assemble(ctx->c2, dv, project); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     need_state(c);
@@ -2361,6 +2403,7 @@ int hot_stage_assemble(hot_ctx* ctx, const double* dv, int project) {
 }
 
 int hot_stage_build_hierarchy(hot_ctx* ctx, int levels, int embedding) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_build_hierarchy(ctx->c2, levels, embedding); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     if (!c.have_H) throw std::logic_error("no matrix assembled");
@@ -2370,11 +2413,16 @@ int hot_stage_build_hierarchy(hot_ctx* ctx, int levels, int embedding) {
 }
 
 int hot_stage_level_count(hot_ctx* ctx, int* levels) {
+  if (ctx->c2) {
+    *levels = hotb200::ctx2d_level_count(ctx->c2);
+    return HOT_OK;
+  }
   *levels = ctx->c.nlevels;
   return HOT_OK;
 }
 
 int hot_stage_level_shape(hot_ctx* ctx, int level, int* rows, int* slots) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_level_shape(ctx->c2, level, rows, slots); });
   return guard(ctx, [&] {
     if (level < 0 || level >= ctx->c.nlevels) throw std::logic_error("no such level");
     *rows = ctx->c.L[level].n;
@@ -2383,6 +2431,8 @@ int hot_stage_level_shape(hot_ctx* ctx, int level, int* rows, int* slots) {
 }
 
 int hot_stage_level_matrix(hot_ctx* ctx, int level, double* blocks, int* cols, int* coords, unsigned char* dirichlet) {
+  if (ctx && ctx->c2)
+    return guard(ctx, [&] { hotb200::ctx2d_level_matrix(ctx->c2, level, blocks, cols, coords, dirichlet); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     if (level < 0 || level >= c.nlevels) throw std::logic_error("no such level");
@@ -2410,6 +2460,7 @@ int hot_stage_level_matrix(hot_ctx* ctx, int level, double* blocks, int* cols, i
 }
 
 int hot_stage_matvec(hot_ctx* ctx, int level, const double* x, double* y) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_matvec(ctx->c2, level, x, y); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     if (level < 0 || level >= c.nlevels) throw std::logic_error("no such level");
@@ -2423,6 +2474,7 @@ int hot_stage_matvec(hot_ctx* ctx, int level, const double* x, double* y) {
 }
 
 int hot_stage_vcycle(hot_ctx* ctx, const double* b, double* u, int* coarse_iterations) {
+  if (ctx && ctx->c2) return guard(ctx, [&] { hotb200::ctx2d_vcycle(ctx->c2, b, u, coarse_iterations); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     if (c.nlevels < 1) throw std::logic_error("no hierarchy");
@@ -2439,6 +2491,8 @@ int hot_stage_vcycle(hot_ctx* ctx, const double* b, double* u, int* coarse_itera
 
 int hot_stage_step_grid(hot_ctx* ctx, double* velocity, double* dv, int* outer, long long* inner, int* converged,
                         int frame, long long step) {
+  if (ctx && ctx->c2)
+    return guard(ctx, [&] { hotb200::ctx2d_step_grid(ctx->c2, velocity, dv, outer, inner, converged, frame, step); });
   return guard(ctx, [&] {
     Context& c = ctx->c;
     need_state(c);
@@ -2454,9 +2508,13 @@ int hot_stage_step_grid(hot_ctx* ctx, double* velocity, double* dv, int* outer, 
   });
 }
 
-void* hot_stream(hot_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+void* hot_stream(hot_ctx* ctx) {
+  if (ctx && ctx->c2) return hotb200::ctx2d_stream(ctx->c2);
+  return ctx ? (void*)ctx->c.stream : nullptr;
+}
 
 int hot_profile_enable(hot_ctx* ctx, int enable) {
+  if (ctx && ctx->c2) return HOT_OK;  // the 2D path has no phase profile
   return guard(ctx, [&] {
     Context& c = ctx->c;
     c.sync();
@@ -2475,6 +2533,10 @@ int hot_profile_enable(hot_ctx* ctx, int enable) {
 }
 
 int hot_profile_read(hot_ctx* ctx, char* names, double* total_ms, long long* launches, double* bytes, int cap, int* n) {
+  if (ctx && ctx->c2) {
+    *n = 0;
+    return HOT_OK;
+  }
   return guard(ctx, [&] {
     Context& c = ctx->c;
     c.sync();
@@ -2511,6 +2573,10 @@ long long hot_kernel_launches(hot_ctx* ctx) {
 }
 
 int hot_set_comm_host(hot_ctx* ctx, const hot_comm_host* ops) {
+  if (ctx && ctx->c2) {
+    ctx->c.err = "the 2D path runs on one GPU (slabs are built for dim = 3)";
+    return HOT_E_UNSUPPORTED;
+  }
   if (!ctx) return HOT_E_INVALID_ARGUMENT;
   return guard(ctx, [&] {
     if (!ops) {
@@ -2527,6 +2593,10 @@ int hot_nccl_unique_id(unsigned char id[128]) {
 }
 
 int hot_set_comm_nccl(hot_ctx* ctx, const unsigned char id[128], int rank, int size) {
+  if (ctx && ctx->c2) {
+    ctx->c.err = "the 2D path runs on one GPU (slabs are built for dim = 3)";
+    return HOT_E_UNSUPPORTED;
+  }
   if (!ctx || !id) return HOT_E_INVALID_ARGUMENT;
   return guard(ctx, [&] {
     ctx->c.comm.reset(hotb200::make_nccl_comm(id, rank, size));

@@ -4,10 +4,23 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <stdexcept>
+#include <string>
 
 #include "hot_device.cuh"
 
 namespace hotb200 {
+
+/// Host-side error kinds of the device path (mapped onto hot_status by the C-ABI guard).
+struct SolverFailure : std::runtime_error {  // hotmpm::SolverFailure (common.hpp:124-126)
+  explicit SolverFailure(const std::string& m) : std::runtime_error(m) {}
+};
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+struct Unsupported : std::runtime_error {
+  explicit Unsupported(const std::string& m) : std::runtime_error(m) {}
+};
 
 /// Particle state, structure-of-arrays in the caller's (reference) particle order:
 /// x[a*n+p], v[a*n+p], F[k*n+p] / C[k*n+p] with k = 3*row+col.

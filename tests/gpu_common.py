@@ -83,3 +83,12 @@ def rel_err(a, b):
     a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
     scale = max(np.abs(b).max() if b.size else 0.0, 1e-300)
     return np.abs(a - b).max() / scale if a.size else 0.0
+
+
+def elem_rel_err(a, b, floor=1e-8):
+    """max_i |a_i - b_i| / max(|b_i|, floor * max|b|): per-element relative error."""
+    a, b = np.asarray(a, dtype=float).ravel(), np.asarray(b, dtype=float).ravel()
+    if b.size == 0:
+        return 0.0
+    den = np.maximum(np.abs(b), floor * max(np.abs(b).max(), 1e-300))
+    return float((np.abs(a - b) / den).max())

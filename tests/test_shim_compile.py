@@ -46,6 +46,11 @@ int main() {
   hotmpm::SimulationState<double, 3> sim;
   hotmpm::SolverConfig<double> cfg;
   (void)s.advance_step<double, 3>(sim, cfg, 1.0 / 24);
+  hotmpm::SceneConfig sc2;  // the 2D device path (cli.cpp:145 instantiates d = 2 too)
+  sc2.dim = 2;
+  hotmpm::cuda::Stepper s2(sc2);
+  hotmpm::SimulationState<double, 2> sim2;
+  (void)s2.advance_step<double, 2>(sim2, cfg, 1.0 / 24);
   return 0;
 }
 '''
