@@ -204,9 +204,9 @@ __device__ __forceinline__ void jacobi_pair(double* W, double* U, double* V, dou
     r1.s = 0.0;
   } else {
     const double u = t / dd;
-    const double tmp = sqrt(1.0 + u * u);
-    r1.s = 1.0 / tmp;
-    r1.c = u / tmp;
+    const double inv = rsqrt(1.0 + u * u);  // 1 / sqrt(1 + u^2): one reciprocal root for s and c
+    r1.s = inv;
+    r1.c = u * inv;
   }
   // m <- rot1 applied on the left
   const double a1 = r1.c * a + r1.s * c, b1 = r1.c * b + r1.s * d;
@@ -221,8 +221,8 @@ __device__ __forceinline__ void jacobi_pair(double* W, double* U, double* V, dou
     const double w = sqrt(tau * tau + 1.0);
     const double tt = tau > 0.0 ? 1.0 / (tau + w) : 1.0 / (tau - w);
     const double sign_t = tt > 0.0 ? 1.0 : -1.0;
-    const double n = 1.0 / sqrt(tt * tt + 1.0);
-    jr.s = -sign_t * (b1 / fabs(b1)) * fabs(tt) * n;
+    const double n = rsqrt(tt * tt + 1.0);
+    jr.s = -sign_t * copysign(1.0, b1) * fabs(tt) * n;  // b1 / |b1| (b1 != 0 here)
     jr.c = n;
   }
   // j_left = rot1 * j_right^T
