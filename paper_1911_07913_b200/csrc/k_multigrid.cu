@@ -157,6 +157,9 @@ __global__ void __launch_bounds__(W * 32) k_galerkin_x(LevelView f, double* __re
     }
     for (int tq = lane; tq < 64; tq += 32) {
       const int t0 = tq >> 4, t1 = (tq >> 2) & 3, t2 = tq & 3;
+      // an even coordinate (base -2) reaches coarse targets t = 0..2 only: t = 3 would be zeros,
+      // and k_galerkin_c never reads it (27 to 64 targets per row are written, not always 64)
+      if ((t0 == 3 && base[0] == -2) || (t1 == 3 && base[1] == -2) || (t2 == 3 && base[2] == -2)) continue;
       double acc[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) acc[k] = 0.0;
@@ -220,6 +223,8 @@ __global__ void __launch_bounds__(kMgThreads) k_galerkin_c(LevelView f, LevelVie
         // B - (floor(i/2) - 1) per axis; floor((2A+d)/2) = A + (d < 0 ? -1 : 0)
         const int q0 = O0 + 1 - (d0 < 0 ? -1 : 0), q1 = O1 + 1 - (d1 < 0 ? -1 : 0), q2 = O2 + 1 - (d2 < 0 ? -1 : 0);
         if ((unsigned)q0 > 3u || (unsigned)q1 > 3u || (unsigned)q2 > 3u) continue;
+        // child coordinate 2A + d is even when d == 0: its X has no target 3 (not written, zero)
+        if ((q0 == 3 && d0 == 0) || (q1 == 3 && d1 == 0) || (q2 == 3 && d2 == 0)) continue;
         const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
         const double* x = X + (long long)i * kGalX + 9 * (16 * q0 + 4 * q1 + q2);
 #pragma unroll
