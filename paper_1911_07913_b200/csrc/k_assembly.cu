@@ -210,6 +210,10 @@ __global__ void k_fill_cols(LevelView L, int* __restrict__ cols, unsigned long l
 constexpr int kAsmT = HOT_ASM_T;          // rows (consumer warps) per tile
 constexpr int kAsmCP = HOT_ASM_CP;        // particle records per ring slot
 constexpr int kAsmS = HOT_ASM_S;          // ring slots
+#ifndef HOT_ASM_UNROLL
+#define HOT_ASM_UNROLL 4
+#endif
+constexpr int kAsmUnroll = HOT_ASM_UNROLL;  // particle-loop unroll of a ring slot
 constexpr int kAsmSpan = 3 * kAsmT + 2;   // z extent of a group's bin columns, at most
 constexpr unsigned kRecBytes = kTensorStride * 8;  // 1008 = 63 x 16
 enum : int { kSlotData = 0, kSlotTileEnd = 1, kSlotStop = 2 };
@@ -259,7 +263,7 @@ __device__ __forceinline__ void asm_chunk(const double* __restrict__ S, int kmin
   const double* pa[4];
 #pragma unroll
   for (int mt = 0; mt < NT; ++mt) pa[mt] = S + kRecW + 3 * min(kmin + 8 * mt + qm, 26) + min(qk, 2);
-#pragma unroll
+#pragma unroll kAsmUnroll
   for (int t = 0; t < kAsmCP; ++t) {
     if (t >= cnt) break;  // warp-uniform: the slot's record count
     const int o = t * kTensorStride;
