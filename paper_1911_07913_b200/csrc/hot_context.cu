@@ -1312,8 +1312,8 @@ struct Context {
     launch_level_waves(l.view(), m > 0 ? 1 : 0, q, off, l.wave_of.as<int>(), st);
     l.wave_counts.ensure(sizeof(int) * (nw + 2));
     l.wave_start.ensure(sizeof(int) * (nw + 2));
-    l.wave_cursor.ensure(sizeof(int) * (nw + 2));
-    tmp.ensure(sizeof(int) * (nw / 4096 + 64));
+    l.wave_cursor.ensure(sizeof(int) * bucket_scratch_ints(l.n, nw));
+    tmp.ensure(sizeof(int) * (bucket_scratch_ints(l.n, nw) / 4096 + 64));
     launch_bucket_rows(l.wave_of.as<int>(), l.n, 0, l.wave_counts.as<int>(), l.wave_start.as<int>(),
                        l.wave_cursor.as<int>(), l.wave_rows.as<int>(), nw, tmp.as<int>(), st);
     std::vector<int> counts(nw);
@@ -1321,7 +1321,7 @@ struct Context {
     if (m == 0 && sh.on) {  // this slab's rows per colour, in the same 27 colour buckets
       sh.wave_counts.ensure(sizeof(int) * (nw + 2));
       sh.wave_starts.ensure(sizeof(int) * (nw + 2));
-      sh.wave_cursor.ensure(sizeof(int) * (nw + 2));
+      sh.wave_cursor.ensure(sizeof(int) * bucket_scratch_ints(sh.r_hi - sh.r_lo, nw));
       sh.wave_rows.ensure(sizeof(int) * std::max(sh.r_hi - sh.r_lo, 1));
       launch_bucket_rows(l.wave_of.as<int>(), sh.r_hi - sh.r_lo, 0, sh.wave_counts.as<int>(), sh.wave_starts.as<int>(),
                          sh.wave_cursor.as<int>(), sh.wave_rows.as<int>(), nw, tmp.as<int>(), st, sh.r_lo);

@@ -182,6 +182,9 @@ void launch_galerkin(LevelView fine, LevelView coarse, double* X, cudaStream_t s
 /// D^-1 per row (+ singular flag) and the wave id per row (coarse: offsets = bbox min >> 1).
 void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s);
 void launch_level_waves(LevelView L, int coarse, int modulus, const int* off, int* wave_of, cudaStream_t s);
+/// Ints of `cursor` scratch launch_bucket_rows needs for n rows and nwaves waves (its scan_tmp
+/// needs that / 4096 + 2).
+int bucket_scratch_ints(int n, int nwaves);
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
                         int nwaves, int* scan_tmp, cudaStream_t s, int row_base = 0);  // rows [row_base, +n)
 void launch_plane_starts(const int* coords, int n, int lo0, int nplanes, int* out, cudaStream_t s);

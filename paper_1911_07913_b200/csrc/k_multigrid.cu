@@ -424,13 +424,52 @@ __global__ void k_level_waves(LevelView L, int coarse, int q, int off0, int off1
   }
 }
 
-__global__ void k_wave_count(const int* __restrict__ wave_of, int n, int wmin, int* counts) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAdd(counts + (wave_of[i] - wmin), 1);
+/// Rows bucketed by wave, a STABLE counting sort (rows of a wave in ascending index order, the
+/// same on every run): per block of kBucketRows rows a shared-memory histogram (no contended
+/// global atomics), an exclusive scan over the wave-major (wave, block) counts, then each block
+/// ranks its rows in index order (match_any within 32-row chunks, running counts in shared
+/// memory).  Rows of one wave never couple, so the order inside a wave changes no value; it only
+/// makes the schedule deterministic and keeps a warp's neighbouring rows together.
+constexpr int kBucketRows = 256;
+__global__ void k_wave_block_count(const int* __restrict__ wave_of, int n, int wmin, int nwaves, int* __restrict__ bc) {
+  extern __shared__ int hist[];
+  for (int w = threadIdx.x; w < nwaves; w += blockDim.x) hist[w] = 0;
+  __syncthreads();
+  const int lo = blockIdx.x * kBucketRows, hi = min(n, lo + kBucketRows);
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(hist + (wave_of[i] - wmin), 1);
+  __syncthreads();
+  for (int w = threadIdx.x; w < nwaves; w += blockDim.x) bc[(long long)w * gridDim.x + blockIdx.x] = hist[w];
+  if (blockIdx.x == 0 && threadIdx.x == 0) bc[(long long)nwaves * gridDim.x] = 0;  // the scan's total slot
 }
-__global__ void k_wave_scatter(const int* __restrict__ wave_of, int n, int wmin, int* cursor, int* rows, int base) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    rows[atomicAdd(cursor + (wave_of[i] - wmin), 1)] = base + i;
+__global__ void k_wave_block_scatter(const int* __restrict__ wave_of, int n, int wmin, int nwaves,
+                                     const int* __restrict__ off, int* __restrict__ rows, int base) {
+  extern __shared__ int run[];  // rows of each wave this block has placed so far
+  const int lane = threadIdx.x;  // one warp per block
+  for (int w = lane; w < nwaves; w += 32) run[w] = 0;
+  __syncwarp();
+  const int lo = blockIdx.x * kBucketRows, hi = min(n, lo + kBucketRows);
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const bool v = i < hi;
+    const int w = v ? wave_of[i] - wmin : -1 - lane;  // distinct keys for idle lanes
+    const unsigned mask = __match_any_sync(0xffffffffu, w);
+    const int rank = __popc(mask & ((1u << lane) - 1u));
+    int pos = 0;
+    if (v) pos = off[(long long)w * gridDim.x + blockIdx.x] + run[w] + rank;
+    __syncwarp();
+    if (v && rank == 0) run[w] += __popc(mask);
+    __syncwarp();
+    if (v) rows[pos] = base + i;
+  }
+}
+/// counts[w] and start[w] (exclusive, start[nwaves] = n) from the (wave, block) offsets
+__global__ void k_wave_totals(const int* __restrict__ off, int nblocks, int nwaves, int* __restrict__ counts,
+                              int* __restrict__ start) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= nwaves; w += gridDim.x * blockDim.x) {
+    const int s0 = off[(long long)w * nblocks];
+    start[w] = s0;
+    if (w < nwaves) counts[w] = off[(long long)(w + 1) * nblocks] - s0;
+  }
 }
 
 /// out[p] = first row whose axis-0 coordinate is >= lo0 + p (p = 0..nplanes): the rows are in
@@ -1265,14 +1304,29 @@ void launch_level_dinv(LevelView L, int* singular_flag, cudaStream_t s) {
 void launch_level_waves(LevelView L, int coarse, int modulus, const int* off, int* wave_of, cudaStream_t s) {
   if (L.n) { k_level_waves<<<mgrid(L.n, 256), 256, 0, s>>>(L, coarse, modulus, off[0], off[1], off[2], wave_of); count_launches(1); }
 }
+int bucket_scratch_ints(int n, int nwaves) {
+  const long long nb = std::max(1, (n + kBucketRows - 1) / kBucketRows);
+  return (int)(2 * (nb * nwaves + 1) + 2);
+}
 void launch_bucket_rows(const int* wave_of, int n, int wmin, int* counts, int* start, int* cursor, int* rows,
                         int nwaves, int* scan_tmp, cudaStream_t s, int row_base) {
   wave_of += row_base;
-  cudaMemsetAsync(counts, 0, sizeof(int) * (nwaves + 1), s);
-  if (n) { k_wave_count<<<mgrid(n, 256), 256, 0, s>>>(wave_of, n, wmin, counts); count_launches(1); }
-  launch_exclusive_scan(counts, start, nwaves + 1, scan_tmp, nullptr, s);
-  cudaMemcpyAsync(cursor, start, sizeof(int) * nwaves, cudaMemcpyDeviceToDevice, s);
-  if (n) { k_wave_scatter<<<mgrid(n, 256), 256, 0, s>>>(wave_of, n, wmin, cursor, rows, row_base); count_launches(1); }
+  const int nb = std::max(1, (n + kBucketRows - 1) / kBucketRows);
+  const long long len = (long long)nb * nwaves + 1;
+  int* bc = cursor;         // (wave, block) counts, wave-major, + the total slot
+  int* off = cursor + len;  // their exclusive scan
+  const size_t sm = sizeof(int) * (size_t)std::max(nwaves, 1);
+  set_max_dynamic_smem((const void*)k_wave_block_count, (int)sm);
+  set_max_dynamic_smem((const void*)k_wave_block_scatter, (int)sm);
+  if (n) {
+    k_wave_block_count<<<nb, 256, sm, s>>>(wave_of, n, wmin, nwaves, bc);
+  } else {
+    cudaMemsetAsync(bc, 0, sizeof(int) * len, s);
+  }
+  launch_exclusive_scan(bc, off, (int)len, scan_tmp, nullptr, s);
+  k_wave_totals<<<std::max(1, (nwaves + 256) / 256), 256, 0, s>>>(off, nb, nwaves, counts, start);
+  if (n) k_wave_block_scatter<<<nb, 32, sm, s>>>(wave_of, n, wmin, nwaves, off, rows, row_base);
+  count_launches(n ? 3 : 1);
 }
 void launch_plane_starts(const int* coords, int n, int lo0, int nplanes, int* out, cudaStream_t s) {
   k_plane_starts<<<mgrid(nplanes + 1, 128), 128, 0, s>>>(coords, n, lo0, nplanes, out);
