@@ -846,19 +846,37 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
   // schedule runs it (one GPU small or large, or a slab)
   __shared__ double term[R == 2 ? T : 1][3];
   const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
+  // The next row of this CTA (its blocks, column id and wave ids) is requested before the current
+  // row's polls, so a row whose predecessors finish finds its own data already in registers:
+  // only the poll and the reduction stay on the dependency chain.
+  struct Pre {
+    int i, c, wi, wc;
+    double h[9];
+  };
+  auto fetch = [&](int pass, int k, Pre& P) {
+    P.i = __ldg(order + (pass == 0 ? k : n - 1 - k));
+    P.c = -1;
+    P.wi = P.wc = 0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) P.h[q] = 0.0;
+    if (s < S) {
+      P.c = __ldg(L.cols + (long long)P.i * T + s);
+      const double* hp = L.H + (long long)P.i * 9 * T + s;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) P.h[q] = __ldcs(hp + q * T);
+      P.wi = __ldg(wave_of + P.i);
+      P.wc = __ldg(wave_of + max(P.c, 0));
+    }
+  };
+  Pre nx;
+  if (blockIdx.x < n) fetch(0, blockIdx.x, nx);
   for (int pass = 0; pass < 2; ++pass) {
     for (int k = blockIdx.x; k < n; k += gridDim.x) {
-      const int i = __ldg(order + (pass == 0 ? k : n - 1 - k));
-      int c = -1;
-      double h[9];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) h[q] = 0.0;
-      if (s < S) {
-        c = __ldg(L.cols + (long long)i * T + s);
-        const double* hp = L.H + (long long)i * 9 * T + s;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) h[q] = __ldcs(hp + q * T);
-      }
+      const Pre cur = nx;
+      if (k + (int)gridDim.x < n) fetch(pass, k + gridDim.x, nx);
+      else if (pass == 0) fetch(1, blockIdx.x, nx);
+      const int i = cur.i, c = cur.c;
+      const double* h = cur.h;
       double D[9], rb[3];
       if (s == 0) {
 #pragma unroll
@@ -870,7 +888,7 @@ __global__ void __launch_bounds__(level_pitch(R)) k_sgs_flow(LevelView L, const 
       // forward value) are polled until written; the others still hold the pass's input
       double x0 = 0.0, x1 = 0.0, x2 = 0.0;
       if (c >= 0) {
-        const int wi = __ldg(wave_of + i), wc = __ldg(wave_of + c);
+        const int wi = cur.wi, wc = cur.wc;
         if (pass == 0) {
           if (wc < wi) sgs_poll3(uf + 3 * c, x0, x1, x2);
           else {  // a successor or the row itself: the input
@@ -1225,6 +1243,7 @@ int mgrid(long long n, int threads) {
 int coop_blocks(const void* fn, int threads, int smem = 0) { return resident_blocks(fn, threads, smem); }
 
 }  // namespace
+
 
 template <int R>
 int sgs_flow_blocks() {

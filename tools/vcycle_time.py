@@ -1,6 +1,7 @@
 """Times the V-cycle phases (level-0 smoother, coarse smoother, coarse PCG, ...) on a scene's first
 step: assemble at dv = 0, build the hierarchy, run `reps` V-cycles on a seeded right-hand side
 with the per-phase profile on.  Usage: python tools/vcycle_time.py scenes/cfg2_twisting_bars.json [reps]"""
+import hashlib
 import json
 import os
 import sys
@@ -24,6 +25,6 @@ for _ in range(reps):
     u, it = sim.vcycle(b)
 prof = sim.profile_read()
 out = {"variant": os.environ.get("HOT_LIB_VARIANT", "default"), "nodes": n, "coarse_iterations": it,
-       "u_norm": float(np.linalg.norm(u0))}
+       "u_norm": float(np.linalg.norm(u0)), "u_sha": hashlib.sha256(np.ascontiguousarray(u).tobytes()).hexdigest()[:16]}
 out.update({k: round(v["ms"] / reps, 4) for k, v in prof.items() if v["ms"] > 0})
 print(json.dumps(out))
