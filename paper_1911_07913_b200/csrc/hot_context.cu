@@ -123,6 +123,8 @@ struct Options {
   bool sgs_coarse_barrier = false; // HOT_SGS_COARSE=barrier: grid-barrier coarse smoother
   bool sgs_trace = false;          // HOT_SGS_TRACE: per-wave timing of the barrier smoother
   bool verbose = false;            // HOT_VERBOSE: per-solve diagnostics on stderr
+  bool asm_tiles = false;          // HOT_ASM=tiles: the row-tile level-0 assembly (k_assemble_tiles)
+  long long asm_ring_bins = 256 * 1024;  // HOT_ASM_RING: bins in the pair-sum ring (27,216 B each)
   int stream_min_rows = 8 * 1024;  // HOT_SGS_STREAM_MIN: rows per wave from which level 0 streams
   void read_env() {
     auto eq = [](const char* k, const char* v) {
@@ -135,6 +137,8 @@ struct Options {
     sgs_coarse_barrier = eq("HOT_SGS_COARSE", "barrier");
     sgs_trace = std::getenv("HOT_SGS_TRACE") != nullptr;
     verbose = std::getenv("HOT_VERBOSE") != nullptr;
+    asm_tiles = eq("HOT_ASM", "tiles");
+    if (const char* e = std::getenv("HOT_ASM_RING")) asm_ring_bins = std::max(1LL, std::atoll(e));
     if (const char* e = std::getenv("HOT_SGS_STREAM_MIN")) stream_min_rows = std::atoi(e);
   }
 };
@@ -275,6 +279,7 @@ struct Context {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DBuf scan_tmp2, struct_flags;
   DBuf grid_bar;  // words 0-1: the persistent smoothers' grid barrier; word 8: the assembly's tile counter
+  DBuf asm_pairs;  // ring of per-bin pair sums (level-0 assembly by bins)
   DBuf bin_part;  // per (bin, stencil position) particle sums feeding the node gathers (P2G, gradient)
   DBuf pn_b, pn_x, pn_r, pn_z, pn_p, pn_Ap, pn_dinv, pn_dP;  // projected-Newton PCG on level 0
   DBuf partials, scal, coef_a, coef_b, iflags, bounds;
@@ -1263,7 +1268,17 @@ struct Context {
       v0.lo = sh.a_lo;
       v0.hi = sh.r_hi;
     }
-    launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), grid_bar.as<unsigned int>() + 8, stream);
+    if (opt.asm_tiles) {
+      launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), grid_bar.as<unsigned int>() + 8, stream);
+    } else {
+      // pair sums of the bins through a ring: all bins at once when they fit, else bands
+      const int s_bound = l0.ext[1] * l0.ext[2] + l0.ext[2] + 2;
+      const long long want = std::min<long long>(l0.n, std::max<long long>(4LL * s_bound, opt.asm_ring_bins));
+      const int ring_cap = (int)std::max<long long>(want, 1);
+      asm_pairs.ensure(sizeof(double) * asm_pair_doubles() * (size_t)ring_cap);
+      launch_assemble_bins(bview(), gview(), v0, tu_base(), asm_pairs.as<double>(), ring_cap, s_bound,
+                           sh.on ? sh.p_lo : 0, sh.on ? sh.p_hi : np, grid_bar.as<unsigned int>() + 8, stream);
+    }
     // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
     prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
     have_H = true;

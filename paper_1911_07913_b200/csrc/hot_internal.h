@@ -171,6 +171,13 @@ void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s);
 /// tile_counter: 1 device word (the row tiles' work counter).
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, unsigned int* tile_counter, cudaStream_t s);
+/// The level-0 assembly by bins (k_bin_pairs + k_row_gather, k_assembly.cu): G is a ring of
+/// ring_cap bins x asm_pair_doubles() doubles; s_bound >= the index distance between a node and
+/// any of its 27 neighbours (one dense lattice plane + one line + 1); records of particles
+/// [plo, phi) are present in Tu; counter: 2 device words.
+int asm_pair_doubles();
+void launch_assemble_bins(BinsView bins, GridView g, LevelView L, const double* Tu, double* G, int ring_cap, int s_bound,
+                          long long plo, long long phi, unsigned int* counter, cudaStream_t s);
 
 // ---------------------------------------------------------------- multigrid (k_multigrid.cu)
 /// quad: quadratic node embedding (multigrid.hpp:72-90).

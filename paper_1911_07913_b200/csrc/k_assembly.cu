@@ -25,7 +25,6 @@ namespace hotb200 {
 
 namespace {
 
-constexpr int kAsmWarps = 4;
 constexpr int kUpper = 63;  // slots 62..124
 
 /// Per particle (bin order) one record of kRecStride doubles (1008 B = 63 x 16 B): W (27 x 3),
@@ -315,6 +314,17 @@ __device__ __forceinline__ void asm_fold(double* acc, int kmin, int qm, int qk, 
 /// The row's write-out: upper slots + transposed mirror, mass diagonal, symmetrised diagonal
 /// block (objective.hpp:349-351), Dirichlet projection (objective.hpp:133-144); inactive and pad
 /// slots hold zeros.  zc / uc / ud / di / mi were loaded when the row's tile started.
+/// Matrix store: streaming (evict-first) where nothing else competes for L2, default policy
+/// where the partially written lower-half lines must outlive a stream of loads (k_row_gather).
+template <bool STREAM>
+__device__ __forceinline__ void asm_store(double* p, double v) {
+  if (STREAM)
+    __stcs(p, v);
+  else
+    *p = v;
+}
+
+template <bool STREAM = true>
 __device__ __forceinline__ void asm_write_row(const LevelView& L, int i, int lane, const double* acc,
                                               const int (&zc)[kSlotPitch / 32], const int (&uc)[2],
                                               const bool (&ud)[2], bool di, double mi) {
@@ -322,7 +332,7 @@ __device__ __forceinline__ void asm_write_row(const LevelView& L, int i, int lan
   for (int j = 0; j < kSlotPitch / 32; ++j) {
     if (zc[j] < 0)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + lane + 32 * j, 0.0);
+      for (int k = 0; k < 9; ++k) asm_store<STREAM>(L.H + ((long long)i * 9 + k) * kSlotPitch + lane + 32 * j, 0.0);
   }
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -351,13 +361,13 @@ __device__ __forceinline__ void asm_write_row(const LevelView& L, int i, int lan
       for (int k = 0; k < 9; ++k) Cb[k] = 0.0;
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) __stcs(L.H + ((long long)i * 9 + k) * kSlotPitch + sl, Cb[k]);
+    for (int k = 0; k < 9; ++k) asm_store<STREAM>(L.H + ((long long)i * 9 + k) * kSlotPitch + sl, Cb[k]);
     if (sl != kDiagSlot) {
       const int sm = kSlots - 1 - sl;
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) __stcs(L.H + ((long long)col * 9 + 3 * r + c) * kSlotPitch + sm, Cb[3 * c + r]);
+        for (int c = 0; c < 3; ++c) asm_store<STREAM>(L.H + ((long long)col * 9 + 3 * r + c) * kSlotPitch + sm, Cb[3 * c + r]);
     }
   }
 }
@@ -544,10 +554,312 @@ __global__ void HOT_ASM_BOUNDS k_assemble_tiles(BinsView bins, GridView g, Level
       }
     } else if (m.kind == kSlotTileEnd && row >= 0) {
       __syncwarp();
-      asm_write_row(L, row, lane, acc, zc, uc, ud, di, mi);
+      asm_write_row<true>(L, row, lane, acc, zc, uc, ud, di, mi);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(empty + slot));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Level-0 assembly by bins (the default): pair sums per bin on the fp64 tensor cores, then a row
+// gather.  DESIGN.md §4 "Level-0 assembly by bins".
+//
+// Every particle of bin b (stencil-centre node b) has the same 27 stencil nodes, so the bin's
+// contribution to block (node a, node k), a <= k stencil positions, is one small GEMM over the
+// bin's particles:
+//   P_b[a][k][c][e] = sum_p sum_g W^p_k[g] * M^{p,a}[c][e][g],
+//   M^{p,a}[c][e][g] = sum_f W^p_a[f] T^p[(3c+f),(3e+g)]
+// (objective.hpp:322-347 regrouped).  Stage A (k_bin_pairs) computes the 378 upper pairs x 9
+// entries of every bin ONCE (the row-tile kernel re-formed M per (row, particle): 27 times) as
+// DMMA m8n8k4 tiles with M-dim = k, N-dim = a (8 positions), K-dim = 4 particles of one
+// component g, and bulk-stores the bin's 27,216-byte result; stage B (k_row_gather) sums, per
+// row, the segments of its 27 bins in a fixed order and writes the row, its transposes, the mass
+// diagonal and the Dirichlet projection (asm_write_row).  No atomics; every sum has a fixed
+// order that does not depend on the row range, so slab-sharded assembly stays bitwise equal.
+//
+// Pair layout of a bin: segment of position a at 9 * pair_off(a), entry (k - a) * 9 + (3c + e):
+// the part of a bin one row needs is contiguous, (27 - a) * 72 bytes.
+constexpr int kPairDoubles = 378 * 9;
+constexpr unsigned kPairBytes = kPairDoubles * 8;  // 27,216 = 1701 x 16
+__host__ __device__ constexpr int pair_off(int a) { return 27 * a - a * (a - 1) / 2; }
+static_assert(pair_off(27) == 378, "upper pairs of 27 positions");
+/// Slot index of stencil position k in the 5^3 diagonal storage, relative to position 0.
+__device__ __forceinline__ int spos(int k) { return k + 2 * (k / 3) + 10 * (k / 9); }
+
+constexpr int kBpCP = 12;    // records per ring slot (3 groups of 4 particles)
+constexpr int kBpS = 3;      // ring slots
+constexpr int kBpWarps = 9;  // compute warps: one block entry ce = 3c + e each
+constexpr int kBpGrab = 32;  // bins per work-counter grab
+struct BpMeta {
+  int kind, bin, cnt, last, pad[4];
+};
+constexpr size_t kBpRingBytes = (size_t)kBpS * kBpCP * kRecBytes;
+constexpr size_t kBpOutBytes = 2 * (size_t)kPairBytes;
+constexpr size_t kBpZeroBytes = kRecBytes;
+constexpr size_t kBpBarBytes = (size_t)2 * kBpS * 8;
+constexpr size_t kBpMetaBytes = (size_t)kBpS * sizeof(BpMeta);
+constexpr size_t kBpSmem = kBpRingBytes + kBpOutBytes + kBpZeroBytes + kBpBarBytes + kBpMetaBytes;
+static_assert(kBpRingBytes % 16 == 0 && kBpOutBytes % 16 == 0 && kBpZeroBytes % 16 == 0, "16-byte aligned regions");
+
+__device__ __forceinline__ void bp_named_barrier() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kBpWarps * 32) : "memory");
+}
+
+/// One compute warp of k_bin_pairs: block entry ce = wid, all ten (a tile, k tile >= a tile)
+/// accumulator tiles.  Lane (qk, qm): particle 4u + qk of the group, position 8t + qm of a tile;
+/// the K index of a step is the particle and the step's component g = v is the same for all
+/// lanes, so a lane needs three T entries per step, and the W_a its B entries need are also its
+/// A entries (W_k[v] at k = a).  Lanes past the bin's count read a record of zeros.
+__device__ __forceinline__ void bp_consume(const double* ring, const double* zero_rec, double* outs,
+                                           unsigned long long* full, unsigned long long* empty, const BpMeta* meta,
+                                           double* __restrict__ G, int ring_cap, int wid, int lane) {
+  const int qk = lane & 3, qm = lane >> 2;
+  const int c = wid / 3, e = wid % 3;
+  double Cc[10][2];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) Cc[t][0] = Cc[t][1] = 0.0;
+  int wofs[4], tofs[3][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) wofs[i] = kRecW + 3 * min(8 * i + qm, 26);
+#pragma unroll
+  for (int v = 0; v < 3; ++v)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) tofs[v][f] = kRecT + tslot(3 * c + f, 3 * e + v);
+  int nbins = 0;  // bins this CTA has finished (selects the output buffer)
+  for (int it = 0;; ++it) {
+    const int slot = it % kBpS;
+    mbar_wait_sleep(smem_u32(full + slot), (it / kBpS) & 1);
+    const BpMeta m = meta[slot];
+    if (m.kind == kSlotStop) break;
+    const double* S = ring + (size_t)slot * kBpCP * kTensorStride;
+    const int ngroups = (m.cnt + 3) >> 2;
+    for (int u = 0; u < ngroups; ++u) {
+      const int p = 4 * u + qk;
+      const double* R = p < m.cnt ? S + p * kTensorStride : zero_rec;
+      double W[4][3];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int f = 0; f < 3; ++f) W[i][f] = R[wofs[i] + f];
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        const double t0 = R[tofs[v][0]], t1 = R[tofs[v][1]], t2 = R[tofs[v][2]];
+        int t = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double B = fma(W[i][2], t2, fma(W[i][1], t1, W[i][0] * t0));
+#pragma unroll
+          for (int kt = i; kt < 4; ++kt) dmma_f64(Cc[t++], W[kt][v], B);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(empty + slot));
+    if (m.last) {
+      // the bin's tiles -> its pair layout in shared memory -> one bulk store
+      double* out = outs + (size_t)(nbins & 1) * kPairDoubles;
+      int t = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int kt = i; kt < 4; ++kt) {
+          const int k = 8 * kt + qm;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int a = 8 * i + 2 * qk + j;
+            if (a <= k && k <= 26) out[9 * (pair_off(a) + k - a) + wid] = Cc[t][j];
+            Cc[t][j] = 0.0;
+          }
+          ++t;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // the store issued one bin ago has read the other buffer before anyone passes the barrier
+      if (wid == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      bp_named_barrier();
+      if (wid == 0 && lane == 0) {
+        double* dst = G + (size_t)(m.bin % ring_cap) * kPairDoubles;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(out)),
+                     "r"(kPairBytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      ++nbins;
+    }
+  }
+  if (wid == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+/// Stage A.  Bins [jlo, jhi) in grabs of kBpGrab from a work counter; a bin is skipped when it
+/// is empty, when its records are not in [plo, phi) (slabs), or when none of its 27 nodes is a
+/// row of [rlo, rhi).  G holds ring_cap bins; bin j lives at slot j % ring_cap.
+__global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
+    k_bin_pairs(BinsView bins, GridView g, const double* __restrict__ Tu, double* __restrict__ G, int ring_cap, int jlo,
+                int jhi, int rlo, int rhi, long long plo, long long phi, unsigned int* __restrict__ counter) {
+  extern __shared__ __align__(16) unsigned char bp_sm[];
+  double* ring = reinterpret_cast<double*>(bp_sm);
+  double* outs = reinterpret_cast<double*>(bp_sm + kBpRingBytes);
+  double* zero_rec = reinterpret_cast<double*>(bp_sm + kBpRingBytes + kBpOutBytes);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(bp_sm + kBpRingBytes + kBpOutBytes + kBpZeroBytes);
+  unsigned long long* empty = full + kBpS;
+  BpMeta* meta = reinterpret_cast<BpMeta*>(bp_sm + kBpRingBytes + kBpOutBytes + kBpZeroBytes + kBpBarBytes);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kTensorStride; k += blockDim.x) zero_rec[k] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kBpS; ++q) {
+      mbar_init(full + q, 1);
+      mbar_init(empty + q, kBpWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (wid == kBpWarps) {  // ------------------------------------------------ producer warp
+    int it = 0;
+    const bool all_rows = rlo <= 0 && rhi >= g.n;
+    for (;;) {
+      int j0 = 0;
+      if (lane == 0) j0 = jlo + kBpGrab * (int)atomicAdd(counter, 1u);
+      j0 = __shfl_sync(0xffffffffu, j0, 0);
+      if (j0 >= jhi) break;
+      // each lane looks at one bin of the grab
+      const int j = j0 + lane;
+      int st = 0, cnt = 0;
+      if (j < jhi) {
+        st = __ldg(bins.start + j);
+        cnt = __ldg(bins.start + j + 1) - st;
+        if (st < plo || st + cnt > phi) cnt = 0;
+        if (cnt > 0 && !all_rows) {
+          const int* nb = g.nb27 + 27LL * j;
+          int mn = j, mx = j;
+          for (int e = 0; e < 13; ++e) {
+            const int q = __ldg(nb + e);
+            if (q >= 0) {
+              mn = q;
+              break;
+            }
+          }
+          for (int e = 26; e > 13; --e) {
+            const int q = __ldg(nb + e);
+            if (q >= 0) {
+              mx = q;
+              break;
+            }
+          }
+          if (mx < rlo || mn >= rhi) cnt = 0;
+        }
+      }
+      for (int e = 0; e < kBpGrab; ++e) {
+        const int bst = __shfl_sync(0xffffffffu, st, e), bcnt = __shfl_sync(0xffffffffu, cnt, e);
+        if (lane == 0) {
+          for (int c0 = 0; c0 < bcnt; c0 += kBpCP) {
+            const int slot = it % kBpS;
+            mbar_wait_sleep(smem_u32(empty + slot), ((it / kBpS) & 1) ^ 1);
+            const int k = min(kBpCP, bcnt - c0);
+            meta[slot] = BpMeta{kSlotData, j0 + e, k, c0 + kBpCP >= bcnt ? 1 : 0, {0, 0, 0, 0}};
+            const unsigned mb = smem_u32(full + slot);
+            mbar_expect_tx(mb, k * kRecBytes);
+            bulk_g2s(ring + (size_t)slot * kBpCP * kTensorStride, Tu + (long long)(bst + c0) * kTensorStride,
+                     k * kRecBytes, mb);
+            ++it;
+          }
+        }
+      }
+      it = __shfl_sync(0xffffffffu, it, 0);
+    }
+    if (lane == 0) {
+      const int slot = it % kBpS;
+      mbar_wait_sleep(smem_u32(empty + slot), ((it / kBpS) & 1) ^ 1);
+      meta[slot] = BpMeta{kSlotStop, 0, 0, 0, {0, 0, 0, 0}};
+      mbar_arrive(smem_u32(full + slot));
+    }
+    return;
+  }
+  bp_consume(ring, zero_rec, outs, full, empty, meta, G, ring_cap, wid, lane);
+}
+
+/// Stage B.  One warp per row of [rlo, rhi) whose largest neighbour bin lies in [blo, bhi) (the
+/// band whose pair sums stage A has just produced; blo < 0 and bhi > n: every row); rows are
+/// handed out in index order, so the rows in flight are a narrow band and the lower-half lines
+/// their transposes complete stay in L2 (the pair sums are loaded evict-first).  The row's 27
+/// bins in neighbour-table order (x, y, z ascending); the row sits at position a = 26 - e of bin
+/// e, whose segment of 9 (27 - a) doubles is contiguous; entry idx belongs to position
+/// k = a + idx / 9, upper slot spos(k) - spos(a).
+constexpr int kRgWarps = 8;
+__device__ __forceinline__ double ld_evict_first(const double* p, unsigned long long policy) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy));
+  return v;
+}
+__global__ void __launch_bounds__(kRgWarps * 32)
+    k_row_gather(BinsView bins, GridView g, LevelView L, const double* __restrict__ G, int ring_cap, int rlo, int rhi,
+                 int blo, int bhi, long long plo, long long phi, unsigned int* __restrict__ counter) {
+  __shared__ __align__(16) double accs[kRgWarps][kUpper * 9];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* acc = accs[wid];
+  const unsigned long long policy = l2_evict_first_policy();
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = rlo + kRgWarps * (int)atomicAdd(counter, 1u);
+    __syncthreads();
+    const int row = s_base + wid;
+    if (s_base >= rhi) break;
+    if (row >= rhi) continue;
+    int j = -1, cnt = 0;
+    if (lane < 27) {
+      j = __ldg(g.nb27 + 27LL * row + lane);
+      if (j >= 0) {
+        const int st = __ldg(bins.start + j);
+        cnt = __ldg(bins.start + j + 1) - st;
+        if (st < plo || st + cnt > phi) cnt = 0;
+      }
+    }
+    const unsigned present = __ballot_sync(0xffffffffu, j >= 0);
+    const int mx = __shfl_sync(0xffffffffu, j, 31 - __clz((int)present));
+    if (mx < blo || mx >= bhi) continue;
+    unsigned live = __ballot_sync(0xffffffffu, cnt > 0);
+    for (int k = lane; k < kUpper * 9; k += 32) acc[k] = 0.0;
+    int zc[kSlotPitch / 32], uc[2];
+    bool ud[2];
+    const int* crow = L.cols + (long long)row * kSlotPitch;
+#pragma unroll
+    for (int q = 0; q < kSlotPitch / 32; ++q) zc[q] = lane + 32 * q < kSlots ? __ldg(crow + lane + 32 * q) : -1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) uc[q] = lane + 32 * q < kUpper ? __ldg(crow + kDiagSlot + lane + 32 * q) : -1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) ud[q] = uc[q] >= 0 && g.dir[uc[q]] != 0;
+    const bool di = g.dir[row] != 0;
+    const double mi = g.mass[row];
+    __syncwarp();
+    while (live) {
+      const int eb = __ffs((int)live) - 1;
+      live &= live - 1;
+      const int jb = __shfl_sync(0xffffffffu, j, eb);
+      const int a = 26 - eb, len = 9 * (27 - a);
+      const int shift = 9 * (spos(a) - a);
+      const double* seg = G + (size_t)(jb % ring_cap) * kPairDoubles + 9 * pair_off(a);
+      const int nit = (len + 31) >> 5;  // 1..8, warp-uniform
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < nit) {
+          const int idx = lane + 32 * r;
+          v[r] = idx < len ? ld_evict_first(seg + idx, policy) : 0.0;
+        }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < nit) {
+          const int idx = lane + 32 * r;
+          if (idx < len) {
+            const int k = a + idx / 9;
+            acc[idx + 18 * (k / 3) + 90 * (k / 9) - shift] += v[r];
+          }
+        }
+    }
+    __syncwarp();
+    asm_write_row<false>(L, row, lane, acc, zc, uc, ud, di, mi);
   }
 }
 
@@ -599,6 +911,48 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
   const long long blocks = std::min<long long>(resident, tiles);
   k_assemble_tiles<<<(int)blocks, (kAsmT + 1) * 32, kAsmSmem, s>>>(bins, g, L, Tu, tile_counter);
   count_launches(1);
+}
+
+int asm_pair_doubles() { return kPairDoubles; }
+
+void launch_assemble_bins(BinsView bins, GridView g, LevelView L, const double* Tu, double* G, int ring_cap, int s_bound,
+                          long long plo, long long phi, unsigned int* counter, cudaStream_t s) {
+  if (L.hi <= L.lo) return;
+  const int n = g.n;
+  const int resident = resident_blocks((const void*)k_bin_pairs, (kBpWarps + 1) * 32, (int)kBpSmem);
+  const int rg_resident = resident_blocks((const void*)k_row_gather, kRgWarps * 32, 0);
+  auto stage_a = [&](int b0, int b1) {
+    cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
+    const long long grabs = ((long long)(b1 - b0) + kBpGrab - 1) / kBpGrab;
+    k_bin_pairs<<<(int)std::min<long long>(resident, grabs), (kBpWarps + 1) * 32, kBpSmem, s>>>(
+        bins, g, Tu, G, ring_cap, b0, b1, L.lo, L.hi, plo, phi, counter);
+  };
+  auto stage_b = [&](int r0, int r1, int blo, int bhi) {
+    if (r1 <= r0) return;
+    const long long blocks = ((long long)(r1 - r0) + kRgWarps - 1) / kRgWarps;
+    cudaMemsetAsync(counter + 1, 0, sizeof(unsigned int), s);
+    k_row_gather<<<(int)std::min<long long>(rg_resident, blocks), kRgWarps * 32, 0, s>>>(
+        bins, g, L, G, ring_cap, r0, r1, blo, bhi, plo, phi, counter + 1);
+  };
+  const bool all = L.lo <= 0 && L.hi >= n;
+  const int jbeg = all ? 0 : std::max(0, L.lo - s_bound), jend = all ? n : std::min(n, L.hi + s_bound);
+  if (jend - jbeg <= ring_cap) {  // one band: distinct slots for every bin of the range
+    stage_a(jbeg, jend);
+    stage_b(L.lo, L.hi, -1, 1 << 30);
+    count_launches(2);
+    return;
+  }
+  // bands of bins through the ring: after band [b0, b1) every row whose largest neighbour bin
+  // is below b1 can be finished; its smallest neighbour bin is above b0 - 2 s_bound
+  const int band = ring_cap - 2 * s_bound;
+  if (band <= 0) throw std::logic_error("launch_assemble_bins: ring smaller than 2 lattice planes");
+  for (int b0 = jbeg; b0 < jend; b0 += band) {
+    const int b1 = std::min(b0 + band, jend);
+    const bool first = b0 == jbeg, last = b1 == jend;
+    stage_a(b0, b1);
+    stage_b(std::max(L.lo, b0 - s_bound), std::min(L.hi, b1), first ? -1 : b0, last ? 1 << 30 : b1);
+    count_launches(2);
+  }
 }
 
 }  // namespace hotb200
