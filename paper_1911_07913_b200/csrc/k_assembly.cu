@@ -383,6 +383,16 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned bar, unsigned parity) {
 
 }
 
+/// Non-blocking probe of an mbarrier phase.
+__device__ __forceinline__ bool mbar_test(unsigned bar, unsigned parity) {
+  unsigned done;
+  asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+               : "=r"(done)
+               : "r"(bar), "r"(parity)
+               : "memory");
+  return done != 0;
+}
+
 __device__ __forceinline__ void mbar_arrive(unsigned bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -578,12 +588,17 @@ __global__ void HOT_ASM_BOUNDS k_assemble_tiles(BinsView bins, GridView g, Level
 // diagonal and the Dirichlet projection (asm_write_row).  No atomics; every sum has a fixed
 // order that does not depend on the row range, so slab-sharded assembly stays bitwise equal.
 //
-// Pair layout of a bin: segment of position a at 9 * pair_off(a), entry (k - a) * 9 + (3c + e):
-// the part of a bin one row needs is contiguous, (27 - a) * 72 bytes.
-constexpr int kPairDoubles = 378 * 9;
-constexpr unsigned kPairBytes = kPairDoubles * 8;  // 27,216 = 1701 x 16
+// Pair layout of a bin: segment of position a at pair_seg_off(a), entry (k - a) * 9 + (3c + e):
+// the part of a bin one row needs is contiguous, (27 - a) * 72 bytes, and 16-byte aligned.
 __host__ __device__ constexpr int pair_off(int a) { return 27 * a - a * (a - 1) / 2; }
 static_assert(pair_off(27) == 378, "upper pairs of 27 positions");
+/// First double of position a's segment: segments of odd length (a even) are padded by one
+/// double, so every segment starts on a 16-byte boundary (bulk copies).
+__host__ __device__ constexpr int pair_seg_off(int a) { return 9 * pair_off(a) + (a + 1) / 2; }
+__host__ __device__ constexpr int pair_seg_len(int a) { return (9 * (27 - a) + 1) & ~1; }  // doubles copied
+constexpr int kPairDoubles = pair_seg_off(27);
+constexpr unsigned kPairBytes = kPairDoubles * 8;  // 27,328 = 1708 x 16
+static_assert(kPairDoubles == 3416 && pair_seg_off(1) == 244 && pair_seg_off(2) == 478, "padded pair layout");
 /// Slot index of stencil position k in the 5^3 diagonal storage, relative to position 0.
 __device__ __forceinline__ int spos(int k) { return k + 2 * (k / 3) + 10 * (k / 9); }
 
@@ -597,8 +612,9 @@ struct BpMeta {
 constexpr size_t kBpRingBytes = (size_t)kBpS * kBpCP * kRecBytes;
 constexpr size_t kBpOutBytes = 2 * (size_t)kPairBytes;
 constexpr size_t kBpZeroBytes = kRecBytes;
-constexpr size_t kBpBarBytes = (size_t)2 * kBpS * 8;
-constexpr size_t kBpMetaBytes = (size_t)kBpS * sizeof(BpMeta);
+constexpr size_t kBpBarBytes = (size_t)(2 * kBpS + 4) * 8;  // ring full / empty, output full[2] / free[2]
+constexpr int kBpQueue = 8;  // bins between the producer's push and their store (< ring + 2 outputs)
+constexpr size_t kBpMetaBytes = (size_t)kBpS * sizeof(BpMeta) + kBpQueue * sizeof(int);
 constexpr size_t kBpSmem = kBpRingBytes + kBpOutBytes + kBpZeroBytes + kBpBarBytes + kBpMetaBytes;
 static_assert(kBpRingBytes % 16 == 0 && kBpOutBytes % 16 == 0 && kBpZeroBytes % 16 == 0, "16-byte aligned regions");
 
@@ -610,10 +626,14 @@ __device__ __forceinline__ void bp_named_barrier() {
 /// accumulator tiles.  Lane (qk, qm): particle 4u + qk of the group, position 8t + qm of a tile;
 /// the K index of a step is the particle and the step's component g = v is the same for all
 /// lanes, so a lane needs three T entries per step, and the W_a its B entries need are also its
-/// A entries (W_k[v] at k = a).  Lanes past the bin's count read a record of zeros.
+/// A entries (W_k[v] at k = a).  Lanes past the bin's count read a record of zeros.  A finished
+/// bin's tiles go to one of two output buffers in the pair layout; the warps do not wait for each
+/// other: each arrives on the buffer's mbarrier and the producer warp issues the bulk store.
 __device__ __forceinline__ void bp_consume(const double* ring, const double* zero_rec, double* outs,
                                            unsigned long long* full, unsigned long long* empty, const BpMeta* meta,
-                                           double* __restrict__ G, int ring_cap, int wid, int lane) {
+                                           int wid, int lane) {
+  unsigned long long* ofull = empty + kBpS;
+  unsigned long long* ofree = ofull + 2;
   const int qk = lane & 3, qm = lane >> 2;
   const int c = wid / 3, e = wid % 3;
   double Cc[10][2];
@@ -659,6 +679,8 @@ __device__ __forceinline__ void bp_consume(const double* ring, const double* zer
     if (m.last) {
       // the bin's tiles -> its pair layout in shared memory -> one bulk store
       double* out = outs + (size_t)(nbins & 1) * kPairDoubles;
+      // the store of two bins ago has read this buffer (no wait in practice)
+      if (nbins >= 2) mbar_wait_sleep(smem_u32(ofree + (nbins & 1)), ((nbins >> 1) - 1) & 1);
       int t = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -668,27 +690,18 @@ __device__ __forceinline__ void bp_consume(const double* ring, const double* zer
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const int a = 8 * i + 2 * qk + j;
-            if (a <= k && k <= 26) out[9 * (pair_off(a) + k - a) + wid] = Cc[t][j];
+            if (a <= k && k <= 26) out[pair_seg_off(a) + 9 * (k - a) + wid] = Cc[t][j];
             Cc[t][j] = 0.0;
           }
           ++t;
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      // the store issued one bin ago has read the other buffer before anyone passes the barrier
-      if (wid == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      bp_named_barrier();
-      if (wid == 0 && lane == 0) {
-        double* dst = G + (size_t)(m.bin % ring_cap) * kPairDoubles;
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(out)),
-                     "r"(kPairBytes)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ofull + (nbins & 1)));  // the producer warp stores the bin
       ++nbins;
     }
   }
-  if (wid == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 /// Stage A.  Bins [jlo, jhi) in grabs of kBpGrab from a work counter; a bin is skipped when it
@@ -706,17 +719,45 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
   BpMeta* meta = reinterpret_cast<BpMeta*>(bp_sm + kBpRingBytes + kBpOutBytes + kBpZeroBytes + kBpBarBytes);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < kTensorStride; k += blockDim.x) zero_rec[k] = 0.0;
+  unsigned long long* ofull = empty + kBpS;
+  unsigned long long* ofree = ofull + 2;
+  int* binq = reinterpret_cast<int*>(meta + kBpS);
   if (threadIdx.x == 0) {
     for (int q = 0; q < kBpS; ++q) {
       mbar_init(full + q, 1);
       mbar_init(empty + q, kBpWarps);
     }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(ofull + q, kBpWarps);
+      mbar_init(ofree + q, 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
 
-  if (wid == kBpWarps) {  // ------------------------------------------------ producer warp
-    int it = 0;
+  // Roles rotate between the two CTAs that share an SM (blocks b and b + gridDim / 2): warps map to
+  // the SM's four schedulers by warp id mod 4, so with the producer always last, scheduler 0
+  // would carry 6 of the 18 compute warps and cap the tensor pipes at 75 %.
+  const int rot = blockIdx.x >= (gridDim.x + 1) / 2 ? 1 : 0;
+  const int role = rot ? (wid == 0 ? kBpWarps : wid - 1) : wid;
+  if (role == kBpWarps) {  // ------------------------------------------------ producer warp
+    // Lane 0 runs both pipelines without blocking in either: record chunks into free ring slots,
+    // and the bulk store of every bin whose nine columns have arrived in an output buffer.
+    int it = 0;  // ring slots issued
+    int nb = 0;  // bins pushed (last chunk issued); bin q's id waits in binq[q % kBpQueue]
+    int ns = 0;  // bins stored
+    auto pump_store = [&]() -> bool {
+      if (ns >= nb || !mbar_test(smem_u32(ofull + (ns & 1)), (ns >> 1) & 1)) return false;
+      double* dst = G + (size_t)(binq[ns % kBpQueue] % ring_cap) * kPairDoubles;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"(smem_u32(outs + (size_t)(ns & 1) * kPairDoubles)), "r"(kPairBytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_arrive(smem_u32(ofree + (ns & 1)));
+      ++ns;
+      return true;
+    };
     const bool all_rows = rlo <= 0 && rhi >= g.n;
     for (;;) {
       int j0 = 0;
@@ -731,17 +772,17 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
         cnt = __ldg(bins.start + j + 1) - st;
         if (st < plo || st + cnt > phi) cnt = 0;
         if (cnt > 0 && !all_rows) {
-          const int* nb = g.nb27 + 27LL * j;
+          const int* nb27 = g.nb27 + 27LL * j;
           int mn = j, mx = j;
           for (int e = 0; e < 13; ++e) {
-            const int q = __ldg(nb + e);
+            const int q = __ldg(nb27 + e);
             if (q >= 0) {
               mn = q;
               break;
             }
           }
           for (int e = 26; e > 13; --e) {
-            const int q = __ldg(nb + e);
+            const int q = __ldg(nb27 + e);
             if (q >= 0) {
               mx = q;
               break;
@@ -755,65 +796,102 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
         if (lane == 0) {
           for (int c0 = 0; c0 < bcnt; c0 += kBpCP) {
             const int slot = it % kBpS;
-            mbar_wait_sleep(smem_u32(empty + slot), ((it / kBpS) & 1) ^ 1);
+            while (!mbar_test(smem_u32(empty + slot), ((it / kBpS) & 1) ^ 1))
+              if (!pump_store()) __nanosleep(32);
             const int k = min(kBpCP, bcnt - c0);
-            meta[slot] = BpMeta{kSlotData, j0 + e, k, c0 + kBpCP >= bcnt ? 1 : 0, {0, 0, 0, 0}};
+            const int last = c0 + kBpCP >= bcnt ? 1 : 0;
+            meta[slot] = BpMeta{kSlotData, j0 + e, k, last, {0, 0, 0, 0}};
             const unsigned mb = smem_u32(full + slot);
             mbar_expect_tx(mb, k * kRecBytes);
             bulk_g2s(ring + (size_t)slot * kBpCP * kTensorStride, Tu + (long long)(bst + c0) * kTensorStride,
                      k * kRecBytes, mb);
             ++it;
+            if (last) {
+              binq[nb % kBpQueue] = j0 + e;
+              ++nb;
+            }
+            pump_store();
           }
         }
       }
-      it = __shfl_sync(0xffffffffu, it, 0);
     }
     if (lane == 0) {
       const int slot = it % kBpS;
-      mbar_wait_sleep(smem_u32(empty + slot), ((it / kBpS) & 1) ^ 1);
+      while (!mbar_test(smem_u32(empty + slot), ((it / kBpS) & 1) ^ 1))
+        if (!pump_store()) __nanosleep(32);
       meta[slot] = BpMeta{kSlotStop, 0, 0, 0, {0, 0, 0, 0}};
       mbar_arrive(smem_u32(full + slot));
+      while (ns < nb)
+        if (!pump_store()) __nanosleep(64);
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     return;
   }
-  bp_consume(ring, zero_rec, outs, full, empty, meta, G, ring_cap, wid, lane);
+  bp_consume(ring, zero_rec, outs, full, empty, meta, role, lane);
 }
 
 /// Stage B.  One warp per row of [rlo, rhi) whose largest neighbour bin lies in [blo, bhi) (the
-/// band whose pair sums stage A has just produced; blo < 0 and bhi > n: every row); rows are
-/// handed out in index order, so the rows in flight are a narrow band and the lower-half lines
-/// their transposes complete stay in L2 (the pair sums are loaded evict-first).  The row's 27
-/// bins in neighbour-table order (x, y, z ascending); the row sits at position a = 26 - e of bin
-/// e, whose segment of 9 (27 - a) doubles is contiguous; entry idx belongs to position
-/// k = a + idx / 9, upper slot spos(k) - spos(a).
+/// band whose pair sums stage A has just produced; blo < 0 and bhi > n: every row).  A CTA takes
+/// kRgWarps consecutive rows at a time from a counter, in index order: consecutive rows run
+/// along z, their transposes fill neighbouring slots of the same lower-half lines at about the
+/// same time, and the rows in flight stay a narrow band, so those lines are completed in L2 (the
+/// pair sums are loaded evict-first).  The row's 27 bins in neighbour-table order (x, y, z
+/// ascending); the row sits at position a = 26 - e of bin e, whose segment is read in runs of up
+/// to three positions k (27 doubles, contiguous both in the segment and in the row's upper slots
+/// spos(k) - spos(a)); the loads of two bins are in flight before the first is added.
 constexpr int kRgWarps = 8;
+#ifndef RG_STREAM
+#define RG_STREAM false
+#endif
 __device__ __forceinline__ double ld_evict_first(const double* p, unsigned long long policy) {
   double v;
   asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy));
   return v;
 }
-__global__ void __launch_bounds__(kRgWarps * 32)
+/// Runs of bin position a: run 0 = positions a .. 3 (a / 3) + 2, run r >= 1 = the three positions
+/// of (k0, k1) index a / 3 + r.
+__device__ __forceinline__ void rg_load(const double* __restrict__ seg, int a, int lane, unsigned long long policy,
+                                        double (&v)[9]) {
+  const int m0 = a / 3, nruns = 9 - m0, len0 = 9 * (3 * m0 + 3 - a);
+  v[0] = lane < len0 ? ld_evict_first(seg + lane, policy) : 0.0;
+#pragma unroll
+  for (int r = 1; r < 9; ++r)
+    if (r < nruns) v[r] = lane < 27 ? ld_evict_first(seg + 9 * (3 * (m0 + r) - a) + lane, policy) : 0.0;
+}
+__device__ __forceinline__ void rg_add(double* acc, int a, int lane, const double (&v)[9]) {
+  const int m0 = a / 3, nruns = 9 - m0, len0 = 9 * (3 * m0 + 3 - a), Sa = spos(a);
+  if (lane < len0) acc[lane] += v[0];
+#pragma unroll
+  for (int r = 1; r < 9; ++r)
+    if (r < nruns) {
+      const int m = m0 + r;
+      if (lane < 27) acc[9 * (5 * m + 10 * (m / 3) - Sa) + lane] += v[r];
+    }
+}
+__global__ void __launch_bounds__(kRgWarps * 32, 3)
     k_row_gather(BinsView bins, GridView g, LevelView L, const double* __restrict__ G, int ring_cap, int rlo, int rhi,
                  int blo, int bhi, long long plo, long long phi, unsigned int* __restrict__ counter) {
   __shared__ __align__(16) double accs[kRgWarps][kUpper * 9];
-  __shared__ int s_base;
+  __shared__ int s_base[2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* acc = accs[wid];
   const unsigned long long policy = l2_evict_first_policy();
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_base = rlo + kRgWarps * (int)atomicAdd(counter, 1u);
-    __syncthreads();
-    const int row = s_base + wid;
-    if (s_base >= rhi) break;
+  if (threadIdx.x == 0) s_base[0] = rlo + kRgWarps * (int)atomicAdd(counter, 1u);
+  for (int it = 0;; ++it) {
+    __syncthreads();  // s_base[it & 1] is set; everyone is done with s_base[(it + 1) & 1]
+    const int base = s_base[it & 1];
+    if (base >= rhi) break;
+    if (threadIdx.x == 0) s_base[(it + 1) & 1] = rlo + kRgWarps * (int)atomicAdd(counter, 1u);
+    const int row = base + wid;
     if (row >= rhi) continue;
-    int j = -1, cnt = 0;
+    int j = -1, cnt = 0, slot = 0;
     if (lane < 27) {
       j = __ldg(g.nb27 + 27LL * row + lane);
       if (j >= 0) {
         const int st = __ldg(bins.start + j);
         cnt = __ldg(bins.start + j + 1) - st;
         if (st < plo || st + cnt > phi) cnt = 0;
+        slot = j % ring_cap;
       }
     }
     const unsigned present = __ballot_sync(0xffffffffu, j >= 0);
@@ -834,32 +912,21 @@ __global__ void __launch_bounds__(kRgWarps * 32)
     const double mi = g.mass[row];
     __syncwarp();
     while (live) {
-      const int eb = __ffs((int)live) - 1;
+      const int e1 = __ffs((int)live) - 1;
       live &= live - 1;
-      const int jb = __shfl_sync(0xffffffffu, j, eb);
-      const int a = 26 - eb, len = 9 * (27 - a);
-      const int shift = 9 * (spos(a) - a);
-      const double* seg = G + (size_t)(jb % ring_cap) * kPairDoubles + 9 * pair_off(a);
-      const int nit = (len + 31) >> 5;  // 1..8, warp-uniform
-      double v[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (r < nit) {
-          const int idx = lane + 32 * r;
-          v[r] = idx < len ? ld_evict_first(seg + idx, policy) : 0.0;
-        }
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (r < nit) {
-          const int idx = lane + 32 * r;
-          if (idx < len) {
-            const int k = a + idx / 9;
-            acc[idx + 18 * (k / 3) + 90 * (k / 9) - shift] += v[r];
-          }
-        }
+      const int e2 = live ? __ffs((int)live) - 1 : -1;
+      live &= live - 1;  // no-op on 0
+      const int a1 = 26 - e1, a2 = 26 - max(e2, 0);
+      const double* seg1 = G + (size_t)__shfl_sync(0xffffffffu, slot, e1) * kPairDoubles + pair_seg_off(a1);
+      const double* seg2 = G + (size_t)__shfl_sync(0xffffffffu, slot, max(e2, 0)) * kPairDoubles + pair_seg_off(a2);
+      double v1[9], v2[9];
+      rg_load(seg1, a1, lane, policy, v1);
+      if (e2 >= 0) rg_load(seg2, a2, lane, policy, v2);
+      rg_add(acc, a1, lane, v1);
+      if (e2 >= 0) rg_add(acc, a2, lane, v2);
     }
     __syncwarp();
-    asm_write_row<false>(L, row, lane, acc, zc, uc, ud, di, mi);
+    asm_write_row<RG_STREAM>(L, row, lane, acc, zc, uc, ud, di, mi);
   }
 }
 
@@ -929,7 +996,7 @@ void launch_assemble_bins(BinsView bins, GridView g, LevelView L, const double* 
   };
   auto stage_b = [&](int r0, int r1, int blo, int bhi) {
     if (r1 <= r0) return;
-    const long long blocks = ((long long)(r1 - r0) + kRgWarps - 1) / kRgWarps;
+    const long long blocks = ((long long)(r1 - r0) + kRgWarps - 1) / kRgWarps;  // one row per warp at least
     cudaMemsetAsync(counter + 1, 0, sizeof(unsigned int), s);
     k_row_gather<<<(int)std::min<long long>(rg_resident, blocks), kRgWarps * 32, 0, s>>>(
         bins, g, L, G, ring_cap, r0, r1, blo, bhi, plo, phi, counter + 1);
