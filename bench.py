@@ -40,7 +40,8 @@ SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
 FP64_PEAK_TFLOPS = 37.06  # fp64 peak measured on this pool's B200: DMMA m8n8k4 37.06, DFMA 34.79 (profiles/r01_fp64_peak.json)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
-TRAFFIC = {"assemble_rows": 3.467671e9, "sgs_level0": 4.086369e9}  # per launch, from profiles/r02_final_ncu_full_summary.txt
+# per launch, from profiles/r02_final2_ncu_full_summary.txt
+TRAFFIC = {"k_bin_pairs": 5.72e9, "k_row_gather": 7.65e9, "k_assemble_tiles": 3.467671e9, "sgs_level0": 4.086369e9}
 UNIT = "particle-steps/s"
 
 
@@ -355,19 +356,46 @@ def main():
     # throughput (its algorithmic flops / the measured fp64 peak).  `roofline_hbm` is the
     # largest HBM-bound phase (the level-0 smoother in practice).
     peaks, peak_kind = measured_peaks()
-    roofline = None
-    if "assemble_rows" in prof and prof["assemble_rows"]["ms"] > 0:
-        ph = prof["assemble_rows"]
+    # The level-0 assembly is two kernels (by bins): k_bin_pairs, bound by the fp64 tensor pipe
+    # (phase "assemble_pairs": all of the assembly's algorithmic flops), and k_row_gather, bound
+    # by HBM (phase "assemble_rows": the pair sums read once, the rows and their column ids).
+    # `roofline` is the one with the longer launch; both are reported, and `assembly` is the two
+    # together against the fp64 peak.  (HOT_ASM=tiles: one kernel, phase "assemble_rows" in flops.)
+    def tensor_line(ph, kernel):
         ach = ph["flops"] / (ph["ms"] / 1000.0) / 1e12
-        roofline = {"bound": "tensor", "pipe": "fp64 DMMA m8n8k4", "kernel": "k_assemble_tiles", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": TRAFFIC.get("assemble_rows"),
-                    "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
-                    "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
-                    "peak_kind": "measured fp64 tensor (DMMA) peak, the higher of DMMA/DFMA (profiles/r01_fp64_peak.json, tools/microbench/dmma.cu)"}
+        return {"bound": "tensor", "pipe": "fp64 DMMA m8n8k4", "kernel": kernel, "achieved": ach,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
+                "traffic": TRAFFIC.get(kernel), "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                "ms_per_launch": ph["ms"] / max(ph["launches"], 1),
+                "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
+                "peak_kind": "measured fp64 tensor (DMMA) peak, the higher of DMMA/DFMA (profiles/r01_fp64_peak.json, tools/microbench/dmma.cu)"}
+
+    def hbm_line(ph, kernel):
+        ach = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
+        return {"bound": "hbm", "kernel": kernel, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": TRAFFIC.get(kernel), "peak_kind": peak_kind,
+                "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                "ms_per_launch": ph["ms"] / max(ph["launches"], 1),
+                "bytes_per_launch": ph["bytes"] / max(ph["launches"], 1)}
+
+    roofline = roofline_pairs = roofline_rows = assembly = None
+    pa, ro = prof.get("assemble_pairs"), prof.get("assemble_rows")
+    if pa and pa["ms"] > 0 and ro and ro["ms"] > 0 and ro["bytes"] > 0:
+        roofline_pairs = tensor_line(pa, "k_bin_pairs")
+        roofline_rows = hbm_line(ro, "k_row_gather")
+        roofline = roofline_rows if roofline_rows["ms_per_launch"] >= roofline_pairs["ms_per_launch"] else roofline_pairs
+        tot_ms = pa["ms"] + ro["ms"]
+        ach = pa["flops"] / (tot_ms / 1000.0) / 1e12
+        assembly = {"kernels": ["k_bin_pairs", "k_row_gather"], "ms_per_step": tot_ms / args.steps, "achieved": ach,
+                    "unit": "TFLOP/s", "peak": FP64_PEAK_TFLOPS, "frac": ach / FP64_PEAK_TFLOPS,
+                    "share_of_step": tot_ms / ms}
+    elif ro and ro["ms"] > 0 and ro["flops"] > 0:
+        roofline = tensor_line(ro, "k_assemble_tiles")
     hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
                   k in ("sgs_level0", "spmv_level0", "residual_restrict", "p2g_bc", "node_gradient", "g2p_strain_advect", "prolong",
-                        "lbfgs_vectors")}
-    top = max(hbm_phases, key=lambda k: hbm_phases[k]["ms"]) if hbm_phases else None
+                        "lbfgs_vectors", "assemble_rows")}
+    smoothers = {k: v for k, v in hbm_phases.items() if k != "assemble_rows"}  # roofline_hbm: outside the assembly
+    top = max(smoothers, key=lambda k: smoothers[k]["ms"]) if smoothers else None
     # every HBM-class phase of the step: algorithmic GB/s and fraction of the measured peak
     hbm_all = {k: {"GBps": round(v["bytes"] / (v["ms"] / 1000.0) / 1e9, 1),
                    "frac": round(v["bytes"] / (v["ms"] / 1000.0) / 1e9 / peaks["hbm_gbs"], 3),
@@ -417,7 +445,9 @@ def main():
                 "outer_iterations": outer, "phase_ms_per_step": phases, "rank0_shard": shard,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps, "outer_iterations": e2e_outer},
-                "gpu_launches": int(launches), "roofline": roofline, "roofline_hbm": roofline_hbm, "hbm_phases": hbm_all,
+                "gpu_launches": int(launches), "roofline": roofline, "roofline_assembly_pairs": roofline_pairs,
+                "roofline_assembly_rows": roofline_rows, "assembly": assembly, "roofline_hbm": roofline_hbm,
+                "hbm_phases": hbm_all,
                 "cpu_baseline": cpu_baseline, "other_configs": other,
                 "clocks": clocks.summary()}
         print(json.dumps(line))

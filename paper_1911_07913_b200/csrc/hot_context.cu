@@ -194,7 +194,7 @@ struct ProfEvent {
 const char* kPhaseNames[] = {"activate_bin", "p2g_bc", "particle_energy", "node_gradient", "particle_tensors",
                              "assemble_rows", "hierarchy", "sgs_level0", "sgs_coarse", "residual_restrict",
                              "coarse_pcg", "prolong", "lbfgs_vectors", "g2p_strain_advect", "upload_download",
-                             "spmv_level0", "slab_comm"};
+                             "spmv_level0", "slab_comm", "assemble_pairs"};
 constexpr int kPhases = sizeof(kPhaseNames) / sizeof(kPhaseNames[0]);
 enum Phase {
   P_ACTIVATE,
@@ -213,7 +213,8 @@ enum Phase {
   P_G2P,
   P_IO,
   P_SPMV0,
-  P_COMM
+  P_COMM,
+  P_ASM_PAIRS
 };
 
 }  // namespace
@@ -1253,6 +1254,46 @@ struct Context {
     l.wave_rows.ensure(sizeof(int) * n);
   }
 
+  /// Level-0 assembly by bins (k_bin_pairs, then k_row_gather).  The bins' pair sums
+  /// go through a ring: all bins at once when they fit, else bands of bins, each followed by the
+  /// rows it completes (a row's bins lie within s_bound indices of it, so after the band
+  /// [b0, b1) every row whose largest neighbour bin is below b1 can finish, and the smallest
+  /// bin it reads is above b0 - 2 s_bound).
+  void assemble_by_bins(const LevelView& v0, double flops) {
+    Level& l0 = L[0];
+    const int n = l0.n;
+    const int s_bound = l0.ext[1] * l0.ext[2] + l0.ext[2] + 2;
+    const int ring_cap =
+        (int)std::max<long long>(std::min<long long>(n, std::max<long long>(4LL * s_bound, opt.asm_ring_bins)), 1);
+    asm_pairs.ensure(sizeof(double) * asm_pair_doubles() * (size_t)ring_cap);
+    double* G = asm_pairs.as<double>();
+    const long long plo = sh.on ? sh.p_lo : 0, phi = sh.on ? sh.p_hi : np;
+    unsigned int* ctr = grid_bar.as<unsigned int>() + 8;
+    unsigned long long* done = active_dev.as<unsigned long long>() + (kMaxLevels - 1);
+    HOT_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned long long), stream));
+    const bool all = v0.lo <= 0 && v0.hi >= n;
+    const int jbeg = all ? 0 : std::max(0, v0.lo - s_bound), jend = all ? n : std::min(n, v0.hi + s_bound);
+    const int band = jend - jbeg <= ring_cap ? std::max(jend - jbeg, 1) : ring_cap - 2 * s_bound;
+    if (band <= 0) throw std::logic_error("assemble_by_bins: ring smaller than 2 lattice planes");
+    for (int b0 = jbeg; b0 < jend; b0 += band) {
+      const int b1 = std::min(b0 + band, jend);
+      const bool first = b0 == jbeg, last = b1 == jend;
+      const int ha = prof_begin(P_ASM_PAIRS);
+      launch_bin_pairs(bview(), gview(), v0, tu_base(), G, ring_cap, b0, b1, plo, phi, ctr, done, stream);
+      prof_end(ha, 0.0, first ? flops : 0.0);
+      const int hb = prof_begin(P_ASSEMBLE);
+      if (first) launch_fill_cols(l0.view(), active_dev.as<unsigned long long>(), stream);
+      launch_row_gather(bview(), gview(), v0, G, ring_cap, first ? v0.lo : std::max(v0.lo, b0 - s_bound),
+                        last ? v0.hi : std::min(v0.hi, b1), first ? -1 : b0, last ? 1 << 30 : b1, plo, phi, ctr + 1,
+                        stream);
+      // algorithmic bytes: the row, its column ids (written and read); the pair sums of every
+      // bin with particles are read once (counted on the device, see prof_slot_bytes)
+      prof_end(hb, first ? (double)(v0.hi - v0.lo) * (9.0 * kSlotPitch * 8 + 2.0 * kSlotPitch * 4) : 0.0);
+      if (first && hb >= 0 && prof_solve + 1 < kProfSolves)
+        slot_terms.push_back(SlotTerm{P_ASSEMBLE, prof_solve + 1, kMaxLevels - 1, 8.0 * asm_pair_doubles()});
+    }
+  }
+
   /// reuse_svd: the last energy evaluation stored the SVD at exactly this dv (solve_qn start).
   void assemble(const double* dvp, bool project, bool reuse_svd = false) {
     Level& l0 = L[0];
@@ -1261,26 +1302,21 @@ struct Context {
     else
       alloc_level(l0);
     particle_tensors(dvp, project, reuse_svd);
-    const int h = prof_begin(P_ASSEMBLE);
-    launch_fill_cols(l0.view(), active_dev.as<unsigned long long>(), stream);
     LevelView v0 = l0.view();
     if (sh.on) {  // this slab's rows and the rows whose transposes complete them
       v0.lo = sh.a_lo;
       v0.hi = sh.r_hi;
     }
-    if (opt.asm_tiles) {
-      launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), grid_bar.as<unsigned int>() + 8, stream);
-    } else {
-      // pair sums of the bins through a ring: all bins at once when they fit, else bands
-      const int s_bound = l0.ext[1] * l0.ext[2] + l0.ext[2] + 2;
-      const long long want = std::min<long long>(l0.n, std::max<long long>(4LL * s_bound, opt.asm_ring_bins));
-      const int ring_cap = (int)std::max<long long>(want, 1);
-      asm_pairs.ensure(sizeof(double) * asm_pair_doubles() * (size_t)ring_cap);
-      launch_assemble_bins(bview(), gview(), v0, tu_base(), asm_pairs.as<double>(), ring_cap, s_bound,
-                           sh.on ? sh.p_lo : 0, sh.on ? sh.p_hi : np, grid_bar.as<unsigned int>() + 8, stream);
-    }
     // algorithmic fp64 work: per particle 27 rows x M (27 x 3 FMA) + 378 upper pairs x 27 FMA
-    prof_end(h, 0.0, (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0));
+    const double flops = (double)np * 2.0 * (27.0 * 81.0 + 378.0 * 27.0);
+    if (opt.asm_tiles) {
+      const int h = prof_begin(P_ASSEMBLE);
+      launch_fill_cols(l0.view(), active_dev.as<unsigned long long>(), stream);
+      launch_assemble_rows(pview(), bview(), gview(), v0, dx, tu_base(), grid_bar.as<unsigned int>() + 8, stream);
+      prof_end(h, 0.0, flops);
+    } else {
+      assemble_by_bins(v0, flops);
+    }
     have_H = true;
     nlevels = 1;
   }
@@ -2567,8 +2603,9 @@ int hot_profile_read(hot_ctx* ctx, char* names, double* total_ms, long long* lau
     if (c.prof_solve >= 0) {
       std::vector<unsigned long long> act((size_t)(c.prof_solve + 1) * hotb200::kMaxLevels);
       HOT_CUDA(cudaMemcpy(act.data(), c.prof_slots.p, sizeof(unsigned long long) * act.size(), cudaMemcpyDeviceToHost));
-      for (const auto& t : c.slot_terms)
-        slot_bytes[t.phase] += t.coef * (double)act[(size_t)t.solve * hotb200::kMaxLevels + t.level];
+      for (const auto& t : c.slot_terms)  // (a term of an assembly outside a solve has no snapshot)
+        if (t.solve <= c.prof_solve)
+          slot_bytes[t.phase] += t.coef * (double)act[(size_t)t.solve * hotb200::kMaxLevels + t.level];
     }
     const int k = std::min(cap, hotb200::kPhases);
     for (int i = 0; i < k; ++i) {

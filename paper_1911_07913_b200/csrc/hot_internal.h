@@ -171,13 +171,19 @@ void launch_fill_cols(LevelView L, unsigned long long* active, cudaStream_t s);
 /// tile_counter: 1 device word (the row tiles' work counter).
 void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, LevelView L, double dx,
                           const double* Tu, unsigned int* tile_counter, cudaStream_t s);
-/// The level-0 assembly by bins (k_bin_pairs + k_row_gather, k_assembly.cu): G is a ring of
-/// ring_cap bins x asm_pair_doubles() doubles; s_bound >= the index distance between a node and
-/// any of its 27 neighbours (one dense lattice plane + one line + 1); records of particles
-/// [plo, phi) are present in Tu; counter: 2 device words.
+/// The level-0 assembly by bins (k_assembly.cu).  Stage A, launch_bin_pairs: the pair sums of bins
+/// [b0, b1) into G, a ring of ring_cap bins x asm_pair_doubles() doubles (bin j at slot
+/// j % ring_cap); bins without particles, without records in [plo, phi), or without a node in
+/// rows [L.lo, L.hi) are skipped; *bins_done (may be null) counts the others.  Stage B,
+/// launch_row_gather: rows [r0, r1) whose largest neighbour bin lies in [blo, bhi) sum their bins'
+/// segments and write the row, its transposes, mass diagonal and Dirichlet projection.
+/// counter: 1 device word each (distinct words).
 int asm_pair_doubles();
-void launch_assemble_bins(BinsView bins, GridView g, LevelView L, const double* Tu, double* G, int ring_cap, int s_bound,
-                          long long plo, long long phi, unsigned int* counter, cudaStream_t s);
+void launch_bin_pairs(BinsView bins, GridView g, LevelView L, const double* Tu, double* G, int ring_cap, int b0, int b1,
+                      long long plo, long long phi, unsigned int* counter, unsigned long long* bins_done,
+                      cudaStream_t s);
+void launch_row_gather(BinsView bins, GridView g, LevelView L, const double* G, int ring_cap, int r0, int r1, int blo,
+                       int bhi, long long plo, long long phi, unsigned int* counter, cudaStream_t s);
 
 // ---------------------------------------------------------------- multigrid (k_multigrid.cu)
 /// quad: quadratic node embedding (multigrid.hpp:72-90).

@@ -709,7 +709,8 @@ __device__ __forceinline__ void bp_consume(const double* ring, const double* zer
 /// row of [rlo, rhi).  G holds ring_cap bins; bin j lives at slot j % ring_cap.
 __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
     k_bin_pairs(BinsView bins, GridView g, const double* __restrict__ Tu, double* __restrict__ G, int ring_cap, int jlo,
-                int jhi, int rlo, int rhi, long long plo, long long phi, unsigned int* __restrict__ counter) {
+                int jhi, int rlo, int rhi, long long plo, long long phi, unsigned int* __restrict__ counter,
+                unsigned long long* __restrict__ bins_done) {
   extern __shared__ __align__(16) unsigned char bp_sm[];
   double* ring = reinterpret_cast<double*>(bp_sm);
   double* outs = reinterpret_cast<double*>(bp_sm + kBpRingBytes);
@@ -824,6 +825,7 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
       while (ns < nb)
         if (!pump_store()) __nanosleep(64);
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (bins_done && nb) atomicAdd(bins_done, (unsigned long long)nb);  // profile: bins with particles
     }
     return;
   }
@@ -839,10 +841,16 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
 /// ascending); the row sits at position a = 26 - e of bin e, whose segment is read in runs of up
 /// to three positions k (27 doubles, contiguous both in the segment and in the row's upper slots
 /// spos(k) - spos(a)); the loads of two bins are in flight before the first is added.
-constexpr int kRgWarps = 8;
+#ifndef RG_WARPS
+#define RG_WARPS 8
+#endif
+#ifndef RG_MINB
+#define RG_MINB 3
+#endif
 #ifndef RG_STREAM
 #define RG_STREAM false
 #endif
+constexpr int kRgWarps = RG_WARPS;
 __device__ __forceinline__ double ld_evict_first(const double* p, unsigned long long policy) {
   double v;
   asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy));
@@ -868,7 +876,7 @@ __device__ __forceinline__ void rg_add(double* acc, int a, int lane, const doubl
       if (lane < 27) acc[9 * (5 * m + 10 * (m / 3) - Sa) + lane] += v[r];
     }
 }
-__global__ void __launch_bounds__(kRgWarps * 32, 3)
+__global__ void __launch_bounds__(kRgWarps * 32, RG_MINB)
     k_row_gather(BinsView bins, GridView g, LevelView L, const double* __restrict__ G, int ring_cap, int rlo, int rhi,
                  int blo, int bhi, long long plo, long long phi, unsigned int* __restrict__ counter) {
   __shared__ __align__(16) double accs[kRgWarps][kUpper * 9];
@@ -982,44 +990,27 @@ void launch_assemble_rows(const ParticlesView& P, BinsView bins, GridView g, Lev
 
 int asm_pair_doubles() { return kPairDoubles; }
 
-void launch_assemble_bins(BinsView bins, GridView g, LevelView L, const double* Tu, double* G, int ring_cap, int s_bound,
-                          long long plo, long long phi, unsigned int* counter, cudaStream_t s) {
-  if (L.hi <= L.lo) return;
-  const int n = g.n;
+void launch_bin_pairs(BinsView bins, GridView g, LevelView L, const double* Tu, double* G, int ring_cap, int b0, int b1,
+                      long long plo, long long phi, unsigned int* counter, unsigned long long* bins_done,
+                      cudaStream_t s) {
+  if (b1 <= b0) return;
   const int resident = resident_blocks((const void*)k_bin_pairs, (kBpWarps + 1) * 32, (int)kBpSmem);
-  const int rg_resident = resident_blocks((const void*)k_row_gather, kRgWarps * 32, 0);
-  auto stage_a = [&](int b0, int b1) {
-    cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
-    const long long grabs = ((long long)(b1 - b0) + kBpGrab - 1) / kBpGrab;
-    k_bin_pairs<<<(int)std::min<long long>(resident, grabs), (kBpWarps + 1) * 32, kBpSmem, s>>>(
-        bins, g, Tu, G, ring_cap, b0, b1, L.lo, L.hi, plo, phi, counter);
-  };
-  auto stage_b = [&](int r0, int r1, int blo, int bhi) {
-    if (r1 <= r0) return;
-    const long long blocks = ((long long)(r1 - r0) + kRgWarps - 1) / kRgWarps;  // one row per warp at least
-    cudaMemsetAsync(counter + 1, 0, sizeof(unsigned int), s);
-    k_row_gather<<<(int)std::min<long long>(rg_resident, blocks), kRgWarps * 32, 0, s>>>(
-        bins, g, L, G, ring_cap, r0, r1, blo, bhi, plo, phi, counter + 1);
-  };
-  const bool all = L.lo <= 0 && L.hi >= n;
-  const int jbeg = all ? 0 : std::max(0, L.lo - s_bound), jend = all ? n : std::min(n, L.hi + s_bound);
-  if (jend - jbeg <= ring_cap) {  // one band: distinct slots for every bin of the range
-    stage_a(jbeg, jend);
-    stage_b(L.lo, L.hi, -1, 1 << 30);
-    count_launches(2);
-    return;
-  }
-  // bands of bins through the ring: after band [b0, b1) every row whose largest neighbour bin
-  // is below b1 can be finished; its smallest neighbour bin is above b0 - 2 s_bound
-  const int band = ring_cap - 2 * s_bound;
-  if (band <= 0) throw std::logic_error("launch_assemble_bins: ring smaller than 2 lattice planes");
-  for (int b0 = jbeg; b0 < jend; b0 += band) {
-    const int b1 = std::min(b0 + band, jend);
-    const bool first = b0 == jbeg, last = b1 == jend;
-    stage_a(b0, b1);
-    stage_b(std::max(L.lo, b0 - s_bound), std::min(L.hi, b1), first ? -1 : b0, last ? 1 << 30 : b1);
-    count_launches(2);
-  }
+  cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
+  const long long grabs = ((long long)(b1 - b0) + kBpGrab - 1) / kBpGrab;
+  k_bin_pairs<<<(int)std::min<long long>(resident, grabs), (kBpWarps + 1) * 32, kBpSmem, s>>>(
+      bins, g, Tu, G, ring_cap, b0, b1, L.lo, L.hi, plo, phi, counter, bins_done);
+  count_launches(1);
+}
+
+void launch_row_gather(BinsView bins, GridView g, LevelView L, const double* G, int ring_cap, int r0, int r1, int blo,
+                       int bhi, long long plo, long long phi, unsigned int* counter, cudaStream_t s) {
+  if (r1 <= r0) return;
+  const int resident = resident_blocks((const void*)k_row_gather, kRgWarps * 32, 0);
+  cudaMemsetAsync(counter, 0, sizeof(unsigned int), s);
+  const long long blocks = ((long long)(r1 - r0) + kRgWarps - 1) / kRgWarps;
+  k_row_gather<<<(int)std::min<long long>(resident, blocks), kRgWarps * 32, 0, s>>>(bins, g, L, G, ring_cap, r0, r1, blo,
+                                                                                   bhi, plo, phi, counter);
+  count_launches(1);
 }
 
 }  // namespace hotb200

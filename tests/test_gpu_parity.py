@@ -143,6 +143,53 @@ def test_assembly_matches_oracle(project):
     assert _sym_err(m) == 0.0  # exact block symmetry (test_objective.cpp:185)
 
 
+def _assembled(sc, particles, env, dv_seed=5, project=True):
+    """Level-0 matrix of a fresh context created under the given HOT_ASM* environment (the knobs
+    are read once per context)."""
+    import os
+
+    from paper_1911_07913_b200 import Simulation
+    saved = {k: os.environ.pop(k, None) for k in ("HOT_ASM", "HOT_ASM_RING")}
+    os.environ.update(env)
+    try:
+        sim = Simulation(sc)
+    finally:
+        for k in ("HOT_ASM", "HOT_ASM_RING"):
+            os.environ.pop(k, None)
+            if saved[k] is not None:
+                os.environ[k] = saved[k]
+    sim.set_particles(**particles)
+    n = sim.stage_prepare(0.01)
+    dv = np.random.default_rng(dv_seed).uniform(-0.2, 0.2, 3 * n)
+    sim.assemble(dv, project)
+    m = sim.level_matrix(0)
+    sim.close()
+    return m
+
+
+@pytest.mark.parametrize("project", [True, False])
+def test_assembly_by_bins_matches_row_tiles_and_bands(project):
+    """The two level-0 assembly paths (by bins: k_bin_pairs + k_row_gather, the default; row tiles:
+    k_assemble_tiles) give the same matrix up to summation order, and the by-bins path gives the
+    same bits whether all bins' pair sums are resident or go through a small ring in bands."""
+    rng = np.random.default_rng(11)
+    sc = scene_from_dict(block_scene_dict(youngs=5e4, colliders=[
+        {"shape": {"kind": "half_space", "point": [0.0, 0.021, 0.0], "normal": [0.0, 1.0, 0.0]},
+         "motion": {"kind": "static"}}]))
+    p = random_block_particles(rng, 0.02, 9, f_spread=0.4, v_spread=0.3)
+    # ragged bins: drop a third of the particles (bins of 0..8 particles, chunks of 1..3 groups)
+    keep = rng.uniform(size=p["x"].shape[0]) > 0.33
+    p = {k: v[keep] for k, v in p.items()}
+    bins = _assembled(sc, p, {}, project=project)
+    tiles = _assembled(sc, p, {"HOT_ASM": "tiles"}, project=project)
+    band = _assembled(sc, p, {"HOT_ASM_RING": "1"}, project=project)  # clamped up to 4 lattice planes
+    assert np.array_equal(bins["cols"], tiles["cols"])
+    scale = np.abs(tiles["blocks"]).max()
+    assert np.abs(bins["blocks"] - tiles["blocks"]).max() <= 1e-13 * scale
+    assert _sym_err(bins) == 0.0
+    assert np.array_equal(bins["blocks"], band["blocks"])
+
+
 def test_hierarchy_and_vcycle():
     pr = _stretched_block_pair(seed=6, cells=6, youngs=1e6)
     n = pr.prepare(0.01)
