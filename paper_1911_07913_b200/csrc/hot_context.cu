@@ -1263,16 +1263,17 @@ struct Context {
     Level& l0 = L[0];
     const int n = l0.n;
     const int s_bound = l0.ext[1] * l0.ext[2] + l0.ext[2] + 2;
-    const int ring_cap =
-        (int)std::max<long long>(std::min<long long>(n, std::max<long long>(4LL * s_bound, opt.asm_ring_bins)), 1);
+    // bins that can have a node among this rank's rows (slabs: the slab and a margin)
+    const bool all = v0.lo <= 0 && v0.hi >= n;
+    const int jbeg = all ? 0 : std::max(0, v0.lo - s_bound), jend = all ? n : std::min(n, v0.hi + s_bound);
+    const int ring_cap = (int)std::max<long long>(
+        std::min<long long>(jend - jbeg, std::max<long long>(4LL * s_bound, opt.asm_ring_bins)), 1);
     asm_pairs.ensure(sizeof(double) * asm_pair_doubles() * (size_t)ring_cap);
     double* G = asm_pairs.as<double>();
     const long long plo = sh.on ? sh.p_lo : 0, phi = sh.on ? sh.p_hi : np;
     unsigned int* ctr = grid_bar.as<unsigned int>() + 8;
     unsigned long long* done = active_dev.as<unsigned long long>() + (kMaxLevels - 1);
     HOT_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned long long), stream));
-    const bool all = v0.lo <= 0 && v0.hi >= n;
-    const int jbeg = all ? 0 : std::max(0, v0.lo - s_bound), jend = all ? n : std::min(n, v0.hi + s_bound);
     const int band = jend - jbeg <= ring_cap ? std::max(jend - jbeg, 1) : ring_cap - 2 * s_bound;
     if (band <= 0) throw std::logic_error("assemble_by_bins: ring smaller than 2 lattice planes");
     for (int b0 = jbeg; b0 < jend; b0 += band) {

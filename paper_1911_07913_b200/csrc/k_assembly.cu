@@ -857,25 +857,47 @@ __device__ __forceinline__ double ld_evict_first(const double* p, unsigned long 
   return v;
 }
 /// Runs of bin position a: run 0 = positions a .. 3 (a / 3) + 2, run r >= 1 = the three positions
-/// of (k0, k1) index a / 3 + r.
+/// of (k0, k1) index a / 3 + r; 9 - a / 3 runs.  The run count is warp-uniform, and a switch that
+/// falls through from the last run issues exactly that many loads / adds (predicated-off
+/// instructions of a fully unrolled loop cost as many issue slots as live ones).
+#define RG_RUN_LOAD(r) v[r] = lane < 27 ? ld_evict_first(seg + 9 * (3 * (m0 + r) - a) + lane, policy) : 0.0
 __device__ __forceinline__ void rg_load(const double* __restrict__ seg, int a, int lane, unsigned long long policy,
                                         double (&v)[9]) {
-  const int m0 = a / 3, nruns = 9 - m0, len0 = 9 * (3 * m0 + 3 - a);
-  v[0] = lane < len0 ? ld_evict_first(seg + lane, policy) : 0.0;
-#pragma unroll
-  for (int r = 1; r < 9; ++r)
-    if (r < nruns) v[r] = lane < 27 ? ld_evict_first(seg + 9 * (3 * (m0 + r) - a) + lane, policy) : 0.0;
+  const int m0 = a / 3, len0 = 9 * (3 * m0 + 3 - a);
+  switch (9 - m0) {
+    case 9: RG_RUN_LOAD(8); [[fallthrough]];
+    case 8: RG_RUN_LOAD(7); [[fallthrough]];
+    case 7: RG_RUN_LOAD(6); [[fallthrough]];
+    case 6: RG_RUN_LOAD(5); [[fallthrough]];
+    case 5: RG_RUN_LOAD(4); [[fallthrough]];
+    case 4: RG_RUN_LOAD(3); [[fallthrough]];
+    case 3: RG_RUN_LOAD(2); [[fallthrough]];
+    case 2: RG_RUN_LOAD(1); [[fallthrough]];
+    default: v[0] = lane < len0 ? ld_evict_first(seg + lane, policy) : 0.0;
+  }
 }
+#undef RG_RUN_LOAD
+#define RG_RUN_ADD(r)                                                          \
+  {                                                                            \
+    const int m = m0 + r;                                                      \
+    if (lane < 27) acc[9 * (5 * m + 10 * (m / 3) - Sa) + lane] += v[r];        \
+  }
 __device__ __forceinline__ void rg_add(double* acc, int a, int lane, const double (&v)[9]) {
-  const int m0 = a / 3, nruns = 9 - m0, len0 = 9 * (3 * m0 + 3 - a), Sa = spos(a);
-  if (lane < len0) acc[lane] += v[0];
-#pragma unroll
-  for (int r = 1; r < 9; ++r)
-    if (r < nruns) {
-      const int m = m0 + r;
-      if (lane < 27) acc[9 * (5 * m + 10 * (m / 3) - Sa) + lane] += v[r];
-    }
+  const int m0 = a / 3, len0 = 9 * (3 * m0 + 3 - a), Sa = spos(a);
+  switch (9 - m0) {
+    case 9: RG_RUN_ADD(8); [[fallthrough]];
+    case 8: RG_RUN_ADD(7); [[fallthrough]];
+    case 7: RG_RUN_ADD(6); [[fallthrough]];
+    case 6: RG_RUN_ADD(5); [[fallthrough]];
+    case 5: RG_RUN_ADD(4); [[fallthrough]];
+    case 4: RG_RUN_ADD(3); [[fallthrough]];
+    case 3: RG_RUN_ADD(2); [[fallthrough]];
+    case 2: RG_RUN_ADD(1); [[fallthrough]];
+    default:
+      if (lane < len0) acc[lane] += v[0];
+  }
 }
+#undef RG_RUN_ADD
 __global__ void __launch_bounds__(kRgWarps * 32, RG_MINB)
     k_row_gather(BinsView bins, GridView g, LevelView L, const double* __restrict__ G, int ring_cap, int rlo, int rhi,
                  int blo, int bhi, long long plo, long long phi, unsigned int* __restrict__ counter) {

@@ -20,6 +20,6 @@ timeout 300 $PCMD > $O/prof_short.log 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file $O/dram.csv $PCMD > $O/ncu_dram.log 2>&1
 echo dram_rc=$? >> $O/ncu_dram.log
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_assemble_tiles|k_sgs_stream|k_sgs_flow|k_bin_p2g|k_bin_force" \
-  -c 8 -f -o $O/full $PCMD > $O/ncu_full.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_bin_pairs|k_row_gather|k_sgs_stream|k_sgs_flow|k_bin_p2g|k_bin_force" \
+  -c 10 -f -o $O/full $PCMD > $O/ncu_full.log 2>&1
 echo full_rc=$? >> $O/ncu_full.log
