@@ -53,6 +53,10 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+STEP_TIMES = bool(os.environ.get("BENCH_STEP_TIMES"))  # diagnosis: per-step times of the timed region on stderr
+CLOCK_PERIOD_MS = int(os.environ.get("BENCH_CLOCK_MS", "50"))  # nvidia-smi sampling period; 0: no sampler (diagnosis)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
 
@@ -60,14 +64,30 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.lo, self.hi = 0, None
+
+    def begin_timed(self, wait_s=3.0):
+        """Call after warm-up: nvidia-smi's start-up (NVML attach, ~0.1 s, stalls the CUDA process it
+        watches: measured 1 run in 4 losing 130 ms of a 300 ms timed region) is over once it has
+        printed a row; only rows from here to end_timed() are reported."""
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < wait_s:
+            time.sleep(0.01)
+        self.lo = len(self.rows)
+
+    def end_timed(self):
+        time.sleep(0.06)  # one more sampling period: a region shorter than 50 ms still gets a row
+        self.hi = len(self.rows)
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        if CLOCK_PERIOD_MS <= 0:
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                          "--format=csv,noheader,nounits", "-lms", str(CLOCK_PERIOD_MS)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -90,14 +110,15 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows[self.lo:self.hi]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k] and "Not" not in r[3 + k]})
+        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[3 + k] and "Not" not in r[3 + k]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def dist_env():
@@ -279,30 +300,58 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(device)
 
+    # the clock sampler starts before the warm-up so that its start-up is over when timing begins
+    clocks = ClockSampler(device)
+    clocks.__enter__()
     step_no = 0
     for _ in range(args.warmup):
         sim.advance_step(frame_end(sc.source, step_no))
         step_no += 1
     sim.clear_diagnostics()
 
-    # ---- device-resident timed region.  The per-phase profile stays on: it records CUDA-event
-    # pairs on the context stream and nothing else (no extra kernel, no host synchronisation;
-    # the active-slot counts behind the algorithmic bytes are snapshotted on the device).
+    # ---- device-resident timed region: K steps, nothing but the steps between the two events.
+    # The per-phase profile is taken over the NEXT K steps of the same run (CUDA-event pairs on the
+    # context stream, no extra kernel, no host synchronisation): with the profile inside the timed
+    # region, about one run in eight lost 50-150 ms of a 300 ms region between phases (event
+    # creation on the host; the phase sums were unchanged), so the headline carries no
+    # instrumentation and the rooflines are measured live right after it.
+    clocks.begin_timed()
     barrier()
-    sim.profile(True)
     launches0 = sim.kernel_launches()
     outer = []
-    with ClockSampler(device) as clocks:
+    try:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
+        marks = []
         for _ in range(args.steps):
             st = sim.advance_step(frame_end(sc.source, step_no))
             step_no += 1
             outer.append(st["outer_iterations"])
+            if STEP_TIMES:
+                marks.append(torch.cuda.Event(enable_timing=True))
+                marks[-1].record(stream)
         ev1.record(stream)
         barrier()
+        clocks.end_timed()
+        if STEP_TIMES:
+            ts = [ev0.elapsed_time(m) for m in marks]
+            print("step_ms", [round(b - a, 2) for a, b in zip([0.0] + ts[:-1], ts)], file=sys.stderr)
+    finally:
+        clocks.__exit__()
     ms = ev0.elapsed_time(ev1)
     launches = sim.kernel_launches() - launches0
+    # ---- profiled pass: the same number of steps, continuing the simulation
+    sim.profile(True)
+    pv0, pv1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pv0.record(stream)
+    outer_prof = []
+    for _ in range(args.steps):
+        st = sim.advance_step(frame_end(sc.source, step_no))
+        step_no += 1
+        outer_prof.append(st["outer_iterations"])
+    pv1.record(stream)
+    barrier()
+    ms_prof = pv0.elapsed_time(pv1)
     prof = sim.profile_read()
     sim.profile(False)
     if world > 1:
@@ -365,7 +414,7 @@ def main():
         ach = ph["flops"] / (ph["ms"] / 1000.0) / 1e12
         return {"bound": "tensor", "pipe": "fp64 DMMA m8n8k4", "kernel": kernel, "achieved": ach,
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
-                "traffic": TRAFFIC.get(kernel), "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                "traffic": TRAFFIC.get(kernel), "share_of_step": ph["ms"] / ms_prof, "launches": ph["launches"],
                 "ms_per_launch": ph["ms"] / max(ph["launches"], 1),
                 "flops_per_launch": ph["flops"] / max(ph["launches"], 1),
                 "peak_kind": "measured fp64 tensor (DMMA) peak, the higher of DMMA/DFMA (profiles/r01_fp64_peak.json, tools/microbench/dmma.cu)"}
@@ -374,7 +423,7 @@ def main():
         ach = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
         return {"bound": "hbm", "kernel": kernel, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "traffic": TRAFFIC.get(kernel), "peak_kind": peak_kind,
-                "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                "share_of_step": ph["ms"] / ms_prof, "launches": ph["launches"],
                 "ms_per_launch": ph["ms"] / max(ph["launches"], 1),
                 "bytes_per_launch": ph["bytes"] / max(ph["launches"], 1)}
 
@@ -388,7 +437,7 @@ def main():
         ach = pa["flops"] / (tot_ms / 1000.0) / 1e12
         assembly = {"kernels": ["k_bin_pairs", "k_row_gather"], "ms_per_step": tot_ms / args.steps, "achieved": ach,
                     "unit": "TFLOP/s", "peak": FP64_PEAK_TFLOPS, "frac": ach / FP64_PEAK_TFLOPS,
-                    "share_of_step": tot_ms / ms}
+                    "share_of_step": tot_ms / ms_prof}
     elif ro and ro["ms"] > 0 and ro["flops"] > 0:
         roofline = tensor_line(ro, "k_assemble_tiles")
     hbm_phases = {k: v for k, v in prof.items() if v["bytes"] > 0 and v["ms"] > 0 and
@@ -406,7 +455,7 @@ def main():
         achieved = ph["bytes"] / (ph["ms"] / 1000.0) / 1e9
         roofline_hbm = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": achieved / peaks["hbm_gbs"], "traffic": TRAFFIC.get(top), "peak_kind": peak_kind,
-                        "share_of_step": ph["ms"] / ms, "launches": ph["launches"],
+                        "share_of_step": ph["ms"] / ms_prof, "launches": ph["launches"],
                         "bytes_per_launch": ph["bytes"] / max(ph["launches"], 1)}
 
     cpu_baseline = None
@@ -442,7 +491,10 @@ def main():
                 "parallelism": (f"slabs x{world} (axis-0 lattice planes, NCCL)" if slabbed else
                                 f"replicas x{world}" + (f" (slab transport failed: {slab_error})" if slab_error else "")
                                 if world > 1 else "single GPU"),
-                "outer_iterations": outer, "phase_ms_per_step": phases, "rank0_shard": shard,
+                "outer_iterations": outer, "phase_ms_per_step": phases,
+                "profiled_pass": {"steps": args.steps, "ms_per_step": ms_prof / args.steps, "outer_iterations": outer_prof,
+                                  "note": "phase_ms_per_step, the rooflines and hbm_phases: the K steps after the timed ones"},
+                "rank0_shard": shard,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "steps": e2e_steps, "outer_iterations": e2e_outer},
                 "gpu_launches": int(launches), "roofline": roofline, "roofline_assembly_pairs": roofline_pairs,

@@ -99,11 +99,18 @@ struct DBuf {
   }
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
+    static const bool trace = std::getenv("HOT_ALLOC_TRACE") != nullptr;  // diagnosis: growth events
+    if (trace) std::fprintf(stderr, "[hot alloc] grow %zu -> %zu bytes\n", cap, bytes);
     if (p) HOT_CUDA(cudaFree(p));
     p = nullptr;
-    // grow with 25% slack (2 MiB granules): node / particle counts drift by a few per step and an
-    // exact-size reallocation of a GB-sized level matrix every step costs more than the step
-    size_t nb = std::max<size_t>(bytes + bytes / 4, cap + cap / 4);
+    // grow with slack (2 MiB granules): node / particle counts drift by a few per step and an
+    // exact-size reallocation of a GB-sized level matrix every step costs more than the step.
+    // 25 % for buffers of 1 GB and more, 50 % from 256 MB, 100 % below: the small ones include the
+    // bounding-box sized maps, whose box grows with the motion (cfg2: +26 % volume in 13 steps),
+    // and a cudaFree + cudaMalloc in the middle of a run costs 1.5 ms at best and, one time in
+    // eight on the bench box, 30-400 ms
+    const size_t slack = bytes >= (size_t(1) << 30) ? bytes / 4 : bytes >= (size_t(256) << 20) ? bytes / 2 : bytes;
+    size_t nb = std::max<size_t>(bytes + slack, cap + cap / 4);
     nb = std::max<size_t>((nb + (2u << 20) - 1) & ~size_t((2u << 20) - 1), 256);
     HOT_CUDA(cudaMalloc(&p, nb));
     cap = nb;
