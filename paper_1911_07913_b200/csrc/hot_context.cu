@@ -2467,6 +2467,7 @@ int hot_stage_build_hierarchy(hot_ctx* ctx, int levels, int embedding) {
     Context& c = ctx->c;
     if (!c.have_H) throw std::logic_error("no matrix assembled");
     c.build_hierarchy(levels, embedding);
+    c.prof_snapshot_slots();  // the staged V-cycle / SpMV profile bytes refer to this hierarchy
     for (int m = 0; m < c.nlevels; ++m) c.L[m].active_slots = c.count_active_slots(m);
   });
 }
