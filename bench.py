@@ -23,6 +23,7 @@ DESIGN.md §6): scaling "strong", value = the scene's particle-steps / the max o
 device time.  --mode replicas runs N independent copies instead ("weak").
 """
 import argparse
+import atexit
 import json
 import os
 import statistics
@@ -102,7 +103,7 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *a):
-        if self.proc:
+        if self.proc and self.proc.poll() is None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -303,6 +304,7 @@ def main():
     # the clock sampler starts before the warm-up so that its start-up is over when timing begins
     clocks = ClockSampler(device)
     clocks.__enter__()
+    atexit.register(clocks.__exit__)  # never leave nvidia-smi looping if a step raises
     step_no = 0
     for _ in range(args.warmup):
         sim.advance_step(frame_end(sc.source, step_no))
