@@ -1283,6 +1283,8 @@ struct Context {
     HOT_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned long long), stream));
     const int band = jend - jbeg <= ring_cap ? std::max(jend - jbeg, 1) : ring_cap - 2 * s_bound;
     if (band <= 0) throw std::logic_error("assemble_by_bins: ring smaller than 2 lattice planes");
+    if (jend <= jbeg)  // no rows: still leave the column ids and the active-slot count defined
+      launch_fill_cols(l0.view(), active_dev.as<unsigned long long>(), stream);
     for (int b0 = jbeg; b0 < jend; b0 += band) {
       const int b1 = std::min(b0 + band, jend);
       const bool first = b0 == jbeg, last = b1 == jend;
