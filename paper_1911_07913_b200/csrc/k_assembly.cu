@@ -602,8 +602,14 @@ static_assert(kPairDoubles == 3416 && pair_seg_off(1) == 244 && pair_seg_off(2) 
 /// Slot index of stencil position k in the 5^3 diagonal storage, relative to position 0.
 __device__ __forceinline__ int spos(int k) { return k + 2 * (k / 3) + 10 * (k / 9); }
 
-constexpr int kBpCP = 12;    // records per ring slot (3 groups of 4 particles)
-constexpr int kBpS = 3;      // ring slots
+#ifndef HOT_BP_CP
+#define HOT_BP_CP 12
+#endif
+#ifndef HOT_BP_S
+#define HOT_BP_S 3
+#endif
+constexpr int kBpCP = HOT_BP_CP;  // records per ring slot (groups of 4 particles)
+constexpr int kBpS = HOT_BP_S;    // ring slots
 constexpr int kBpWarps = 9;  // compute warps: one block entry ce = 3c + e each
 constexpr int kBpGrab = 32;  // bins per work-counter grab
 struct BpMeta {
