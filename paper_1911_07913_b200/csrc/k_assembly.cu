@@ -3,13 +3,16 @@
 // Stage 1 (one thread per particle): virtual F -> SVD -> dP/dF projected in the diagonal
 //   space -> one 1008-byte record per particle: the 27 W_k = F^nT grad w_k, then kappa*T as
 //   its 45 unique entries (hot_particle.cuh: kRecW, kRecT, tslot).
-// Stage 2 (one warp per row, rows from a work counter): gather over the 27 neighbouring
-//   particle bins, records staged by the bulk-copy engine, the per-particle rank-3 block
-//   updates on the fp64 tensor cores (DMMA), accumulated into the row's upper-triangle slots
-//   in shared memory (fixed order, no atomics).  Each unordered block pair is computed once by
-//   the row with the smaller index and written together with its transpose, so block (i,j) ==
+// Stage 2, by bins (the default; k_bin_pairs + k_row_gather below): every particle of a bin has
+//   the same 27 stencil nodes, so the bin's sums over its particles for the 378 unordered
+//   stencil-position pairs are formed ONCE, as DMMA tiles on the fp64 tensor cores (records
+//   staged by the bulk-copy engine, the result bulk-stored to a ring of bins); then one warp per
+//   row adds the segments of its 27 bins in a fixed order (no atomics) and writes the row.
+//   Each unordered block pair is written together with its transpose, so block (i,j) ==
 //   block(j,i)^T exactly (the reference's symmetry_error() == 0 invariant).  The mass diagonal
 //   and the Dirichlet projection (objective.hpp:133-144) are fused into the write-out.
+// Stage 2, by row tiles (HOT_ASM=tiles; k_assemble_tiles): one warp per row gathers over the 27
+//   neighbouring bins and forms the per-particle rank-3 block updates per (row, particle).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -619,14 +622,10 @@ constexpr size_t kBpRingBytes = (size_t)kBpS * kBpCP * kRecBytes;
 constexpr size_t kBpOutBytes = 2 * (size_t)kPairBytes;
 constexpr size_t kBpZeroBytes = kRecBytes;
 constexpr size_t kBpBarBytes = (size_t)(2 * kBpS + 4) * 8;  // ring full / empty, output full[2] / free[2]
-constexpr int kBpQueue = 8;  // bins between the producer's push and their store (< ring + 2 outputs)
+constexpr int kBpQueue = kBpS + 5;  // > bins between the producer's push and their store (ring slots + 2 outputs + 1)
 constexpr size_t kBpMetaBytes = (size_t)kBpS * sizeof(BpMeta) + kBpQueue * sizeof(int);
 constexpr size_t kBpSmem = kBpRingBytes + kBpOutBytes + kBpZeroBytes + kBpBarBytes + kBpMetaBytes;
 static_assert(kBpRingBytes % 16 == 0 && kBpOutBytes % 16 == 0 && kBpZeroBytes % 16 == 0, "16-byte aligned regions");
-
-__device__ __forceinline__ void bp_named_barrier() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kBpWarps * 32) : "memory");
-}
 
 /// One compute warp of k_bin_pairs: block entry ce = wid, all ten (a tile, k tile >= a tile)
 /// accumulator tiles.  Lane (qk, qm): particle 4u + qk of the group, position 8t + qm of a tile;
