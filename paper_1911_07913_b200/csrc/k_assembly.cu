@@ -841,8 +841,7 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
 /// band whose pair sums stage A has just produced; blo < 0 and bhi > n: every row).  A CTA takes
 /// kRgWarps consecutive rows at a time from a counter, in index order: consecutive rows run
 /// along z, their transposes fill neighbouring slots of the same lower-half lines at about the
-/// same time, and the rows in flight stay a narrow band, so those lines are completed in L2 (the
-/// pair sums are loaded evict-first).  The row's 27 bins in neighbour-table order (x, y, z
+/// same time, and the rows in flight stay a narrow band, so those lines are completed in L2.  The row's 27 bins in neighbour-table order (x, y, z
 /// ascending); the row sits at position a = 26 - e of bin e, whose segment is read in runs of up
 /// to three positions k (27 doubles, contiguous both in the segment and in the row's upper slots
 /// spos(k) - spos(a)); the loads of two bins are in flight before the first is added.
@@ -856,18 +855,16 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
 #define RG_STREAM false
 #endif
 constexpr int kRgWarps = RG_WARPS;
-__device__ __forceinline__ double ld_evict_first(const double* p, unsigned long long policy) {
-  double v;
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy));
-  return v;
-}
+/// Pair-sum load: L2 only (no L1 allocation), default L2 policy.  With the rows of a CTA
+/// consecutive, the sectors two runs or two rows share are L2 hits; an evict-first hint lost them
+/// (k_row_gather 2.15 against 2.01 ms).
+__device__ __forceinline__ double ld_pair(const double* p) { return __ldcg(p); }
 /// Runs of bin position a: run 0 = positions a .. 3 (a / 3) + 2, run r >= 1 = the three positions
 /// of (k0, k1) index a / 3 + r; 9 - a / 3 runs.  The run count is warp-uniform, and a switch that
 /// falls through from the last run issues exactly that many loads / adds (predicated-off
 /// instructions of a fully unrolled loop cost as many issue slots as live ones).
-#define RG_RUN_LOAD(r) v[r] = lane < 27 ? ld_evict_first(seg + 9 * (3 * (m0 + r) - a) + lane, policy) : 0.0
-__device__ __forceinline__ void rg_load(const double* __restrict__ seg, int a, int lane, unsigned long long policy,
-                                        double (&v)[9]) {
+#define RG_RUN_LOAD(r) v[r] = lane < 27 ? ld_pair(seg + 9 * (3 * (m0 + r) - a) + lane) : 0.0
+__device__ __forceinline__ void rg_load(const double* __restrict__ seg, int a, int lane, double (&v)[9]) {
   const int m0 = a / 3, len0 = 9 * (3 * m0 + 3 - a);
   switch (9 - m0) {
     case 9: RG_RUN_LOAD(8); [[fallthrough]];
@@ -878,7 +875,7 @@ __device__ __forceinline__ void rg_load(const double* __restrict__ seg, int a, i
     case 4: RG_RUN_LOAD(3); [[fallthrough]];
     case 3: RG_RUN_LOAD(2); [[fallthrough]];
     case 2: RG_RUN_LOAD(1); [[fallthrough]];
-    default: v[0] = lane < len0 ? ld_evict_first(seg + lane, policy) : 0.0;
+    default: v[0] = lane < len0 ? ld_pair(seg + lane) : 0.0;
   }
 }
 #undef RG_RUN_LOAD
@@ -910,7 +907,6 @@ __global__ void __launch_bounds__(kRgWarps * 32, RG_MINB)
   __shared__ int s_base[2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* acc = accs[wid];
-  const unsigned long long policy = l2_evict_first_policy();
   if (threadIdx.x == 0) s_base[0] = rlo + kRgWarps * (int)atomicAdd(counter, 1u);
   for (int it = 0;; ++it) {
     __syncthreads();  // s_base[it & 1] is set; everyone is done with s_base[(it + 1) & 1]
@@ -955,8 +951,8 @@ __global__ void __launch_bounds__(kRgWarps * 32, RG_MINB)
       const double* seg1 = G + (size_t)__shfl_sync(0xffffffffu, slot, e1) * kPairDoubles + pair_seg_off(a1);
       const double* seg2 = G + (size_t)__shfl_sync(0xffffffffu, slot, max(e2, 0)) * kPairDoubles + pair_seg_off(a2);
       double v1[9], v2[9];
-      rg_load(seg1, a1, lane, policy, v1);
-      if (e2 >= 0) rg_load(seg2, a2, lane, policy, v2);
+      rg_load(seg1, a1, lane, v1);
+      if (e2 >= 0) rg_load(seg2, a2, lane, v2);
       rg_add(acc, a1, lane, v1);
       if (e2 >= 0) rg_add(acc, a2, lane, v2);
     }
