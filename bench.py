@@ -41,7 +41,7 @@ SCENE = os.path.join(ROOT, "scenes", "cfg2_twisting_bars.json")
 METRIC = "implicit MPM particle-steps/sec (fp64, fixed tol)"
 FP64_PEAK_TFLOPS = 37.06  # fp64 peak measured on this pool's B200: DMMA m8n8k4 37.06, DFMA 34.79 (profiles/r01_fp64_peak.json)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full` (profiles/), or None
-# per launch, from profiles/r02_final3_ncu_full_summary.txt
+# per launch, from profiles/r02_final4_ncu_full_summary.txt
 TRAFFIC = {"k_bin_pairs": 5.72e9, "k_row_gather": 7.48e9, "k_assemble_tiles": 3.467671e9, "sgs_level0": 4.086369e9}
 UNIT = "particle-steps/s"
 
