@@ -741,11 +741,9 @@ __global__ void __launch_bounds__((kBpWarps + 1) * 32, 2)
   }
   __syncthreads();
 
-  // Roles rotate between the two CTAs that share an SM (blocks b and b + gridDim / 2): warps map to
-  // the SM's four schedulers by warp id mod 4, so with the producer always last, scheduler 0
-  // would carry 6 of the 18 compute warps and cap the tensor pipes at 75 %.
-  const int rot = blockIdx.x >= (gridDim.x + 1) / 2 ? 1 : 0;
-  const int role = rot ? (wid == 0 ? kBpWarps : wid - 1) : wid;
+  // (Rotating the producer's warp slot between the CTAs of an SM, by block index or by arrival
+  // order on the SM, measured no different: the schedulers are not what limits the tensor pipe.)
+  const int role = wid;
   if (role == kBpWarps) {  // ------------------------------------------------ producer warp
     // Lane 0 runs both pipelines without blocking in either: record chunks into free ring slots,
     // and the bulk store of every bin whose nine columns have arrived in an output buffer.
