@@ -147,6 +147,44 @@ def test_nccl_transport_single_rank(tmp_path):
         np.testing.assert_array_equal(res[k], ref[k])
 
 
+def _gpu_count():
+    from paper_1911_07913_b200 import capi
+
+    return capi.lib().hot_device_count()
+
+
+@pytest.mark.skipif(_gpu_count() < 2, reason="needs two GPUs: NCCL refuses two ranks on one device")
+def test_nccl_transport_two_gpus(tmp_path):
+    """Two ranks on two GPUs over the library's NCCL transport: the send/recv halo
+    pairs and the grouped in-place broadcasts at size 2; every rank bitwise equal to one GPU."""
+    ref = run_ranks(tmp_path, "cfg1_stretched.json", 1, 3, tag="single")[0]
+    port = _free_port()
+    procs, outs = [], []
+    for r in range(2):
+        out = str(tmp_path / f"nccl2_{r}.npz")
+        env = dict(ENV, SLAB_DEVICE=str(r))
+        procs.append(subprocess.Popen([sys.executable, WORKER, str(r), "2", str(port),
+                                       os.path.join(SCENES, "cfg1_stretched.json"), "3", out, "nccl"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, env=env))
+        outs.append(out)
+    logs = []
+    for p in procs:
+        try:
+            o, _ = p.communicate(timeout=600)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+        logs.append(o)
+    for p, o in zip(procs, logs):
+        assert p.returncode == 0, o[-4000:]
+    for out in outs:
+        res = dict(np.load(out))
+        assert res["sharded"].any()
+        for k in ("x", "v", "F", "C"):
+            np.testing.assert_array_equal(res[k], ref[k])
+
+
 def _scene_file(tmp_path, name, objects, materials=None):
     d = {"dim": 3, "dx": 1.0 / 64, "gravity": [0.0, -9.8, 0.0], "fps": 500, "frames": 4, "epsilon": 1e-05, "seed": 7,
          "ppc": 8, "domain": {"min": [0.0, 0.0, 0.0], "max": [1.0, 1.0, 1.0]},
